@@ -1,0 +1,253 @@
+"""ctypes wrapper of the CPU oracle (oracle/isdc_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs, never by the product package ``paper_1401_7824_b200``.  It shares no code
+with the CUDA path; see DESIGN.md §5 ("oracle").  Every function cites the paper passage it follows
+in isdc_oracle.c.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import time
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "isdc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC", "-Wall"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no FMA contraction, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lquadmath", "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(_LIB)
+        _declare(_lib)
+    return _lib
+
+
+class OraProblem(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("n", C.c_int), ("M", C.c_int),
+        ("dt", C.c_double), ("nu", C.c_double),
+        ("fe", C.c_int), ("fe_a", C.c_double * 3), ("G", C.c_void_p),
+        ("mode", C.c_int), ("L", C.c_int), ("inner_tol", C.c_double), ("inner_cap", C.c_int),
+        ("sweep_tol", C.c_double), ("max_sweeps", C.c_int), ("fixed_sweeps", C.c_int),
+        ("nu1", C.c_int), ("nu2", C.c_int), ("omega", C.c_double), ("guess", C.c_int),
+    ]
+
+
+_dp = C.POINTER(C.c_double)
+
+
+def _declare(L):
+    L.ora_tables.argtypes = [C.c_int, _dp, _dp, _dp, _dp]
+    L.ora_apply_B.argtypes = [C.c_int, C.c_int, _dp, _dp]
+    L.ora_apply_L.argtypes = [C.c_int, C.c_int, _dp, _dp]
+    L.ora_apply_S.argtypes = [C.c_int, C.c_int, C.c_double, _dp, _dp]
+    L.ora_level_coefs.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp]
+    L.ora_jacobi.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _dp, _dp]
+    L.ora_defect_norm.argtypes = [C.c_int, C.c_int, C.c_double, _dp, _dp]
+    L.ora_defect_norm.restype = C.c_double
+    L.ora_restrict.argtypes = [C.c_int, C.c_int, _dp, _dp]
+    L.ora_prolong_add.argtypes = [C.c_int, C.c_int, _dp, _dp]
+    L.ora_coarse_inverse.argtypes = [C.c_int, C.c_double, C.c_double, _dp]
+    L.ora_vcycle.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double, _dp, _dp]
+    L.ora_fe_eval.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, _dp, _dp]
+    PP = C.POINTER(_dp)
+    L.ora_rhs.argtypes = [C.POINTER(OraProblem), C.c_double, C.c_int, PP, PP, _dp]
+    L.ora_residual.argtypes = [C.POINTER(OraProblem), C.c_double, PP, _dp]
+    L.ora_residual.restype = C.c_double
+    L.ora_sweep_state.argtypes = [C.POINTER(OraProblem), C.c_double, PP, PP, C.POINTER(C.c_int)]
+    L.ora_step.argtypes = [C.POINTER(OraProblem), _dp, C.c_double, C.POINTER(C.c_int),
+                           C.POINTER(C.c_long), _dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                           C.POINTER(C.c_int)]
+    L.ora_num_threads.restype = C.c_int
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def _c(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def num_threads() -> int:
+    return lib().ora_num_threads()
+
+
+# ---------------------------------------------------------------------------------------------
+# tables and operators
+# ---------------------------------------------------------------------------------------------
+def tables(M: int):
+    """(tau[M], Q[M,M], S[M-1,M], dtau[M-1]) for Gauss-Lobatto nodes (Eq. 2)."""
+    tau, Q = np.zeros(M), np.zeros((M, M))
+    S, dtau = np.zeros((M - 1, M)), np.zeros(M - 1)
+    if lib().ora_tables(M, _p(tau), _p(Q), _p(S), _p(dtau)):
+        raise ValueError(M)
+    return tau, Q, S, dtau
+
+
+def apply_B(u):
+    u = _c(u); out = np.empty_like(u)
+    lib().ora_apply_B(u.ndim, u.shape[0], _p(u), _p(out)); return out
+
+
+def apply_L(u):
+    u = _c(u); out = np.empty_like(u)
+    lib().ora_apply_L(u.ndim, u.shape[0], _p(u), _p(out)); return out
+
+
+def apply_S(u, gamma):
+    u = _c(u); out = np.empty_like(u)
+    lib().ora_apply_S(u.ndim, u.shape[0], gamma, _p(u), _p(out)); return out
+
+
+def level_coefs(dim, n, gamma, omega=0.8):
+    c = np.zeros(4)
+    lib().ora_level_coefs(dim, n, gamma, omega, _p(c)); return c
+
+
+def jacobi(b, u, gamma, sweeps=1, omega=0.8):
+    b = _c(b); u = _c(u).copy()
+    lib().ora_jacobi(u.ndim, u.shape[0], gamma, omega, sweeps, _p(b), _p(u)); return u
+
+
+def defect_norm(b, u, gamma):
+    b = _c(b); u = _c(u)
+    return lib().ora_defect_norm(u.ndim, u.shape[0], gamma, _p(b), _p(u))
+
+
+def restrict(d):
+    d = _c(d); nc = (d.shape[0] - 1) // 2
+    out = np.zeros((nc,) * d.ndim)
+    lib().ora_restrict(d.ndim, d.shape[0], _p(d), _p(out)); return out
+
+
+def prolong_add(ec, uf):
+    ec = _c(ec); uf = _c(uf).copy()
+    lib().ora_prolong_add(ec.ndim, ec.shape[0], _p(ec), _p(uf)); return uf
+
+
+def coarse_inverse(dim, gamma, omega=0.8):
+    P = 9 if dim == 2 else 27
+    G = np.zeros((P, P))
+    if lib().ora_coarse_inverse(dim, gamma, omega, _p(G)):
+        raise ValueError("singular")
+    return G
+
+
+def vcycle(b, u, gamma, nu1=2, nu2=2, omega=0.8, cycles=1):
+    b = _c(b); u = _c(u).copy()
+    for _ in range(cycles):
+        lib().ora_vcycle(u.ndim, u.shape[0], gamma, nu1, nu2, omega, _p(b), _p(u))
+    return u
+
+
+def fe_eval(fe, u, a=(0.0, 0.0, 0.0), G=None, ct=1.0):
+    u = _c(u); out = np.empty_like(u)
+    av = np.array(a, dtype=np.float64)
+    Gp = _p(_c(G)) if G is not None else None
+    lib().ora_fe_eval(fe, u.ndim, u.shape[0], _p(av), Gp, ct, _p(u), _p(out)); return out
+
+
+# ---------------------------------------------------------------------------------------------
+# problem-level entry points
+# ---------------------------------------------------------------------------------------------
+class Problem:
+    """Mirror of synth.Config plus run-time choices; holds the ctypes struct and keeps G alive."""
+
+    def __init__(self, cfg, G=None, mode=0, guess=0):
+        self.cfg = cfg
+        self.G = None if G is None else _c(G)
+        self.s = OraProblem()
+        s = self.s
+        s.dim, s.n, s.M = cfg.dim, cfg.n, cfg.M
+        s.dt, s.nu, s.fe = cfg.dt, cfg.nu, cfg.fe
+        for i in range(3):
+            s.fe_a[i] = cfg.fe_a[i]
+        s.G = self.G.ctypes.data if self.G is not None else None
+        s.mode, s.L, s.inner_tol, s.inner_cap = mode, cfg.L, cfg.inner_tol, cfg.inner_cap
+        s.sweep_tol, s.max_sweeps, s.fixed_sweeps = cfg.sweep_tol, cfg.max_sweeps, cfg.fixed_sweeps
+        s.nu1, s.nu2, s.omega, s.guess = cfg.nu1, cfg.nu2, cfg.omega, guess
+
+
+def _ptrs(fields):
+    arr = (_dp * len(fields))()
+    for i, f in enumerate(fields):
+        arr[i] = _p(f)
+    return arr
+
+
+def rhs(prob: Problem, t_n, m, uold, unew):
+    """b of Eq. (5) for substep m (0-based) from node fields uold[M], unew[M]."""
+    uold = [_c(x) for x in uold]; unew = [_c(x) for x in unew]
+    b = np.empty_like(uold[0])
+    lib().ora_rhs(C.byref(prob.s), t_n, m, _ptrs(uold), _ptrs(unew), _p(b))
+    return b
+
+
+def residual(prob: Problem, t_n, u):
+    """(max_m ||r~_m||, per_node[M-1]) of the node fields u[M] (weighted residual, DESIGN R15)."""
+    u = [_c(x) for x in u]
+    per = np.zeros(prob.cfg.M - 1)
+    r = lib().ora_residual(C.byref(prob.s), t_n, _ptrs(u), _p(per))
+    return r, per
+
+
+def sweep(prob: Problem, t_n, uold):
+    """One sweep from node fields uold[M]; returns (unew[M], cycles[M-1])."""
+    uold = [_c(x) for x in uold]
+    unew = [uold[0]] + [np.empty_like(uold[0]) for _ in range(prob.cfg.M - 1)]
+    cyc = (C.c_int * (prob.cfg.M - 1))()
+    lib().ora_sweep_state(C.byref(prob.s), t_n, _ptrs(uold), _ptrs(unew), cyc)
+    return unew, list(cyc)
+
+
+def step(prob: Problem, u0, t_n):
+    """One time step; returns (u_M, stats dict)."""
+    cfg = prob.cfg
+    u = _c(u0).copy()
+    kmax = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
+    hist = np.zeros(kmax)
+    ncyc = (C.c_int * (kmax * (cfg.M - 1)))()
+    sw, vc, caps, conv = C.c_int(0), C.c_long(0), C.c_int(0), C.c_int(0)
+    t0 = time.perf_counter()
+    rc = lib().ora_step(C.byref(prob.s), _p(u), t_n, C.byref(sw), C.byref(vc), _p(hist), ncyc,
+                        C.byref(caps), C.byref(conv))
+    el = time.perf_counter() - t0
+    if rc:
+        raise RuntimeError("ora_step failed")
+    k = sw.value
+    return u, dict(sweeps=k, vcycles=vc.value, res_hist=hist[:k].copy(),
+                   node_cycles=np.array(ncyc[: k * (cfg.M - 1)]).reshape(k, cfg.M - 1),
+                   cap_hits=caps.value, converged=bool(conv.value), seconds=el)
+
+
+def run(prob: Problem, u0, steps=None):
+    """``steps`` time steps from t = 0 (t_n = float(n)*dt, DESIGN R28)."""
+    cfg = prob.cfg
+    steps = cfg.steps if steps is None else steps
+    u = _c(u0).copy()
+    stats = []
+    for s in range(steps):
+        u, st = step(prob, u, float(s) * cfg.dt)
+        stats.append(st)
+    return u, stats

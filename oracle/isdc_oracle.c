@@ -1,0 +1,672 @@
+/*
+ * isdc_oracle.c -- plain, slow, obviously-correct CPU oracle for the ISDC hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header, table or constant
+ * generator with the CUDA path (paper_1401_7824_b200/csrc); both follow the paper and the
+ * canonical expression trees written out in DESIGN.md §4 ("canonical arithmetic").
+ *
+ * Paper: Speck, Ruprecht, Minion, Emmett, Krause, "Inexact spectral deferred corrections"
+ * (arXiv:1401.7824), /root/reference/PAPER.md.  Citation key P:n = PAPER.md line n.
+ *
+ * Compile: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC ... -lquadmath
+ * (no FMA contraction: every a*b+c below is a rounded multiply followed by a rounded add).
+ *
+ * Layout: dense fp64 arrays, n^d interior points, x fastest: idx = i + n*(j + n*k).
+ * Homogeneous Dirichlet data: every value outside 0..n-1 reads as 0.
+ *
+ * Pins (tests/test_oracle_*.py): every function below is pinned by a closed form, an invariant,
+ * a special case or brute force, except where a header comment says "parity unpinned".
+ */
+#include <math.h>
+#include <quadmath.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef __float128 qf;
+
+int ora_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Quadrature tables (Eq. 2).  Gauss-Lobatto nodes on [0,1]; Q_{m,j} = int_0^{tau_m}  */
+/* l_j(s) ds, S_{m,j} = int_{tau_m}^{tau_{m+1}} l_j(s) ds (node-to-node weights s_{m,j}).      */
+/* Everything in binary128, rounded once to binary64 at the end.                               */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Legendre P_n(x) and P_n'(x) by the three-term recurrence (k+1)P_{k+1} = (2k+1)xP_k - kP_{k-1}. */
+static void legendre_pd(int n, qf x, qf *p, qf *dp) {
+    qf p0 = 1, p1 = x;
+    if (n == 0) { *p = 1; *dp = 0; return; }
+    for (int k = 1; k < n; ++k) {
+        qf p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1);
+        p0 = p1; p1 = p2;
+    }
+    *p = p1;
+    /* (1 - x^2) P_n' = n (P_{n-1} - x P_n), valid for |x| < 1 (interior Lobatto nodes). */
+    *dp = n * (p0 - x * p1) / (1 - x * x);
+}
+
+/* Gauss-Lobatto nodes on [-1,1]: +-1 and the roots of P'_{M-1}; Newton on P'_{M-1} with
+ * P'' from the Legendre ODE (1-x^2)P'' - 2xP' + n(n+1)P = 0. */
+static int lobatto_q(int M, qf *x) {
+    if (M < 2 || M > 16) return -1;
+    int n = M - 1;
+    x[0] = -1; x[M - 1] = 1;
+    for (int k = 1; k < M - 1; ++k) {
+        qf xi = -cosq(M_PIq * k / n);
+        for (int it = 0; it < 100; ++it) {
+            qf p, dp;
+            legendre_pd(n, xi, &p, &dp);
+            qf d2p = (2 * xi * dp - n * (n + 1) * p) / (1 - xi * xi);
+            qf dx = dp / d2p;
+            xi -= dx;
+            if (fabsq(dx) < 1e-33Q) break;
+        }
+        x[k] = xi;
+    }
+    return 0;
+}
+
+/* Q_{m,j} = int_0^{tau_m} l_j, by exact integration of the monomial expansion of l_j. */
+static void q_matrix_q(int M, const qf *tau, qf *Q) {
+    for (int j = 0; j < M; ++j) {
+        qf c[32];
+        memset(c, 0, sizeof c);
+        c[0] = 1;
+        int deg = 0;
+        for (int k = 0; k < M; ++k) {
+            if (k == j) continue;
+            qf den = tau[j] - tau[k];
+            /* c(s) <- c(s) * (s - tau_k) / den */
+            for (int p = deg + 1; p >= 1; --p) c[p] = (c[p - 1] - tau[k] * c[p]) / den;
+            c[0] = (-tau[k] * c[0]) / den;
+            ++deg;
+        }
+        for (int m = 0; m < M; ++m) {
+            qf acc = 0, tp = tau[m];
+            for (int p = 0; p <= deg; ++p) { acc += c[p] * tp / (p + 1); tp *= tau[m]; }
+            Q[m * M + j] = acc;
+        }
+    }
+}
+
+/* tau[M], Q[M*M], S[(M-1)*M], dtau[M-1] (all binary64, each rounded once from binary128). */
+int ora_tables(int M, double *tau, double *Q, double *S, double *dtau) {
+    qf x[32], t[32], Qq[32 * 32];
+    if (lobatto_q(M, x)) return -1;
+    for (int m = 0; m < M; ++m) t[m] = (x[m] + 1) / 2;
+    t[0] = 0; t[M - 1] = 1;
+    q_matrix_q(M, t, Qq);
+    for (int m = 0; m < M; ++m) tau[m] = (double)t[m];
+    for (int i = 0; i < M * M; ++i) Q[i] = (double)Qq[i];
+    for (int m = 0; m + 1 < M; ++m) {
+        dtau[m] = (double)(t[m + 1] - t[m]);
+        for (int j = 0; j < M; ++j) S[m * M + j] = (double)(Qq[(m + 1) * M + j] - Qq[m * M + j]);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Grid access                                                                                 */
+/* ------------------------------------------------------------------------------------------ */
+static inline double at(const double *u, int d, int n, int i, int j, int k) {
+    if (i < 0 || j < 0 || i >= n || j >= n) return 0.0;
+    if (d == 3) {
+        if (k < 0 || k >= n) return 0.0;
+        return u[(size_t)i + (size_t)n * ((size_t)j + (size_t)n * (size_t)k)];
+    }
+    return u[(size_t)i + (size_t)n * (size_t)j];
+}
+static inline size_t npts(int d, int n) { return d == 3 ? (size_t)n * n * n : (size_t)n * n; }
+
+/* In-plane partial sums of the canonical trees:
+ *   r(i,j,k) = q(i-1,j,k) + q(i+1,j,k)
+ *   f(i,j,k) = r(i,j,k) + (q(i,j-1,k) + q(i,j+1,k))      in-plane face sum (4 terms)
+ *   e(i,j,k) = r(i,j-1,k) + r(i,j+1,k)                    in-plane diagonal sum (4 terms)
+ * 3D adds   F = f(k) + (q(k-1) + q(k+1))                  6 faces
+ *           E = e(k) + (f(k-1) + f(k+1))                  12 edges
+ * A row/plane outside the domain contributes exact zeros. */
+static inline double r_(const double *q, int d, int n, int i, int j, int k) {
+    return at(q, d, n, i - 1, j, k) + at(q, d, n, i + 1, j, k);
+}
+static inline double f_(const double *q, int d, int n, int i, int j, int k) {
+    return r_(q, d, n, i, j, k) + (at(q, d, n, i, j - 1, k) + at(q, d, n, i, j + 1, k));
+}
+static inline double e_(const double *q, int d, int n, int i, int j, int k) {
+    return r_(q, d, n, i, j - 1, k) + r_(q, d, n, i, j + 1, k);
+}
+/* faces (2D: 4, 3D: 6) and edges/corners-of-the-9-point (2D: 4 diagonals, 3D: 12 edges) */
+static inline double faces(const double *q, int d, int n, int i, int j, int k) {
+    if (d == 2) return f_(q, d, n, i, j, 0);
+    return f_(q, d, n, i, j, k) + (at(q, d, n, i, j, k - 1) + at(q, d, n, i, j, k + 1));
+}
+static inline double edges(const double *q, int d, int n, int i, int j, int k) {
+    if (d == 2) return e_(q, d, n, i, j, 0);
+    return e_(q, d, n, i, j, k) + (f_(q, d, n, i, j, k - 1) + f_(q, d, n, i, j, k + 1));
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Compact (Mehrstellen) pair, P:68-72 and SPEC S:144 (2D); 3D: standard 19-point pair.        */
+/*   2D: L_h = 1/(6h^2)[1 4 1; 4 -20 4; 1 4 1],  B_h = 1/12[0 1 0; 1 8 1; 0 1 0]               */
+/*   3D: L_h = 1/(6h^2)(centre -24, faces 2, edges 1),  B_h = 1/12(centre 6, faces 1)          */
+/* Constants (host, binary64, in this order): N2 = N*N;                                        */
+/*   2D kB0 = 8/12, kB1 = 1/12, kL0 = (-20*N2)/6, kL1 = (4*N2)/6, kL2 = N2/6                   */
+/*   3D kB0 = 6/12, kB1 = 1/12, kL0 = (-24*N2)/6, kL1 = (2*N2)/6, kL2 = N2/6                   */
+/*   B q = kB0*q + kB1*faces;   L q = (kL0*q + kL1*faces) + kL2*edges                          */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct { double kB0, kB1, kL0, kL1, kL2; } bl_consts;
+
+static bl_consts make_bl(int d, int n) {
+    bl_consts c;
+    double N = (double)(n + 1), N2 = N * N;
+    if (d == 2) {
+        c.kB0 = 8.0 / 12.0; c.kB1 = 1.0 / 12.0;
+        c.kL0 = (-20.0 * N2) / 6.0; c.kL1 = (4.0 * N2) / 6.0; c.kL2 = N2 / 6.0;
+    } else {
+        c.kB0 = 6.0 / 12.0; c.kB1 = 1.0 / 12.0;
+        c.kL0 = (-24.0 * N2) / 6.0; c.kL1 = (2.0 * N2) / 6.0; c.kL2 = N2 / 6.0;
+    }
+    return c;
+}
+static inline double B_at(const bl_consts *c, const double *q, int d, int n, int i, int j, int k) {
+    return c->kB0 * at(q, d, n, i, j, k) + c->kB1 * faces(q, d, n, i, j, k);
+}
+static inline double L_at(const bl_consts *c, const double *q, int d, int n, int i, int j, int k) {
+    return (c->kL0 * at(q, d, n, i, j, k) + c->kL1 * faces(q, d, n, i, j, k)) +
+           c->kL2 * edges(q, d, n, i, j, k);
+}
+
+#define FOR_POINTS(d, n)                                                        \
+    _Pragma("omp parallel for collapse(2) schedule(static)")                    \
+    for (int kk = 0; kk < ((d) == 3 ? (n) : 1); ++kk)                          \
+        for (int jj = 0; jj < (n); ++jj)                                        \
+            for (int ii = 0; ii < (n); ++ii)
+#define IDX(d, n) ((size_t)ii + (size_t)(n) * ((size_t)jj + (size_t)(n) * (size_t)kk))
+
+void ora_apply_B(int d, int n, const double *q, double *out) {
+    bl_consts c = make_bl(d, n);
+    FOR_POINTS(d, n) out[IDX(d, n)] = B_at(&c, q, d, n, ii, jj, kk);
+}
+void ora_apply_L(int d, int n, const double *q, double *out) {
+    bl_consts c = make_bl(d, n);
+    FOR_POINTS(d, n) out[IDX(d, n)] = L_at(&c, q, d, n, ii, jj, kk);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Node-system operator S_l = B_h - gamma L_h on level l ("W - dt_m A", A = nu L_h),      */
+/* rediscretised with h_l = 1/N_l.  g = gamma*(N_l*N_l) (exact: N_l^2 is a power of two).      */
+/*   2D: c0 = (8 + 40g)/12, c1 = (1 - 8g)/12, c2 = (-2g)/12                                    */
+/*   3D: c0 = (6 + 48g)/12, c1 = (1 - 4g)/12, c2 = (-2g)/12                                    */
+/*   S u = (c0*u + c1*faces) + c2*edges ;  weighted Jacobi: u + wd*(b - S u), wd = omega/c0    */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct { double c0, c1, c2, wd; } s_coef;
+
+static s_coef make_s(int d, int n, double gamma, double omega) {
+    s_coef s;
+    double N = (double)(n + 1);
+    double g = gamma * (N * N);
+    if (d == 2) {
+        s.c0 = (8.0 + 40.0 * g) / 12.0; s.c1 = (1.0 - 8.0 * g) / 12.0; s.c2 = (-2.0 * g) / 12.0;
+    } else {
+        s.c0 = (6.0 + 48.0 * g) / 12.0; s.c1 = (1.0 - 4.0 * g) / 12.0; s.c2 = (-2.0 * g) / 12.0;
+    }
+    s.wd = omega / s.c0;
+    return s;
+}
+static inline double S_at(const s_coef *s, const double *u, int d, int n, int i, int j, int k) {
+    return (s->c0 * at(u, d, n, i, j, k) + s->c1 * faces(u, d, n, i, j, k)) +
+           s->c2 * edges(u, d, n, i, j, k);
+}
+
+void ora_level_coefs(int d, int n, double gamma, double omega, double *c4) {
+    s_coef s = make_s(d, n, gamma, omega);
+    c4[0] = s.c0; c4[1] = s.c1; c4[2] = s.c2; c4[3] = s.wd;
+}
+
+void ora_apply_S(int d, int n, double gamma, const double *u, double *out) {
+    s_coef s = make_s(d, n, gamma, 0.8);
+    FOR_POINTS(d, n) out[IDX(d, n)] = S_at(&s, u, d, n, ii, jj, kk);
+}
+
+/* one weighted-Jacobi sweep, out of place */
+static void jacobi(const s_coef *s, int d, int n, const double *b, const double *u, double *out) {
+    FOR_POINTS(d, n) {
+        size_t p = IDX(d, n);
+        out[p] = u[p] + s->wd * (b[p] - S_at(s, u, d, n, ii, jj, kk));
+    }
+}
+void ora_jacobi(int d, int n, double gamma, double omega, int sweeps, const double *b, double *u) {
+    s_coef s = make_s(d, n, gamma, omega);
+    size_t P = npts(d, n);
+    double *t = malloc(P * sizeof(double));
+    for (int it = 0; it < sweeps; ++it) {
+        jacobi(&s, d, n, b, u, t);
+        memcpy(u, t, P * sizeof(double));
+    }
+    free(t);
+}
+
+static void defect(const s_coef *s, int d, int n, const double *b, const double *u, double *r) {
+    FOR_POINTS(d, n) {
+        size_t p = IDX(d, n);
+        r[p] = b[p] - S_at(s, u, d, n, ii, jj, kk);
+    }
+}
+static double maxabs(const double *a, size_t P) {
+    double m = 0.0;
+#pragma omp parallel for reduction(max : m)
+    for (size_t p = 0; p < P; ++p) {
+        double v = fabs(a[p]);
+        if (isnan(v)) v = INFINITY;  /* non-finite values surface as Inf */
+        if (v > m) m = v;
+    }
+    return m;
+}
+double ora_defect_norm(int d, int n, double gamma, const double *b, const double *u) {
+    s_coef s = make_s(d, n, gamma, 0.8);
+    size_t P = npts(d, n);
+    double *r = malloc(P * sizeof(double));
+    defect(&s, d, n, b, u, r);
+    double m = maxabs(r, P);
+    free(r);
+    return m;
+}
+
+/* Full-weighting restriction: coarse (I,J[,K]) <-> fine 2I+1.
+ *   2D: bc = ((4*d + 2*faces) + edges) * 0.0625
+ *   3D: bc = ((8*d + 4*faces) + (2*edges + corners)) * 0.015625,
+ *       corners = e(k-1) + e(k+1)  (8 corners of the 27-point cube)                           */
+void ora_restrict(int d, int nf, const double *df, double *bc) {
+    int nc = (nf - 1) / 2;
+    FOR_POINTS(d, nc) {
+        int x = 2 * ii + 1, y = 2 * jj + 1, z = (d == 3) ? 2 * kk + 1 : 0;
+        double c = at(df, d, nf, x, y, z);
+        double fa = faces(df, d, nf, x, y, z), ed = edges(df, d, nf, x, y, z);
+        double v;
+        if (d == 2) {
+            v = ((4.0 * c + 2.0 * fa) + ed) * 0.0625;
+        } else {
+            double co = e_(df, d, nf, x, y, z - 1) + e_(df, d, nf, x, y, z + 1);
+            v = ((8.0 * c + 4.0 * fa) + (2.0 * ed + co)) * 0.015625;
+        }
+        bc[IDX(d, nc)] = v;
+    }
+}
+
+/* Bi/trilinear prolongation + correction: u += P e.  Per axis: odd fine index x -> coarse
+ * (x-1)/2 (weight 1); even x -> coarse pair (x/2-1, x/2) summed (a + b), weight 1/2; pairs are
+ * summed x innermost, then y, then z; the sum is scaled once by 0.5^(#even axes).            */
+void ora_prolong_add(int d, int nc, const double *ec, double *uf) {
+    int nf = 2 * nc + 1;
+    FOR_POINTS(d, nf) {
+        int xs[2], ys[2], zs[2], nx, ny, nz;
+        double w = 1.0;
+        if (ii & 1) { xs[0] = (ii - 1) / 2; nx = 1; } else { xs[0] = ii / 2 - 1; xs[1] = ii / 2; nx = 2; w *= 0.5; }
+        if (jj & 1) { ys[0] = (jj - 1) / 2; ny = 1; } else { ys[0] = jj / 2 - 1; ys[1] = jj / 2; ny = 2; w *= 0.5; }
+        if (d == 2) { zs[0] = 0; nz = 1; }
+        else if (kk & 1) { zs[0] = (kk - 1) / 2; nz = 1; }
+        else { zs[0] = kk / 2 - 1; zs[1] = kk / 2; nz = 2; w *= 0.5; }
+        double sz = 0.0;
+        for (int c = 0; c < nz; ++c) {
+            double sy = 0.0;
+            for (int b = 0; b < ny; ++b) {
+                double sx = at(ec, d, nc, xs[0], ys[b], zs[c]);
+                if (nx == 2) sx = sx + at(ec, d, nc, xs[1], ys[b], zs[c]);
+                sy = (b == 0) ? sx : sy + sx;
+            }
+            sz = (c == 0) ? sy : sz + sy;
+        }
+        size_t p = IDX(d, nf);
+        uf[p] = uf[p] + sz * w;
+    }
+}
+
+/* Coarsest level n = 3: exact solve with the inverse of the 9x9 / 27x27 matrix of S, built from
+ * the binary64 coefficients (c0,c1,c2) and inverted by Gauss-Jordan elimination with partial
+ * pivoting in binary128, rounded once (reading R12).  e_i = sum_j Ginv_ij b_j,
+ * accumulated left to right over ascending j starting from Ginv_i0*b_0. */
+int ora_coarse_inverse(int d, double gamma, double omega, double *Ginv) {
+    int n = 3, P = (d == 3) ? 27 : 9;
+    s_coef s = make_s(d, n, gamma, omega);
+    qf A[27][54];
+    for (int r = 0; r < P; ++r) for (int c = 0; c < 2 * P; ++c) A[r][c] = 0;
+    for (int r = 0; r < P; ++r) {
+        int ri = r % 3, rj = (r / 3) % 3, rk = r / 9;
+        for (int c = 0; c < P; ++c) {
+            int ci = c % 3, cj = (c / 3) % 3, ck = c / 9;
+            int di = abs(ri - ci), dj = abs(rj - cj), dk = abs(rk - ck);
+            if (di > 1 || dj > 1 || dk > 1) continue;
+            int nd = di + dj + dk;
+            double v = (nd == 0) ? s.c0 : (nd == 1) ? s.c1 : (nd == 2) ? s.c2 : 0.0;
+            A[r][c] = (qf)v;
+        }
+        A[r][P + r] = 1;
+    }
+    for (int c = 0; c < P; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < P; ++r) if (fabsq(A[r][c]) > fabsq(A[piv][c])) piv = r;
+        if (A[piv][c] == 0) return -1;
+        if (piv != c) for (int k = 0; k < 2 * P; ++k) { qf t = A[c][k]; A[c][k] = A[piv][k]; A[piv][k] = t; }
+        qf inv = 1 / A[c][c];
+        for (int k = 0; k < 2 * P; ++k) A[c][k] *= inv;
+        for (int r = 0; r < P; ++r) {
+            if (r == c || A[r][c] == 0) continue;
+            qf f = A[r][c];
+            for (int k = 0; k < 2 * P; ++k) A[r][k] -= f * A[c][k];
+        }
+    }
+    for (int r = 0; r < P; ++r) for (int c = 0; c < P; ++c) Ginv[r * P + c] = (double)A[r][P + c];
+    return 0;
+}
+static void coarse_apply(int P, const double *Ginv, const double *b, double *e) {
+    for (int i = 0; i < P; ++i) {
+        double acc = Ginv[i * P] * b[0];
+        for (int j = 1; j < P; ++j) acc = acc + Ginv[i * P + j] * b[j];
+        e[i] = acc;
+    }
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Geometric multigrid V(nu1,nu2) cycle on S_l ("V-cycles"; components per B:configs[1] */
+/* and DESIGN.md R11-R14): nu1 weighted-Jacobi sweeps; d = b - S u; b_c = R d; e_c = V(0,b_c)  */
+/* on level l+1 (correction scheme, zero initial guess, same gamma); u += P e_c; nu2 sweeps.   */
+/* On n = 3 the cycle is the exact solve.                                                      */
+/* ------------------------------------------------------------------------------------------ */
+static void vcycle_rec(int d, int n, double gamma, int nu1, int nu2, double omega,
+                       const double *b, double *u) {
+    size_t P = npts(d, n);
+    if (n == 3) {
+        /* one-entry cache of the coarse inverse (the oracle is single-threaded at this level) */
+        static double Ginv[27 * 27], cg = -1.0, co = -1.0;
+        static int cd = 0;
+        if (cd != d || cg != gamma || co != omega) {
+            ora_coarse_inverse(d, gamma, omega, Ginv);
+            cd = d; cg = gamma; co = omega;
+        }
+        coarse_apply((int)P, Ginv, b, u);
+        return;
+    }
+    s_coef s = make_s(d, n, gamma, omega);
+    double *t = malloc(P * sizeof(double));
+    for (int it = 0; it < nu1; ++it) { jacobi(&s, d, n, b, u, t); memcpy(u, t, P * sizeof(double)); }
+    defect(&s, d, n, b, u, t);
+    int nc = (n - 1) / 2;
+    size_t Pc = npts(d, nc);
+    double *bc = malloc(Pc * sizeof(double)), *ec = calloc(Pc, sizeof(double));
+    ora_restrict(d, n, t, bc);
+    vcycle_rec(d, nc, gamma, nu1, nu2, omega, bc, ec);
+    ora_prolong_add(d, nc, ec, u);
+    for (int it = 0; it < nu2; ++it) { jacobi(&s, d, n, b, u, t); memcpy(u, t, P * sizeof(double)); }
+    free(t); free(bc); free(ec);
+}
+void ora_vcycle(int d, int n, double gamma, int nu1, int nu2, double omega, const double *b, double *u) {
+    vcycle_rec(d, n, gamma, nu1, nu2, omega, b, u);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Explicit part f^E (Eq. 4; kinds from B:configs; R20-R22)                 */
+/*   NONE: not evaluated (all f^E terms are dropped);  CUBIC: u - (u*u)*u;                     */
+/*   FORCING: G*ct (ct = cos(t_j), host scalar);                                               */
+/*   ADVECTION (CD4, zero ghosts): dx = (8*(u(x+1)-u(x-1)) - (u(x+2)-u(x-2)))*kx, kx=(a_x*N)/12,*/
+/*   f = -((dx + dy) + dz)   (2D: -(dx + dy))                                                   */
+/* ------------------------------------------------------------------------------------------ */
+enum { FE_NONE = 0, FE_CUBIC = 1, FE_FORCING = 2, FE_ADVECTION = 3 };
+
+static void fe_eval(int fe, int d, int n, const double *a, const double *G, double ct,
+                    const double *u, double *out) {
+    double N = (double)(n + 1);
+    double kx = (a[0] * N) / 12.0, ky = (a[1] * N) / 12.0, kz = (a[2] * N) / 12.0;
+    FOR_POINTS(d, n) {
+        size_t p = IDX(d, n);
+        double v = 0.0;
+        if (fe == FE_CUBIC) {
+            double x = u[p];
+            v = x - (x * x) * x;
+        } else if (fe == FE_FORCING) {
+            v = G[p] * ct;
+        } else if (fe == FE_ADVECTION) {
+            int i = ii, j = jj, k = kk;
+            double dx = (8.0 * (at(u, d, n, i + 1, j, k) - at(u, d, n, i - 1, j, k)) -
+                         (at(u, d, n, i + 2, j, k) - at(u, d, n, i - 2, j, k))) * kx;
+            double dy = (8.0 * (at(u, d, n, i, j + 1, k) - at(u, d, n, i, j - 1, k)) -
+                         (at(u, d, n, i, j + 2, k) - at(u, d, n, i, j - 2, k))) * ky;
+            if (d == 3) {
+                double dz = (8.0 * (at(u, d, n, i, j, k + 1) - at(u, d, n, i, j, k - 1)) -
+                             (at(u, d, n, i, j, k + 2) - at(u, d, n, i, j, k - 2))) * kz;
+                v = -((dx + dy) + dz);
+            } else {
+                v = -(dx + dy);
+            }
+        }
+        out[p] = v;
+    }
+}
+void ora_fe_eval(int fe, int d, int n, const double *a, const double *G, double ct,
+                 const double *u, double *out) {
+    fe_eval(fe, d, n, a, G, ct, u, out);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Problem / state                                                                             */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct {
+    int dim, n, M;
+    double dt, nu;
+    int fe;
+    double fe_a[3];
+    const double *G;     /* forcing profile (FE_FORCING), n^d, else NULL */
+    int mode;            /* 0 = ISDC (exactly L cycles), 1 = SDC (cycles to inner tolerance) */
+    int L;
+    double inner_tol;    /* SDC: stop when ||b - S u|| <= inner_tol * max(1, ||b||) */
+    int inner_cap;
+    double sweep_tol;    /* stop when ||r~|| < sweep_tol (strict, "below") */
+    int max_sweeps;
+    int fixed_sweeps;    /* >0: exactly this many sweeps, no tolerance test (config 1) */
+    int nu1, nu2;
+    double omega;
+    int guess;           /* 0 = u_{m+1}^k; 1 = zero; 2 = u_m^{k+1} (P:187-189 ablation) */
+} ora_problem;
+
+/* Right-hand side of Eq. (5) for substep m (0-based: node m -> m+1), regrouped by linearity of
+ * B_h and L_h (SURVEY §8(c1) "check by expansion"):
+ *   v = (unew_m + dtm*(fE(unew_m) - fE(uold_m))) + sum_j a_j*fE(uold_j),  a_j = dt*S_{m,j}
+ *   w = sum_j beta_j*uold_j - gm*uold_{m+1},  beta_j = (nu*dt)*S_{m,j},  gm = nu*dtm, dtm = dt*dtau_m
+ *   b = B v + L w
+ * Sums over j are left folds in ascending j starting from the j = 0 term.
+ * The f^E(unew_m)-f^E(uold_m) and sum a_j fE terms are absent when fE = NONE.                  */
+static void rhs_m(const ora_problem *P, const double *tau, const double *S, const double *dtau,
+                  double t_n, int m, double *const *uold, double *const *unew, double *b,
+                  double *v, double *w, double *ftmp, double *ftmp2) {
+    int d = P->dim, n = P->n, M = P->M;
+    size_t NP = npts(d, n);
+    double dtm = P->dt * dtau[m];
+    double gm = P->nu * dtm;
+    double nudt = P->nu * P->dt;
+    bl_consts c = make_bl(d, n);
+    /* w */
+    for (size_t p = 0; p < NP; ++p) {
+        double acc = (nudt * S[m * M + 0]) * uold[0][p];
+        for (int j = 1; j < M; ++j) acc = acc + (nudt * S[m * M + j]) * uold[j][p];
+        w[p] = acc - gm * uold[m + 1][p];
+    }
+    /* v */
+    if (P->fe == FE_NONE) {
+        memcpy(v, unew[m], NP * sizeof(double));
+    } else {
+        /* sum_j a_j fE(uold_j) */
+        double *acc = ftmp2;
+        for (int j = 0; j < M; ++j) {
+            double ct = cos(t_n + P->dt * tau[j]);
+            fe_eval(P->fe, d, n, P->fe_a, P->G, ct, uold[j], ftmp);
+            double aj = P->dt * S[m * M + j];
+            for (size_t p = 0; p < NP; ++p) acc[p] = (j == 0) ? aj * ftmp[p] : acc[p] + aj * ftmp[p];
+        }
+        double ctm = cos(t_n + P->dt * tau[m]);
+        fe_eval(P->fe, d, n, P->fe_a, P->G, ctm, unew[m], v);      /* v <- fE(unew_m) */
+        fe_eval(P->fe, d, n, P->fe_a, P->G, ctm, uold[m], ftmp);   /* ftmp <- fE(uold_m) */
+        for (size_t p = 0; p < NP; ++p) v[p] = (unew[m][p] + dtm * (v[p] - ftmp[p])) + acc[p];
+    }
+    FOR_POINTS(d, n) {
+        size_t p = IDX(d, n);
+        b[p] = B_at(&c, v, d, n, ii, jj, kk) + L_at(&c, w, d, n, ii, jj, kk);
+    }
+}
+
+/* Weighted SDC residual (R15-R16): for nodes m = 1..M-1 (0-based),
+ *   p_m = (u_m - u_0) - sum_j qa_j fE(u_j),  qa_j = dt*Q_{m,j}   (fE = NONE: p_m = u_m - u_0)
+ *   z_m = sum_j qb_j u_j,                    qb_j = (nu*dt)*Q_{m,j}
+ *   r~_m = B p_m - L z_m ;  reported: max_m ||r~_m||_inf (and per node)                        */
+double ora_residual_state(const ora_problem *P, const double *tau, const double *Q, double t_n,
+                          double *const *u, double *per_node) {
+    int d = P->dim, n = P->n, M = P->M;
+    size_t NP = npts(d, n);
+    bl_consts c = make_bl(d, n);
+    double nudt = P->nu * P->dt;
+    double *pm = malloc(NP * sizeof(double)), *zm = malloc(NP * sizeof(double));
+    double *ft = malloc(NP * sizeof(double)), *r = malloc(NP * sizeof(double));
+    double *facc = (P->fe == FE_NONE) ? NULL : malloc(NP * sizeof(double));
+    double best = 0.0;
+    for (int m = 1; m < M; ++m) {
+        if (P->fe != FE_NONE) {
+            for (int j = 0; j < M; ++j) {
+                double ct = cos(t_n + P->dt * tau[j]);
+                fe_eval(P->fe, d, n, P->fe_a, P->G, ct, u[j], ft);
+                double qa = P->dt * Q[m * M + j];
+                for (size_t p = 0; p < NP; ++p) facc[p] = (j == 0) ? qa * ft[p] : facc[p] + qa * ft[p];
+            }
+        }
+        for (size_t p = 0; p < NP; ++p) {
+            double diff = u[m][p] - u[0][p];
+            pm[p] = (P->fe == FE_NONE) ? diff : diff - facc[p];
+            double acc = (nudt * Q[m * M + 0]) * u[0][p];
+            for (int j = 1; j < M; ++j) acc = acc + (nudt * Q[m * M + j]) * u[j][p];
+            zm[p] = acc;
+        }
+        FOR_POINTS(d, n) {
+            size_t p = IDX(d, n);
+            r[p] = B_at(&c, pm, d, n, ii, jj, kk) - L_at(&c, zm, d, n, ii, jj, kk);
+        }
+        double nm = maxabs(r, NP);
+        if (per_node) per_node[m - 1] = nm;
+        if (nm > best || isinf(nm)) best = nm;
+    }
+    free(pm); free(zm); free(ft); free(r); free(facc);
+    return best;
+}
+
+/* One node solve: ISDC = exactly L V-cycles; SDC = cycle until the defect test
+ * ||b - S u|| <= inner_tol*max(1,||b||) passes (tested before every cycle, so 0 cycles is
+ * possible), at most inner_cap cycles.  Returns cycles used; *cap_hit set when the cap ended it. */
+static int node_solve(const ora_problem *P, double gamma, const double *b, double *u, int *cap_hit) {
+    int d = P->dim, n = P->n;
+    *cap_hit = 0;
+    if (P->mode == 0) {
+        for (int l = 0; l < P->L; ++l) vcycle_rec(d, n, gamma, P->nu1, P->nu2, P->omega, b, u);
+        return P->L;
+    }
+    double thr = P->inner_tol * fmax(1.0, maxabs(b, npts(d, n)));
+    int cyc = 0;
+    for (;;) {
+        double dn = ora_defect_norm(d, n, gamma, b, u);
+        if (dn <= thr) break;
+        if (cyc >= P->inner_cap) { *cap_hit = 1; break; }
+        vcycle_rec(d, n, gamma, P->nu1, P->nu2, P->omega, b, u);
+        ++cyc;
+    }
+    return cyc;
+}
+
+/* One SDC/ISDC sweep k -> k+1 (Eq. 4 in the weighted form Eq. 5; node order
+ * m = 0..M-2 is sequential since u_{m+1}^{k+1} needs u_m^{k+1}).  uold/unew: M fields each;
+ * unew[0] must already hold u_0.  cycles[m] = V-cycles of node solve m. Returns cap hits. */
+int ora_sweep(const ora_problem *P, const double *tau, const double *S, const double *dtau,
+              double t_n, double *const *uold, double *const *unew, int *cycles) {
+    int d = P->dim, n = P->n, M = P->M;
+    size_t NP = npts(d, n);
+    double *b = malloc(NP * sizeof(double)), *v = malloc(NP * sizeof(double));
+    double *w = malloc(NP * sizeof(double)), *f1 = malloc(NP * sizeof(double));
+    double *f2 = malloc(NP * sizeof(double));
+    int caps = 0;
+    for (int m = 0; m + 1 < M; ++m) {
+        rhs_m(P, tau, S, dtau, t_n, m, uold, unew, b, v, w, f1, f2);
+        if (P->guess == 0) memcpy(unew[m + 1], uold[m + 1], NP * sizeof(double));
+        else if (P->guess == 1) memset(unew[m + 1], 0, NP * sizeof(double));
+        else memcpy(unew[m + 1], unew[m], NP * sizeof(double));
+        double gamma = P->nu * (P->dt * dtau[m]);
+        int cap = 0;
+        cycles[m] = node_solve(P, gamma, b, unew[m + 1], &cap);
+        caps += cap;
+    }
+    free(b); free(v); free(w); free(f1); free(f2);
+    return caps;
+}
+
+/* One time step [t_n, t_n + dt] (spread start S:299): u_j^0 = u_0 for all j, then
+ * sweep until ||r~|| < sweep_tol (or exactly fixed_sweeps sweeps, or max_sweeps).  On return
+ * u0 holds u_M (Lobatto end node).  res_hist[k] = residual after sweep k+1; node_cycles[k*(M-1)+m]
+ * = cycles of node solve m in sweep k+1.  Returns 0, or -1 on bad tables. */
+int ora_step(const ora_problem *P, double *u0, double t_n, int *sweeps, long *vcycles,
+             double *res_hist, int *node_cycles, int *cap_hits, int *converged) {
+    int d = P->dim, n = P->n, M = P->M;
+    size_t NP = npts(d, n);
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    if (ora_tables(M, tau, Q, S, dtau)) return -1;
+    double *A[32], *Bf[32];
+    for (int j = 0; j < M; ++j) {
+        A[j] = (j == 0) ? u0 : malloc(NP * sizeof(double));
+        Bf[j] = (j == 0) ? u0 : malloc(NP * sizeof(double));
+        if (j) memcpy(A[j], u0, NP * sizeof(double));
+    }
+    double **uold = A, **unew = Bf;
+    int k = 0, conv = 0, caps = 0;
+    long vc = 0;
+    int kmax = P->fixed_sweeps > 0 ? P->fixed_sweeps : P->max_sweeps;
+    while (k < kmax) {
+        int cyc[32];
+        caps += ora_sweep(P, tau, S, dtau, t_n, uold, unew, cyc);
+        for (int m = 0; m + 1 < M; ++m) { vc += cyc[m]; if (node_cycles) node_cycles[k * (M - 1) + m] = cyc[m]; }
+        double res = ora_residual_state(P, tau, Q, t_n, unew, NULL);
+        if (res_hist) res_hist[k] = res;
+        ++k;
+        double **t = uold; uold = unew; unew = t;
+        if (P->fixed_sweeps <= 0 && res < P->sweep_tol) { conv = 1; break; }
+    }
+    if (P->fixed_sweeps > 0) conv = 1;
+    memcpy(u0, uold[M - 1], NP * sizeof(double));
+    for (int j = 1; j < M; ++j) { free(A[j]); free(Bf[j]); }
+    *sweeps = k; *vcycles = vc; *converged = conv;
+    if (cap_hits) *cap_hits = caps;
+    return 0;
+}
+
+/* Exposed for the per-operation parity tests: RHS of substep m and residual of a given state. */
+void ora_rhs(const ora_problem *P, double t_n, int m, double *const *uold, double *const *unew, double *b) {
+    int M = P->M;
+    size_t NP = npts(P->dim, P->n);
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    ora_tables(M, tau, Q, S, dtau);
+    double *v = malloc(NP * sizeof(double)), *w = malloc(NP * sizeof(double));
+    double *f1 = malloc(NP * sizeof(double)), *f2 = malloc(NP * sizeof(double));
+    rhs_m(P, tau, S, dtau, t_n, m, uold, unew, b, v, w, f1, f2);
+    free(v); free(w); free(f1); free(f2);
+}
+double ora_residual(const ora_problem *P, double t_n, double *const *u, double *per_node) {
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    ora_tables(P->M, tau, Q, S, dtau);
+    return ora_residual_state(P, tau, Q, t_n, u, per_node);
+}
+int ora_sweep_state(const ora_problem *P, double t_n, double *const *uold, double *const *unew, int *cycles) {
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    ora_tables(P->M, tau, Q, S, dtau);
+    return ora_sweep(P, tau, S, dtau, t_n, uold, unew, cycles);
+}

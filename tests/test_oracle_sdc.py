@@ -1,0 +1,284 @@
+"""Pins of the oracle's sweep / residual / step (Eqs. 2-5; P:96-138 experiments).
+
+Independent references:
+* per-Fourier-mode scalar recursion of exactly solved SDC (discrete sine modes are eigenvectors
+  of B_h and L_h, so the PDE sweep reduces to the Dahlquist sweep with z = dt*nu*lam_L/lam_B),
+* the collocation limit (I - zQ)^{-1} 1 and its diagonal Pade closed forms at the end node,
+* the order-per-sweep property,
+* the paper's own heat problem and its exact solution, Table 1's SDC sweep counts
+  (P:120-138), and the initial-guess ablation,
+* dense Newton/LU solution of the full collocation system on tiny grids (nonlinear and advective
+  f^E), and invariants (cycle accounting P:82, K <= K~ P:83, fixed point of the sweep).
+"""
+import dataclasses
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from synth import Config, FE_ADVECTION, FE_CUBIC, FE_FORCING, FE_NONE, MODE_ISDC, MODE_SDC
+
+
+def sym(ks, n):
+    h = 1.0 / (n + 1)
+    c = [math.cos(k * math.pi * h) for k in ks]
+    if len(ks) == 2:
+        return (-20 + 8 * c[0] + 8 * c[1] + 4 * c[0] * c[1]) / (6 * h * h), (8 + 2 * c[0] + 2 * c[1]) / 12
+    s = sum(c); pr = c[0] * c[1] + c[0] * c[2] + c[1] * c[2]
+    return (-24 + 4 * s + 4 * pr) / (6 * h * h), (6 + 2 * s) / 12
+
+
+def scalar_sdc(z, M, K, tables, a0=1.0, g=None, dt=None):
+    """Exactly solved SDC on u' = (z/dt) u + g(t) per mode; returns node values."""
+    tau, Q, S, dtau = tables
+    u = np.full(M, a0)
+    for _ in range(K):
+        un = np.empty(M); un[0] = a0
+        for m in range(M - 1):
+            zm = z * dtau[m]
+            acc = sum(S[m, j] * (z * u[j] + (dt * g[j] if g is not None else 0.0)) for j in range(M))
+            un[m + 1] = (un[m] - zm * u[m + 1] + acc) / (1 - zm)
+        u = un
+    return u
+
+
+def heat_cfg(n, M, dt, nu, **kw):
+    base = dict(sweep_tol=1e-13, max_sweeps=200, inner_tol=1e-13, inner_cap=200)
+    base.update(kw)
+    return Config(0, 2 if kw.pop("dim", 2) == 2 else 3, n, M, dt, nu, FE_NONE, **base)
+
+
+@pytest.mark.parametrize("ks,M,K,nu", [((1, 1), 3, 1, 1.0), ((2, 3), 3, 3, 10.0), ((1, 2), 5, 2, 1.0),
+                                        ((3, 1), 5, 4, 100.0), ((1, 2, 1), 3, 2, 1.0)])
+def test_sweeps_match_scalar_recursion(ora, ks, M, K, nu):
+    n = 15
+    dim = len(ks)
+    cfg = Config(0, dim, n, M, 0.01, nu, FE_NONE, fixed_sweeps=K, inner_tol=1e-14, inner_cap=200)
+    u0 = synth.sine_mode(n, ks)
+    prob = ora.Problem(cfg, mode=MODE_SDC)
+    u, st = ora.step(prob, u0, 0.0)
+    lL, lB = sym(ks, n)
+    z = cfg.dt * nu * lL / lB
+    amp = scalar_sdc(z, M, K, ora.tables(M))[-1]
+    np.testing.assert_allclose(u, amp * u0, rtol=0, atol=1e-11)
+    assert st["sweeps"] == K
+
+
+@pytest.mark.parametrize("M", [3, 5])
+def test_collocation_limit_and_pade(ora, M):
+    n, ks, nu, dt = 15, (2, 1), 1.0, 0.02
+    cfg = Config(0, 2, n, M, dt, nu, FE_NONE, sweep_tol=1e-13, inner_tol=1e-14, inner_cap=200)
+    u0 = synth.sine_mode(n, ks)
+    for mode in (MODE_ISDC, MODE_SDC):
+        u, st = ora.step(ora.Problem(cfg, mode=mode), u0, 0.0)
+        assert st["converged"]
+        lL, lB = sym(ks, n)
+        z = dt * nu * lL / lB
+        tau, Q, S, dtau = ora.tables(M)
+        coll = np.linalg.solve(np.eye(M) - z * Q, np.ones(M))
+        if M == 3:
+            pade = (1 + z / 2 + z * z / 12) / (1 - z / 2 + z * z / 12)
+        else:
+            P = lambda x: 1 + x / 2 + 3 * x * x / 28 + x ** 3 / 84 + x ** 4 / 1680
+            pade = P(z) / P(-z)
+        assert abs(coll[-1] - pade) < 1e-14
+        np.testing.assert_allclose(u, pade * u0, atol=1e-12)
+
+
+def test_forcing_mode_collocation(ora):
+    """Config-3 type forcing on mode (2,2): u = (I - zQ)^{-1}(a 1 + dt Q cos t)."""
+    n, M, dt, nu, a = 15, 5, 0.01, 0.1, 0.7
+    cfg = Config(0, 2, n, M, dt, nu, FE_FORCING, sweep_tol=1e-13, inner_tol=1e-14)
+    G = synth.forcing_field(n)
+    u0 = a * G
+    t_n = 3 * dt
+    for mode in (MODE_ISDC, MODE_SDC):
+        u, st = ora.step(ora.Problem(cfg, G, mode=mode), u0, t_n)
+        assert st["converged"]
+        lL, lB = sym((2, 2), n)
+        z = dt * nu * lL / lB
+        tau, Q, S, dtau = ora.tables(M)
+        ct = np.array([math.cos(t_n + dt * t) for t in tau])
+        coll = np.linalg.solve(np.eye(M) - z * Q, a * np.ones(M) + dt * Q @ ct)
+        np.testing.assert_allclose(u, coll[-1] * G, atol=1e-12)
+
+
+def test_order_per_sweep(ora):
+    """Each sweep raises the order by one: global error at T vs the semi-discrete
+    exact solution exp(T nu lam_L/lam_B) has observed order K +- 0.3 for K = 1..4 (M = 5)."""
+    n, ks, nu, T, M = 15, (1, 1), 1.0, 0.02, 5
+    lL, lB = sym(ks, n)
+    u0 = synth.sine_mode(n, ks)
+    exact = math.exp(T * nu * lL / lB)
+    for K in (1, 2, 3, 4):
+        errs = []
+        for nsteps in (4, 8, 16):
+            dt = T / nsteps
+            cfg = Config(0, 2, n, M, dt, nu, FE_NONE, fixed_sweeps=K, inner_tol=1e-15, inner_cap=200)
+            prob = ora.Problem(cfg, mode=MODE_SDC)
+            u = u0.copy()
+            for s in range(nsteps):
+                u, _ = ora.step(prob, u, float(s) * dt)
+            errs.append(np.abs(u - exact * u0).max())
+        orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+        assert all(abs(o - K) < 0.3 for o in orders), (K, orders, errs)
+
+
+def test_residual_spread_state_closed_form(ora):
+    """Spread state u_j = u_0 = phi (f^E = 0): r~_m = -nu dt tau_m lam_L phi, max at tau_M = 1."""
+    n, M, dt, nu = 15, 5, 0.01, 2.0
+    cfg = Config(0, 2, n, M, dt, nu, FE_NONE)
+    phi = synth.sine_mode(n, (1, 3))
+    r, per = ora.residual(ora.Problem(cfg), 0.0, [phi] * M)
+    lL, lB = sym((1, 3), n)
+    tau = ora.tables(M)[0]
+    np.testing.assert_allclose(per, nu * dt * np.abs(lL) * tau[1:] * np.abs(phi).max(), rtol=1e-12)
+    assert r == per.max()
+
+
+def test_residual_zero_at_collocation_solution(ora):
+    n, M, dt, nu, ks = 15, 3, 0.01, 1.0, (1, 2)
+    cfg = Config(0, 2, n, M, dt, nu, FE_NONE)
+    phi = synth.sine_mode(n, ks)
+    lL, lB = sym(ks, n)
+    tau, Q, S, dtau = ora.tables(M)
+    coll = np.linalg.solve(np.eye(M) - dt * nu * lL / lB * Q, np.ones(M))
+    r, _ = ora.residual(ora.Problem(cfg), 0.0, [c * phi for c in coll])
+    assert r < 1e-12
+
+
+def test_paper_heat_problem_and_table1_sdc_sweeps(ora):
+    """P:96-103 heat problem, P:114-117 parameters, Table 1a: SDC sweep counts match
+    the paper's; ISDC needs at least as many sweeps (K <= K~) and fewer V-cycles when stiff;
+    the converged nu = 1, M = 5 step is within 10x the spatial floor of exp(-2 pi^2 nu t)."""
+    gold = {}
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "paper_table1.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        f = line.split()
+        gold[(int(f[0]), int(f[1]))] = tuple(int(x) for x in f[2:6])
+    n = 63
+    u0 = synth.sine_mode(n, (1, 1))
+    for (nu, M), (sdc_c, sdc_s, isdc_c, isdc_s) in gold.items():
+        if M == 7 and nu != 10:
+            continue  # keep the CPU suite short
+        cfg = Config(0, 2, n, M, 0.001, float(nu), FE_NONE, sweep_tol=5e-8, max_sweeps=100)
+        us, ss = ora.step(ora.Problem(cfg, mode=MODE_SDC), u0, 0.0)
+        ui, si = ora.step(ora.Problem(cfg, mode=MODE_ISDC), u0, 0.0)
+        assert ss["converged"] and si["converged"]
+        assert abs(ss["sweeps"] - sdc_s) <= 1, (nu, M, ss["sweeps"], sdc_s)
+        assert si["sweeps"] >= ss["sweeps"]
+        assert si["vcycles"] == si["sweeps"] * (M - 1) * 2
+        if nu >= 10:
+            assert si["vcycles"] < ss["vcycles"]
+        if nu == 1 and M == 5:
+            lL, lB = sym((1, 1), n)
+            floor = abs(math.exp(0.001 * nu * lL / lB) - math.exp(-2 * math.pi ** 2 * nu * 0.001))
+            assert np.abs(ui - math.exp(-2 * math.pi ** 2 * nu * 0.001) * u0).max() < 10 * floor
+
+
+def test_initial_guess_ablation(ora):
+    """with a zero (or u_m^{k+1}) initial guess ISDC fails to converge, SDC still does."""
+    n = 63
+    u0 = synth.sine_mode(n, (1, 1))
+    cfg = Config(0, 2, n, 5, 0.001, 100.0, FE_NONE, sweep_tol=5e-8, max_sweeps=60)
+    _, warm = ora.step(ora.Problem(cfg, mode=MODE_ISDC, guess=0), u0, 0.0)
+    assert warm["converged"]
+    for g in (1, 2):
+        _, st = ora.step(ora.Problem(cfg, mode=MODE_ISDC, guess=g), u0, 0.0)
+        assert not st["converged"]
+    _, sdc_warm = ora.step(ora.Problem(cfg, mode=MODE_SDC, guess=0), u0, 0.0)
+    _, sdc_zero = ora.step(ora.Problem(cfg, mode=MODE_SDC, guess=1), u0, 0.0)
+    # "the number of required multigrid V-cycles increases dramatically"; with this
+    # build's V(2,2) weighted-Jacobi cycle the increase is ~1.5x (SPEC's 2x is its own MG's figure)
+    assert sdc_zero["converged"] and sdc_zero["vcycles"] >= 1.3 * sdc_warm["vcycles"]
+
+
+def _dense(ora, fn, n, dim):
+    P = n ** dim
+    A = np.zeros((P, P))
+    for i in range(P):
+        e = np.zeros(P); e[i] = 1.0
+        A[:, i] = fn(e.reshape((n,) * dim)).ravel()
+    return A
+
+
+@pytest.mark.parametrize("fe,dim", [(FE_CUBIC, 2), (FE_ADVECTION, 2), (FE_ADVECTION, 3), (FE_CUBIC, 3)])
+def test_converged_isdc_is_collocation_solution(ora, fe, dim):
+    """Brute force: Newton + dense LU on the full (weighted) collocation system, n = 7."""
+    n, M, dt, nu = 7, 3, 0.02, 0.5
+    a = (1.0, 0.5, 0.25)
+    cfg = Config(0, dim, n, M, dt, nu, fe, fe_a=a, sweep_tol=1e-13, max_sweeps=200)
+    rng = np.random.default_rng(11)
+    u0 = 0.5 * rng.uniform(-1, 1, (n,) * dim)
+    u, st = ora.step(ora.Problem(cfg), u0, 0.0)
+    assert st["converged"]
+    P = n ** dim
+    B = _dense(ora, ora.apply_B, n, dim)
+    Lm = _dense(ora, ora.apply_L, n, dim)
+    tau, Q, S, dtau = ora.tables(M)
+    if fe == FE_ADVECTION:
+        Fm = _dense(ora, lambda x: ora.fe_eval(fe, x, a), n, dim)
+        fE = lambda x: Fm @ x
+        dfE = lambda x: Fm
+    else:
+        fE = lambda x: x - x ** 3
+        dfE = lambda x: np.diag(1 - 3 * x ** 2)
+    x0 = u0.ravel()
+    U = np.tile(x0, (M, 1))
+
+    def F(U):
+        out = []
+        for m in range(1, M):
+            acc = B @ (U[m] - x0)
+            for j in range(M):
+                acc = acc - dt * Q[m, j] * (B @ fE(U[j]) + nu * Lm @ U[j])
+            out.append(acc)
+        return np.concatenate(out)
+
+    for _ in range(20):
+        Jm = np.zeros(((M - 1) * P, (M - 1) * P))
+        for m in range(1, M):
+            for j in range(1, M):
+                blk = -dt * Q[m, j] * (B @ dfE(U[j]) + nu * Lm)
+                if j == m:
+                    blk = blk + B
+                Jm[(m - 1) * P:m * P, (j - 1) * P:j * P] = blk
+        dU = np.linalg.solve(Jm, -F(U))
+        U[1:] += dU.reshape(M - 1, P)
+        if np.abs(dU).max() < 1e-15:
+            break
+    np.testing.assert_allclose(u.ravel(), U[-1], atol=1e-11)
+
+
+def test_isdc_fixed_point_and_accounting(ora):
+    """At the collocation solution a sweep changes nothing beyond rounding; ISDC cycle
+    accounting is exactly K~(M-1)L; SDC solves may need zero cycles."""
+    n, M, dt, nu, ks = 15, 5, 0.01, 3.0, (2, 1)
+    cfg = Config(0, 2, n, M, dt, nu, FE_NONE)
+    phi = synth.sine_mode(n, ks)
+    lL, lB = sym(ks, n)
+    tau, Q, S, dtau = ora.tables(M)
+    coll = np.linalg.solve(np.eye(M) - dt * nu * lL / lB * Q, np.ones(M))
+    state = [c * phi for c in coll]
+    for mode in (MODE_ISDC, MODE_SDC):
+        new, cyc = ora.sweep(ora.Problem(cfg, mode=mode), 0.0, state)
+        for a, b in zip(new, state):
+            np.testing.assert_allclose(a, b, atol=1e-13)
+        if mode == MODE_ISDC:
+            assert cyc == [2] * (M - 1)
+        else:
+            assert max(cyc) <= 1
+
+
+def test_config1_reference_behaviour(ora):
+    """Config 1 (B:configs[0]) seed 0: 8 fixed sweeps; ISDC uses 32 cycles (= 8*2*2), SDC more."""
+    cfg, u0, G = synth.problem_inputs(1, 0)
+    ui, si = ora.step(ora.Problem(cfg, mode=MODE_ISDC), u0, 0.0)
+    us, ss = ora.step(ora.Problem(cfg, mode=MODE_SDC), u0, 0.0)
+    assert si["sweeps"] == ss["sweeps"] == 8
+    assert si["vcycles"] == 32 and ss["vcycles"] > 32
+    # residuals decrease overall and both end near the exact-solve value (~2e-2)
+    assert si["res_hist"][-1] < si["res_hist"][0] and 1e-2 < si["res_hist"][-1] < 5e-2
