@@ -1,0 +1,179 @@
+/*
+ * isdc.h -- C ABI of the B200 (sm_100a) ISDC hot-path library  libisdc.so
+ *
+ * Inexact spectral deferred corrections (Speck, Ruprecht, Minion, Emmett, Krause,
+ * arXiv:1401.7824; /root/reference/PAPER.md, cited as P:<line>).  Each semi-implicit SDC sweep
+ * (Eq. 4) is written in the weighted Mehrstellen form (Eq. 5)
+ *
+ *     (B_h - dt_m nu L_h) u_{m+1}^{k+1} = B_h v_m + L_h w_m
+ *
+ * and solved only approximately with L V(nu1,nu2) multigrid cycles (ISDC) or to a tolerance
+ * (classical SDC).  Convergence is monitored with the max norm of the (B_h-weighted)
+ * SDC residual (reading R15).
+ *
+ * Conventions shared by every call
+ *  - Grid: d in {2,3}; n interior points per direction with n + 1 = 2^p (p >= 2); h = 1/(n+1);
+ *    homogeneous Dirichlet data on the unit square/cube.
+ *  - Field layout at the boundary: dense fp64, n^d values, C-contiguous with x fastest
+ *    (index i + n*(j + n*k)) -- a torch tensor of shape (n,n) or (n,n,n).  Internally the library
+ *    keeps pitched copies (row pitch n+1 doubles) inside the caller's workspace.
+ *  - Ownership: the caller owns every buffer passed in (device fields, host arrays, the
+ *    workspace).  The library never calls cudaMalloc; it owns only the handle, host-side tables
+ *    and CUDA graphs.  Pointers named *_dev are device pointers, *_host are host pointers.
+ *  - Streams: all device work is ordered on the stream given to isdc_create (NULL = legacy
+ *    default stream).  Calls that return host scalars synchronise that stream.
+ *  - Threads: a handle is not thread-safe; distinct handles are independent.
+ *  - Errors: every call returns an isdc_status and never aborts or throws across the ABI.
+ *    ISDC_ERR_CUDA carries the CUDA error text in isdc_last_error(h).  Non-convergence (sweep
+ *    cap, SDC inner cap) is NOT an error: it is reported through *converged and counters.
+ *  - Arithmetic: fp64, no FMA contraction, canonical expression trees of DESIGN.md §4 -- the
+ *    results are bit-identical to the CPU oracle (oracle/), which shares no code with this library.
+ */
+#ifndef ISDC_H
+#define ISDC_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct isdc_ctx *isdc_handle;
+
+typedef enum {
+    ISDC_OK = 0,
+    ISDC_ERR_INVALID_ARG = 1,  /* n != 2^p - 1, d not in {2,3}, dt <= 0, nu <= 0, L < 1, NULL ptr */
+    ISDC_ERR_UNSUPPORTED = 2,  /* node type other than Gauss-Lobatto, M outside [2, 8]           */
+    ISDC_ERR_CUDA = 3,         /* a CUDA runtime error; text in isdc_last_error                   */
+    ISDC_ERR_NONFINITE = 4,    /* a norm came out NaN/Inf; state kept for inspection              */
+    ISDC_ERR_WORKSPACE = 5     /* workspace NULL, too small or not 256-byte aligned               */
+} isdc_status;
+
+/* Collocation node family.  Only Gauss-Lobatto is built. */
+typedef enum {
+    ISDC_NODES_GAUSS_LOBATTO = 0,
+    ISDC_NODES_GAUSS_RADAU_RIGHT = 1,
+    ISDC_NODES_GAUSS_LEGENDRE = 2
+} isdc_nodes;
+
+/* Explicit part f^E of the IMEX split.  Kinds of B:configs (R20-R22). */
+typedef enum {
+    ISDC_FE_NONE = 0,          /* f^E == 0: implicit SDC, Eq. (3)                                 */
+    ISDC_FE_CUBIC = 1,         /* f^E(u) = u - u^3 (Allen-Cahn type, config 2)                    */
+    ISDC_FE_FORCING = 2,       /* f^E(x,t) = G(x) cos(t), G given as a field (config 3)           */
+    ISDC_FE_ADVECTION_CD4 = 3  /* f^E(u) = -a . grad u, 4th-order central differences (config 5) */
+} isdc_fe_kind;
+
+typedef enum {
+    ISDC_MODE_ISDC_FIXED = 0,  /* exactly L V-cycles per node solve                        */
+    ISDC_MODE_SDC_TOL = 1      /* V-cycles until ||b - S u|| <= inner_tol*max(1,||b||)  */
+} isdc_mode;
+
+typedef struct {
+    int dim;          /* 2 or 3                                                                  */
+    int n;            /* interior points per direction, n = 2^p - 1, p >= 2                      */
+    int coarsest_n;   /* must be 3 (exact 3^d solve on the coarsest level)                       */
+} isdc_grid;
+
+typedef struct {
+    int nu1, nu2;     /* pre/post weighted-Jacobi sweeps per level (2, 2)                        */
+    double omega;     /* Jacobi damping (0.8)                                                    */
+} isdc_mg_opts;
+
+typedef struct {
+    isdc_mode mode;
+    int L;            /* ISDC: V-cycles per node solve (2)                                */
+    double inner_tol; /* SDC: relative defect tolerance (1e-12, R18)                   */
+    int inner_cap;    /* SDC: max V-cycles per node solve (50)                                   */
+    double sweep_tol; /* sweep until ||r~||_inf < sweep_tol (strict)                      */
+    int max_sweeps;   /* sweep cap per step (200)                                                */
+    int fixed_sweeps; /* > 0: exactly this many sweeps per step, no tolerance test (config 1)     */
+    int guess;        /* node-solve initial guess: 0 = u_{m+1}^k, 1 = zero, 2 = u_m^{k+1} */
+} isdc_solve_opts;
+
+typedef struct {
+    isdc_grid grid;
+    int M;                       /* collocation nodes, 2 <= M <= 8                               */
+    isdc_nodes nodes;
+    double dt, nu;               /* step size and diffusion coefficient                          */
+    isdc_fe_kind fe;
+    double fe_params[3];         /* ADVECTION_CD4: velocity a = (a_x, a_y, a_z)                  */
+    const double *fe_field_dev;  /* FORCING: G, dense n^d device field (copied at create), else NULL */
+    isdc_mg_opts mg;
+    isdc_solve_opts solve;
+} isdc_problem;
+
+/* Per-step statistics (Table 1 accounting; SPEC RunStats S:249-252). */
+typedef struct {
+    int sweeps;          /* K (SDC) or K~ (ISDC) sweeps performed in the step                   */
+    long vcycles;        /* V-cycles over all node solves of the step (K~(M-1)L in ISDC)        */
+    int cap_hits;        /* SDC node solves that stopped at inner_cap                           */
+    int converged;       /* residual < sweep_tol reached (always 1 with fixed_sweeps)           */
+    double final_residual;
+} isdc_step_stats;
+
+/* Bytes of device workspace a problem needs (fields, MG hierarchy, reductions, tables). */
+isdc_status isdc_workspace_bytes(const isdc_problem *prob, size_t *bytes);
+
+/* Validate prob, lay out the workspace (device, >= isdc_workspace_bytes, 256-B aligned), build the
+ * quadrature tables (binary128 -> binary64), level coefficients and coarse inverses, and bind
+ * cuda_stream (a cudaStream_t or NULL).  On success *out is a new handle. */
+isdc_status isdc_create(const isdc_problem *prob, void *workspace_dev, size_t bytes,
+                        void *cuda_stream, isdc_handle *out);
+
+/* Set u_0 (dense device field, copied) and the step counter (t_n = (double)step_index*dt,
+ * DESIGN.md R28); spreads u_j = u_0 for all nodes. */
+isdc_status isdc_set_initial(isdc_handle h, const double *u0_dev, int step_index);
+/* Same with a host buffer (pinned or pageable); the H2D copy is stream-ordered. */
+isdc_status isdc_set_initial_host(isdc_handle h, const double *u0_host, int step_index);
+
+/* One sweep k -> k+1 over nodes m = 1..M-1: RHS assembly, node solves, then the residual
+ * of the new iterate.  res_per_node[M-1], res_max and cycles[M-1] are host outputs (nullable). */
+isdc_status isdc_sweep(isdc_handle h, double *res_per_node, double *res_max, int *cycles);
+
+/* One time step: spread (already done by set_initial or the previous step), sweep until the
+ * residual is below sweep_tol (or fixed_sweeps / max_sweeps), then u_0 <- u_M, step_index++.
+ * res_hist (host, capacity max(max_sweeps, fixed_sweeps)) receives the residual after each sweep;
+ * node_cycles (host, capacity cap*(M-1)) the V-cycles of every node solve.  Both nullable. */
+isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, int *node_cycles);
+
+/* Run nsteps time steps (equivalent to nsteps isdc_step calls); stats[nsteps] nullable. */
+isdc_status isdc_run(isdc_handle h, int nsteps, isdc_step_stats *stats);
+
+/* One V(nu1,nu2)-cycle on the node system S u = b, S = B_h - gamma_m L_h, of substep node_m
+ * (0-based, 0..M-2; gamma_m = nu*(dt*dtau_m)), applied in place to the dense device field u_dev
+ * with right-hand side b_dev.  defect_before/after: ||b - S u||_inf before/after the cycle
+ * (host, nullable). */
+isdc_status mg_vcycle(isdc_handle h, int node_m, const double *b_dev, double *u_dev,
+                      double *defect_before, double *defect_after);
+
+/* Weighted SDC residual max_m ||r~_m||_inf of the current node state (R15). */
+isdc_status residual_norm(isdc_handle h, double *per_node, double *max_norm);
+
+/* Copy node `node` (0..M-1; M-1 = end of step) of the current iterate into a dense field. */
+isdc_status isdc_get_solution(isdc_handle h, int node, double *out_dev);
+isdc_status isdc_get_solution_host(isdc_handle h, int node, double *out_host);
+
+/* Load a full node state u[0..M-1] (dense device fields; used by parity tests). */
+isdc_status isdc_set_state(isdc_handle h, const double *const *u_dev, int step_index);
+
+/* Host copies of the tables: tau[M], Q[M*M], S[(M-1)*M], dtau[M-1] (nullable each). */
+isdc_status isdc_get_tables(isdc_handle h, double *tau, double *Q, double *S, double *dtau);
+
+/* RHS b of Eq. (5) for substep node_m (0..M-2) at time t_n = (double)step_index*dt, from the
+ * previous iterate uold_dev[0..M-1] and the new value unew_m_dev = u_m^{k+1}; all dense device
+ * fields (parity tests). */
+isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold_dev,
+                     const double *unew_m_dev, double *b_dev);
+
+/* Number of kernel launches issued by this handle since creation (launch accounting). */
+long isdc_kernel_launches(isdc_handle h);
+
+isdc_status isdc_destroy(isdc_handle h);
+const char *isdc_last_error(isdc_handle h);
+const char *isdc_status_string(isdc_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISDC_H */

