@@ -112,6 +112,12 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     }
     return v;
 }
+// running max of absolute values that keeps NaN (bits of a positive NaN exceed +Inf)
+__device__ __forceinline__ double amax(double acc, double absval) {
+    unsigned long long a = (unsigned long long)__double_as_longlong(acc);
+    unsigned long long b = (unsigned long long)__double_as_longlong(absval);
+    return __longlong_as_double((long long)(a > b ? a : b));
+}
 // every thread of the block must call; one atomicMax per block into *slot
 __device__ __forceinline__ void block_max_to(unsigned long long *slot, double absval) {
     __shared__ unsigned long long red_s[32];

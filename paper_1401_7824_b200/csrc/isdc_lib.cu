@@ -7,12 +7,15 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/isdc.h"
 #include "kernels_generic.cuh"
-#include "kernels_fast.cuh"
+#include "kernels_fast2d.cuh"
+#include "kernels_tail.cuh"
 #include "tables.h"
 
 namespace {
@@ -29,6 +32,7 @@ struct Level {
 }  // namespace
 
 struct isdc_ctx {
+    struct Pending { int a, b, cls; double bytes; };
     isdc_problem P;
     cudaStream_t s = nullptr;
     std::string err;
@@ -47,6 +51,31 @@ struct isdc_ctx {
     int step_index = 0;
     long launches = 0;
     bool fast = true;          // use the tuned fine-level kernels
+    std::map<std::tuple<const void *, int, int, int>, CUtensorMap> tmaps;  // TMA descriptors by (buffer, box)
+    double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
+    double cthost[ISDC_MAXM];
+    int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
+    TailParams tailp[ISDC_MAXM];
+    size_t tail_smem = 0;
+    // CUDA graphs of whole ISDC sweeps, keyed by (cur, spread, profiling)
+    cudaStream_t cap = nullptr;
+    bool graphs = true;
+    struct Graph { cudaGraphExec_t exec = nullptr; std::vector<Pending> events; long nkernels = 0; };
+    std::map<std::tuple<int, int, int>, Graph> sweep_graphs;
+    bool capturing = false;
+    // live kernel timing (isdc_profile_*)
+    int prof = 0;               // 0 off, 1 fine smoother only, 2 every class
+    std::vector<cudaEvent_t> evpool;
+    int evused = 0;
+    std::vector<Pending> pend;
+    double prof_ms[8] = {0}, prof_bytes[8] = {0};
+    long prof_cnt[8] = {0};
+    ~isdc_ctx() {
+        for (auto &g : sweep_graphs)
+            if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+        for (auto e : evpool) cudaEventDestroy(e);
+        if (cap) cudaStreamDestroy(cap);
+    }
 };
 
 #define CUDA_TRY(h, call)                                                                    \
@@ -173,7 +202,8 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     int Pc = (d == 3) ? 27 : 9;
     double *Gi = (double *)take((size_t)(M - 1) * Pc * Pc * sizeof(double));
     unsigned long long *red = (unsigned long long *)take(kRedSlots * sizeof(unsigned long long));
-    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; }
+    double *ctd = (double *)take(ISDC_MAXM * sizeof(double));
+    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; }
     return off;
 }
 
@@ -185,18 +215,93 @@ dim3 point_grid(const GridDesc &g, dim3 blk) {
 // ---------------------------------------------------------------------------------------------
 // launch helpers (every launch is counted)
 // ---------------------------------------------------------------------------------------------
+enum { PROF_SMOOTH = 0, PROF_RESTRICT = 1, PROF_PROLONG = 2, PROF_RHS = 3, PROF_RESID = 4, PROF_COARSE = 5 };
+
+int prof_event(isdc_ctx *h) {
+    if (h->evused == (int)h->evpool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        h->evpool.push_back(e);
+    }
+    return h->evused++;
+}
+// returns a pending-record index (or -1 when profiling is off)
+int prof_begin(isdc_ctx *h, int cls) {
+    if (h->prof == 0 || (h->prof == 1 && cls != PROF_SMOOTH)) return -1;
+    int a = prof_event(h);
+    if (a < 0) return -1;
+    cudaEventRecordWithFlags(h->evpool[a], h->s, h->capturing ? cudaEventRecordExternal : 0);
+    return a;
+}
+void prof_end(isdc_ctx *h, int a, int cls, double bytes) {
+    if (a < 0) return;
+    int b = prof_event(h);
+    if (b < 0) return;
+    cudaEventRecordWithFlags(h->evpool[b], h->s, h->capturing ? cudaEventRecordExternal : 0);
+    h->pend.push_back({a, b, cls, bytes});
+    if (!h->capturing && h->evused > 16384) {  // bound the pool: fold what has completed
+        cudaStreamSynchronize(h->s);
+        for (auto &p : h->pend) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, h->evpool[p.a], h->evpool[p.b]);
+            h->prof_ms[p.cls] += ms; h->prof_cnt[p.cls] += 1; h->prof_bytes[p.cls] += p.bytes;
+        }
+        h->pend.clear();
+        h->evused = 0;
+    }
+}
+isdc_status prof_collect(isdc_ctx *h) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    for (auto &p : h->pend) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->evpool[p.a], h->evpool[p.b]);
+        h->prof_ms[p.cls] += ms; h->prof_cnt[p.cls] += 1; h->prof_bytes[p.cls] += p.bytes;
+    }
+    h->pend.clear();
+    h->evused = 0;
+    return ISDC_OK;
+}
+double npts_of(const isdc_ctx *h, const GridDesc &g) {
+    return h->d == 3 ? (double)g.n * g.n * g.n : (double)g.n * g.n;
+}
+
 const dim3 kBlk(32, 8, 1);
+
+const CUtensorMap *tmap(isdc_ctx *h, const double *base, const GridDesc &g, int bx, int by, int bz = 0) {
+    auto key = std::make_tuple((const void *)base, bx, by, bz);
+    auto it = h->tmaps.find(key);
+    if (it != h->tmaps.end()) return &it->second;
+    CUtensorMap m;
+    if (!tma_make_map(&m, base, g.n, g.pitch, bz > 0 ? g.n : 0, bx, by, bz > 0 ? bz : 1)) return nullptr;
+    return &(h->tmaps[key] = m);
+}
+
+bool use_fast2d(const isdc_ctx *h, int level) { return h->fast && h->d == 2 && h->lev[level].g.n >= 63; }
+
+// two fused Jacobi sweeps on the fine 2D level
+isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
+                           const SCoef &c, unsigned long long *norm_slot, int level) {
+    const CUtensorMap *mu = tmap(h, in, g, f2d::UW, f2d::UH);
+    const CUtensorMap *mb = tmap(h, b, g, f2d::BW, f2d::BH);
+    if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    ++h->launches;
+    int pe = prof_begin(h, level == 0 ? PROF_SMOOTH : PROF_COARSE);
+    dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + f2d::TY - 1) / f2d::TY);
+    size_t sm = sizeof(f2d::SmemSmooth) + 128;
+    if (norm_slot) f2d::k_smooth2<true><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, norm_slot);
+    else f2d::k_smooth2<false><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr);
+    prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
 
 isdc_status launch_jacobi(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                           const SCoef &c, int level) {
     ++h->launches;
-    if (h->d == 2) {
-        if (level == 0 && h->fast) fast_jacobi2d(out, in, b, g, c, h->s);
-        else k_jacobi<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
-    } else {
-        if (level == 0 && h->fast) fast_jacobi3d(out, in, b, g, c, h->s);
-        else k_jacobi<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
-    }
+    int pe = prof_begin(h, level == 0 ? PROF_SMOOTH : PROF_COARSE);
+    if (h->d == 2) k_jacobi<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
+    else k_jacobi<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
+    prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -211,18 +316,33 @@ isdc_status launch_defect_norm(isdc_ctx *h, const double *u, const double *b, co
 }
 
 isdc_status launch_restrict(isdc_ctx *h, double *bc, const GridDesc &gc, const double *u, const double *b,
-                            const GridDesc &gf, const SCoef &c) {
+                            const GridDesc &gf, const SCoef &c, int level) {
     ++h->launches;
-    if (h->d == 2) k_restrict_defect<2><<<point_grid<2>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
+    int pe = prof_begin(h, level == 0 ? PROF_RESTRICT : PROF_COARSE);
+    if (use_fast2d(h, level)) {
+        const CUtensorMap *mu = tmap(h, u, gf, f2d::RUW, f2d::RUH);
+        const CUtensorMap *mb = tmap(h, b, gf, f2d::RBW, f2d::RBH);
+        if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+        dim3 grd((gc.n + f2d::RCX - 1) / f2d::RCX, (gc.n + f2d::RCY - 1) / f2d::RCY);
+        f2d::k_restrict<<<grd, f2d::RNT, sizeof(f2d::SmemRestrict) + 128, h->s>>>(*mu, *mb, bc, gf.n, gc.n,
+                                                                                     gc.pitch, c);
+    } else if (h->d == 2) k_restrict_defect<2><<<point_grid<2>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
     else k_restrict_defect<3><<<point_grid<3>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
+    prof_end(h, pe, level == 0 ? PROF_RESTRICT : PROF_COARSE, 16.0 * npts_of(h, gf) + 8.0 * npts_of(h, gc));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
 
-isdc_status launch_prolong(isdc_ctx *h, double *u, const GridDesc &gf, const double *e, const GridDesc &gc) {
+isdc_status launch_prolong(isdc_ctx *h, double *u, const GridDesc &gf, const double *e, const GridDesc &gc,
+                           int level) {
     ++h->launches;
-    if (h->d == 2) k_prolong_add<2><<<point_grid<2>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
+    int pe = prof_begin(h, level == 0 ? PROF_PROLONG : PROF_COARSE);
+    if (use_fast2d(h, level)) {
+        dim3 grd(((gf.n + 1) / 2 + 255) / 256, gf.n);
+        f2d::k_prolong<<<grd, 256, 0, h->s>>>(u, gf.n, gf.pitch, e, gc.n, gc.pitch);
+    } else if (h->d == 2) k_prolong_add<2><<<point_grid<2>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
     else k_prolong_add<3><<<point_grid<3>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
+    prof_end(h, pe, level == 0 ? PROF_PROLONG : PROF_COARSE, 16.0 * npts_of(h, gf) + 8.0 * npts_of(h, gc));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -231,8 +351,10 @@ isdc_status launch_coarse(isdc_ctx *h, double *u, const double *b, const GridDes
     ++h->launches;
     int Pc = (h->d == 3) ? 27 : 9;
     const double *Gi = h->Ginv + (size_t)m * Pc * Pc;
+    int pe = prof_begin(h, PROF_COARSE);
     if (h->d == 2) k_coarse_solve<2><<<1, 32, 0, h->s>>>(u, b, g, Gi);
     else k_coarse_solve<3><<<1, 32, 0, h->s>>>(u, b, g, Gi);
+    prof_end(h, pe, PROF_COARSE, 16.0 * Pc);
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -282,8 +404,34 @@ isdc_status read_slots(isdc_ctx *h, int first, int count, double *out) {
     }
     return ISDC_OK;
 }
+// forcing phases cos(t_j), t_j = t_n + dt*tau_j, t_n = (double)step_index*dt (R28)
+isdc_status upload_ct(isdc_ctx *h) {
+    double tn = (double)h->step_index * h->P.dt;
+    for (int j = 0; j < h->M; ++j) h->cthost[j] = std::cos(tn + h->P.dt * h->tau[j]);
+    CUDA_TRY(h, cudaMemcpyAsync(h->ctdev, h->cthost, h->M * sizeof(double), cudaMemcpyHostToDevice, h->s));
+    return ISDC_OK;
+}
+
 isdc_status clear_slots(isdc_ctx *h, int first, int count) {
     CUDA_TRY(h, cudaMemsetAsync(h->red + first, 0, count * sizeof(unsigned long long), h->s));
+    return ISDC_OK;
+}
+
+// `sweeps` Jacobi sweeps from *cur, ping-ponging between X and T; *cur ends on the result
+isdc_status smooth(isdc_ctx *h, int l, double *X, double *T, const double *b, const SCoef &c, const double *&cur,
+                   int sweeps) {
+    const GridDesc &g = h->lev[l].g;
+    while (sweeps > 0) {
+        double *dst = (cur == T) ? X : T;
+        if (use_fast2d(h, l) && sweeps >= 2) {
+            TRY(launch_smooth2(h, dst, cur, b, g, c, nullptr, l));
+            sweeps -= 2;
+        } else {
+            TRY(launch_jacobi(h, dst, cur, b, g, c, l));
+            sweeps -= 1;
+        }
+        cur = dst;
+    }
     return ISDC_OK;
 }
 
@@ -292,17 +440,27 @@ isdc_status clear_slots(isdc_ctx *h, int first, int count) {
 // X holds the iterate on exit; src (nullable) is the initial iterate when it lives elsewhere
 // (first cycle of a node solve reads u_{m+1}^k in place, never writing it).
 // ---------------------------------------------------------------------------------------------
+isdc_status launch_tail(isdc_ctx *h, int l, int m, const double *b, const double *u_in, double *u_out) {
+    TailParams P = h->tailp[m];
+    P.b_in = b; P.u_in = u_in; P.u_out = u_out;
+    P.pitch = h->lev[l].g.pitch;
+    ++h->launches;
+    int pe = prof_begin(h, l == 0 ? PROF_SMOOTH : PROF_COARSE);
+    if (h->d == 2) k_tail<2><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
+    else k_tail<3><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
+    prof_end(h, pe, l == 0 ? PROF_SMOOTH : PROF_COARSE, 16.0 * npts_of(h, h->lev[l].g));
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
 isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double *b, const double *src) {
     Level &L = h->lev[l];
     const GridDesc &g = L.g;
+    if (l == h->tail_l0) return launch_tail(h, l, m, b, src ? src : X, X);
     if (g.n == 3) return launch_coarse(h, X, b, g, m);
     const SCoef &c = L.coef[m];
     const double *cur = src ? src : X;
-    for (int it = 0; it < h->P.mg.nu1; ++it) {
-        double *dst = (cur == T) ? X : T;
-        TRY(launch_jacobi(h, dst, cur, b, g, c, l));
-        cur = dst;
-    }
+    TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1));
     double *curw;
     if (cur != X && cur != T) {  // nu1 == 0 with a foreign initial iterate
         TRY(copy_field(h, X, cur, g));
@@ -311,23 +469,22 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
         curw = const_cast<double *>(cur);
     }
     Level &C = h->lev[l + 1];
-    TRY(launch_restrict(h, C.b, C.g, curw, b, g, c));
-    TRY(zero_field(h, C.e, C.g));
-    TRY(vcycle(h, l + 1, m, C.e, C.t, C.b, nullptr));
-    TRY(launch_prolong(h, curw, g, C.e, C.g));
-    const double *cu = curw;
-    for (int it = 0; it < h->P.mg.nu2; ++it) {
-        double *dst = (cu == T) ? X : T;
-        TRY(launch_jacobi(h, dst, cu, b, g, c, l));
-        cu = dst;
+    TRY(launch_restrict(h, C.b, C.g, curw, b, g, c, l));
+    if (l + 1 == h->tail_l0) {
+        TRY(launch_tail(h, l + 1, m, C.b, nullptr, C.e));
+    } else {
+        TRY(zero_field(h, C.e, C.g));
+        TRY(vcycle(h, l + 1, m, C.e, C.t, C.b, nullptr));
     }
+    TRY(launch_prolong(h, curw, g, C.e, C.g, l));
+    const double *cu = curw;
+    TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2));
     if (cu != X) TRY(copy_field(h, X, cu, g));
     return ISDC_OK;
 }
 
 // fills the host-side parameter blocks of substep m / residual node m at time t_n
 void fill_vw(isdc_ctx *h, VWParams &P, int m, double *const *uold, const double *unew_m) {
-    double tn = (double)h->step_index * h->P.dt;
     P.M = h->M; P.m = m;
     for (int j = 0; j < h->M; ++j) P.uold[j] = uold[j];
     P.unew_m = unew_m;
@@ -337,17 +494,49 @@ void fill_vw(isdc_ctx *h, VWParams &P, int m, double *const *uold, const double 
     for (int j = 0; j < h->M; ++j) {
         P.a[j] = dt * h->S[m * h->M + j];
         P.beta[j] = nudt * h->S[m * h->M + j];
-        P.ct[j] = std::cos(tn + dt * h->tau[j]);
     }
+    P.ct = h->ctdev;
     P.fe = h->fe;
     P.g = h->lev[0].g;
 }
 
+bool fast2d_pointwise_fe(const isdc_ctx *h) { return h->fast && h->d == 2 && h->fe.kind <= 2 && h->n >= 63; }
+
 isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_m, double *bout, bool bnorm) {
+    if (fast2d_pointwise_fe(h)) {
+        f2d::RhsArgs A;
+        for (int j = 0; j < h->M; ++j) A.uold[j] = uold[j];
+        A.unew_m = unew_m; A.G = h->Gp; A.ct = h->ctdev;
+        A.M = h->M; A.m = m; A.fe = h->fe.kind; A.n = h->n; A.pitch = h->lev[0].g.pitch;
+        double dt = h->P.dt, nu = h->P.nu, nudt = nu * dt;
+        A.dtm = dt * h->dtau[m];
+        A.gm = nu * A.dtm;
+        for (int j = 0; j < h->M; ++j) {
+            A.a[j] = dt * h->S[m * h->M + j];
+            A.beta[j] = nudt * h->S[m * h->M + j];
+        }
+        A.bl = h->bl;
+        unsigned long long *slot = nullptr;
+        if (bnorm) {
+            TRY(clear_slots(h, SLOT_BNORM, 1));
+            slot = h->red + SLOT_BNORM;
+        }
+        const GridDesc &g = h->lev[0].g;
+        dim3 grd((g.n + f2d::QX - 1) / f2d::QX, (g.n + f2d::QY - 1) / f2d::QY);
+        ++h->launches;
+        int pe = prof_begin(h, PROF_RHS);
+        if (A.fe == 0) f2d::k_rhs<0><<<grd, f2d::QNT, 0, h->s>>>(A, bout, slot);
+        else if (A.fe == 1) f2d::k_rhs<1><<<grd, f2d::QNT, 0, h->s>>>(A, bout, slot);
+        else f2d::k_rhs<2><<<grd, f2d::QNT, 0, h->s>>>(A, bout, slot);
+        prof_end(h, pe, PROF_RHS, (h->M + 2 + (h->fe.kind == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
+        LAUNCH_CHECK(h);
+        return ISDC_OK;
+    }
     VWParams P;
     fill_vw(h, P, m, uold, unew_m);
     const GridDesc &g = h->lev[0].g;
     ++h->launches;
+    int pe = prof_begin(h, PROF_RHS);
     if (h->d == 2) k_vw<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
     else k_vw<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
     LAUNCH_CHECK(h);
@@ -359,17 +548,40 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
     ++h->launches;
     if (h->d == 2) k_bvw<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(bout, h->V, h->W, g, h->bl, slot);
     else k_bvw<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(bout, h->V, h->W, g, h->bl, slot);
+    prof_end(h, pe, PROF_RHS, (h->M + 2 + (h->fe.kind == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
 
-// residual of node fields u[0..M-1] -> per node (host) and max
-isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double *maxn) {
+// residual of node fields u[0..M-1]: enqueue the kernels (slots SLOT_RES0..), then read them
+isdc_status enqueue_residual(isdc_ctx *h, double *const *u) {
     const GridDesc &g = h->lev[0].g;
     int M = h->M;
     TRY(clear_slots(h, SLOT_RES0, M - 1));
-    double tn = (double)h->step_index * h->P.dt;
+    if (fast2d_pointwise_fe(h)) {
+        f2d::ResArgs A;
+        for (int j = 0; j < M; ++j) A.u[j] = u[j];
+        A.G = h->Gp; A.ct = h->ctdev; A.M = M; A.fe = h->fe.kind; A.n = h->n; A.pitch = g.pitch;
+        double dt = h->P.dt, nudt = h->P.nu * dt;
+        for (int m = 0; m < M; ++m)
+            for (int j = 0; j < M; ++j) {
+                A.qa[m][j] = dt * h->Q[m * M + j];
+                A.qb[m][j] = nudt * h->Q[m * M + j];
+            }
+        A.bl = h->bl;
+        size_t sm = 2 * (size_t)(M - 1) * f2d::ZH * f2d::ZW * sizeof(double);
+        dim3 grd((g.n + f2d::ZX - 1) / f2d::ZX, (g.n + f2d::ZY - 1) / f2d::ZY);
+        ++h->launches;
+        int pe = prof_begin(h, PROF_RESID);
+        if (A.fe == 0) f2d::k_resid<0><<<grd, f2d::ZNT, sm, h->s>>>(A, h->red + SLOT_RES0);
+        else if (A.fe == 1) f2d::k_resid<1><<<grd, f2d::ZNT, sm, h->s>>>(A, h->red + SLOT_RES0);
+        else f2d::k_resid<2><<<grd, f2d::ZNT, sm, h->s>>>(A, h->red + SLOT_RES0);
+        prof_end(h, pe, PROF_RESID, (M + (h->fe.kind == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
+        LAUNCH_CHECK(h);
+        return ISDC_OK;
+    }
     double dt = h->P.dt, nudt = h->P.nu * dt;
+    int pe = prof_begin(h, PROF_RESID);
     for (int m = 1; m < M; ++m) {
         PZParams P;
         P.M = M; P.m = m;
@@ -377,8 +589,8 @@ isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double
             P.u[j] = u[j];
             P.qa[j] = dt * h->Q[m * M + j];
             P.qb[j] = nudt * h->Q[m * M + j];
-            P.ct[j] = std::cos(tn + dt * h->tau[j]);
         }
+        P.ct = h->ctdev;
         P.fe = h->fe;
         P.g = g;
         h->launches += 2;
@@ -391,6 +603,12 @@ isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double
         }
         LAUNCH_CHECK(h);
     }
+    prof_end(h, pe, PROF_RESID, (M + (h->fe.kind == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
+    return ISDC_OK;
+}
+
+isdc_status read_residual(isdc_ctx *h, double *per_node, double *maxn) {
+    int M = h->M;
     double tmp[ISDC_MAXM];
     TRY(read_slots(h, SLOT_RES0, M - 1, tmp));
     double mx = 0.0;
@@ -437,8 +655,83 @@ isdc_status node_solve(isdc_ctx *h, int m, double *X, const double *src, int *cy
     return ISDC_OK;
 }
 
+isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double *maxn) {
+    TRY(enqueue_residual(h, u));
+    return read_residual(h, per_node, maxn);
+}
+
+// all device work of one ISDC-mode sweep (no host synchronisation): RHS, L cycles per node, residual
+isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
+    int M = h->M;
+    double *uold[ISDC_MAXM];
+    int nw = 1 - h->cur;
+    for (int j = 0; j < M; ++j) uold[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
+    double **unew = h->U[nw];
+    for (int m = 0; m + 1 < M; ++m) {
+        TRY(run_rhs(h, m, uold, unew[m], h->Bf, false));
+        const double *src;
+        if (h->P.solve.guess == 1) { TRY(zero_field(h, unew[m + 1], h->lev[0].g)); src = nullptr; }
+        else if (h->P.solve.guess == 2) src = unew[m];
+        else src = uold[m + 1];
+        for (int l = 0; l < h->P.solve.L; ++l) TRY(vcycle(h, 0, m, unew[m + 1], h->T, h->Bf, l == 0 ? src : nullptr));
+    }
+    return enqueue_residual(h, unew);
+}
+
+isdc_status graph_sweep(isdc_ctx *h) {
+    auto key = std::make_tuple(h->cur, h->spread ? 1 : 0, h->prof);
+    auto it = h->sweep_graphs.find(key);
+    if (it == h->sweep_graphs.end()) {
+        if (!h->cap) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+        cudaStream_t user = h->s;
+        size_t pend0 = h->pend.size();
+        long l0 = h->launches;
+        h->s = h->cap;
+        h->capturing = true;
+        cudaError_t e = cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal);
+        isdc_status st = (e == cudaSuccess) ? enqueue_isdc_sweep(h) : ISDC_ERR_CUDA;
+        cudaGraph_t g = nullptr;
+        cudaError_t e2 = cudaStreamEndCapture(h->cap, &g);
+        h->capturing = false;
+        h->s = user;
+        if (e != cudaSuccess || e2 != cudaSuccess || st != ISDC_OK) {
+            if (g) cudaGraphDestroy(g);
+            if (st == ISDC_OK) h->err = std::string("graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
+            return st == ISDC_OK ? ISDC_ERR_CUDA : st;
+        }
+        isdc_ctx::Graph G;
+        G.nkernels = h->launches - l0;
+        h->launches = l0;   // capture is not execution
+        G.events.assign(h->pend.begin() + pend0, h->pend.end());
+        h->pend.resize(pend0);
+        CUDA_TRY(h, cudaGraphInstantiate(&G.exec, g, 0));
+        cudaGraphDestroy(g);
+        it = h->sweep_graphs.emplace(key, G).first;
+    }
+    CUDA_TRY(h, cudaGraphLaunch(it->second.exec, h->s));
+    h->launches += it->second.nkernels;
+    if (h->prof) {  // the graph's event pairs hold this launch's timings
+        CUDA_TRY(h, cudaStreamSynchronize(h->s));
+        for (auto &p : it->second.events) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, h->evpool[p.a], h->evpool[p.b]);
+            h->prof_ms[p.cls] += ms; h->prof_cnt[p.cls] += 1; h->prof_bytes[p.cls] += p.bytes;
+        }
+    }
+    return ISDC_OK;
+}
+
 isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *cycles, int *cap_hits) {
     int M = h->M;
+    if (h->P.solve.mode == ISDC_MODE_ISDC_FIXED) {
+        if (h->graphs) TRY(graph_sweep(h));
+        else TRY(enqueue_isdc_sweep(h));
+        for (int m = 0; m + 1 < M; ++m) if (cycles) cycles[m] = h->P.solve.L;
+        if (cap_hits) *cap_hits = 0;
+        h->cur = 1 - h->cur;
+        h->spread = false;
+        return read_residual(h, res_per_node, res_max);
+    }
     double *uold[ISDC_MAXM];
     int nw = 1 - h->cur;
     for (int j = 0; j < M; ++j) uold[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
@@ -512,6 +805,21 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     h->fe.G = h->Gp;
     const char *env = getenv("ISDC_GENERIC_KERNELS");
     h->fast = !(env && env[0] == '1');
+    if (h->fast && !tma_encoder()) h->fast = false;
+    static bool attrs = false;
+    if (!attrs) {
+        cudaFuncSetAttribute(f2d::k_smooth2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSmooth) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSmooth) + 128);
+        cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemRestrict) + 128);
+        int rs = 2 * (ISDC_MAXM - 1) * f2d::ZH * f2d::ZW * (int)sizeof(double);
+        cudaFuncSetAttribute(f2d::k_resid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
+        cudaFuncSetAttribute(f2d::k_resid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
+        cudaFuncSetAttribute(f2d::k_resid<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
+        attrs = true;
+    }
     int Pc = (h->d == 3) ? 27 : 9;
     std::vector<double> Gi((size_t)(h->M - 1) * Pc * Pc);
     for (int m = 0; m + 1 < h->M; ++m) {
@@ -523,6 +831,32 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
             return ISDC_ERR_INVALID_ARG;
         }
     }
+    const char *eg = getenv("ISDC_NO_GRAPHS");
+    h->graphs = !(eg && eg[0] == '1');
+    // single-CTA tail: levels n <= 63 (2D) / 15 (3D) in shared memory
+    if (h->fast) {
+        int tail_n = (h->d == 2) ? 63 : 15;
+        for (int l = 0; l < h->nlev; ++l)
+            if (h->lev[l].g.n <= tail_n) { h->tail_l0 = l; break; }
+        if (h->tail_l0 >= 0) {
+            for (int m = 0; m + 1 < h->M; ++m) {
+                TailParams &T = h->tailp[m];
+                T.nlev = h->nlev - h->tail_l0;
+                for (int i = 0; i < T.nlev; ++i) {
+                    T.n[i] = h->lev[h->tail_l0 + i].g.n;
+                    T.c[i] = h->lev[h->tail_l0 + i].coef[m];
+                }
+                T.nu1 = prob->mg.nu1; T.nu2 = prob->mg.nu2;
+                T.Ginv = h->Ginv + (size_t)m * Pc * Pc;
+                T.b_in = nullptr; T.u_in = nullptr; T.u_out = nullptr; T.pitch = 0;
+            }
+            h->tail_smem = (h->d == 2) ? tail_smem_bytes<2>(h->tailp[0]) : tail_smem_bytes<3>(h->tailp[0]);
+            cudaError_t ea = (h->d == 2)
+                ? cudaFuncSetAttribute(k_tail<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem)
+                : cudaFuncSetAttribute(k_tail<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem);
+            if (ea != cudaSuccess) h->tail_l0 = -1;
+        }
+    }
     cudaError_t e = cudaMemcpyAsync(h->Ginv, Gi.data(), Gi.size() * sizeof(double), cudaMemcpyHostToDevice, h->s);
     if (e == cudaSuccess && h->Gp) {
         // the pad column of every pitched field is never read; copy G into the pitched layout
@@ -531,9 +865,32 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         e = cudaMemcpy2DAsync(h->Gp, g.pitch * sizeof(double), prob->fe_field_dev, g.n * sizeof(double),
                               g.n * sizeof(double), rows, cudaMemcpyDeviceToDevice, h->s);
     }
+    if (e == cudaSuccess && upload_ct(h) != ISDC_OK) e = cudaErrorUnknown;
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->s);
     if (e != cudaSuccess) { delete h; return ISDC_ERR_CUDA; }
     *out = h;
+    return ISDC_OK;
+}
+
+isdc_status isdc_profile_enable(isdc_handle h, int on) {
+    if (!h) return ISDC_ERR_INVALID_ARG;
+    h->prof = on < 0 ? 0 : (on > 2 ? 2 : on);
+    return ISDC_OK;
+}
+
+isdc_status isdc_profile_reset(isdc_handle h) {
+    if (!h) return ISDC_ERR_INVALID_ARG;
+    TRY(prof_collect(h));
+    for (int i = 0; i < 8; ++i) { h->prof_ms[i] = 0; h->prof_bytes[i] = 0; h->prof_cnt[i] = 0; }
+    return ISDC_OK;
+}
+
+isdc_status isdc_profile_get(isdc_handle h, int cls, double *total_ms, long *launches, double *alg_bytes) {
+    if (!h || cls < 0 || cls >= 8) return ISDC_ERR_INVALID_ARG;
+    TRY(prof_collect(h));
+    if (total_ms) *total_ms = h->prof_ms[cls];
+    if (launches) *launches = h->prof_cnt[cls];
+    if (alg_bytes) *alg_bytes = h->prof_bytes[cls];
     return ISDC_OK;
 }
 
@@ -550,21 +907,21 @@ isdc_status isdc_set_initial(isdc_handle h, const double *u0, int step_index) {
     if (!h || !u0) return ISDC_ERR_INVALID_ARG;
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyDeviceToDevice));
     h->cur = 0; h->spread = true; h->step_index = step_index;
-    return ISDC_OK;
+    return upload_ct(h);
 }
 
 isdc_status isdc_set_initial_host(isdc_handle h, const double *u0, int step_index) {
     if (!h || !u0) return ISDC_ERR_INVALID_ARG;
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyHostToDevice));
     h->cur = 0; h->spread = true; h->step_index = step_index;
-    return ISDC_OK;
+    return upload_ct(h);
 }
 
 isdc_status isdc_set_state(isdc_handle h, const double *const *u, int step_index) {
     if (!h || !u) return ISDC_ERR_INVALID_ARG;
     for (int j = 0; j < h->M; ++j) TRY(dense_to_pitched(h, h->U[0][j], u[j], cudaMemcpyDeviceToDevice));
     h->cur = 0; h->spread = false; h->step_index = step_index;
-    return ISDC_OK;
+    return upload_ct(h);
 }
 
 isdc_status isdc_get_solution(isdc_handle h, int node, double *out) {
@@ -623,6 +980,7 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     h->cur = 0;
     h->spread = true;
     h->step_index += 1;
+    TRY(upload_ct(h));
     if (stats) {
         stats->sweeps = k; stats->vcycles = vc; stats->cap_hits = caps; stats->converged = conv;
         stats->final_residual = res;

@@ -1,0 +1,435 @@
+// kernels_fast2d.cuh -- tuned fine-level 2D kernels (sm_100a): TMA-staged tiles, register-rolled
+// vertical stencil windows, fused sweeps.  Every value is produced by the canonical expression
+// trees of DESIGN.md §4 in the same order as the generic kernels, so results are bit-identical.
+#pragma once
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace f2d {
+
+// ---------------------------------------------------------------------------------------------
+// Fused two-sweep weighted Jacobi (one HBM pass: read u, b; write u''), DESIGN.md §6.1.
+// Tile: 64 x 32 outputs per CTA, 128 threads (4 warps).  Smem: u box 68x36 at (x0-2, y0-2),
+// b box 68x34 at (x0-2, y0-1) (TMA, zero fill outside the domain), t = first sweep on the
+// 66x34 region at (x0-1, y0-1) (zero outside the domain).  Thread (lane, warp) owns tile
+// columns lane and lane+32 and rolls a 3-row window down its warp's band of rows.
+// Optional: NORM -> ||b - S u||_inf over the tile (the SDC defect test of the incoming iterate).
+// ---------------------------------------------------------------------------------------------
+constexpr int TX = 64, TY = 32, NT = 128;
+constexpr int UW = TX + 4, UH = TY + 4;
+constexpr int BW = TX + 4, BH = TY + 2;
+constexpr int TW = TX + 2, TH = TY + 2;
+
+struct __align__(128) SmemSmooth {
+    alignas(128) double u[UH][UW];
+    alignas(128) double b[BH][BW];
+    alignas(128) double t[TH][TW];
+    uint64_t bar;
+};
+
+template <bool NORM>
+__global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensorMap tu,
+                                                const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
+                                                int n, int pitch, SCoef c, unsigned long long *slot) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SmemSmooth &S = *reinterpret_cast<SmemSmooth *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    if (tid == 0) {
+        tma_prefetch_desc(&tu);
+        tma_prefetch_desc(&tb);
+        mbar_init(&S.bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&S.bar, (UW * UH + BW * BH) * 8);
+        tma_load_2d(&S.u[0][0], &tu, x0 - 2, y0 - 2, &S.bar);
+        tma_load_2d(&S.b[0][0], &tb, x0 - 2, y0 - 1, &S.bar);
+    }
+    mbar_wait(&S.bar, 0);
+
+    const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
+    double dmax = 0.0;
+    // ---- sweep 1, main columns 0..63 of the t region (rows -1..32, warp bands of 9 rows)
+    {
+        const int rs = -1 + 9 * w, re = min(rs + 9, TY + 1);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int x = lane + 32 * hh;          // tile column; u smem col x+2
+            const int gx = x0 + x;
+            const bool xin = gx < n;
+            double um = S.u[rs + 1][x + 2];         // row rs-1
+            double rm = S.u[rs + 1][x + 1] + S.u[rs + 1][x + 3];
+            double uc = S.u[rs + 2][x + 2];         // row rs
+            double rc = S.u[rs + 2][x + 1] + S.u[rs + 2][x + 3];
+            for (int y = rs; y < re; ++y) {
+                double up = S.u[y + 3][x + 2];
+                double rp = S.u[y + 3][x + 1] + S.u[y + 3][x + 3];
+                double f = rc + (um + up);
+                double e = rm + rp;
+                double su = (c0 * uc + c1 * f) + c2 * e;
+                int gy = y0 + y;
+                bool in = xin && gy >= 0 && gy < n;
+                double bv = S.b[y + 1][x + 2];
+                double d = bv - su;
+                if (NORM && in && y >= 0 && y < TY) dmax = amax(dmax, fabs(d));
+                S.t[y + 1][x + 1] = in ? uc + wd * d : 0.0;
+                um = uc; uc = up; rm = rc; rc = rp;
+            }
+        }
+    }
+    // ---- sweep 1, halo columns -1 and 64 (rows -1..32): 68 points, direct 9-point reads
+    if (tid < 2 * TH) {
+        const int x = (tid < TH) ? -1 : TX;
+        const int y = (tid < TH ? tid : tid - TH) - 1;
+        const int gx = x0 + x, gy = y0 + y;
+        double v = 0.0;
+        if (gx >= 0 && gx < n && gy >= 0 && gy < n) {
+            const int cx = x + 2, cy = y + 2;
+            double r_m = S.u[cy - 1][cx - 1] + S.u[cy - 1][cx + 1];
+            double r_c = S.u[cy][cx - 1] + S.u[cy][cx + 1];
+            double r_p = S.u[cy + 1][cx - 1] + S.u[cy + 1][cx + 1];
+            double f = r_c + (S.u[cy - 1][cx] + S.u[cy + 1][cx]);
+            double e = r_m + r_p;
+            double uc = S.u[cy][cx];
+            double su = (c0 * uc + c1 * f) + c2 * e;
+            v = uc + wd * (S.b[y + 1][x + 2] - su);
+        }
+        S.t[y + 1][x + 1] = v;
+    }
+    if (NORM) block_max_to(slot, dmax);  // contains a __syncthreads
+    __syncthreads();
+    // ---- sweep 2 on the 64 x 32 tile (warp bands of 8 rows)
+    {
+        const int rs = 8 * w, re = rs + 8;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int x = lane + 32 * hh;          // t smem col x+1
+            const int gx = x0 + x;
+            double tm = S.t[rs][x + 1];             // row rs-1
+            double rm = S.t[rs][x] + S.t[rs][x + 2];
+            double tc = S.t[rs + 1][x + 1];
+            double rc = S.t[rs + 1][x] + S.t[rs + 1][x + 2];
+            for (int y = rs; y < re; ++y) {
+                double tp = S.t[y + 2][x + 1];
+                double rp = S.t[y + 2][x] + S.t[y + 2][x + 2];
+                double f = rc + (tm + tp);
+                double e = rm + rp;
+                double su = (c0 * tc + c1 * f) + c2 * e;
+                double v = tc + wd * (S.b[y + 1][x + 2] - su);
+                int gy = y0 + y;
+                if (gx < n && gy < n) out[(long long)gy * pitch + gx] = v;
+                tm = tc; tc = tp; rm = rc; rc = rp;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Defect + full-weighting restriction (one pass: read u, b; write b_c), DESIGN.md §6.2.
+// Coarse tile 32 x 16 -> fine defect region x in [2I0, 2I0+64], y in [2J0, 2J0+32].
+// Smem: u box 68x35 at (2I0-2, 2J0-1), b box 68x33 at (2I0-2, 2J0), d (65 x 33).
+// ---------------------------------------------------------------------------------------------
+constexpr int RCX = 32, RCY = 16, RNT = 256;
+constexpr int RUW = 2 * RCX + 4, RUH = 2 * RCY + 3;
+constexpr int RBW = 2 * RCX + 4, RBH = 2 * RCY + 1;
+constexpr int RDW = 2 * RCX + 1, RDH = 2 * RCY + 1;
+
+struct __align__(128) SmemRestrict {
+    alignas(128) double u[RUH][RUW];
+    alignas(128) double b[RBH][RBW];
+    alignas(128) double d[RDH][RDW + 1];
+    uint64_t bar;
+};
+
+__global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtensorMap tu,
+                                                  const __grid_constant__ CUtensorMap tb, double *__restrict__ bc,
+                                                  int nf, int nc, int pitch_c, SCoef c) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SmemRestrict &S = *reinterpret_cast<SmemRestrict *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    const int tid = threadIdx.x;
+    const int I0 = blockIdx.x * RCX, J0 = blockIdx.y * RCY;
+    const int fx0 = 2 * I0, fy0 = 2 * J0;   // fine origin of the d region
+    if (tid == 0) {
+        tma_prefetch_desc(&tu);
+        tma_prefetch_desc(&tb);
+        mbar_init(&S.bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&S.bar, (RUW * RUH + RBW * RBH) * 8);
+        tma_load_2d(&S.u[0][0], &tu, fx0 - 2, fy0 - 1, &S.bar);
+        tma_load_2d(&S.b[0][0], &tb, fx0 - 2, fy0, &S.bar);
+    }
+    mbar_wait(&S.bar, 0);
+    const double c0 = c.c0, c1 = c.c1, c2 = c.c2;
+    // defect on the (2RCX+1) x (2RCY+1) fine region; d(x,y) with u smem (x+2, y+1)
+    for (int p = tid; p < RDW * RDH; p += RNT) {
+        const int x = p % RDW, y = p / RDW;
+        const int cx = x + 2, cy = y + 1;
+        double r_m = S.u[cy - 1][cx - 1] + S.u[cy - 1][cx + 1];
+        double r_c = S.u[cy][cx - 1] + S.u[cy][cx + 1];
+        double r_p = S.u[cy + 1][cx - 1] + S.u[cy + 1][cx + 1];
+        double f = r_c + (S.u[cy - 1][cx] + S.u[cy + 1][cx]);
+        double e = r_m + r_p;
+        double su = (c0 * S.u[cy][cx] + c1 * f) + c2 * e;
+        S.d[y][x] = S.b[y][x + 2] - su;   // outside the fine domain only feeds coarse points we skip
+    }
+    __syncthreads();
+    for (int p = tid; p < RCX * RCY; p += RNT) {
+        const int I = p % RCX, J = p / RCX;
+        const int gI = I0 + I, gJ = J0 + J;
+        if (gI >= nc || gJ >= nc) continue;
+        const int x = 2 * I + 1, y = 2 * J + 1;   // d-region coordinates of the coarse point
+        double rd0 = S.d[y - 1][x - 1] + S.d[y - 1][x + 1];
+        double rd1 = S.d[y][x - 1] + S.d[y][x + 1];
+        double rd2 = S.d[y + 1][x - 1] + S.d[y + 1][x + 1];
+        double fd = rd1 + (S.d[y - 1][x] + S.d[y + 1][x]);
+        double ed = rd0 + rd2;
+        bc[(long long)gJ * pitch_c + gI] = ((4.0 * S.d[y][x] + 2.0 * fd) + ed) * 0.0625;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Bilinear prolongation + correction u += P e, two fine points (2t, 2t+1) per thread with 16-byte
+// accesses on u, DESIGN.md §6.3.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf, int pitch_f,
+                                                 const double *__restrict__ e, int nc, int pitch_c) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;   // column pair
+    const int y = blockIdx.y;
+    const int x = 2 * t;
+    if (x >= nf) return;
+    auto E = [&](int X, int Y) -> double {
+        return (X >= 0 && X < nc && Y >= 0 && Y < nc) ? e[(long long)Y * pitch_c + X] : 0.0;
+    };
+    const bool ye = !(y & 1);
+    const int Ya = ye ? y / 2 - 1 : (y - 1) / 2, Yb = y / 2;
+    // even column x = 2t: coarse pair (t-1, t); odd column 2t+1: coarse t
+    double se, so;
+    {
+        double sx_a = E(t - 1, Ya) + E(t, Ya);
+        double so_a = E(t, Ya);
+        if (ye) {
+            double sx_b = E(t - 1, Yb) + E(t, Yb);
+            double so_b = E(t, Yb);
+            se = (sx_a + sx_b) * 0.25;
+            so = (so_a + so_b) * 0.5;
+        } else {
+            se = sx_a * 0.5;
+            so = so_a;
+        }
+    }
+    double *row = u + (long long)y * pitch_f;
+    if (x + 1 < nf) {
+        double2 v = *reinterpret_cast<double2 *>(row + x);
+        v.x = v.x + se;
+        v.y = v.y + so;
+        *reinterpret_cast<double2 *>(row + x) = v;
+    } else {
+        row[x] = row[x] + se;
+    }
+}
+
+}  // namespace f2d
+
+namespace f2d {
+
+// ---------------------------------------------------------------------------------------------
+// Single-pass RHS of Eq. (5): v and w on the tile + 1 halo are formed
+// from the M+1 node fields (and G) straight from global memory into shared memory, then
+// b = B v + L w is applied from shared memory.  f^E kinds none / cubic / forcing (pointwise).
+// ---------------------------------------------------------------------------------------------
+constexpr int QX = 64, QY = 32, QNT = 256;
+constexpr int QW = QX + 2, QH = QY + 2;
+
+struct RhsArgs {
+    const double *uold[ISDC_MAXM];
+    const double *unew_m;
+    const double *G;
+    const double *ct;
+    int M, m, fe, n, pitch;
+    double dtm, gm;
+    double a[ISDC_MAXM], beta[ISDC_MAXM];
+    BLConst bl;
+};
+
+template <int FE>
+__global__ void __launch_bounds__(QNT) k_rhs(RhsArgs A, double *__restrict__ bout, unsigned long long *slot) {
+    __shared__ double vs[QH][QW];
+    __shared__ double ws[QH][QW];
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * QX, y0 = blockIdx.y * QY;
+    const int n = A.n, M = A.M, m = A.m;
+    for (int p = tid; p < QW * QH; p += QNT) {
+        const int lx = p % QW, ly = p / QW;
+        const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+        double v = 0.0, w = 0.0;
+        if (gx >= 0 && gx < n && gy >= 0 && gy < n) {
+            const long long q = (long long)gy * A.pitch + gx;
+            double uj[ISDC_MAXM];
+#pragma unroll
+            for (int j = 0; j < ISDC_MAXM; ++j)
+                if (j < M) uj[j] = A.uold[j][q];
+            double acc = A.beta[0] * uj[0];
+#pragma unroll
+            for (int j = 1; j < ISDC_MAXM; ++j)
+                if (j < M) acc = acc + A.beta[j] * uj[j];
+            double uo1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < ISDC_MAXM; ++j)
+                if (j == m + 1) uo1 = uj[j];
+            w = acc - A.gm * uo1;
+            const double un = A.unew_m[q];
+            if (FE == 0) {
+                v = un;
+            } else {
+                double uom = 0.0;
+#pragma unroll
+                for (int j = 0; j < ISDC_MAXM; ++j)
+                    if (j == m) uom = uj[j];
+                double fa, fn, fo;
+                if (FE == 1) {
+                    fa = A.a[0] * (uj[0] - (uj[0] * uj[0]) * uj[0]);
+#pragma unroll
+                    for (int j = 1; j < ISDC_MAXM; ++j)
+                        if (j < M) fa = fa + A.a[j] * (uj[j] - (uj[j] * uj[j]) * uj[j]);
+                    fn = un - (un * un) * un;
+                    fo = uom - (uom * uom) * uom;
+                } else {
+                    const double g = A.G[q];
+                    fa = A.a[0] * (g * A.ct[0]);
+#pragma unroll
+                    for (int j = 1; j < ISDC_MAXM; ++j)
+                        if (j < M) fa = fa + A.a[j] * (g * A.ct[j]);
+                    fn = g * A.ct[m];
+                    fo = g * A.ct[m];
+                }
+                v = (un + A.dtm * (fn - fo)) + fa;
+            }
+        }
+        vs[ly][lx] = v;
+        ws[ly][lx] = w;
+    }
+    __syncthreads();
+    const BLConst c = A.bl;
+    double bmax = 0.0;
+    for (int p = tid; p < QX * QY; p += QNT) {
+        const int lx = p % QX, ly = p / QX;
+        const int gx = x0 + lx, gy = y0 + ly;
+        if (gx >= n || gy >= n) continue;
+        const int cx = lx + 1, cy = ly + 1;
+        double fv = (vs[cy][cx - 1] + vs[cy][cx + 1]) + (vs[cy - 1][cx] + vs[cy + 1][cx]);
+        double rwm = ws[cy - 1][cx - 1] + ws[cy - 1][cx + 1];
+        double rwc = ws[cy][cx - 1] + ws[cy][cx + 1];
+        double rwp = ws[cy + 1][cx - 1] + ws[cy + 1][cx + 1];
+        double fw = rwc + (ws[cy - 1][cx] + ws[cy + 1][cx]);
+        double ew = rwm + rwp;
+        double Bv = c.kB0 * vs[cy][cx] + c.kB1 * fv;
+        double Lw = (c.kL0 * ws[cy][cx] + c.kL1 * fw) + c.kL2 * ew;
+        double b = Bv + Lw;
+        bout[(long long)gy * A.pitch + gx] = b;
+        bmax = amax(bmax, fabs(b));
+    }
+    if (slot) block_max_to(slot, bmax);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Single-pass weighted SDC residual of nodes m = 1..M-1: p_m and z_m on
+// the tile + 1 halo for every m from one read of the M node fields, then r~_m = B p_m - L z_m
+// and a per-node max into slots[m-1].
+// ---------------------------------------------------------------------------------------------
+constexpr int ZX = 32, ZY = 32, ZNT = 256;
+constexpr int ZW = ZX + 2, ZH = ZY + 2;
+
+struct ResArgs {
+    const double *u[ISDC_MAXM];
+    const double *G;
+    const double *ct;
+    int M, fe, n, pitch;
+    double qa[ISDC_MAXM][ISDC_MAXM];   // [m][j] = dt*Q_{m,j}
+    double qb[ISDC_MAXM][ISDC_MAXM];   // [m][j] = (nu*dt)*Q_{m,j}
+    BLConst bl;
+};
+
+template <int FE>
+__global__ void __launch_bounds__(ZNT) k_resid(ResArgs A, unsigned long long *slots) {
+    extern __shared__ __align__(16) double zsm[];
+    const int M = A.M;
+    double *ps = zsm;                                  // [M-1][ZH][ZW]
+    double *zs = zsm + (size_t)(M - 1) * ZH * ZW;      // [M-1][ZH][ZW]
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * ZX, y0 = blockIdx.y * ZY, n = A.n;
+    for (int p = tid; p < ZW * ZH; p += ZNT) {
+        const int lx = p % ZW, ly = p / ZW;
+        const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+        const bool in = gx >= 0 && gx < n && gy >= 0 && gy < n;
+        double uj[ISDC_MAXM], fj[ISDC_MAXM];
+        if (in) {
+            const long long q = (long long)gy * A.pitch + gx;
+#pragma unroll
+            for (int j = 0; j < ISDC_MAXM; ++j)
+                if (j < M) uj[j] = A.u[j][q];
+            if (FE == 1) {
+#pragma unroll
+                for (int j = 0; j < ISDC_MAXM; ++j)
+                    if (j < M) fj[j] = uj[j] - (uj[j] * uj[j]) * uj[j];
+            } else if (FE == 2) {
+                const double g = A.G[q];
+#pragma unroll
+                for (int j = 0; j < ISDC_MAXM; ++j)
+                    if (j < M) fj[j] = g * A.ct[j];
+            }
+        }
+#pragma unroll
+        for (int m = 1; m < ISDC_MAXM; ++m) {
+            if (m >= M) break;
+            double pv = 0.0, zv = 0.0;
+            if (in) {
+                double diff = uj[m] - uj[0];
+                if (FE != 0) {
+                    double fa = A.qa[m][0] * fj[0];
+#pragma unroll
+                    for (int j = 1; j < ISDC_MAXM; ++j)
+                        if (j < M) fa = fa + A.qa[m][j] * fj[j];
+                    diff = diff - fa;
+                }
+                pv = diff;
+                double acc = A.qb[m][0] * uj[0];
+#pragma unroll
+                for (int j = 1; j < ISDC_MAXM; ++j)
+                    if (j < M) acc = acc + A.qb[m][j] * uj[j];
+                zv = acc;
+            }
+            ps[(m - 1) * ZH * ZW + p] = pv;
+            zs[(m - 1) * ZH * ZW + p] = zv;
+        }
+    }
+    __syncthreads();
+    const BLConst c = A.bl;
+    for (int m = 1; m < M; ++m) {
+        const double *P_ = ps + (m - 1) * ZH * ZW;
+        const double *Z_ = zs + (m - 1) * ZH * ZW;
+        double rmax = 0.0;
+        for (int p = tid; p < ZX * ZY; p += ZNT) {
+            const int lx = p % ZX, ly = p / ZX;
+            if (x0 + lx >= n || y0 + ly >= n) continue;
+            const int q = (ly + 1) * ZW + lx + 1;
+            double fp = (P_[q - 1] + P_[q + 1]) + (P_[q - ZW] + P_[q + ZW]);
+            double rzm = Z_[q - ZW - 1] + Z_[q - ZW + 1];
+            double rzc = Z_[q - 1] + Z_[q + 1];
+            double rzp = Z_[q + ZW - 1] + Z_[q + ZW + 1];
+            double fz = rzc + (Z_[q - ZW] + Z_[q + ZW]);
+            double ez = rzm + rzp;
+            double Bp = c.kB0 * P_[q] + c.kB1 * fp;
+            double Lz = (c.kL0 * Z_[q] + c.kL1 * fz) + c.kL2 * ez;
+            rmax = amax(rmax, fabs(Bp - Lz));
+        }
+        block_max_to(slots + (m - 1), rmax);
+        __syncthreads();
+    }
+}
+
+}  // namespace f2d

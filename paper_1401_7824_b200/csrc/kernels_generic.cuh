@@ -12,7 +12,7 @@ struct VWParams {                 // RHS of Eq. (5) for substep m (DESIGN.md §4
     double dtm, gm;               // dt*dtau_m, nu*dtm
     double a[ISDC_MAXM];          // dt*S_{m,j}
     double beta[ISDC_MAXM];       // (nu*dt)*S_{m,j}
-    double ct[ISDC_MAXM];         // cos(t_n + dt*tau_j)
+    const double *ct;             // device: cos(t_n + dt*tau_j), j = 0..M-1
     FeDesc fe;
     GridDesc g;
 };
@@ -22,7 +22,7 @@ struct PZParams {                 // residual of node m
     int M, m;
     double qa[ISDC_MAXM];         // dt*Q_{m,j}
     double qb[ISDC_MAXM];         // (nu*dt)*Q_{m,j}
-    double ct[ISDC_MAXM];
+    const double *ct;             // device: cos(t_n + dt*tau_j)
     FeDesc fe;
     GridDesc g;
 };

@@ -87,6 +87,9 @@ def lib():
         L.isdc_destroy.argtypes = [_vp]
         L.isdc_last_error.argtypes = [_vp]
         L.isdc_last_error.restype = C.c_char_p
+        L.isdc_profile_enable.argtypes = [_vp, C.c_int]
+        L.isdc_profile_reset.argtypes = [_vp]
+        L.isdc_profile_get.argtypes = [_vp, C.c_int, _dp, C.POINTER(C.c_long), _dp]
         L.isdc_build_tables.argtypes = [C.c_int, _dp, _dp, _dp, _dp]
         L.isdc_coarse_inverse.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, _dp]
         _lib = L
@@ -96,7 +99,11 @@ def lib():
 EXPORTED = ["isdc_workspace_bytes", "isdc_create", "isdc_set_initial", "isdc_set_initial_host", "isdc_sweep",
             "isdc_step", "isdc_run", "mg_vcycle", "residual_norm", "isdc_get_solution",
             "isdc_get_solution_host", "isdc_set_state", "isdc_get_tables", "isdc_rhs", "isdc_kernel_launches",
-            "isdc_destroy", "isdc_last_error", "isdc_status_string"]
+            "isdc_destroy", "isdc_last_error", "isdc_status_string", "isdc_profile_enable", "isdc_profile_reset",
+            "isdc_profile_get"]
+
+PROFILE_CLASSES = {0: "fine_smoother", 1: "fine_defect_restrict", 2: "fine_prolong_correct", 3: "rhs", 4: "residual",
+                   5: "coarse_levels"}
 
 
 def _np_ptr(a: np.ndarray):
@@ -254,6 +261,22 @@ class ISDC:
         arr = (_vp * self.M)(*[t.data_ptr() for t in ts])
         self.set_initial(un, step_index)
         self._check(self.L.isdc_rhs(self.h, m, arr, un.data_ptr(), out.data_ptr()))
+        return out
+
+    def profile(self, level: int = 1):
+        """0 off, 1 time the fine-level smoother only (bench's timed region), 2 time every class."""
+        self._check(self.L.isdc_profile_enable(self.h, int(level)))
+
+    def profile_reset(self):
+        self._check(self.L.isdc_profile_reset(self.h))
+
+    def profile_get(self):
+        """{class: (total_ms, launches, algorithmic_bytes)} accumulated since the last reset."""
+        out = {}
+        for cls, name in PROFILE_CLASSES.items():
+            ms, n, by = C.c_double(0), C.c_long(0), C.c_double(0)
+            self._check(self.L.isdc_profile_get(self.h, cls, C.byref(ms), C.byref(n), C.byref(by)))
+            out[name] = (ms.value, n.value, by.value)
         return out
 
     @property
