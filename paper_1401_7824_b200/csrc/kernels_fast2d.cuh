@@ -9,13 +9,13 @@ namespace f2d {
 
 // ---------------------------------------------------------------------------------------------
 // Fused two-sweep weighted Jacobi (one HBM pass: read u, b; write u''), DESIGN.md §6.1.
-// Tile: 64 x 32 outputs per CTA, 128 threads (4 warps).  Smem: u box 68x36 at (x0-2, y0-2),
+// Tile: 64 x 32 outputs per CTA, 256 threads (8 warps).  Smem: u box 68x36 at (x0-2, y0-2),
 // b box 68x34 at (x0-2, y0-1) (TMA, zero fill outside the domain), t = first sweep on the
-// 66x34 region at (x0-1, y0-1) (zero outside the domain).  Thread (lane, warp) owns tile
-// columns lane and lane+32 and rolls a 3-row window down its warp's band of rows.
+// 66x34 region at (x0-1, y0-1) (zero outside the domain).  Warp w owns the 32-column half
+// (w & 1) of a band of rows (w >> 1); each lane rolls a 3-row register window down its column.
 // Optional: NORM -> ||b - S u||_inf over the tile (the SDC defect test of the incoming iterate).
 // ---------------------------------------------------------------------------------------------
-constexpr int TX = 64, TY = 32, NT = 128;
+constexpr int TX = 64, TY = 32, NT = 256;
 constexpr int UW = TX + 4, UH = TY + 4;
 constexpr int BW = TX + 4, BH = TY + 2;
 constexpr int TW = TX + 2, TH = TY + 2;
@@ -51,11 +51,11 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
 
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
     double dmax = 0.0;
-    // ---- sweep 1, main columns 0..63 of the t region (rows -1..32, warp bands of 9 rows)
+    // ---- sweep 1, main columns 0..63 of the t region (rows -1..32, 4 bands of 9 rows)
     {
-        const int rs = -1 + 9 * w, re = min(rs + 9, TY + 1);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        const int band = w >> 1, hh = w & 1;
+        const int rs = -1 + 9 * band, re = min(rs + 9, TY + 1);
+        {
             const int x = lane + 32 * hh;          // tile column; u smem col x+2
             const int gx = x0 + x;
             const bool xin = gx < n;
@@ -100,11 +100,11 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
     }
     if (NORM) block_max_to(slot, dmax);  // contains a __syncthreads
     __syncthreads();
-    // ---- sweep 2 on the 64 x 32 tile (warp bands of 8 rows)
+    // ---- sweep 2 on the 64 x 32 tile (4 bands of 8 rows)
     {
-        const int rs = 8 * w, re = rs + 8;
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        const int band = w >> 1, hh = w & 1;
+        const int rs = 8 * band, re = rs + 8;
+        {
             const int x = lane + 32 * hh;          // t smem col x+1
             const int gx = x0 + x;
             double tm = S.t[rs][x + 1];             // row rs-1
@@ -165,17 +165,34 @@ __global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtens
     }
     mbar_wait(&S.bar, 0);
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2;
-    // defect on the (2RCX+1) x (2RCY+1) fine region; d(x,y) with u smem (x+2, y+1)
-    for (int p = tid; p < RDW * RDH; p += RNT) {
-        const int x = p % RDW, y = p / RDW;
-        const int cx = x + 2, cy = y + 1;
-        double r_m = S.u[cy - 1][cx - 1] + S.u[cy - 1][cx + 1];
-        double r_c = S.u[cy][cx - 1] + S.u[cy][cx + 1];
-        double r_p = S.u[cy + 1][cx - 1] + S.u[cy + 1][cx + 1];
-        double f = r_c + (S.u[cy - 1][cx] + S.u[cy + 1][cx]);
-        double e = r_m + r_p;
-        double su = (c0 * S.u[cy][cx] + c1 * f) + c2 * e;
-        S.d[y][x] = S.b[y][x + 2] - su;   // outside the fine domain only feeds coarse points we skip
+    // defect on the (2RCX+1) x (2RCY+1) fine region; d(x,y) with u smem (x+2, y+1).
+    // Columns 0..63: warp w owns column half (w & 1) of row band (w >> 1) (4 bands of <= 9 rows)
+    // with a rolling 3-row register window; column 64 by threads 0..32 directly.
+    {
+        const int lane = tid & 31, w = tid >> 5;
+        const int band = w >> 1, hh = w & 1;
+        const int rs = 9 * band, re = min(rs + 9, RDH);
+        const int x = lane + 32 * hh, cx = x + 2;
+        double um = S.u[rs][cx], rm = S.u[rs][cx - 1] + S.u[rs][cx + 1];           // row rs-1
+        double uc = S.u[rs + 1][cx], rc = S.u[rs + 1][cx - 1] + S.u[rs + 1][cx + 1];
+        for (int y = rs; y < re; ++y) {
+            double up = S.u[y + 2][cx], rp = S.u[y + 2][cx - 1] + S.u[y + 2][cx + 1];
+            double f = rc + (um + up);
+            double e = rm + rp;
+            double su = (c0 * uc + c1 * f) + c2 * e;
+            S.d[y][x] = S.b[y][x + 2] - su;
+            um = uc; uc = up; rm = rc; rc = rp;
+        }
+        if (tid < RDH) {
+            const int y = tid, xx = RDW - 1, cxx = xx + 2, cy = y + 1;
+            double r_m = S.u[cy - 1][cxx - 1] + S.u[cy - 1][cxx + 1];
+            double r_c = S.u[cy][cxx - 1] + S.u[cy][cxx + 1];
+            double r_p = S.u[cy + 1][cxx - 1] + S.u[cy + 1][cxx + 1];
+            double f = r_c + (S.u[cy - 1][cxx] + S.u[cy + 1][cxx]);
+            double e = r_m + r_p;
+            double su = (c0 * S.u[cy][cxx] + c1 * f) + c2 * e;
+            S.d[y][xx] = S.b[y][xx + 2] - su;
+        }
     }
     __syncthreads();
     for (int p = tid; p < RCX * RCY; p += RNT) {
