@@ -15,6 +15,7 @@
 #include "../../include/isdc.h"
 #include "kernels_generic.cuh"
 #include "kernels_fast2d.cuh"
+#include "kernels_fast3d.cuh"
 #include "kernels_tail.cuh"
 #include "tables.h"
 
@@ -46,6 +47,8 @@ struct isdc_ctx {
     bool spread = true;        // latest iterate is the spread state u_j = u_0 (no copies made)
     double *T = nullptr, *Bf = nullptr, *V = nullptr, *W = nullptr;  // fine scratch
     double *Gp = nullptr;      // forcing profile (pitched)
+    double *Fs[2][ISDC_MAXM];  // stored f^E(u_j) per iterate set (3D CD4 fast path), Fs[*][0] shared
+    double *FT = nullptr;      // f^E of the isdc_rhs staging buffer T
     double *Ginv = nullptr;    // (M-1) coarse inverses, P x P each
     unsigned long long *red = nullptr;  // reduction slots
     int step_index = 0;
@@ -54,6 +57,8 @@ struct isdc_ctx {
     std::map<std::tuple<const void *, int, int, int>, CUtensorMap> tmaps;  // TMA descriptors by (buffer, box)
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
+    int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
     TailParams tailp[ISDC_MAXM];
     size_t tail_smem = 0;
@@ -186,6 +191,19 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     double *T = (double *)take(fe), *Bf = (double *)take(fe), *V = (double *)take(fe), *W = (double *)take(fe);
     double *Gp = (p->fe == ISDC_FE_FORCING) ? (double *)take(fe) : nullptr;
     if (h) { h->T = T; h->Bf = Bf; h->V = V; h->W = W; h->Gp = Gp; }
+    // stored f^E fields for the 3D CD4 fast path: shared F_0, two sets of M-1, staging scratch
+    if (h) { for (int s_ = 0; s_ < 2; ++s_) for (int j = 0; j < ISDC_MAXM; ++j) h->Fs[s_][j] = nullptr; }
+    if (d == 3 && p->fe == ISDC_FE_ADVECTION_CD4) {
+        double *f0 = (double *)take(fe);
+        if (h) h->Fs[0][0] = h->Fs[1][0] = f0;
+        for (int s_ = 0; s_ < 2; ++s_)
+            for (int j = 1; j < M; ++j) {
+                double *f = (double *)take(fe);
+                if (h) h->Fs[s_][j] = f;
+            }
+        double *ft = (double *)take(fe);
+        if (h) h->FT = ft;
+    }
     // coarse levels
     int nl = 0;
     for (int m = n; m >= 3; m = (m - 1) / 2) ++nl;
@@ -277,6 +295,41 @@ const CUtensorMap *tmap(isdc_ctx *h, const double *base, const GridDesc &g, int 
 }
 
 bool use_fast2d(const isdc_ctx *h, int level) { return h->fast && h->d == 2 && h->lev[level].g.n >= 63; }
+bool use_fast3d(const isdc_ctx *h, int level, int kind = 1) {
+    return h->fast && h->d == 3 && h->lev[level].g.n >= 31 && (h->fast3d_mask & kind);
+}
+
+// z-chunk length for a z-streaming 3D kernel with `tiles` xy tiles over `planes` output planes, one
+// resident CTA per SM and `halo` extra planes per chunk: minimise waves x (chunk + halo)
+int pick_chunk(const isdc_ctx *h, int tiles, int planes, int halo) {
+    int best = planes, bestc = 0;
+    long long bestcost = -1;
+    for (int zc = 8; zc <= planes + 7; zc += 4) {
+        int chunks = (planes + zc - 1) / zc;
+        int zc_eff = (planes + chunks - 1) / chunks;     // balanced chunk length
+        if (chunks == bestc) continue;
+        long long waves = ((long long)tiles * chunks + h->nsm - 1) / h->nsm;
+        long long cost = waves * (zc_eff + halo);
+        if (bestcost < 0 || cost < bestcost) { bestcost = cost; best = zc_eff; bestc = chunks; }
+    }
+    return best;
+}
+
+isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
+                              const SCoef &c, int level) {
+    const CUtensorMap *mu = tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1);
+    const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, f3d::S_BH, 1);
+    if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    ++h->launches;
+    int pe = prof_begin(h, level == 0 ? PROF_SMOOTH : PROF_COARSE);
+    int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + f3d::S_TY - 1) / f3d::S_TY;
+    int zc = pick_chunk(h, tx * ty, g.n, 4);
+    dim3 grd(tx, ty, (g.n + zc - 1) / zc);
+    f3d::k_smooth2<<<grd, f3d::NT, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
+    prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
 
 // two fused Jacobi sweeps on the fine 2D level
 isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
@@ -291,6 +344,64 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
     if (norm_slot) f2d::k_smooth2<true><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, norm_slot);
     else f2d::k_smooth2<false><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr);
     prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+// f^E(u) (CD4 advection) into a stored field (3D fast path), DESIGN.md §6.11
+bool need_F(const isdc_ctx *h) {
+    return h->d == 3 && h->fe.kind == 3 && (use_fast3d(h, 0, 8) || use_fast3d(h, 0, 16));
+}
+isdc_status launch_fe(isdc_ctx *h, double *F, const double *u) {
+    if (!need_F(h)) return ISDC_OK;
+    const GridDesc &g = h->lev[0].g;
+    const CUtensorMap *mu = tmap(h, u, g, f3d::FE_W, f3d::FE_H, 1);
+    if (!mu) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    ++h->launches;
+    int pe = prof_begin(h, PROF_RHS);
+    int tx = (g.n + f3d::RW - 1) / f3d::RW, ty = (g.n + f3d::RH - 1) / f3d::RH;
+    int zc = pick_chunk(h, tx * ty, g.n, 4);
+    dim3 grd(tx, ty, (g.n + zc - 1) / zc);
+    f3d::k_fe_cd4<<<grd, f3d::NT, f3d::FE_SMEM, h->s>>>(*mu, F, g.n, g.pitch, g.plane, h->fe.kx, h->fe.ky, h->fe.kz, zc);
+    prof_end(h, pe, PROF_RHS, 0.0);   // implementation traffic, not in the algorithmic bytes
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+constexpr int kMaxDynSmem = 232448 - 1024;   // 227 KB opt-in per CTA on sm_100, less static shared memory
+
+// B a +- L c streaming kernel (3D RHS / residual), DESIGN.md §6.10.  fields[k] are pitched level-0
+// fields; picks the region height (RR) and pipeline depth that fit shared memory.
+template <int MODE>
+isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, f3d::BLArgs A, int prof_cls, double bytes) {
+    const GridDesc &g = h->lev[0].g;
+    int rr = 4, ns = 3;
+    while (ns >= 2 && f3d::BLShape<4>::smem(K, ns) > (size_t)kMaxDynSmem) --ns;
+    if (ns < 3) { rr = 2; ns = 4; while (ns >= 2 && f3d::BLShape<2>::smem(K, ns) > (size_t)kMaxDynSmem) --ns; }
+    if (ns < 2) { h->err = "too many fields for the 3D stream kernel"; return ISDC_ERR_UNSUPPORTED; }
+    int rh = f3d::NW * rr;
+    f3d::BLMaps maps;
+    for (int k = 0; k < K; ++k) {
+        const CUtensorMap *mk = tmap(h, fields[k], g, f3d::RW + 2, rh, 1);
+        if (!mk) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+        maps.m[k] = *mk;
+    }
+    A.K = K; A.n = g.n; A.pitch = g.pitch; A.plane = g.plane; A.bl = h->bl; A.ct = h->ctdev;
+    int tx = (g.n + f3d::RW - 3) / (f3d::RW - 2), ty = (g.n + rh - 3) / (rh - 2);
+    A.zc = pick_chunk(h, tx * ty, g.n, 2);
+    dim3 grd(tx, ty, (g.n + A.zc - 1) / A.zc);
+    size_t sm = (rr == 4) ? f3d::BLShape<4>::smem(K, ns) : f3d::BLShape<2>::smem(K, ns);
+    ++h->launches;
+    int pe = prof_begin(h, prof_cls);
+    int fe = h->fe.kind;
+#define ISDC_BL(FE_, RR_) f3d::k_bl<FE_, MODE, RR_><<<grd, f3d::NT, sm, h->s>>>(maps, A, ns)
+    if (rr == 4) {
+        if (fe == 0) ISDC_BL(0, 4); else if (fe == 1) ISDC_BL(1, 4); else if (fe == 2) ISDC_BL(2, 4); else ISDC_BL(3, 4);
+    } else {
+        if (fe == 0) ISDC_BL(0, 2); else if (fe == 1) ISDC_BL(1, 2); else if (fe == 2) ISDC_BL(2, 2); else ISDC_BL(3, 2);
+    }
+#undef ISDC_BL
+    prof_end(h, pe, prof_cls, bytes);
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -326,6 +437,14 @@ isdc_status launch_restrict(isdc_ctx *h, double *bc, const GridDesc &gc, const d
         dim3 grd((gc.n + f2d::RCX - 1) / f2d::RCX, (gc.n + f2d::RCY - 1) / f2d::RCY);
         f2d::k_restrict<<<grd, f2d::RNT, sizeof(f2d::SmemRestrict) + 128, h->s>>>(*mu, *mb, bc, gf.n, gc.n,
                                                                                      gc.pitch, c);
+    } else if (use_fast3d(h, level, 2)) {
+        const CUtensorMap *mu = tmap(h, u, gf, f3d::R_UW, f3d::R_UH, 1);
+        const CUtensorMap *mb = tmap(h, b, gf, f3d::R_BW, f3d::R_BH, 1);
+        if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+        int tx = (gc.n + f3d::R_CX - 1) / f3d::R_CX, ty = (gc.n + f3d::R_CY - 1) / f3d::R_CY;
+        int kc = pick_chunk(h, tx * ty, gc.n, 2);
+        dim3 grd(tx, ty, (gc.n + kc - 1) / kc);
+        f3d::k_restrict<<<grd, f3d::NT, f3d::R_SMEM, h->s>>>(*mu, *mb, bc, gf.n, gc.n, gc.pitch, gc.plane, c, kc);
     } else if (h->d == 2) k_restrict_defect<2><<<point_grid<2>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
     else k_restrict_defect<3><<<point_grid<3>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
     prof_end(h, pe, level == 0 ? PROF_RESTRICT : PROF_COARSE, 16.0 * npts_of(h, gf) + 8.0 * npts_of(h, gc));
@@ -340,6 +459,9 @@ isdc_status launch_prolong(isdc_ctx *h, double *u, const GridDesc &gf, const dou
     if (use_fast2d(h, level)) {
         dim3 grd(((gf.n + 1) / 2 + 255) / 256, gf.n);
         f2d::k_prolong<<<grd, 256, 0, h->s>>>(u, gf.n, gf.pitch, e, gc.n, gc.pitch);
+    } else if (use_fast3d(h, level, 4)) {
+        dim3 grd(((gf.n + 1) / 2 + 255) / 256, gf.n, gf.n);
+        f3d::k_prolong<<<grd, 256, 0, h->s>>>(u, gf.n, gf.pitch, gf.plane, e, gc.n, gc.pitch, gc.plane);
     } else if (h->d == 2) k_prolong_add<2><<<point_grid<2>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
     else k_prolong_add<3><<<point_grid<3>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
     prof_end(h, pe, level == 0 ? PROF_PROLONG : PROF_COARSE, 16.0 * npts_of(h, gf) + 8.0 * npts_of(h, gc));
@@ -426,6 +548,9 @@ isdc_status smooth(isdc_ctx *h, int l, double *X, double *T, const double *b, co
         if (use_fast2d(h, l) && sweeps >= 2) {
             TRY(launch_smooth2(h, dst, cur, b, g, c, nullptr, l));
             sweeps -= 2;
+        } else if (use_fast3d(h, l) && sweeps >= 2) {
+            TRY(launch_smooth2_3d(h, dst, cur, b, g, c, l));
+            sweeps -= 2;
         } else {
             TRY(launch_jacobi(h, dst, cur, b, g, c, l));
             sweeps -= 1;
@@ -502,7 +627,29 @@ void fill_vw(isdc_ctx *h, VWParams &P, int m, double *const *uold, const double 
 
 bool fast2d_pointwise_fe(const isdc_ctx *h) { return h->fast && h->d == 2 && h->fe.kind <= 2 && h->n >= 63; }
 
-isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_m, double *bout, bool bnorm) {
+isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_m, double *bout, bool bnorm,
+                    double *const *Fold = nullptr, const double *Fnew = nullptr) {
+    if (use_fast3d(h, 0, 8) && (h->fe.kind != 3 || (Fold && Fnew))) {
+        const int M = h->M, fe = h->fe.kind;
+        const double *fields[f3d::BL_MAXF];
+        f3d::BLArgs A;
+        int K = 0;
+        A.iu0 = K; for (int j = 0; j < M; ++j) fields[K++] = uold[j];
+        A.iun = K; fields[K++] = unew_m;
+        A.iuG = A.iF0 = A.iFn = 0;
+        if (fe == 2) { A.iuG = K; fields[K++] = h->Gp; }
+        if (fe == 3) { A.iF0 = K; for (int j = 0; j < M; ++j) fields[K++] = Fold[j]; A.iFn = K; fields[K++] = Fnew; }
+        A.M = M; A.m = m;
+        double dt = h->P.dt, nu = h->P.nu, nudt = nu * dt;
+        A.dtm = dt * h->dtau[m];
+        A.gm = nu * A.dtm;
+        for (int j = 0; j < M; ++j) { A.a[j] = dt * h->S[m * M + j]; A.beta[j] = nudt * h->S[m * M + j]; }
+        A.out = bout;
+        A.slot = nullptr;
+        if (bnorm) { TRY(clear_slots(h, SLOT_BNORM, 1)); A.slot = h->red + SLOT_BNORM; }
+        // algorithmic bytes: the M + 1 node fields (+G) read and b written
+        return launch_bl<0>(h, fields, K, A, PROF_RHS, (M + 2 + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, h->lev[0].g));
+    }
     if (fast2d_pointwise_fe(h)) {
         f2d::RhsArgs A;
         for (int j = 0; j < h->M; ++j) A.uold[j] = uold[j];
@@ -554,10 +701,30 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
 }
 
 // residual of node fields u[0..M-1]: enqueue the kernels (slots SLOT_RES0..), then read them
-isdc_status enqueue_residual(isdc_ctx *h, double *const *u) {
+isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = nullptr) {
     const GridDesc &g = h->lev[0].g;
     int M = h->M;
     TRY(clear_slots(h, SLOT_RES0, M - 1));
+    if (use_fast3d(h, 0, 16) && (h->fe.kind != 3 || F)) {
+        const int fe = h->fe.kind;
+        const double *fields[f3d::BL_MAXF];
+        f3d::BLArgs A;
+        int K = 0;
+        A.iu0 = K; for (int j = 0; j < M; ++j) fields[K++] = u[j];
+        A.iun = A.iuG = A.iF0 = A.iFn = 0;
+        if (fe == 2) { A.iuG = K; fields[K++] = h->Gp; }
+        if (fe == 3) { A.iF0 = K; for (int j = 0; j < M; ++j) fields[K++] = F[j]; }
+        A.M = M; A.dtm = A.gm = 0.0; A.out = nullptr;
+        double dt = h->P.dt, nudt = h->P.nu * dt;
+        for (int m = 1; m < M; ++m) {
+            A.m = m;
+            for (int j = 0; j < M; ++j) { A.a[j] = dt * h->Q[m * M + j]; A.beta[j] = nudt * h->Q[m * M + j]; }
+            A.slot = h->red + SLOT_RES0 + m - 1;
+            // algorithmic bytes of the whole residual: M node fields (+G) once, spread over the M-1 launches
+            TRY(launch_bl<1>(h, fields, K, A, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g) / (M - 1)));
+        }
+        return ISDC_OK;
+    }
     if (fast2d_pointwise_fe(h)) {
         f2d::ResArgs A;
         for (int j = 0; j < M; ++j) A.u[j] = u[j];
@@ -655,8 +822,9 @@ isdc_status node_solve(isdc_ctx *h, int m, double *X, const double *src, int *cy
     return ISDC_OK;
 }
 
-isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double *maxn) {
-    TRY(enqueue_residual(h, u));
+isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double *maxn,
+                         double *const *F = nullptr) {
+    TRY(enqueue_residual(h, u, F));
     return read_residual(h, per_node, maxn);
 }
 
@@ -667,15 +835,19 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
     int nw = 1 - h->cur;
     for (int j = 0; j < M; ++j) uold[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
     double **unew = h->U[nw];
+    double *Fold[ISDC_MAXM];
+    for (int j = 0; j < M; ++j) Fold[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
+    double **Fnew = h->Fs[nw];
     for (int m = 0; m + 1 < M; ++m) {
-        TRY(run_rhs(h, m, uold, unew[m], h->Bf, false));
+        TRY(run_rhs(h, m, uold, unew[m], h->Bf, false, Fold, Fnew[m]));
         const double *src;
         if (h->P.solve.guess == 1) { TRY(zero_field(h, unew[m + 1], h->lev[0].g)); src = nullptr; }
         else if (h->P.solve.guess == 2) src = unew[m];
         else src = uold[m + 1];
         for (int l = 0; l < h->P.solve.L; ++l) TRY(vcycle(h, 0, m, unew[m + 1], h->T, h->Bf, l == 0 ? src : nullptr));
+        TRY(launch_fe(h, Fnew[m + 1], unew[m + 1]));
     }
-    return enqueue_residual(h, unew);
+    return enqueue_residual(h, unew, Fnew);
 }
 
 isdc_status graph_sweep(isdc_ctx *h) {
@@ -736,10 +908,13 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
     int nw = 1 - h->cur;
     for (int j = 0; j < M; ++j) uold[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
     double **unew = h->U[nw];
+    double *Fold[ISDC_MAXM];
+    for (int j = 0; j < M; ++j) Fold[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
+    double **Fnew = h->Fs[nw];
     int caps = 0;
     bool sdc = h->P.solve.mode == ISDC_MODE_SDC_TOL;
     for (int m = 0; m + 1 < M; ++m) {
-        TRY(run_rhs(h, m, uold, unew[m], h->Bf, sdc));
+        TRY(run_rhs(h, m, uold, unew[m], h->Bf, sdc, Fold, Fnew[m]));
         const double *src;
         const GridDesc &g = h->lev[0].g;
         if (h->P.solve.guess == 1) { TRY(zero_field(h, unew[m + 1], g)); src = nullptr; }
@@ -747,13 +922,14 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
         else src = uold[m + 1];
         int cyc, cap;
         TRY(node_solve(h, m, unew[m + 1], src, &cyc, &cap));
+        TRY(launch_fe(h, Fnew[m + 1], unew[m + 1]));
         caps += cap;
         if (cycles) cycles[m] = cyc;
     }
     h->cur = nw;
     h->spread = false;
     if (cap_hits) *cap_hits = caps;
-    return run_residual(h, h->U[h->cur], res_per_node, res_max);
+    return run_residual(h, h->U[h->cur], res_per_node, res_max, h->Fs[h->cur]);
 }
 
 }  // namespace
@@ -806,6 +982,13 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     const char *env = getenv("ISDC_GENERIC_KERNELS");
     h->fast = !(env && env[0] == '1');
     if (h->fast && !tma_encoder()) h->fast = false;
+    if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
+    {
+        int dev = 0, nsm = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+            h->nsm = nsm;
+    }
     static bool attrs = false;
     if (!attrs) {
         cudaFuncSetAttribute(f2d::k_smooth2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -814,6 +997,16 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSmooth) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
+        cudaFuncSetAttribute(f3d::k_smooth2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::R_SMEM);
+        cudaFuncSetAttribute(f3d::k_fe_cd4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::FE_SMEM);
+#define ISDC_BL_ATTR(FE_, MODE_, RR_) \
+        cudaFuncSetAttribute(f3d::k_bl<FE_, MODE_, RR_>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+        ISDC_BL_ATTR(0, 0, 4) ISDC_BL_ATTR(1, 0, 4) ISDC_BL_ATTR(2, 0, 4) ISDC_BL_ATTR(3, 0, 4)
+        ISDC_BL_ATTR(0, 1, 4) ISDC_BL_ATTR(1, 1, 4) ISDC_BL_ATTR(2, 1, 4) ISDC_BL_ATTR(3, 1, 4)
+        ISDC_BL_ATTR(0, 0, 2) ISDC_BL_ATTR(1, 0, 2) ISDC_BL_ATTR(2, 0, 2) ISDC_BL_ATTR(3, 0, 2)
+        ISDC_BL_ATTR(0, 1, 2) ISDC_BL_ATTR(1, 1, 2) ISDC_BL_ATTR(2, 1, 2) ISDC_BL_ATTR(3, 1, 2)
+#undef ISDC_BL_ATTR
         int rs = 2 * (ISDC_MAXM - 1) * f2d::ZH * f2d::ZW * (int)sizeof(double);
         cudaFuncSetAttribute(f2d::k_resid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
         cudaFuncSetAttribute(f2d::k_resid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
@@ -906,6 +1099,7 @@ long isdc_kernel_launches(isdc_handle h) { return h ? h->launches : 0; }
 isdc_status isdc_set_initial(isdc_handle h, const double *u0, int step_index) {
     if (!h || !u0) return ISDC_ERR_INVALID_ARG;
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyDeviceToDevice));
+    TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
     h->cur = 0; h->spread = true; h->step_index = step_index;
     return upload_ct(h);
 }
@@ -913,13 +1107,17 @@ isdc_status isdc_set_initial(isdc_handle h, const double *u0, int step_index) {
 isdc_status isdc_set_initial_host(isdc_handle h, const double *u0, int step_index) {
     if (!h || !u0) return ISDC_ERR_INVALID_ARG;
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyHostToDevice));
+    TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
     h->cur = 0; h->spread = true; h->step_index = step_index;
     return upload_ct(h);
 }
 
 isdc_status isdc_set_state(isdc_handle h, const double *const *u, int step_index) {
     if (!h || !u) return ISDC_ERR_INVALID_ARG;
-    for (int j = 0; j < h->M; ++j) TRY(dense_to_pitched(h, h->U[0][j], u[j], cudaMemcpyDeviceToDevice));
+    for (int j = 0; j < h->M; ++j) {
+        TRY(dense_to_pitched(h, h->U[0][j], u[j], cudaMemcpyDeviceToDevice));
+        TRY(launch_fe(h, h->Fs[0][j], h->U[0][j]));
+    }
     h->cur = 0; h->spread = false; h->step_index = step_index;
     return upload_ct(h);
 }
@@ -977,6 +1175,7 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     if (o.fixed_sweeps > 0) conv = 1;
     // u_0 <- u_M (Lobatto end node), next step starts from the spread state
     TRY(copy_field(h, h->U[0][0], h->U[h->cur][h->M - 1], h->lev[0].g));
+    if (need_F(h)) TRY(copy_field(h, h->Fs[0][0], h->Fs[h->cur][h->M - 1], h->lev[0].g));
     h->cur = 0;
     h->spread = true;
     h->step_index += 1;
@@ -1019,9 +1218,12 @@ isdc_status mg_vcycle(isdc_handle h, int node_m, const double *b, double *u, dou
 
 isdc_status residual_norm(isdc_handle h, double *per_node, double *max_norm) {
     if (!h) return ISDC_ERR_INVALID_ARG;
-    double *u[ISDC_MAXM];
-    for (int j = 0; j < h->M; ++j) u[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
-    return run_residual(h, u, per_node, max_norm);
+    double *u[ISDC_MAXM], *F[ISDC_MAXM];
+    for (int j = 0; j < h->M; ++j) {
+        u[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
+        F[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
+    }
+    return run_residual(h, u, per_node, max_norm, F);
 }
 
 isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold, const double *unew_m, double *b) {
@@ -1034,7 +1236,13 @@ isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold, const
         TRY(dense_to_pitched(h, uo[j], uold[j], cudaMemcpyDeviceToDevice));
     }
     TRY(dense_to_pitched(h, h->U[0][1], unew_m, cudaMemcpyDeviceToDevice));
-    TRY(run_rhs(h, node_m, uo, h->U[0][1], h->Bf, false));
+    double *Fo[ISDC_MAXM];
+    for (int j = 0; j < M; ++j) {
+        Fo[j] = (j == 0) ? h->FT : h->Fs[1][j];
+        TRY(launch_fe(h, Fo[j], uo[j]));
+    }
+    TRY(launch_fe(h, h->Fs[0][1], h->U[0][1]));
+    TRY(run_rhs(h, node_m, uo, h->U[0][1], h->Bf, false, Fo, h->Fs[0][1]));
     TRY(pitched_to_dense(h, b, h->Bf, cudaMemcpyDeviceToDevice));
     CUDA_TRY(h, cudaStreamSynchronize(h->s));
     h->spread = true;  // the staged data overwrote the iterate sets

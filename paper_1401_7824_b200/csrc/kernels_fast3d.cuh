@@ -1,0 +1,628 @@
+// kernels_fast3d.cuh -- tuned 3D kernels (sm_100a) for the levels n >= 31: 2.5D z-streaming with
+// TMA-loaded xy planes (3D tensor maps, zero fill outside the domain = the Dirichlet data), a
+// register ring in z per owned point and a 6-row register window in y, so every 19-point
+// application costs 18 shared loads per 4 points.  Every value is produced by the canonical
+// trees of DESIGN.md §4 in the same order as the generic kernels (bit-identical results):
+//   r = q(x-1) + q(x+1);  f = r + (q(y-1) + q(y+1));  e = r(y-1) + r(y+1)
+//   faces = f(z) + (q(z-1) + q(z+1));  edges = e(z) + (f(z-1) + f(z+1))
+//   S u = (c0 u + c1 faces) + c2 edges;  Jacobi u + wd (b - S u)
+//
+// Thread layout shared by the streaming kernels: 8 warps, lane = column of a 32-wide region,
+// warp w owns rows 4w..4w+3 of a 32-row region.
+// TMA boxes must start at an even x (16-byte aligned global start of every row), so boxes that
+// need an odd left halo start one column further left.
+#pragma once
+#include "common.cuh"
+#include "tma.cuh"
+#include <type_traits>
+
+namespace f3d {
+
+constexpr int NW = 8;            // warps per CTA
+constexpr int NT = NW * 32;      // threads per CTA
+constexpr int R = 4;             // rows per thread
+constexpr int RW = 32;           // region width (one lane per column)
+constexpr int RH = NW * R;       // region height
+
+__host__ __device__ constexpr int a128(int b) { return (b + 127) / 128 * 128; }
+
+// In-plane partial sums of the R owned rows from a plane in shared memory (row stride `ld`):
+// window rows row0 .. row0+R+1 (centre rows row0+1 .. row0+R), columns col0 .. col0+2 (centre
+// col0+1).  q = centre value, f = face sum, e = edge sum, all in the canonical order.
+template <bool WANT_E, int RR = R>
+__device__ __forceinline__ void plane_partials(const double *__restrict__ P, int ld, int row0, int col0, double (&q)[RR],
+                                               double (&f)[RR], double (&e)[RR]) {
+    double v0[RR + 2], v1[RR + 2], v2[RR + 2];
+#pragma unroll
+    for (int k = 0; k < RR + 2; ++k) {
+        const double *row = P + (row0 + k) * ld + col0;
+        v0[k] = row[0];
+        v1[k] = row[1];
+        v2[k] = row[2];
+    }
+    double rr[RR + 2];
+#pragma unroll
+    for (int k = 0; k < RR + 2; ++k) rr[k] = v0[k] + v2[k];
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+        q[r] = v1[r + 1];
+        f[r] = rr[r + 1] + (v1[r] + v1[r + 2]);
+        if (WANT_E) e[r] = rr[r] + rr[r + 2];
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused two-sweep weighted Jacobi, one HBM pass (read u, b; write u''), DESIGN.md §6.7.
+// Output tile 30 x 30 (x, y) x a z chunk [z0, z1).  Sweep 1 runs on the 32 x 32 region
+// (tile + 1 halo) at plane p-1 while u plane p is ingested; its result t goes to a shared plane;
+// sweep 2 runs on the tile at plane p-2 from t's register ring and the t plane's neighbours.
+// u box 34 x 34 at (x0-2, y0-2); b box 34 x 32 at (x0-2, y0-1); t plane 34 x 34 (pad ring).
+// ---------------------------------------------------------------------------------------------
+constexpr int S_TX = RW - 2, S_TY = RH - 2;
+constexpr int S_UW = RW + 2, S_UH = RH + 2;
+constexpr int S_BW = RW + 2, S_BH = RH;
+constexpr int S_TW = RW + 2, S_TH = RH + 2;
+constexpr int S_NS = 6;          // TMA pipeline depth (planes in flight)
+constexpr int S_UPL = a128(S_UW * S_UH * 8), S_BPL = a128(S_BW * S_BH * 8), S_TPL = a128(S_TW * S_TH * 8);
+constexpr size_t S_SMEM = (size_t)S_NS * (S_UPL + S_BPL) + 2 * S_TPL + 8 * S_NS + 128;
+
+// Register state of one thread (R owned points).  Rings are indexed by the iteration that
+// produced the value (mod 3 for centre/face sums, mod 2 for edge sums and b), so after unrolling
+// the z loop by 6 every index is a compile-time constant and no value is ever moved.
+struct SmoothRegs {
+    double q[3][R], f[3][R], e[2][R];      // u(p): centre, face, edge partials
+    double tq[3][R], tf[3][R], te[2][R];   // t(p-1) (first sweep), same partials
+    double bb[2][R];                       // b(p-1)
+};
+
+struct SmoothCtx {
+    const double *Us, *Bs;
+    double *Ts;
+    uint64_t *bar;
+    double *optr;
+    long long plane;
+    int pitch, n, w, lane, z0, nit;
+    bool xin, xout, yin[R], yout[R];
+    double c0, c1, c2, wd;
+};
+
+template <int K>   // K = it % 6
+__device__ __forceinline__ void smooth_step(const SmoothCtx &C, SmoothRegs &G, int it) {
+    constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3;   // it, it-1, it-2 (mod 3)
+    constexpr int i2 = K % 2, m2 = (K + 1) % 2;                       // it, it-1 (mod 2)
+    const int s = it % S_NS, p = C.z0 - 2 + it;
+    mbar_wait(&C.bar[s], (it / S_NS) & 1);
+    plane_partials<true>(C.Us + s * (S_UPL / 8), S_UW, R * C.w, C.lane, G.q[i3], G.f[i3], G.e[i2]);
+    double *T = C.Ts + i2 * (S_TPL / 8);
+    if (it >= 2) {   // sweep 1 at plane p-1 on the 32 x 32 region
+        const int gz = p - 1;
+        const bool zin = gz >= 0 && gz < C.n;
+        const double *Bp = C.Bs + s * (S_BPL / 8);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double faces = G.f[m3][r] + (G.q[mm3][r] + G.q[i3][r]);
+            const double edges = G.e[m2][r] + (G.f[mm3][r] + G.f[i3][r]);
+            const double su = (C.c0 * G.q[m3][r] + C.c1 * faces) + C.c2 * edges;
+            const double bv = Bp[(R * C.w + r) * S_BW + C.lane + 1];
+            const double t = (C.xin && C.yin[r] && zin) ? G.q[m3][r] + C.wd * (bv - su) : 0.0;
+            T[(R * C.w + r + 1) * S_TW + C.lane + 1] = t;
+            G.bb[i2][r] = bv;
+        }
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void smooth_step2(const SmoothCtx &C, SmoothRegs &G, int it) {
+    constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3;
+    constexpr int i2 = K % 2, m2 = (K + 1) % 2;
+    if (it < 2) return;
+    const double *T = C.Ts + i2 * (S_TPL / 8);
+    plane_partials<true>(T, S_TW, R * C.w, C.lane, G.tq[i3], G.tf[i3], G.te[i2]);
+    if (it >= 4) {   // sweep 2 at plane p-2 on the 30 x 30 tile
+        const int gz = C.z0 - 4 + it;
+        double *op = C.optr + (long long)gz * C.plane;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double faces = G.tf[m3][r] + (G.tq[mm3][r] + G.tq[i3][r]);
+            const double edges = G.te[m2][r] + (G.tf[mm3][r] + G.tf[i3][r]);
+            const double su = (C.c0 * G.tq[m3][r] + C.c1 * faces) + C.c2 * edges;
+            const double o = G.tq[m3][r] + C.wd * (G.bb[m2][r] - su);
+            if (C.xout && C.yout[r]) op[(long long)r * C.pitch] = o;
+        }
+    }
+}
+
+// u box 34 x 34 at (x0-2, y0-2); b box 34 x 32 at (x0-2, y0-1); t plane 34 x 34 (pad ring).
+__global__ void __launch_bounds__(NT, 1) k_smooth2(const __grid_constant__ CUtensorMap tu,
+                                                   const __grid_constant__ CUtensorMap tb,
+                                                   double *__restrict__ out, int n, int pitch, long long plane,
+                                                   SCoef c, int zc) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
+    SmoothCtx C;
+    C.Us = reinterpret_cast<const double *>(sm);
+    C.Bs = reinterpret_cast<const double *>(sm + S_NS * S_UPL);
+    C.Ts = reinterpret_cast<double *>(sm + S_NS * (S_UPL + S_BPL));
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S_NS * (S_UPL + S_BPL) + 2 * S_TPL);
+    C.bar = bar;
+    const int tid = threadIdx.x;
+    C.lane = tid & 31; C.w = tid >> 5;
+    const int x0 = blockIdx.x * S_TX, y0 = blockIdx.y * S_TY;
+    const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, n);
+    C.z0 = z0; C.nit = z1 - z0 + 4; C.n = n; C.pitch = pitch; C.plane = plane;
+    double *Usw = reinterpret_cast<double *>(sm), *Bsw = reinterpret_cast<double *>(sm + S_NS * S_UPL);
+    auto issue = [&](int it) {
+        const int s = it % S_NS, p = z0 - 2 + it;
+        mbar_expect_tx(&bar[s], (S_UW * S_UH + S_BW * S_BH) * 8);
+        tma_load_3d(Usw + s * (S_UPL / 8), &tu, x0 - 2, y0 - 2, p, &bar[s]);
+        tma_load_3d(Bsw + s * (S_BPL / 8), &tb, x0 - 2, y0 - 1, p - 1, &bar[s]);
+    };
+    if (tid == 0) {
+        tma_prefetch_desc(&tu);
+        tma_prefetch_desc(&tb);
+        for (int s = 0; s < S_NS; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int it = 0; it < S_NS && it < C.nit; ++it) issue(it);
+
+    C.c0 = c.c0; C.c1 = c.c1; C.c2 = c.c2; C.wd = c.wd;
+    const int lx = C.lane - 1, ly0 = R * C.w - 1;        // region coordinates of the owned points
+    const int gx = x0 + lx;
+    C.xin = gx >= 0 && gx < n;
+    C.xout = lx >= 0 && lx < S_TX && gx < n;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int ly = ly0 + r, gy = y0 + ly;
+        C.yin[r] = gy >= 0 && gy < n;
+        C.yout[r] = ly >= 0 && ly < S_TY && gy < n;
+    }
+    C.optr = out + (long long)(y0 + ly0) * pitch + gx;
+    SmoothRegs G;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int r = 0; r < R; ++r) G.bb[k][r] = 0.0;
+    const int nit = C.nit;
+#define ISDC_SMOOTH_STEP(K)                                            \
+    {                                                                  \
+        const int it = base + (K);                                     \
+        if (it < nit) {                                                \
+            smooth_step<K>(C, G, it);                                  \
+            __syncthreads();                                           \
+            if (tid == 0 && it + S_NS < nit) issue(it + S_NS);         \
+            smooth_step2<K>(C, G, it);                                 \
+        }                                                              \
+    }
+    for (int base = 0; base < nit; base += 6) {
+        ISDC_SMOOTH_STEP(0) ISDC_SMOOTH_STEP(1) ISDC_SMOOTH_STEP(2)
+        ISDC_SMOOTH_STEP(3) ISDC_SMOOTH_STEP(4) ISDC_SMOOTH_STEP(5)
+    }
+#undef ISDC_SMOOTH_STEP
+}
+
+// ---------------------------------------------------------------------------------------------
+// Defect + full-weighting restriction, one HBM pass (read u, b; write b_c), DESIGN.md §6.8.
+// Coarse tile 15 x 15 x a coarse z chunk [K0, K1).  Fine defect region 31 x 31 at
+// (2 I0, 2 J0), streamed over fine planes 2 K0 .. 2 K1; d(z) goes to a shared plane, coarse
+// threads take its in-plane partials (face / edge / centre) and combine three planes.
+// u box 36 x 34 at (2 I0 - 2, 2 J0 - 1); b box 32 x 32 at (2 I0, 2 J0).
+// ---------------------------------------------------------------------------------------------
+constexpr int R_CX = 15, R_CY = 15;
+constexpr int R_UW = RW + 4, R_UH = RH + 2;
+constexpr int R_BW = RW, R_BH = RH;
+constexpr int R_DW = RW, R_DH = RH;
+constexpr int R_NS = 4;
+constexpr int R_UPL = a128(R_UW * R_UH * 8), R_BPL = a128(R_BW * R_BH * 8), R_DPL = a128(R_DW * R_DH * 8);
+constexpr size_t R_SMEM = (size_t)R_NS * (R_UPL + R_BPL) + 2 * R_DPL + 8 * R_NS + 128;
+
+__global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUtensorMap tu,
+                                                    const __grid_constant__ CUtensorMap tb,
+                                                    double *__restrict__ bc, int nf, int nc, int pitch_c,
+                                                    long long plane_c, SCoef c, int kc) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
+    double *Us = reinterpret_cast<double *>(sm);
+    double *Bs = reinterpret_cast<double *>(sm + R_NS * R_UPL);
+    double *Ds = reinterpret_cast<double *>(sm + R_NS * (R_UPL + R_BPL));
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + R_NS * (R_UPL + R_BPL) + 2 * R_DPL);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int I0 = blockIdx.x * R_CX, J0 = blockIdx.y * R_CY;
+    const int K0 = blockIdx.z * kc, K1 = min(K0 + kc, nc);
+    const int fx0 = 2 * I0, fy0 = 2 * J0;
+    const int nit = 2 * (K1 - K0) + 3;     // u planes 2K0-1 .. 2K1+1
+    auto issue = [&](int it) {
+        const int s = it % R_NS, p = 2 * K0 - 1 + it;
+        mbar_expect_tx(&bar[s], (R_UW * R_UH + R_BW * R_BH) * 8);
+        tma_load_3d(Us + s * (R_UPL / 8), &tu, fx0 - 2, fy0 - 1, p, &bar[s]);
+        tma_load_3d(Bs + s * (R_BPL / 8), &tb, fx0, fy0, p - 1, &bar[s]);
+    };
+    if (tid == 0) {
+        tma_prefetch_desc(&tu);
+        tma_prefetch_desc(&tb);
+        for (int s = 0; s < R_NS; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int it = 0; it < R_NS && it < nit; ++it) issue(it);
+
+    const double c0 = c.c0, c1 = c.c1, c2 = c.c2;
+    // coarse role
+    const bool crole = tid < R_CX * R_CY;
+    const int ci = tid % R_CX, cj = tid / R_CX;
+    const int gI = I0 + ci, gJ = J0 + cj;
+    const bool cout_ok = crole && gI < nc && gJ < nc;
+    const int dx = 2 * ci + 1, dy = 2 * cj + 1;
+    double fdl = 0, edl = 0, dcl = 0, fdm = 0, edm = 0, dcm = 0;   // partials at planes 2K (lower), 2K+1 (mid)
+
+    double qa[R], qb[R], fa[R], fb[R], eb[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) qa[r] = qb[r] = fa[r] = fb[r] = eb[r] = 0.0;
+    for (int it = 0; it < nit; ++it) {
+        const int s = it % R_NS;
+        mbar_wait(&bar[s], (it / R_NS) & 1);
+        double qn[R], fn[R], en[R];
+        plane_partials<true>(Us + s * (R_UPL / 8), R_UW, R * w, lane + 1, qn, fn, en);
+        const bool dd = it >= 2;     // defect at fine plane p-1
+        double *D = Ds + (it & 1) * (R_DPL / 8);
+        if (dd) {
+            const double *Bp = Bs + s * (R_BPL / 8);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double faces = fb[r] + (qa[r] + qn[r]);
+                const double edges = eb[r] + (fa[r] + fn[r]);
+                const double su = (c0 * qb[r] + c1 * faces) + c2 * edges;
+                D[(R * w + r) * R_DW + lane] = Bp[(R * w + r) * R_BW + lane] - su;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) { qa[r] = qb[r]; qb[r] = qn[r]; fa[r] = fb[r]; fb[r] = fn[r]; eb[r] = en[r]; }
+        __syncthreads();
+        if (tid == 0 && it + R_NS < nit) issue(it + R_NS);
+        if (dd && crole) {
+            const int j = it - 2;    // fine plane 2K0 + j
+            const double *d0 = D + (dy - 1) * R_DW + dx, *d1 = d0 + R_DW, *d2 = d1 + R_DW;
+            const double rd0 = d0[-1] + d0[1], rd1 = d1[-1] + d1[1], rd2 = d2[-1] + d2[1];
+            const double fd = rd1 + (d0[0] + d2[0]);
+            const double ed = rd0 + rd2;
+            const double dc = d1[0];
+            if (j & 1) {
+                fdm = fd; edm = ed; dcm = dc;
+            } else {
+                if (j >= 2) {
+                    const double F = fdm + (dcl + dc);
+                    const double E = edm + (fdl + fd);
+                    const double C = edl + ed;
+                    const int K = K0 + j / 2 - 1;
+                    if (cout_ok) bc[(long long)K * plane_c + (long long)gJ * pitch_c + gI] =
+                        ((8.0 * dcm + 4.0 * F) + (2.0 * E + C)) * 0.015625;
+                }
+                fdl = fd; edl = ed; dcl = dc;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Trilinear prolongation + correction u += P e, two fine points (2t, 2t+1) per thread with
+// 16-byte accesses on u; coarse values through the read-only path (L1/L2), DESIGN.md §6.9.
+// Sums nest x, then y, then z; one multiply by 0.5^(#even axes).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf, int pitch_f, long long plane_f,
+                                                 const double *__restrict__ e, int nc, int pitch_c,
+                                                 long long plane_c) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y, z = blockIdx.z;
+    const int x = 2 * t;
+    if (x >= nf) return;
+    auto E = [&](int X, int Y, int Z) -> double {
+        return (X >= 0 && X < nc && Y >= 0 && Y < nc && Z >= 0 && Z < nc)
+                   ? __ldg(e + (long long)Z * plane_c + (long long)Y * pitch_c + X)
+                   : 0.0;
+    };
+    const bool ye = !(y & 1), ze = !(z & 1);
+    const int Ya = ye ? y / 2 - 1 : (y - 1) / 2, Yb = y / 2;
+    const int Za = ze ? z / 2 - 1 : (z - 1) / 2, Zb = z / 2;
+    auto sy = [&](int Z, double &se, double &so) {
+        double sea = E(t - 1, Ya, Z) + E(t, Ya, Z), soa = E(t, Ya, Z);
+        if (ye) {
+            double seb = E(t - 1, Yb, Z) + E(t, Yb, Z), sob = E(t, Yb, Z);
+            se = sea + seb; so = soa + sob;
+        } else {
+            se = sea; so = soa;
+        }
+    };
+    double se, so;
+    sy(Za, se, so);
+    if (ze) {
+        double se2, so2;
+        sy(Zb, se2, so2);
+        se = se + se2; so = so + so2;
+    }
+    double w = (ye ? 0.5 : 1.0) * (ze ? 0.5 : 1.0);
+    double we = w * 0.5;   // the even column also averages in x
+    double *row = u + (long long)z * plane_f + (long long)y * pitch_f;
+    if (x + 1 < nf) {
+        double2 v = *reinterpret_cast<double2 *>(row + x);
+        v.x = v.x + se * we;
+        v.y = v.y + so * w;
+        *reinterpret_cast<double2 *>(row + x) = v;
+    } else {
+        row[x] = row[x] + se * we;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// B a (+|-) L c streaming kernel: the RHS of Eq. (5) (b = B v + L w) and the
+// weighted SDC residual of one node (r~ = B p - L z, §4.5), DESIGN.md §6.10.  Per plane p, the K
+// input fields arrive by TMA (34 x RH boxes at (x0-2, y0-1)); every thread forms the pointwise
+// pair (a, c) at its RR points of the (30 + 2) x RH region, writes it to shared planes, then
+// takes in-plane partials (a: centre + faces, c: centre + faces + edges) into register rings and
+// emits the tile (30 x (RH-2)) at plane p-1.  f^E: 0 none, 1 u - u^3, 2 G cos t, 3 stored F
+// fields (CD4 advection, computed once per new node field by k_fe_cd4).
+// ---------------------------------------------------------------------------------------------
+constexpr int BL_MAXF = 2 * ISDC_MAXM + 2;
+struct BLMaps {
+    CUtensorMap m[BL_MAXF];
+};
+struct BLArgs {
+    int K;                         // fields per plane
+    int M, m;                      // nodes; RHS substep m (0-based) or residual node m (1..M-1)
+    int iu0, iun, iuG, iF0, iFn;   // field slots: old/current u_j at iu0+j, u_m^{k+1} at iun, G at iuG,
+                                   // stored F_j at iF0+j, F(u_m^{k+1}) at iFn
+    const double *ct;              // device cos(t_j)
+    double dtm, gm;                // RHS: dt*dtau_m, nu*dt*dtau_m
+    double a[ISDC_MAXM], beta[ISDC_MAXM];   // RHS: dt*S_mj, nu*dt*S_mj;  residual: dt*Q_mj, nu*dt*Q_mj
+    BLConst bl;
+    int n, pitch;
+    long long plane;
+    int zc;
+    double *out;                   // RHS: b (pitched); residual: unused
+    unsigned long long *slot;      // max |out| (RHS: optional, residual: required)
+};
+
+template <int RR>
+struct BLShape {
+    static constexpr int RH = NW * RR;                 // region rows
+    static constexpr int TX = RW - 2, TY = RH - 2;     // output tile
+    static constexpr int FW = RW + 2, FH = RH;         // input box 34 x RH at (x0-2, y0-1)
+    static constexpr int PW = RW + 2, PH = RH + 2;     // a / c planes with a pad ring
+    static constexpr int FPL = a128(FW * FH * 8), PPL = a128(PW * PH * 8);
+    static size_t smem(int K, int ns) { return (size_t)ns * K * FPL + 4 * (size_t)PPL + 8 * 8 + 128; }
+};
+
+template <int RR>
+struct BLRegs {
+    double aq[3][RR], af[3][RR];               // a: centre, faces (by iteration mod 3)
+    double cq[3][RR], cf[3][RR], ce[2][RR];    // c: centre, faces, edges
+};
+
+// pointwise (a, c) at one point from the stage fields at smem offset `o`
+template <int FE, int MODE>
+__device__ __forceinline__ void bl_point(const BLArgs &A, const double *F, int fpl, int o, double &av, double &cv) {
+    const int M = A.M;
+    auto fld = [&](int slot) -> double { return F[slot * fpl + o]; };
+    if (MODE == 0) {   // RHS substep m: a = v, c = w
+        const int m = A.m;
+        double acc = A.beta[0] * fld(A.iu0);
+#pragma unroll
+        for (int j = 1; j < ISDC_MAXM; ++j)
+            if (j < M) acc = acc + A.beta[j] * fld(A.iu0 + j);
+        cv = acc - A.gm * fld(A.iu0 + m + 1);
+        const double un = fld(A.iun);
+        if (FE == 0) {
+            av = un;
+        } else {
+            double fa, fn, fo;
+            if (FE == 1) {
+                double uj = fld(A.iu0);
+                fa = A.a[0] * (uj - (uj * uj) * uj);
+#pragma unroll
+                for (int j = 1; j < ISDC_MAXM; ++j)
+                    if (j < M) { uj = fld(A.iu0 + j); fa = fa + A.a[j] * (uj - (uj * uj) * uj); }
+                const double uo = fld(A.iu0 + m);
+                fn = un - (un * un) * un;
+                fo = uo - (uo * uo) * uo;
+            } else if (FE == 2) {
+                const double g = fld(A.iuG);
+                fa = A.a[0] * (g * A.ct[0]);
+#pragma unroll
+                for (int j = 1; j < ISDC_MAXM; ++j)
+                    if (j < M) fa = fa + A.a[j] * (g * A.ct[j]);
+                fn = g * A.ct[m];
+                fo = g * A.ct[m];
+            } else {
+                fa = A.a[0] * fld(A.iF0);
+#pragma unroll
+                for (int j = 1; j < ISDC_MAXM; ++j)
+                    if (j < M) fa = fa + A.a[j] * fld(A.iF0 + j);
+                fn = fld(A.iFn);
+                fo = fld(A.iF0 + m);
+            }
+            av = (un + A.dtm * (fn - fo)) + fa;
+        }
+    } else {           // residual node m: a = p, c = z
+        const int m = A.m;
+        double diff = fld(A.iu0 + m) - fld(A.iu0);
+        if (FE != 0) {
+            double fa;
+            if (FE == 1) {
+                double uj = fld(A.iu0);
+                fa = A.a[0] * (uj - (uj * uj) * uj);
+#pragma unroll
+                for (int j = 1; j < ISDC_MAXM; ++j)
+                    if (j < M) { uj = fld(A.iu0 + j); fa = fa + A.a[j] * (uj - (uj * uj) * uj); }
+            } else if (FE == 2) {
+                const double g = fld(A.iuG);
+                fa = A.a[0] * (g * A.ct[0]);
+#pragma unroll
+                for (int j = 1; j < ISDC_MAXM; ++j)
+                    if (j < M) fa = fa + A.a[j] * (g * A.ct[j]);
+            } else {
+                fa = A.a[0] * fld(A.iF0);
+#pragma unroll
+                for (int j = 1; j < ISDC_MAXM; ++j)
+                    if (j < M) fa = fa + A.a[j] * fld(A.iF0 + j);
+            }
+            diff = diff - fa;
+        }
+        av = diff;
+        double acc = A.beta[0] * fld(A.iu0);
+#pragma unroll
+        for (int j = 1; j < ISDC_MAXM; ++j)
+            if (j < M) acc = acc + A.beta[j] * fld(A.iu0 + j);
+        cv = acc;
+    }
+}
+
+template <int FE, int MODE, int RR>
+__global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
+    using SH = BLShape<RR>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    const int K = A.K;
+    double *Fs = reinterpret_cast<double *>(sm);                                   // ns stages x K boxes
+    double *Ps = reinterpret_cast<double *>(sm + (size_t)ns * K * SH::FPL);        // a[2], c[2]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + (size_t)ns * K * SH::FPL + 4 * SH::PPL);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int n = A.n;
+    const int x0 = blockIdx.x * SH::TX, y0 = blockIdx.y * SH::TY;
+    const int z0 = blockIdx.z * A.zc, z1 = min(z0 + A.zc, n);
+    const int nit = z1 - z0 + 2;              // ingest planes z0-1 .. z1
+    auto issue = [&](int it) {
+        const int s = it % ns, p = z0 - 1 + it;
+        mbar_expect_tx(&bar[s], K * SH::FW * SH::FH * 8);
+        for (int k = 0; k < K; ++k)
+            tma_load_3d(Fs + ((size_t)s * K + k) * (SH::FPL / 8), &maps.m[k], x0 - 2, y0 - 1, p, &bar[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < ns; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int it = 0; it < ns && it < nit; ++it) issue(it);
+
+    const int lx = lane - 1, ly0 = RR * w - 1;
+    const int gx = x0 + lx;
+    const bool xin = gx >= 0 && gx < n, xout = lx >= 0 && lx < SH::TX && gx < n;
+    bool yin[RR], yout[RR];
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+        const int ly = ly0 + r, gy = y0 + ly;
+        yin[r] = gy >= 0 && gy < n;
+        yout[r] = ly >= 0 && ly < SH::TY && gy < n;
+    }
+    const BLConst c = A.bl;
+    double vmax = 0.0;
+    BLRegs<RR> G;
+    auto step = [&](auto Kc, int it) {
+        constexpr int Kk = decltype(Kc)::value;
+        constexpr int i3 = Kk % 3, m3 = (Kk + 2) % 3, mm3 = (Kk + 1) % 3;
+        constexpr int i2 = Kk % 2, m2 = (Kk + 1) % 2;
+        const int s = it % ns, p = z0 - 1 + it;
+        mbar_wait(&bar[s], (it / ns) & 1);
+        const bool zin = p >= 0 && p < n;
+        const double *F = Fs + (size_t)s * K * (SH::FPL / 8);
+        double *Pa = Ps + (2 * i2) * (SH::PPL / 8), *Pc = Ps + (2 * i2 + 1) * (SH::PPL / 8);
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+            double av = 0.0, cv = 0.0;
+            if (xin && yin[r] && zin) bl_point<FE, MODE>(A, F, SH::FPL / 8, (RR * w + r) * SH::FW + lane + 1, av, cv);
+            Pa[(RR * w + r + 1) * SH::PW + lane + 1] = av;
+            Pc[(RR * w + r + 1) * SH::PW + lane + 1] = cv;
+        }
+        __syncthreads();
+        if (tid == 0 && it + ns < nit) issue(it + ns);
+        double dummy[RR];
+        plane_partials<false, RR>(Pa, SH::PW, RR * w, lane, G.aq[i3], G.af[i3], dummy);
+        plane_partials<true, RR>(Pc, SH::PW, RR * w, lane, G.cq[i3], G.cf[i3], G.ce[i2]);
+        if (it >= 2) {   // output plane p-1
+            const int gz = p - 1;
+            double *op = (MODE == 0) ? A.out + (long long)gz * A.plane + (long long)(y0 + ly0) * A.pitch + gx : nullptr;
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                const double fa_ = G.af[m3][r] + (G.aq[mm3][r] + G.aq[i3][r]);
+                const double fc_ = G.cf[m3][r] + (G.cq[mm3][r] + G.cq[i3][r]);
+                const double ec_ = G.ce[m2][r] + (G.cf[mm3][r] + G.cf[i3][r]);
+                const double Ba = c.kB0 * G.aq[m3][r] + c.kB1 * fa_;
+                const double Lc = (c.kL0 * G.cq[m3][r] + c.kL1 * fc_) + c.kL2 * ec_;
+                const double val = (MODE == 0) ? Ba + Lc : Ba - Lc;
+                if (xout && yout[r]) {
+                    if (MODE == 0) op[(long long)r * A.pitch] = val;
+                    vmax = amax(vmax, fabs(val));
+                }
+            }
+        }
+    };
+    for (int base = 0; base < nit; base += 6) {
+        if (base + 0 < nit) step(std::integral_constant<int, 0>{}, base + 0);
+        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
+        if (base + 3 < nit) step(std::integral_constant<int, 3>{}, base + 3);
+        if (base + 4 < nit) step(std::integral_constant<int, 4>{}, base + 4);
+        if (base + 5 < nit) step(std::integral_constant<int, 5>{}, base + 5);
+    }
+    if (A.slot) block_max_to(A.slot, vmax);
+}
+
+// ---------------------------------------------------------------------------------------------
+// f^E = -a . grad u with CD4 differences and zero ghosts, stored once per new
+// node field so that the RHS / residual kernels read it pointwise.  32 x 32 tile, z-streaming
+// with a 5-plane ring of 36 x 36 boxes at (x0-2, y0-2).  DESIGN.md §6.11.
+// ---------------------------------------------------------------------------------------------
+constexpr int FE_W = RW + 4, FE_H = RH + 4;
+constexpr int FE_NS = 8;   // ring: 5 planes in use + 3 in flight
+constexpr int FE_PL = a128(FE_W * FE_H * 8);
+constexpr size_t FE_SMEM = (size_t)FE_NS * FE_PL + 8 * FE_NS + 128;
+
+__global__ void __launch_bounds__(NT, 1) k_fe_cd4(const __grid_constant__ CUtensorMap tu, double *__restrict__ Fout,
+                                                  int n, int pitch, long long plane, double kx, double ky,
+                                                  double kz, int zc) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    double *Us = reinterpret_cast<double *>(sm);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + (size_t)FE_NS * FE_PL);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int x0 = blockIdx.x * RW, y0 = blockIdx.y * RH;
+    const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, n);
+    const int nit = z1 - z0 + 4;              // planes z0-2 .. z1+1
+    auto issue = [&](int it) {
+        const int s = it % FE_NS;
+        mbar_expect_tx(&bar[s], FE_W * FE_H * 8);
+        tma_load_3d(Us + s * (FE_PL / 8), &tu, x0 - 2, y0 - 2, z0 - 2 + it, &bar[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < FE_NS; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int it = 0; it < FE_NS && it < nit; ++it) issue(it);
+    const int gx = x0 + lane;
+    for (int it = 0; it < nit; ++it) {
+        mbar_wait(&bar[it % FE_NS], (it / FE_NS) & 1);
+        if (it >= 4) {   // centre plane z = z0-2+it-2
+            const int gz = z0 - 4 + it;
+            const double *Pm2 = Us + ((it - 4) % FE_NS) * (FE_PL / 8), *Pm1 = Us + ((it - 3) % FE_NS) * (FE_PL / 8);
+            const double *P0 = Us + ((it - 2) % FE_NS) * (FE_PL / 8), *Pp1 = Us + ((it - 1) % FE_NS) * (FE_PL / 8);
+            const double *Pp2 = Us + (it % FE_NS) * (FE_PL / 8);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int ly = R * w + r, gy = y0 + ly;
+                const int o = (ly + 2) * FE_W + lane + 2;
+                const double dx = (8.0 * (P0[o + 1] - P0[o - 1]) - (P0[o + 2] - P0[o - 2])) * kx;
+                const double dy = (8.0 * (P0[o + FE_W] - P0[o - FE_W]) - (P0[o + 2 * FE_W] - P0[o - 2 * FE_W])) * ky;
+                const double dz = (8.0 * (Pp1[o] - Pm1[o]) - (Pp2[o] - Pm2[o])) * kz;
+                if (gx < n && gy < n) Fout[(long long)gz * plane + (long long)gy * pitch + gx] = -((dx + dy) + dz);
+            }
+        }
+        __syncthreads();
+        // the slot of plane it-4 is free now: refill it with plane it+4 (= it-4+FE_NS)
+        if (tid == 0 && it >= 4 && it - 4 + FE_NS < nit) issue(it - 4 + FE_NS);
+    }
+}
+
+}  // namespace f3d

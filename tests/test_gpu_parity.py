@@ -46,7 +46,8 @@ def test_tables_bitwise(gpu, ora, M):
 
 # --------------------------------------------------------------------------------- V-cycle
 @pytest.mark.parametrize("dim,n,M,dt,nu", [(2, 63, 3, 0.01, 1.0), (2, 127, 5, 0.01, 0.1), (2, 255, 5, 0.005, 1e-3),
-                                           (3, 15, 3, 0.01, 1.0), (3, 31, 5, 0.002, 0.01), (3, 63, 3, 0.01, 1.0)])
+                                           (3, 15, 3, 0.01, 1.0), (3, 31, 5, 0.002, 0.01), (3, 63, 3, 0.01, 1.0),
+                                           (3, 127, 3, 0.01, 1.0), (3, 127, 5, 0.002, 0.01)])
 def test_vcycle_bitwise(gpu, ora, dim, n, M, dt, nu):
     cfg = synth.Config(0, dim, n, M, dt, nu, FE_NONE)
     h = make(gpu, cfg)
@@ -93,10 +94,11 @@ def test_rhs_and_residual_bitwise(gpu, ora, dim, fe):
 
 
 # ------------------------------------------------------------------------------------- sweep
-@pytest.mark.parametrize("dim,fe,mode", [(2, FE_NONE, MODE_ISDC), (2, FE_CUBIC, MODE_SDC), (2, FE_FORCING, MODE_ISDC),
-                                         (3, FE_ADVECTION, MODE_ISDC), (3, FE_NONE, MODE_SDC)])
-def test_sweep_bitwise(gpu, ora, dim, fe, mode):
-    n = 31 if dim == 3 else 127
+@pytest.mark.parametrize("dim,fe,mode,n", [(2, FE_NONE, MODE_ISDC, 127), (2, FE_CUBIC, MODE_SDC, 127),
+                                           (2, FE_FORCING, MODE_ISDC, 127), (3, FE_ADVECTION, MODE_ISDC, 31),
+                                           (3, FE_NONE, MODE_SDC, 31), (3, FE_NONE, MODE_ISDC, 63),
+                                           (3, FE_ADVECTION, MODE_ISDC, 63), (3, FE_CUBIC, MODE_SDC, 63)])
+def test_sweep_bitwise(gpu, ora, dim, fe, mode, n):
     M = 5 if fe != FE_NONE else 3
     cfg = synth.Config(0, dim, n, M, 0.01, 0.5, fe, fe_a=(1.0, 0.5, 0.25))
     G = synth.forcing_field(n, dim) if fe == FE_FORCING else None
