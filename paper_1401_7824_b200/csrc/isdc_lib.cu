@@ -58,6 +58,7 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    int smooth3d_rows = 4;     // ISDC_SMOOTH3D_ROWS: rows per thread of the 3D fused smoother (2 or 4)
     int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
     TailParams tailp[ISDC_MAXM];
@@ -325,7 +326,8 @@ isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const 
     int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + f3d::S_TY - 1) / f3d::S_TY;
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
-    f3d::k_smooth2<<<grd, f3d::NT, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
+    if (h->smooth3d_rows == 4) f3d::k_smooth2<4><<<grd, 256, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
+    else f3d::k_smooth2<2><<<grd, 512, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
     prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -371,13 +373,18 @@ isdc_status launch_fe(isdc_ctx *h, double *F, const double *u) {
 constexpr int kMaxDynSmem = 232448 - 1024;   // 227 KB opt-in per CTA on sm_100, less static shared memory
 
 // B a +- L c streaming kernel (3D RHS / residual), DESIGN.md §6.10.  fields[k] are pitched level-0
-// fields; picks the region height (RR) and pipeline depth that fit shared memory.
+// fields; nm outputs per pass.  Picks the region height (RR) and pipeline depth that fit shared
+// memory and registers: RHS (nm = 1) prefers RR = 4; residual passes with nm = 2 use RR = 2.
 template <int MODE>
-isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, f3d::BLArgs A, int prof_cls, double bytes) {
+isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f3d::BLArgs A, int prof_cls,
+                      double bytes) {
     const GridDesc &g = h->lev[0].g;
-    int rr = 4, ns = 3;
-    while (ns >= 2 && f3d::BLShape<4>::smem(K, ns) > (size_t)kMaxDynSmem) --ns;
-    if (ns < 3) { rr = 2; ns = 4; while (ns >= 2 && f3d::BLShape<2>::smem(K, ns) > (size_t)kMaxDynSmem) --ns; }
+    int rr = (nm == 1) ? 4 : 2, ns = 4;
+    auto smem_of = [&](int r_, int ns_) {
+        return r_ == 4 ? f3d::BLShape<4>::smem(K, ns_, nm) : f3d::BLShape<2>::smem(K, ns_, nm);
+    };
+    while (ns >= 2 && smem_of(rr, ns) > (size_t)kMaxDynSmem) --ns;
+    if (rr == 4 && ns < 3) { rr = 2; ns = 4; while (ns >= 2 && smem_of(rr, ns) > (size_t)kMaxDynSmem) --ns; }
     if (ns < 2) { h->err = "too many fields for the 3D stream kernel"; return ISDC_ERR_UNSUPPORTED; }
     int rh = f3d::NW * rr;
     f3d::BLMaps maps;
@@ -390,16 +397,21 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, f3d::BLAr
     int tx = (g.n + f3d::RW - 3) / (f3d::RW - 2), ty = (g.n + rh - 3) / (rh - 2);
     A.zc = pick_chunk(h, tx * ty, g.n, 2);
     dim3 grd(tx, ty, (g.n + A.zc - 1) / A.zc);
-    size_t sm = (rr == 4) ? f3d::BLShape<4>::smem(K, ns) : f3d::BLShape<2>::smem(K, ns);
+    size_t sm = smem_of(rr, ns);
     ++h->launches;
     int pe = prof_begin(h, prof_cls);
     int fe = h->fe.kind;
-#define ISDC_BL(FE_, RR_) f3d::k_bl<FE_, MODE, RR_><<<grd, f3d::NT, sm, h->s>>>(maps, A, ns)
-    if (rr == 4) {
-        if (fe == 0) ISDC_BL(0, 4); else if (fe == 1) ISDC_BL(1, 4); else if (fe == 2) ISDC_BL(2, 4); else ISDC_BL(3, 4);
-    } else {
-        if (fe == 0) ISDC_BL(0, 2); else if (fe == 1) ISDC_BL(1, 2); else if (fe == 2) ISDC_BL(2, 2); else ISDC_BL(3, 2);
-    }
+#define ISDC_BL(FE_, RR_, NM_) f3d::k_bl<FE_, MODE, RR_, NM_><<<grd, f3d::NT, sm, h->s>>>(maps, A, ns)
+#define ISDC_BL_FE(RR_, NM_)                                                   \
+    do {                                                                       \
+        if (fe == 0) ISDC_BL(0, RR_, NM_);                                     \
+        else if (fe == 1) ISDC_BL(1, RR_, NM_);                                \
+        else if (fe == 2) ISDC_BL(2, RR_, NM_);                                \
+        else ISDC_BL(3, RR_, NM_);                                             \
+    } while (0)
+    if (nm == 1) { if (rr == 4) ISDC_BL_FE(4, 1); else ISDC_BL_FE(2, 1); }
+    else ISDC_BL_FE(2, 2);
+#undef ISDC_BL_FE
 #undef ISDC_BL
     prof_end(h, pe, prof_cls, bytes);
     LAUNCH_CHECK(h);
@@ -639,16 +651,16 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         A.iuG = A.iF0 = A.iFn = 0;
         if (fe == 2) { A.iuG = K; fields[K++] = h->Gp; }
         if (fe == 3) { A.iF0 = K; for (int j = 0; j < M; ++j) fields[K++] = Fold[j]; A.iFn = K; fields[K++] = Fnew; }
-        A.M = M; A.m = m;
+        A.M = M; A.mnode[0] = m;
         double dt = h->P.dt, nu = h->P.nu, nudt = nu * dt;
         A.dtm = dt * h->dtau[m];
         A.gm = nu * A.dtm;
-        for (int j = 0; j < M; ++j) { A.a[j] = dt * h->S[m * M + j]; A.beta[j] = nudt * h->S[m * M + j]; }
+        for (int j = 0; j < M; ++j) { A.a[0][j] = dt * h->S[m * M + j]; A.beta[0][j] = nudt * h->S[m * M + j]; }
         A.out = bout;
-        A.slot = nullptr;
-        if (bnorm) { TRY(clear_slots(h, SLOT_BNORM, 1)); A.slot = h->red + SLOT_BNORM; }
+        for (int k = 0; k < f3d::BL_MAXNM; ++k) A.slot[k] = nullptr;
+        if (bnorm) { TRY(clear_slots(h, SLOT_BNORM, 1)); A.slot[0] = h->red + SLOT_BNORM; }
         // algorithmic bytes: the M + 1 node fields (+G) read and b written
-        return launch_bl<0>(h, fields, K, A, PROF_RHS, (M + 2 + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, h->lev[0].g));
+        return launch_bl<0>(h, fields, K, 1, A, PROF_RHS, (M + 2 + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, h->lev[0].g));
     }
     if (fast2d_pointwise_fe(h)) {
         f2d::RhsArgs A;
@@ -716,12 +728,18 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         if (fe == 3) { A.iF0 = K; for (int j = 0; j < M; ++j) fields[K++] = F[j]; }
         A.M = M; A.dtm = A.gm = 0.0; A.out = nullptr;
         double dt = h->P.dt, nudt = h->P.nu * dt;
-        for (int m = 1; m < M; ++m) {
-            A.m = m;
-            for (int j = 0; j < M; ++j) { A.a[j] = dt * h->Q[m * M + j]; A.beta[j] = nudt * h->Q[m * M + j]; }
-            A.slot = h->red + SLOT_RES0 + m - 1;
-            // algorithmic bytes of the whole residual: M node fields (+G) once, spread over the M-1 launches
-            TRY(launch_bl<1>(h, fields, K, A, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g) / (M - 1)));
+        const int passes = (M - 1 + 1) / 2;   // two nodes per pass
+        for (int m0 = 1; m0 < M; m0 += 2) {
+            const int nm = (m0 + 1 < M) ? 2 : 1;
+            for (int k = 0; k < f3d::BL_MAXNM; ++k) A.slot[k] = nullptr;
+            for (int k = 0; k < nm; ++k) {
+                const int m = m0 + k;
+                A.mnode[k] = m;
+                for (int j = 0; j < M; ++j) { A.a[k][j] = dt * h->Q[m * M + j]; A.beta[k][j] = nudt * h->Q[m * M + j]; }
+                A.slot[k] = h->red + SLOT_RES0 + m - 1;
+            }
+            // algorithmic bytes of the whole residual: M node fields (+G) once, spread over the passes
+            TRY(launch_bl<1>(h, fields, K, nm, A, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g) / passes));
         }
         return ISDC_OK;
     }
@@ -983,6 +1001,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     h->fast = !(env && env[0] == '1');
     if (h->fast && !tma_encoder()) h->fast = false;
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
+    if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -997,15 +1016,17 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSmooth) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
-        cudaFuncSetAttribute(f3d::k_smooth2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
         cudaFuncSetAttribute(f3d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::R_SMEM);
         cudaFuncSetAttribute(f3d::k_fe_cd4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::FE_SMEM);
-#define ISDC_BL_ATTR(FE_, MODE_, RR_) \
-        cudaFuncSetAttribute(f3d::k_bl<FE_, MODE_, RR_>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-        ISDC_BL_ATTR(0, 0, 4) ISDC_BL_ATTR(1, 0, 4) ISDC_BL_ATTR(2, 0, 4) ISDC_BL_ATTR(3, 0, 4)
-        ISDC_BL_ATTR(0, 1, 4) ISDC_BL_ATTR(1, 1, 4) ISDC_BL_ATTR(2, 1, 4) ISDC_BL_ATTR(3, 1, 4)
-        ISDC_BL_ATTR(0, 0, 2) ISDC_BL_ATTR(1, 0, 2) ISDC_BL_ATTR(2, 0, 2) ISDC_BL_ATTR(3, 0, 2)
-        ISDC_BL_ATTR(0, 1, 2) ISDC_BL_ATTR(1, 1, 2) ISDC_BL_ATTR(2, 1, 2) ISDC_BL_ATTR(3, 1, 2)
+#define ISDC_BL_ATTR(FE_, MODE_, RR_, NM_) \
+        cudaFuncSetAttribute(f3d::k_bl<FE_, MODE_, RR_, NM_>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+#define ISDC_BL_ATTR4(MODE_, RR_, NM_) \
+        ISDC_BL_ATTR(0, MODE_, RR_, NM_) ISDC_BL_ATTR(1, MODE_, RR_, NM_) ISDC_BL_ATTR(2, MODE_, RR_, NM_) ISDC_BL_ATTR(3, MODE_, RR_, NM_)
+        ISDC_BL_ATTR4(0, 4, 1) ISDC_BL_ATTR4(0, 2, 1) ISDC_BL_ATTR4(1, 4, 1) ISDC_BL_ATTR4(1, 2, 1) ISDC_BL_ATTR4(1, 2, 2)
+        ISDC_BL_ATTR4(0, 2, 2)
+#undef ISDC_BL_ATTR4
 #undef ISDC_BL_ATTR
         int rs = 2 * (ISDC_MAXM - 1) * f2d::ZH * f2d::ZW * (int)sizeof(double);
         cudaFuncSetAttribute(f2d::k_resid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);

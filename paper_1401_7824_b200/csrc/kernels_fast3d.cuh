@@ -66,90 +66,98 @@ constexpr int S_NS = 6;          // TMA pipeline depth (planes in flight)
 constexpr int S_UPL = a128(S_UW * S_UH * 8), S_BPL = a128(S_BW * S_BH * 8), S_TPL = a128(S_TW * S_TH * 8);
 constexpr size_t S_SMEM = (size_t)S_NS * (S_UPL + S_BPL) + 2 * S_TPL + 8 * S_NS + 128;
 
-// Register state of one thread (R owned points).  Rings are indexed by the iteration that
+// Register state of one thread (SR owned points).  Rings are indexed by the iteration that
 // produced the value (mod 3 for centre/face sums, mod 2 for edge sums and b), so after unrolling
 // the z loop by 6 every index is a compile-time constant and no value is ever moved.
+template <int SR>
 struct SmoothRegs {
-    double q[3][R], f[3][R], e[2][R];      // u(p): centre, face, edge partials
-    double tq[3][R], tf[3][R], te[2][R];   // t(p-1) (first sweep), same partials
-    double bb[2][R];                       // b(p-1)
+    double q[3][SR], f[3][SR], e[2][SR];      // u(p): centre, face, edge partials
+    double tq[3][SR], tf[3][SR], te[2][SR];   // t(p-1) (first sweep), same partials
+    double bb[2][SR];                         // b(p-1)
 };
 
+template <int SR>
 struct SmoothCtx {
     const double *Us, *Bs;
     double *Ts;
     uint64_t *bar;
-    double *optr;
+    double *optr;                  // output address of the owned column at plane z0 - 4, row ly0
     long long plane;
-    int pitch, n, w, lane, z0, nit;
-    bool xin, xout, yin[R], yout[R];
+    int pitch, n, row0, lane, z0;
+    unsigned inxy, oks;            // bit r: owned point r inside the domain (xy) / an output point
     double c0, c1, c2, wd;
 };
 
-template <int K>   // K = it % 6
-__device__ __forceinline__ void smooth_step(const SmoothCtx &C, SmoothRegs &G, int it) {
+template <int SR, int K>   // K = it % 6 = it % S_NS (the z loop is unrolled by 6 from it = 0)
+__device__ __forceinline__ void smooth_step(const SmoothCtx<SR> &C, SmoothRegs<SR> &G, int it, uint32_t phase) {
+    static_assert(S_NS == 6, "stage index = K");
     constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3;   // it, it-1, it-2 (mod 3)
     constexpr int i2 = K % 2, m2 = (K + 1) % 2;                       // it, it-1 (mod 2)
-    const int s = it % S_NS, p = C.z0 - 2 + it;
-    mbar_wait(&C.bar[s], (it / S_NS) & 1);
-    plane_partials<true>(C.Us + s * (S_UPL / 8), S_UW, R * C.w, C.lane, G.q[i3], G.f[i3], G.e[i2]);
+    constexpr int s = K;
+    mbar_wait(&C.bar[s], phase);
+    plane_partials<true, SR>(C.Us + s * (S_UPL / 8), S_UW, C.row0, C.lane, G.q[i3], G.f[i3], G.e[i2]);
     double *T = C.Ts + i2 * (S_TPL / 8);
-    if (it >= 2) {   // sweep 1 at plane p-1 on the 32 x 32 region
-        const int gz = p - 1;
-        const bool zin = gz >= 0 && gz < C.n;
-        const double *Bp = C.Bs + s * (S_BPL / 8);
+    if (it >= 2) {   // sweep 1 at plane gz = p-1 on the 32 x 32 region
+        const int gz = C.z0 - 3 + it;
+        const unsigned in = ((unsigned)gz < (unsigned)C.n) ? C.inxy : 0u;
+        const double *Bp = C.Bs + s * (S_BPL / 8) + C.row0 * S_BW + C.lane + 1;
+        double *Tp = T + (C.row0 + 1) * S_TW + C.lane + 1;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < SR; ++r) {
             const double faces = G.f[m3][r] + (G.q[mm3][r] + G.q[i3][r]);
             const double edges = G.e[m2][r] + (G.f[mm3][r] + G.f[i3][r]);
             const double su = (C.c0 * G.q[m3][r] + C.c1 * faces) + C.c2 * edges;
-            const double bv = Bp[(R * C.w + r) * S_BW + C.lane + 1];
-            const double t = (C.xin && C.yin[r] && zin) ? G.q[m3][r] + C.wd * (bv - su) : 0.0;
-            T[(R * C.w + r + 1) * S_TW + C.lane + 1] = t;
+            const double bv = Bp[r * S_BW];
+            const double t = G.q[m3][r] + C.wd * (bv - su);
+            Tp[r * S_TW] = ((in >> r) & 1u) ? t : 0.0;
             G.bb[i2][r] = bv;
         }
     }
 }
 
-template <int K>
-__device__ __forceinline__ void smooth_step2(const SmoothCtx &C, SmoothRegs &G, int it) {
+template <int SR, int K>
+__device__ __forceinline__ void smooth_step2(const SmoothCtx<SR> &C, SmoothRegs<SR> &G, int it) {
     constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3;
     constexpr int i2 = K % 2, m2 = (K + 1) % 2;
     if (it < 2) return;
     const double *T = C.Ts + i2 * (S_TPL / 8);
-    plane_partials<true>(T, S_TW, R * C.w, C.lane, G.tq[i3], G.tf[i3], G.te[i2]);
-    if (it >= 4) {   // sweep 2 at plane p-2 on the 30 x 30 tile
-        const int gz = C.z0 - 4 + it;
-        double *op = C.optr + (long long)gz * C.plane;
+    plane_partials<true, SR>(T, S_TW, C.row0, C.lane, G.tq[i3], G.tf[i3], G.te[i2]);
+    if (it >= 4) {   // sweep 2 at plane p-2 = z0 - 4 + it on the 30 x 30 tile
+        double *op = C.optr + (long long)it * C.plane;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < SR; ++r) {
             const double faces = G.tf[m3][r] + (G.tq[mm3][r] + G.tq[i3][r]);
             const double edges = G.te[m2][r] + (G.tf[mm3][r] + G.tf[i3][r]);
             const double su = (C.c0 * G.tq[m3][r] + C.c1 * faces) + C.c2 * edges;
             const double o = G.tq[m3][r] + C.wd * (G.bb[m2][r] - su);
-            if (C.xout && C.yout[r]) op[(long long)r * C.pitch] = o;
+            if ((C.oks >> r) & 1u) *op = o;
+            op += C.pitch;
         }
     }
 }
 
 // u box 34 x 34 at (x0-2, y0-2); b box 34 x 32 at (x0-2, y0-1); t plane 34 x 34 (pad ring).
-__global__ void __launch_bounds__(NT, 1) k_smooth2(const __grid_constant__ CUtensorMap tu,
-                                                   const __grid_constant__ CUtensorMap tb,
-                                                   double *__restrict__ out, int n, int pitch, long long plane,
-                                                   SCoef c, int zc) {
+// SR rows per thread, 32 / SR warps (the region is always 32 x 32).
+template <int SR>
+__global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_constant__ CUtensorMap tu,
+                                                                const __grid_constant__ CUtensorMap tb,
+                                                                double *__restrict__ out, int n, int pitch,
+                                                                long long plane, SCoef c, int zc) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
-    SmoothCtx C;
+    SmoothCtx<SR> C;
     C.Us = reinterpret_cast<const double *>(sm);
     C.Bs = reinterpret_cast<const double *>(sm + S_NS * S_UPL);
     C.Ts = reinterpret_cast<double *>(sm + S_NS * (S_UPL + S_BPL));
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S_NS * (S_UPL + S_BPL) + 2 * S_TPL);
     C.bar = bar;
     const int tid = threadIdx.x;
-    C.lane = tid & 31; C.w = tid >> 5;
+    C.lane = tid & 31;
+    C.row0 = SR * (tid >> 5);
     const int x0 = blockIdx.x * S_TX, y0 = blockIdx.y * S_TY;
     const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, n);
-    C.z0 = z0; C.nit = z1 - z0 + 4; C.n = n; C.pitch = pitch; C.plane = plane;
+    const int nit = z1 - z0 + 4;
+    C.z0 = z0; C.n = n; C.pitch = pitch; C.plane = plane;
     double *Usw = reinterpret_cast<double *>(sm), *Bsw = reinterpret_cast<double *>(sm + S_NS * S_UPL);
     auto issue = [&](int it) {
         const int s = it % S_NS, p = z0 - 2 + it;
@@ -165,37 +173,38 @@ __global__ void __launch_bounds__(NT, 1) k_smooth2(const __grid_constant__ CUten
     }
     __syncthreads();
     if (tid == 0)
-        for (int it = 0; it < S_NS && it < C.nit; ++it) issue(it);
+        for (int it = 0; it < S_NS && it < nit; ++it) issue(it);
 
     C.c0 = c.c0; C.c1 = c.c1; C.c2 = c.c2; C.wd = c.wd;
-    const int lx = C.lane - 1, ly0 = R * C.w - 1;        // region coordinates of the owned points
+    const int lx = C.lane - 1, ly0 = C.row0 - 1;        // region coordinates of the owned points
     const int gx = x0 + lx;
-    C.xin = gx >= 0 && gx < n;
-    C.xout = lx >= 0 && lx < S_TX && gx < n;
+    const bool xin = gx >= 0 && gx < n;
+    const bool xout = lx >= 0 && lx < S_TX && gx < n;
+    C.inxy = 0u; C.oks = 0u;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < SR; ++r) {
         const int ly = ly0 + r, gy = y0 + ly;
-        C.yin[r] = gy >= 0 && gy < n;
-        C.yout[r] = ly >= 0 && ly < S_TY && gy < n;
+        if (xin && gy >= 0 && gy < n) C.inxy |= 1u << r;
+        if (xout && ly >= 0 && ly < S_TY && gy < n) C.oks |= 1u << r;
     }
-    C.optr = out + (long long)(y0 + ly0) * pitch + gx;
-    SmoothRegs G;
+    C.optr = out + (long long)(z0 - 4) * plane + (long long)(y0 + ly0) * pitch + gx;
+    SmoothRegs<SR> G;
 #pragma unroll
     for (int k = 0; k < 2; ++k)
 #pragma unroll
-        for (int r = 0; r < R; ++r) G.bb[k][r] = 0.0;
-    const int nit = C.nit;
+        for (int r = 0; r < SR; ++r) G.bb[k][r] = 0.0;
 #define ISDC_SMOOTH_STEP(K)                                            \
     {                                                                  \
         const int it = base + (K);                                     \
         if (it < nit) {                                                \
-            smooth_step<K>(C, G, it);                                  \
+            smooth_step<SR, K>(C, G, it, phase);                       \
             __syncthreads();                                           \
             if (tid == 0 && it + S_NS < nit) issue(it + S_NS);         \
-            smooth_step2<K>(C, G, it);                                 \
+            smooth_step2<SR, K>(C, G, it);                             \
         }                                                              \
     }
     for (int base = 0; base < nit; base += 6) {
+        const uint32_t phase = (base / 6) & 1;
         ISDC_SMOOTH_STEP(0) ISDC_SMOOTH_STEP(1) ISDC_SMOOTH_STEP(2)
         ISDC_SMOOTH_STEP(3) ISDC_SMOOTH_STEP(4) ISDC_SMOOTH_STEP(5)
     }
@@ -364,23 +373,26 @@ __global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf,
 // fields (CD4 advection, computed once per new node field by k_fe_cd4).
 // ---------------------------------------------------------------------------------------------
 constexpr int BL_MAXF = 2 * ISDC_MAXM + 2;
+constexpr int BL_MAXNM = 4;        // outputs (residual nodes) per pass
 struct BLMaps {
     CUtensorMap m[BL_MAXF];
 };
 struct BLArgs {
     int K;                         // fields per plane
-    int M, m;                      // nodes; RHS substep m (0-based) or residual node m (1..M-1)
+    int M;                         // nodes
+    int mnode[BL_MAXNM];           // RHS: substep m (0-based); residual: the pass's nodes m (1..M-1)
     int iu0, iun, iuG, iF0, iFn;   // field slots: old/current u_j at iu0+j, u_m^{k+1} at iun, G at iuG,
                                    // stored F_j at iF0+j, F(u_m^{k+1}) at iFn
     const double *ct;              // device cos(t_j)
     double dtm, gm;                // RHS: dt*dtau_m, nu*dt*dtau_m
-    double a[ISDC_MAXM], beta[ISDC_MAXM];   // RHS: dt*S_mj, nu*dt*S_mj;  residual: dt*Q_mj, nu*dt*Q_mj
+    double a[BL_MAXNM][ISDC_MAXM], beta[BL_MAXNM][ISDC_MAXM];   // RHS: dt*S_mj, nu*dt*S_mj;
+                                                                // residual: dt*Q_mj, nu*dt*Q_mj
     BLConst bl;
     int n, pitch;
     long long plane;
     int zc;
     double *out;                   // RHS: b (pitched); residual: unused
-    unsigned long long *slot;      // max |out| (RHS: optional, residual: required)
+    unsigned long long *slot[BL_MAXNM];   // max |out| per output (RHS: optional, residual: required)
 };
 
 template <int RR>
@@ -390,7 +402,9 @@ struct BLShape {
     static constexpr int FW = RW + 2, FH = RH;         // input box 34 x RH at (x0-2, y0-1)
     static constexpr int PW = RW + 2, PH = RH + 2;     // a / c planes with a pad ring
     static constexpr int FPL = a128(FW * FH * 8), PPL = a128(PW * PH * 8);
-    static size_t smem(int K, int ns) { return (size_t)ns * K * FPL + 4 * (size_t)PPL + 8 * 8 + 128; }
+    static size_t smem(int K, int ns, int nm) {
+        return (size_t)ns * K * FPL + 4 * (size_t)nm * PPL + 8 * 8 + 128;
+    }
 };
 
 template <int RR>
@@ -399,17 +413,19 @@ struct BLRegs {
     double cq[3][RR], cf[3][RR], ce[2][RR];    // c: centre, faces, edges
 };
 
-// pointwise (a, c) at one point from the stage fields at smem offset `o`
+// pointwise (a, c) of output k at one point from the stage fields at smem offset `o`
+// (DESIGN.md §4.4 RHS, §4.5 residual)
 template <int FE, int MODE>
-__device__ __forceinline__ void bl_point(const BLArgs &A, const double *F, int fpl, int o, double &av, double &cv) {
-    const int M = A.M;
+__device__ __forceinline__ void bl_point(const BLArgs &A, int k, const double *F, int fpl, int o, double &av,
+                                         double &cv) {
+    const int M = A.M, m = A.mnode[k];
+    const double *a = A.a[k], *beta = A.beta[k];
     auto fld = [&](int slot) -> double { return F[slot * fpl + o]; };
     if (MODE == 0) {   // RHS substep m: a = v, c = w
-        const int m = A.m;
-        double acc = A.beta[0] * fld(A.iu0);
+        double acc = beta[0] * fld(A.iu0);
 #pragma unroll
         for (int j = 1; j < ISDC_MAXM; ++j)
-            if (j < M) acc = acc + A.beta[j] * fld(A.iu0 + j);
+            if (j < M) acc = acc + beta[j] * fld(A.iu0 + j);
         cv = acc - A.gm * fld(A.iu0 + m + 1);
         const double un = fld(A.iun);
         if (FE == 0) {
@@ -418,74 +434,74 @@ __device__ __forceinline__ void bl_point(const BLArgs &A, const double *F, int f
             double fa, fn, fo;
             if (FE == 1) {
                 double uj = fld(A.iu0);
-                fa = A.a[0] * (uj - (uj * uj) * uj);
+                fa = a[0] * (uj - (uj * uj) * uj);
 #pragma unroll
                 for (int j = 1; j < ISDC_MAXM; ++j)
-                    if (j < M) { uj = fld(A.iu0 + j); fa = fa + A.a[j] * (uj - (uj * uj) * uj); }
+                    if (j < M) { uj = fld(A.iu0 + j); fa = fa + a[j] * (uj - (uj * uj) * uj); }
                 const double uo = fld(A.iu0 + m);
                 fn = un - (un * un) * un;
                 fo = uo - (uo * uo) * uo;
             } else if (FE == 2) {
                 const double g = fld(A.iuG);
-                fa = A.a[0] * (g * A.ct[0]);
+                fa = a[0] * (g * A.ct[0]);
 #pragma unroll
                 for (int j = 1; j < ISDC_MAXM; ++j)
-                    if (j < M) fa = fa + A.a[j] * (g * A.ct[j]);
+                    if (j < M) fa = fa + a[j] * (g * A.ct[j]);
                 fn = g * A.ct[m];
                 fo = g * A.ct[m];
             } else {
-                fa = A.a[0] * fld(A.iF0);
+                fa = a[0] * fld(A.iF0);
 #pragma unroll
                 for (int j = 1; j < ISDC_MAXM; ++j)
-                    if (j < M) fa = fa + A.a[j] * fld(A.iF0 + j);
+                    if (j < M) fa = fa + a[j] * fld(A.iF0 + j);
                 fn = fld(A.iFn);
                 fo = fld(A.iF0 + m);
             }
             av = (un + A.dtm * (fn - fo)) + fa;
         }
     } else {           // residual node m: a = p, c = z
-        const int m = A.m;
         double diff = fld(A.iu0 + m) - fld(A.iu0);
         if (FE != 0) {
             double fa;
             if (FE == 1) {
                 double uj = fld(A.iu0);
-                fa = A.a[0] * (uj - (uj * uj) * uj);
+                fa = a[0] * (uj - (uj * uj) * uj);
 #pragma unroll
                 for (int j = 1; j < ISDC_MAXM; ++j)
-                    if (j < M) { uj = fld(A.iu0 + j); fa = fa + A.a[j] * (uj - (uj * uj) * uj); }
+                    if (j < M) { uj = fld(A.iu0 + j); fa = fa + a[j] * (uj - (uj * uj) * uj); }
             } else if (FE == 2) {
                 const double g = fld(A.iuG);
-                fa = A.a[0] * (g * A.ct[0]);
+                fa = a[0] * (g * A.ct[0]);
 #pragma unroll
                 for (int j = 1; j < ISDC_MAXM; ++j)
-                    if (j < M) fa = fa + A.a[j] * (g * A.ct[j]);
+                    if (j < M) fa = fa + a[j] * (g * A.ct[j]);
             } else {
-                fa = A.a[0] * fld(A.iF0);
+                fa = a[0] * fld(A.iF0);
 #pragma unroll
                 for (int j = 1; j < ISDC_MAXM; ++j)
-                    if (j < M) fa = fa + A.a[j] * fld(A.iF0 + j);
+                    if (j < M) fa = fa + a[j] * fld(A.iF0 + j);
             }
             diff = diff - fa;
         }
         av = diff;
-        double acc = A.beta[0] * fld(A.iu0);
+        double acc = beta[0] * fld(A.iu0);
 #pragma unroll
         for (int j = 1; j < ISDC_MAXM; ++j)
-            if (j < M) acc = acc + A.beta[j] * fld(A.iu0 + j);
+            if (j < M) acc = acc + beta[j] * fld(A.iu0 + j);
         cv = acc;
     }
 }
 
-template <int FE, int MODE, int RR>
+// NM outputs per pass (RHS: 1; residual: nodes per pass).  Registers: 14 * RR * NM doubles of rings.
+template <int FE, int MODE, int RR, int NM>
 __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
     using SH = BLShape<RR>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const int K = A.K;
     double *Fs = reinterpret_cast<double *>(sm);                                   // ns stages x K boxes
-    double *Ps = reinterpret_cast<double *>(sm + (size_t)ns * K * SH::FPL);        // a[2], c[2]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + (size_t)ns * K * SH::FPL + 4 * SH::PPL);
+    double *Ps = reinterpret_cast<double *>(sm + (size_t)ns * K * SH::FPL);        // [buf][k][a|c]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + (size_t)ns * K * SH::FPL + 4 * NM * SH::PPL);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int n = A.n;
     const int x0 = blockIdx.x * SH::TX, y0 = blockIdx.y * SH::TY;
@@ -508,51 +524,66 @@ __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps map
     const int lx = lane - 1, ly0 = RR * w - 1;
     const int gx = x0 + lx;
     const bool xin = gx >= 0 && gx < n, xout = lx >= 0 && lx < SH::TX && gx < n;
-    bool yin[RR], yout[RR];
+    unsigned inxy = 0u, oks = 0u;
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
         const int ly = ly0 + r, gy = y0 + ly;
-        yin[r] = gy >= 0 && gy < n;
-        yout[r] = ly >= 0 && ly < SH::TY && gy < n;
+        if (xin && gy >= 0 && gy < n) inxy |= 1u << r;
+        if (xout && ly >= 0 && ly < SH::TY && gy < n) oks |= 1u << r;
     }
     const BLConst c = A.bl;
-    double vmax = 0.0;
-    BLRegs<RR> G;
+    double vmax[NM];
+    BLRegs<RR> G[NM];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) vmax[k] = 0.0;
+    double *orow = (MODE == 0) ? A.out + (long long)(z0 - 2) * A.plane + (long long)(y0 + ly0) * A.pitch + gx : nullptr;
     auto step = [&](auto Kc, int it) {
         constexpr int Kk = decltype(Kc)::value;
         constexpr int i3 = Kk % 3, m3 = (Kk + 2) % 3, mm3 = (Kk + 1) % 3;
         constexpr int i2 = Kk % 2, m2 = (Kk + 1) % 2;
         const int s = it % ns, p = z0 - 1 + it;
         mbar_wait(&bar[s], (it / ns) & 1);
-        const bool zin = p >= 0 && p < n;
+        const unsigned in = ((unsigned)p < (unsigned)n) ? inxy : 0u;
         const double *F = Fs + (size_t)s * K * (SH::FPL / 8);
-        double *Pa = Ps + (2 * i2) * (SH::PPL / 8), *Pc = Ps + (2 * i2 + 1) * (SH::PPL / 8);
+        const int o0 = (RR * w) * SH::FW + lane + 1;
+        const int po = (RR * w + 1) * SH::PW + lane + 1;
 #pragma unroll
         for (int r = 0; r < RR; ++r) {
-            double av = 0.0, cv = 0.0;
-            if (xin && yin[r] && zin) bl_point<FE, MODE>(A, F, SH::FPL / 8, (RR * w + r) * SH::FW + lane + 1, av, cv);
-            Pa[(RR * w + r + 1) * SH::PW + lane + 1] = av;
-            Pc[(RR * w + r + 1) * SH::PW + lane + 1] = cv;
+#pragma unroll
+            for (int k = 0; k < NM; ++k) {
+                double av = 0.0, cv = 0.0;
+                if ((in >> r) & 1u) bl_point<FE, MODE>(A, k, F, SH::FPL / 8, o0 + r * SH::FW, av, cv);
+                double *Pa = Ps + ((i2 * NM + k) * 2) * (SH::PPL / 8);
+                Pa[po + r * SH::PW] = av;
+                Pa[SH::PPL / 8 + po + r * SH::PW] = cv;
+            }
         }
         __syncthreads();
         if (tid == 0 && it + ns < nit) issue(it + ns);
-        double dummy[RR];
-        plane_partials<false, RR>(Pa, SH::PW, RR * w, lane, G.aq[i3], G.af[i3], dummy);
-        plane_partials<true, RR>(Pc, SH::PW, RR * w, lane, G.cq[i3], G.cf[i3], G.ce[i2]);
+#pragma unroll
+        for (int k = 0; k < NM; ++k) {
+            const double *Pa = Ps + ((i2 * NM + k) * 2) * (SH::PPL / 8), *Pc = Pa + SH::PPL / 8;
+            double dummy[RR];
+            plane_partials<false, RR>(Pa, SH::PW, RR * w, lane, G[k].aq[i3], G[k].af[i3], dummy);
+            plane_partials<true, RR>(Pc, SH::PW, RR * w, lane, G[k].cq[i3], G[k].cf[i3], G[k].ce[i2]);
+        }
         if (it >= 2) {   // output plane p-1
-            const int gz = p - 1;
-            double *op = (MODE == 0) ? A.out + (long long)gz * A.plane + (long long)(y0 + ly0) * A.pitch + gx : nullptr;
+            double *op = (MODE == 0) ? orow + (long long)it * A.plane : nullptr;
 #pragma unroll
             for (int r = 0; r < RR; ++r) {
-                const double fa_ = G.af[m3][r] + (G.aq[mm3][r] + G.aq[i3][r]);
-                const double fc_ = G.cf[m3][r] + (G.cq[mm3][r] + G.cq[i3][r]);
-                const double ec_ = G.ce[m2][r] + (G.cf[mm3][r] + G.cf[i3][r]);
-                const double Ba = c.kB0 * G.aq[m3][r] + c.kB1 * fa_;
-                const double Lc = (c.kL0 * G.cq[m3][r] + c.kL1 * fc_) + c.kL2 * ec_;
-                const double val = (MODE == 0) ? Ba + Lc : Ba - Lc;
-                if (xout && yout[r]) {
-                    if (MODE == 0) op[(long long)r * A.pitch] = val;
-                    vmax = amax(vmax, fabs(val));
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    const BLRegs<RR> &g = G[k];
+                    const double fa_ = g.af[m3][r] + (g.aq[mm3][r] + g.aq[i3][r]);
+                    const double fc_ = g.cf[m3][r] + (g.cq[mm3][r] + g.cq[i3][r]);
+                    const double ec_ = g.ce[m2][r] + (g.cf[mm3][r] + g.cf[i3][r]);
+                    const double Ba = c.kB0 * g.aq[m3][r] + c.kB1 * fa_;
+                    const double Lc = (c.kL0 * g.cq[m3][r] + c.kL1 * fc_) + c.kL2 * ec_;
+                    const double val = (MODE == 0) ? Ba + Lc : Ba - Lc;
+                    if ((oks >> r) & 1u) {
+                        if (MODE == 0) op[r * A.pitch] = val;
+                        vmax[k] = amax(vmax[k], fabs(val));
+                    }
                 }
             }
         }
@@ -565,7 +596,9 @@ __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps map
         if (base + 4 < nit) step(std::integral_constant<int, 4>{}, base + 4);
         if (base + 5 < nit) step(std::integral_constant<int, 5>{}, base + 5);
     }
-    if (A.slot) block_max_to(A.slot, vmax);
+#pragma unroll
+    for (int k = 0; k < NM; ++k)
+        if (A.slot[k]) { block_max_to(A.slot[k], vmax[k]); __syncthreads(); }
 }
 
 // ---------------------------------------------------------------------------------------------
