@@ -58,6 +58,7 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    bool stream2d = true;      // ISDC_STREAM2D=0: the tile-based 2D RHS / residual kernels instead
     int smooth3d_rows = 4;     // ISDC_SMOOTH3D_ROWS: rows per thread of the 3D fused smoother (2 or 4)
     int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
@@ -639,8 +640,44 @@ void fill_vw(isdc_ctx *h, VWParams &P, int m, double *const *uold, const double 
 
 bool fast2d_pointwise_fe(const isdc_ctx *h) { return h->fast && h->d == 2 && h->fe.kind <= 2 && h->n >= 63; }
 
+// 2D warp-strip streaming launch geometry: 8 strips of 30 columns per CTA
+dim3 stream2d_grid(const isdc_ctx *h, int &yc) {
+    const int n = h->n;
+    const int strips = (n + f2d::SW_OUT - 1) / f2d::SW_OUT;
+    const int cx = (strips + f2d::SW_NT / 32 - 1) / (f2d::SW_NT / 32);
+    yc = n >= 2047 ? 64 : (n >= 511 ? 32 : 16);
+    return dim3(cx, (n + yc - 1) / yc);
+}
+bool stream2d_ok(const isdc_ctx *h) { return fast2d_pointwise_fe(h) && (h->M == 3 || h->M == 5) && h->stream2d; }
+
 isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_m, double *bout, bool bnorm,
                     double *const *Fold = nullptr, const double *Fnew = nullptr) {
+    if (stream2d_ok(h)) {
+        f2d::StreamArgs A;
+        const int M = h->M;
+        for (int j = 0; j < M; ++j) A.u[j] = uold[j];
+        A.unew = unew_m; A.G = h->Gp; A.ct = h->ctdev;
+        A.M = M; A.m = m; A.n = h->n; A.pitch = h->lev[0].g.pitch;
+        double dt = h->P.dt, nu = h->P.nu, nudt = nu * dt;
+        A.dtm = dt * h->dtau[m];
+        A.gm = nu * A.dtm;
+        for (int j = 0; j < M; ++j) { A.a[0][j] = dt * h->S[m * M + j]; A.beta[0][j] = nudt * h->S[m * M + j]; }
+        A.bl = h->bl;
+        A.out = bout;
+        A.slot = nullptr;
+        if (bnorm) { TRY(clear_slots(h, SLOT_BNORM, 1)); A.slot = h->red + SLOT_BNORM; }
+        dim3 grd = stream2d_grid(h, A.yc);
+        ++h->launches;
+        int pe = prof_begin(h, PROF_RHS);
+        const int fe = h->fe.kind;
+#define ISDC_RS(FE_, M_) f2d::k_rhs_s<FE_, M_><<<grd, f2d::SW_NT, 0, h->s>>>(A)
+        if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
+        else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
+#undef ISDC_RS
+        prof_end(h, pe, PROF_RHS, (M + 2 + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, h->lev[0].g));
+        LAUNCH_CHECK(h);
+        return ISDC_OK;
+    }
     if (use_fast3d(h, 0, 8) && (h->fe.kind != 3 || (Fold && Fnew))) {
         const int M = h->M, fe = h->fe.kind;
         const double *fields[f3d::BL_MAXF];
@@ -741,6 +778,30 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             // algorithmic bytes of the whole residual: M node fields (+G) once, spread over the passes
             TRY(launch_bl<1>(h, fields, K, nm, A, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g) / passes));
         }
+        return ISDC_OK;
+    }
+    if (stream2d_ok(h)) {
+        f2d::StreamArgs A;
+        for (int j = 0; j < M; ++j) A.u[j] = u[j];
+        A.unew = nullptr; A.G = h->Gp; A.ct = h->ctdev;
+        A.M = M; A.m = 0; A.n = h->n; A.pitch = g.pitch;
+        A.dtm = A.gm = 0.0;
+        double dt = h->P.dt, nudt = h->P.nu * dt;
+        for (int m = 0; m < M; ++m)
+            for (int j = 0; j < M; ++j) { A.a[m][j] = dt * h->Q[m * M + j]; A.beta[m][j] = nudt * h->Q[m * M + j]; }
+        A.bl = h->bl;
+        A.out = nullptr;
+        A.slot = h->red + SLOT_RES0;
+        dim3 grd = stream2d_grid(h, A.yc);
+        ++h->launches;
+        int pe = prof_begin(h, PROF_RESID);
+        const int fe = h->fe.kind;
+#define ISDC_RS(FE_, M_) f2d::k_resid_s<FE_, M_><<<grd, f2d::SW_NT, 0, h->s>>>(A)
+        if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
+        else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
+#undef ISDC_RS
+        prof_end(h, pe, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
+        LAUNCH_CHECK(h);
         return ISDC_OK;
     }
     if (fast2d_pointwise_fe(h)) {
@@ -1001,6 +1062,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     h->fast = !(env && env[0] == '1');
     if (h->fast && !tma_encoder()) h->fast = false;
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
+    if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;

@@ -4,6 +4,7 @@
 #pragma once
 #include "common.cuh"
 #include "tma.cuh"
+#include <type_traits>
 
 namespace f2d {
 
@@ -446,6 +447,222 @@ __global__ void __launch_bounds__(ZNT) k_resid(ResArgs A, unsigned long long *sl
         }
         block_max_to(slots + (m - 1), rmax);
         __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Warp-strip y-streaming RHS / residual.  Every warp owns a 32-column
+// strip (lanes = columns x0-1 .. x0+30, outputs x0 .. x0+29) and walks down a chunk of rows:
+// per row it loads the node fields of its column (coalesced, two rows ahead in registers), forms
+// the pointwise values, takes x-neighbour sums with warp shuffles and keeps y rings in
+// registers, emitting row y-1 when row y arrives.  No shared memory, no block barriers.
+//   B q = kB0 q + kB1 f,   L q = (kL0 q + kL1 f) + kL2 e,
+//   r = q(x-1) + q(x+1),  f = r + (q(y-1) + q(y+1)),  e = r(y-1) + r(y+1)
+// ---------------------------------------------------------------------------------------------
+constexpr int SW_NT = 256;          // 8 warps = 8 strips per CTA
+constexpr int SW_OUT = 30;          // outputs per strip
+
+__device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+struct StreamArgs {
+    const double *u[ISDC_MAXM];     // RHS: old node fields; residual: current node fields
+    const double *unew;             // RHS: u_m^{k+1}
+    const double *G;                // forcing profile or null
+    const double *ct;               // device cos(t_j)
+    int M, m, n, pitch, yc;
+    double dtm, gm;                 // RHS
+    double a[ISDC_MAXM][ISDC_MAXM], beta[ISDC_MAXM][ISDC_MAXM];   // RHS: row 0 (dt S_mj, nu dt S_mj);
+                                                                  // residual: rows m (dt Q_mj, nu dt Q_mj)
+    BLConst bl;
+    double *out;                    // RHS b
+    unsigned long long *slot;       // RHS: ||b|| (optional); residual: per-node slots slot[m-1]
+};
+
+// fields loaded per row: u_0..u_{M-1}, [unew], [G], [u_{m+1}, u_m: L1 hits of the first M, loaded
+// by pointer so that no register array is indexed at run time]
+constexpr int SL_UN = 0, SL_G = 1, SL_UO1 = 2, SL_UOM = 3;
+template <int MODE, int FE, int MM>
+__device__ __forceinline__ void stream_load(const StreamArgs &A, long long off, bool in, double (&L)[MM + 4]) {
+#pragma unroll
+    for (int j = 0; j < MM; ++j) L[j] = in ? __ldcs(A.u[j] + off) : 0.0;
+    if (MODE == 0) {
+        L[MM + SL_UN] = in ? __ldcs(A.unew + off) : 0.0;
+        L[MM + SL_UO1] = in ? __ldg(A.u[A.m + 1] + off) : 0.0;
+        if (FE == 1) L[MM + SL_UOM] = in ? __ldg(A.u[A.m] + off) : 0.0;
+    }
+    if (FE == 2) L[MM + SL_G] = in ? __ldg(A.G + off) : 0.0;
+}
+
+template <int FE>
+__device__ __forceinline__ double fe_of(double u) { return u - (u * u) * u; }   // FE == 1
+
+template <int FE, int MM>
+__device__ __forceinline__ void rhs_row(const StreamArgs &A, const double (&L)[MM + 4], bool in, double &v, double &w) {
+    const int m = A.m;
+    double uj[MM];
+#pragma unroll
+    for (int j = 0; j < MM; ++j) uj[j] = L[j];
+    double acc = A.beta[0][0] * uj[0];
+#pragma unroll
+    for (int j = 1; j < MM; ++j)
+        acc = acc + A.beta[0][j] * uj[j];
+    const double uo1 = L[MM + SL_UO1], uom = L[MM + SL_UOM];
+    w = acc - A.gm * uo1;
+    const double un = L[MM + SL_UN];
+    if (FE == 0) {
+        v = un;
+    } else {
+        double fa, fn, fo;
+        if (FE == 1) {
+            fa = A.a[0][0] * fe_of<1>(uj[0]);
+#pragma unroll
+            for (int j = 1; j < MM; ++j)
+                fa = fa + A.a[0][j] * fe_of<1>(uj[j]);
+            fn = fe_of<1>(un);
+            fo = fe_of<1>(uom);
+        } else {
+            const double g = L[MM + SL_G];
+            fa = A.a[0][0] * (g * A.ct[0]);
+#pragma unroll
+            for (int j = 1; j < MM; ++j)
+                fa = fa + A.a[0][j] * (g * A.ct[j]);
+            fn = g * A.ct[m];
+            fo = g * A.ct[m];
+        }
+        v = (un + A.dtm * (fn - fo)) + fa;
+    }
+    if (!in) { v = 0.0; w = 0.0; }
+}
+
+template <int FE, int MM>
+__global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
+    const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5);
+    const int n = A.n;
+    const int x = strip * SW_OUT - 1 + lane;
+    if (strip * SW_OUT >= n) return;                 // whole warp leaves together
+    const int y0 = blockIdx.y * A.yc, y1 = min(y0 + A.yc, n);
+    const bool xin = x >= 0 && x < n, xout = lane >= 1 && lane <= SW_OUT && x < n;
+    const BLConst c = A.bl;
+    double L[3][MM + 4];
+    double vq[3], wq[3], vr[3], wr[3];
+    double bmax = 0.0;
+    const int nit = y1 - y0 + 2;                     // rows y0-1 .. y1
+    auto rowoff = [&](int y) { return (long long)y * A.pitch + x; };
+    auto load = [&](int it, double (&dst)[MM + 4]) {
+        const int y = y0 - 1 + it;
+        stream_load<0, FE, MM>(A, rowoff(y), xin && y >= 0 && y < n && it < nit, dst);
+    };
+    load(0, L[0]);
+    load(1, L[1]);
+    auto step = [&](auto Kc, int it) {
+        constexpr int k = decltype(Kc)::value;       // it % 3
+        constexpr int km1 = (k + 2) % 3, km2 = (k + 1) % 3;
+        load(it + 2, L[km1]);                        // slot of row it-1 is free (row it+2 = it-1 mod 3)
+        const int y = y0 - 1 + it;
+        const bool in = xin && y >= 0 && y < n;
+        double v, w;
+        rhs_row<FE, MM>(A, L[k], in, v, w);
+        vq[k] = v; wq[k] = w;
+        vr[k] = shfl_up1(v) + shfl_dn1(v);
+        wr[k] = shfl_up1(w) + shfl_dn1(w);
+        if (it >= 2 && xout) {                       // output row y-1
+            const double fv = vr[km1] + (vq[km2] + vq[k]);
+            const double fw = wr[km1] + (wq[km2] + wq[k]);
+            const double ew = wr[km2] + wr[k];
+            const double b = (c.kB0 * vq[km1] + c.kB1 * fv) + ((c.kL0 * wq[km1] + c.kL1 * fw) + c.kL2 * ew);
+            A.out[rowoff(y - 1)] = b;
+            bmax = amax(bmax, fabs(b));
+        }
+    };
+    for (int base = 0; base < nit; base += 3) {
+        step(std::integral_constant<int, 0>{}, base);
+        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
+    }
+    if (A.slot) {
+        unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(bmax));
+        if (lane == 0 && v) atomicMax(A.slot, v);
+    }
+}
+
+// residual of nodes m = 1..M-1 in one pass: p_m = (u_m - u_0) [- sum qa_mj fE(u_j)], z_m = sum qb_mj u_j,
+// r~_m = B p_m - L z_m, per-node max into slot[m-1]
+template <int FE, int MM>
+__global__ void __launch_bounds__(SW_NT) k_resid_s(StreamArgs A) {
+    const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5);
+    const int n = A.n;
+    const int x = strip * SW_OUT - 1 + lane;
+    if (strip * SW_OUT >= n) return;
+    const int y0 = blockIdx.y * A.yc, y1 = min(y0 + A.yc, n);
+    const bool xin = x >= 0 && x < n, xout = lane >= 1 && lane <= SW_OUT && x < n;
+    const BLConst c = A.bl;
+    double L[3][MM + 4];
+    double pq[MM - 1][3], pr[MM - 1][3], zq[MM - 1][3], zr[MM - 1][3];
+    double rmax[MM - 1];
+#pragma unroll
+    for (int m = 0; m < MM - 1; ++m) rmax[m] = 0.0;
+    const int nit = y1 - y0 + 2;
+    auto rowoff = [&](int y) { return (long long)y * A.pitch + x; };
+    auto load = [&](int it, double (&dst)[MM + 4]) {
+        const int y = y0 - 1 + it;
+        stream_load<1, FE, MM>(A, rowoff(y), xin && y >= 0 && y < n && it < nit, dst);
+    };
+    load(0, L[0]);
+    load(1, L[1]);
+    auto step = [&](auto Kc, int it) {
+        constexpr int k = decltype(Kc)::value;
+        constexpr int km1 = (k + 2) % 3, km2 = (k + 1) % 3;
+        load(it + 2, L[km1]);
+        const int y = y0 - 1 + it;
+        const bool in = xin && y >= 0 && y < n;
+        double uj[MM], fj[MM];
+#pragma unroll
+        for (int j = 0; j < MM; ++j) uj[j] = L[k][j];
+        if (FE == 1) {
+#pragma unroll
+            for (int j = 0; j < MM; ++j) fj[j] = fe_of<1>(uj[j]);
+        } else if (FE == 2) {
+            const double g = L[k][MM + SL_G];
+#pragma unroll
+            for (int j = 0; j < MM; ++j) fj[j] = g * A.ct[j];
+        }
+#pragma unroll
+        for (int m = 1; m < MM; ++m) {
+            double diff = uj[m] - uj[0];
+            if (FE != 0) {
+                double fa = A.a[m][0] * fj[0];
+#pragma unroll
+                for (int j = 1; j < MM; ++j) fa = fa + A.a[m][j] * fj[j];
+                diff = diff - fa;
+            }
+            double acc = A.beta[m][0] * uj[0];
+#pragma unroll
+            for (int j = 1; j < MM; ++j)
+                acc = acc + A.beta[m][j] * uj[j];
+            const double pv = in ? diff : 0.0, zv = in ? acc : 0.0;
+            pq[m - 1][k] = pv; zq[m - 1][k] = zv;
+            pr[m - 1][k] = shfl_up1(pv) + shfl_dn1(pv);
+            zr[m - 1][k] = shfl_up1(zv) + shfl_dn1(zv);
+            if (it >= 2 && xout) {
+                const double fp = pr[m - 1][km1] + (pq[m - 1][km2] + pq[m - 1][k]);
+                const double fz = zr[m - 1][km1] + (zq[m - 1][km2] + zq[m - 1][k]);
+                const double ez = zr[m - 1][km2] + zr[m - 1][k];
+                const double Bp = c.kB0 * pq[m - 1][km1] + c.kB1 * fp;
+                const double Lz = (c.kL0 * zq[m - 1][km1] + c.kL1 * fz) + c.kL2 * ez;
+                rmax[m - 1] = amax(rmax[m - 1], fabs(Bp - Lz));
+            }
+        }
+    };
+    for (int base = 0; base < nit; base += 3) {
+        step(std::integral_constant<int, 0>{}, base);
+        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
+    }
+#pragma unroll
+    for (int m = 0; m < MM - 1; ++m) {
+        unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(rmax[m]));
+        if (lane == 0 && v) atomicMax(A.slot + m, v);
     }
 }
 
