@@ -58,6 +58,7 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
     bool stream2d = true;      // ISDC_STREAM2D=0: the tile-based 2D RHS / residual kernels instead
     int smooth3d_rows = 4;     // ISDC_SMOOTH3D_ROWS: rows per thread of the 3D fused smoother (2 or 4)
     int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
@@ -335,18 +336,25 @@ isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const 
 }
 
 // two fused Jacobi sweeps on the fine 2D level
+// in == nullptr: the iterate is zero (nothing read).  e != nullptr: u + P e first (fused prolongation).
 isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
-                           const SCoef &c, unsigned long long *norm_slot, int level) {
-    const CUtensorMap *mu = tmap(h, in, g, f2d::UW, f2d::UH);
+                           const SCoef &c, unsigned long long *norm_slot, int level, const double *e = nullptr,
+                           const GridDesc *gc = nullptr) {
     const CUtensorMap *mb = tmap(h, b, g, f2d::BW, f2d::BH);
-    if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    const CUtensorMap *mu = in ? tmap(h, in, g, f2d::UW, f2d::UH) : mb;
+    const CUtensorMap *me = e ? tmap(h, e, *gc, f2d::EW, f2d::EH) : mb;
+    if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
-    int pe = prof_begin(h, level == 0 ? PROF_SMOOTH : PROF_COARSE);
+    const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
+    int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + f2d::TY - 1) / f2d::TY);
     size_t sm = sizeof(f2d::SmemSmooth) + 128;
-    if (norm_slot) f2d::k_smooth2<true><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, norm_slot);
-    else f2d::k_smooth2<false><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr);
-    prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
+    if (norm_slot) f2d::k_smooth2<true, 0><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
+    else if (e) f2d::k_smooth2<false, 2><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    else if (!in) f2d::k_smooth2<false, 1><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    else f2d::k_smooth2<false, 0><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    // algorithmic bytes: read u (unless zero), b (+ e / 4); write u''
+    prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 2.0 : 0.0)) * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -578,27 +586,48 @@ isdc_status smooth(isdc_ctx *h, int l, double *X, double *T, const double *b, co
 // X holds the iterate on exit; src (nullable) is the initial iterate when it lives elsewhere
 // (first cycle of a node solve reads u_{m+1}^k in place, never writing it).
 // ---------------------------------------------------------------------------------------------
+isdc_status tail_dispatch(isdc_ctx *h, const TailParams &P, bool attr_only = false) {
+    if (attr_only) {
+        cudaError_t e = (h->d == 2)
+            ? cudaFuncSetAttribute(k_tail<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem)
+            : cudaFuncSetAttribute(k_tail<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem);
+        return e == cudaSuccess ? ISDC_OK : ISDC_ERR_CUDA;
+    }
+    if (h->d == 2) k_tail<2><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
+    else k_tail<3><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
+    return ISDC_OK;
+}
+
 isdc_status launch_tail(isdc_ctx *h, int l, int m, const double *b, const double *u_in, double *u_out) {
     TailParams P = h->tailp[m];
     P.b_in = b; P.u_in = u_in; P.u_out = u_out;
     P.pitch = h->lev[l].g.pitch;
     ++h->launches;
     int pe = prof_begin(h, l == 0 ? PROF_SMOOTH : PROF_COARSE);
-    if (h->d == 2) k_tail<2><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
-    else k_tail<3><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
+    TRY(tail_dispatch(h, P));
     prof_end(h, pe, l == 0 ? PROF_SMOOTH : PROF_COARSE, 16.0 * npts_of(h, h->lev[l].g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
 
-isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double *b, const double *src) {
+// zero_init: the iterate is zero (coarse-grid correction); X need not hold zeros
+isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double *b, const double *src,
+                   bool zero_init = false) {
     Level &L = h->lev[l];
     const GridDesc &g = L.g;
-    if (l == h->tail_l0) return launch_tail(h, l, m, b, src ? src : X, X);
+    if (l == h->tail_l0) return launch_tail(h, l, m, b, zero_init ? nullptr : (src ? src : X), X);
     if (g.n == 3) return launch_coarse(h, X, b, g, m);
     const SCoef &c = L.coef[m];
     const double *cur = src ? src : X;
-    TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1));
+    if (zero_init && use_fast2d(h, l) && h->fuse2d && h->P.mg.nu1 >= 2) {
+        // first smoothing from the zero iterate: no memset, no read (same expressions on zeros)
+        TRY(launch_smooth2(h, T, nullptr, b, g, c, nullptr, l));
+        cur = T;
+        TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1 - 2));
+    } else {
+        if (zero_init) TRY(zero_field(h, X, g));
+        TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1));
+    }
     double *curw;
     if (cur != X && cur != T) {  // nu1 == 0 with a foreign initial iterate
         TRY(copy_field(h, X, cur, g));
@@ -611,12 +640,19 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
     if (l + 1 == h->tail_l0) {
         TRY(launch_tail(h, l + 1, m, C.b, nullptr, C.e));
     } else {
-        TRY(zero_field(h, C.e, C.g));
-        TRY(vcycle(h, l + 1, m, C.e, C.t, C.b, nullptr));
+        TRY(vcycle(h, l + 1, m, C.e, C.t, C.b, nullptr, true));
     }
-    TRY(launch_prolong(h, curw, g, C.e, C.g, l));
     const double *cu = curw;
-    TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2));
+    if (use_fast2d(h, l) && h->fuse2d && h->P.mg.nu2 >= 2) {
+        // fused bilinear prolongation + correction + two sweeps (one pass)
+        double *dst = (curw == T) ? X : T;
+        TRY(launch_smooth2(h, dst, curw, b, g, c, nullptr, l, C.e, &C.g));
+        cu = dst;
+        TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2 - 2));
+    } else {
+        TRY(launch_prolong(h, curw, g, C.e, C.g, l));
+        TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2));
+    }
     if (cu != X) TRY(copy_field(h, X, cu, g));
     return ISDC_OK;
 }
@@ -1063,6 +1099,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (h->fast && !tma_encoder()) h->fast = false;
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
+    if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;
@@ -1072,9 +1109,13 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     }
     static bool attrs = false;
     if (!attrs) {
-        cudaFuncSetAttribute(f2d::k_smooth2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(f2d::k_smooth2<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSmooth) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(f2d::k_smooth2<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSmooth) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSmooth) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSmooth) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
@@ -1127,10 +1168,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                 T.b_in = nullptr; T.u_in = nullptr; T.u_out = nullptr; T.pitch = 0;
             }
             h->tail_smem = (h->d == 2) ? tail_smem_bytes<2>(h->tailp[0]) : tail_smem_bytes<3>(h->tailp[0]);
-            cudaError_t ea = (h->d == 2)
-                ? cudaFuncSetAttribute(k_tail<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem)
-                : cudaFuncSetAttribute(k_tail<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem);
-            if (ea != cudaSuccess) h->tail_l0 = -1;
+            if (h->tailp[0].nlev > TAIL_MAX_LEVELS || tail_dispatch(h, h->tailp[0], true) != ISDC_OK) h->tail_l0 = -1;
         }
     }
     cudaError_t e = cudaMemcpyAsync(h->Ginv, Gi.data(), Gi.size() * sizeof(double), cudaMemcpyHostToDevice, h->s);

@@ -21,34 +21,63 @@ constexpr int UW = TX + 4, UH = TY + 4;
 constexpr int BW = TX + 4, BH = TY + 2;
 constexpr int TW = TX + 2, TH = TY + 2;
 
+// MODE 0: u from memory.  MODE 1: u == 0 (first smoothing of a coarse correction: nothing is
+// read, the same expressions run on zeros).  MODE 2: u + P e first (fused bilinear prolongation
+// + correction): coarse box EW x EH at (x0/2 - 2, y0/2 - 2) by TMA (zero fill
+// = the coarse zero ring), correction applied to every in-domain point of the u box.
+constexpr int EW = 36, EH = 19;
+
 struct __align__(128) SmemSmooth {
     alignas(128) double u[UH][UW];
     alignas(128) double b[BH][BW];
     alignas(128) double t[TH][TW];
+    alignas(128) double e[EH][EW];
     uint64_t bar;
 };
 
-template <bool NORM>
+template <bool NORM, int MODE = 0>
 __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensorMap tu,
                                                 const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
-                                                int n, int pitch, SCoef c, unsigned long long *slot) {
+                                                int n, int pitch, SCoef c, unsigned long long *slot,
+                                                const __grid_constant__ CUtensorMap te) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemSmooth &S = *reinterpret_cast<SmemSmooth *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     if (tid == 0) {
-        tma_prefetch_desc(&tu);
+        if (MODE != 1) tma_prefetch_desc(&tu);
         tma_prefetch_desc(&tb);
         mbar_init(&S.bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (tid == 0) {
-        mbar_expect_tx(&S.bar, (UW * UH + BW * BH) * 8);
-        tma_load_2d(&S.u[0][0], &tu, x0 - 2, y0 - 2, &S.bar);
+        mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : UW * UH) + BW * BH + (MODE == 2 ? EW * EH : 0)) * 8);
+        if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 - 2, y0 - 2, &S.bar);
         tma_load_2d(&S.b[0][0], &tb, x0 - 2, y0 - 1, &S.bar);
+        if (MODE == 2) tma_load_2d(&S.e[0][0], &te, x0 / 2 - 2, y0 / 2 - 2, &S.bar);
+    }
+    if (MODE == 1) {
+        for (int q = tid; q < UW * UH; q += NT) (&S.u[0][0])[q] = 0.0;
+        __syncthreads();   // every thread reads zeros written by others
     }
     mbar_wait(&S.bar, 0);
+    if (MODE == 2) {
+        // u += P e on the u box (fine (x0-2+lx, y0-2+ly)); local coarse index of the pair / single
+        // coarse neighbour: even lx -> (lx/2, lx/2+1), odd lx -> (lx+1)/2 (same for rows)
+        for (int q = tid; q < UW * UH; q += NT) {
+            const int lx = q % UW, ly = q / UW;
+            const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
+            if (gx < 0 || gx >= n || gy < 0 || gy >= n) continue;
+            const bool xe = !(lx & 1), ye = !(ly & 1);
+            const int xa = xe ? lx / 2 : (lx + 1) / 2, ya = ye ? ly / 2 : (ly + 1) / 2;
+            auto sx = [&](int r) { return xe ? S.e[r][xa] + S.e[r][xa + 1] : S.e[r][xa]; };
+            const double sz = ye ? sx(ya) + sx(ya + 1) : sx(ya);
+            const double w = xe ? (ye ? 0.25 : 0.5) : (ye ? 0.5 : 1.0);
+            S.u[ly][lx] = S.u[ly][lx] + sz * w;
+        }
+        __syncthreads();
+    }
 
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
     double dmax = 0.0;
