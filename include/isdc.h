@@ -170,13 +170,14 @@ isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold_dev,
  * CUDA-graph launch (launch accounting). */
 long isdc_kernel_launches(isdc_handle h);
 
-/* Live kernel timing (bench.py's roofline): on = 1 brackets every fine-level smoother launch (the
- * dominant kernel) with CUDA events on the handle's stream, on = 2 every launch of every class,
- * on = 0 none (events inside CUDA graphs are captured as external event-record nodes).  Classes: 0 fine-level smoother pass, 1 fine
- * defect+restriction, 2 fine prolongation+correction, 3 RHS assembly, 4 residual, 5 coarse levels.
+/* Live kernel timing (bench.py's roofline): on = 1 brackets every fine-level launch (classes 0-2)
+ * with CUDA events on the handle's stream, on = 2 every launch of every class, on = 16 + c only
+ * class c, on = 0 none (events inside CUDA graphs are captured as external event-record nodes).
+ * Classes: 0 fine-level smoother pass, 1 fine (pre-smoother +) defect + restriction, 2 fine
+ * prolongation + correction (+ post-smoother), 3 RHS assembly, 4 residual, 5 coarse levels.
  * isdc_profile_get synchronises, returns the summed event time (ms), the launch count and the
  * ALGORITHMIC bytes those launches must move, and keeps accumulating. */
-isdc_status isdc_profile_enable(isdc_handle h, int on);
+isdc_status isdc_profile_enable(isdc_handle h, int on);   /* 0 off, 1 fine-level classes 0-2, 2 all, 16+c class c only */
 isdc_status isdc_profile_reset(isdc_handle h);
 isdc_status isdc_profile_get(isdc_handle h, int cls, double *total_ms, long *launches, double *alg_bytes);
 

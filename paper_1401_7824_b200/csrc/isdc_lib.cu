@@ -248,7 +248,9 @@ int prof_event(isdc_ctx *h) {
 }
 // returns a pending-record index (or -1 when profiling is off)
 int prof_begin(isdc_ctx *h, int cls) {
-    if (h->prof == 0 || (h->prof == 1 && cls != PROF_SMOOTH)) return -1;
+    // mode 1 (bench's timed region): the fine-level kernel classes only
+    if (h->prof == 0 || (h->prof == 1 && cls != PROF_SMOOTH && cls != PROF_RESTRICT && cls != PROF_PROLONG)) return -1;
+    if (h->prof >= 16 && cls != h->prof - 16) return -1;
     int a = prof_event(h);
     if (a < 0) return -1;
     cudaEventRecordWithFlags(h->evpool[a], h->s, h->capturing ? cudaEventRecordExternal : 0);
@@ -423,6 +425,25 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
 #undef ISDC_BL_FE
 #undef ISDC_BL
     prof_end(h, pe, prof_cls, bytes);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
+// fused pre-smoother (2 sweeps) + defect + full weighting, 2D; in == nullptr: zero iterate
+isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
+                            double *bc, const GridDesc &gc, const SCoef &c, int level) {
+    const CUtensorMap *mb = tmap(h, b, g, f2d::FR_BW, f2d::FR_BH);
+    const CUtensorMap *mu = in ? tmap(h, in, g, f2d::FR_UW, f2d::FR_UH) : mb;
+    if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    ++h->launches;
+    const int cls = level == 0 ? PROF_RESTRICT : PROF_COARSE;
+    int pe = prof_begin(h, cls);
+    dim3 grd((g.n + f2d::FR_TX - 1) / f2d::FR_TX, (g.n + f2d::FR_TY - 1) / f2d::FR_TY);
+    size_t sm = sizeof(f2d::SmemSR) + 128;
+    if (in) f2d::k_smooth2r<0><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    else f2d::k_smooth2r<1><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    // algorithmic bytes: read u (unless zero), b; write u'', b_c
+    prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + 2.0) * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -619,24 +640,29 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
     if (g.n == 3) return launch_coarse(h, X, b, g, m);
     const SCoef &c = L.coef[m];
     const double *cur = src ? src : X;
-    if (zero_init && use_fast2d(h, l) && h->fuse2d && h->P.mg.nu1 >= 2) {
-        // first smoothing from the zero iterate: no memset, no read (same expressions on zeros)
-        TRY(launch_smooth2(h, T, nullptr, b, g, c, nullptr, l));
-        cur = T;
-        TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1 - 2));
+    Level &C = h->lev[l + 1];
+    double *curw;
+    if (use_fast2d(h, l) && h->fuse2d && h->P.mg.nu1 >= 2) {
+        // last two pre-sweeps fused with the defect and full weighting (one pass); a zero
+        // iterate is neither stored nor read (same expressions on zeros)
+        bool zero = zero_init;
+        if (h->P.mg.nu1 > 2) {
+            if (zero) { TRY(zero_field(h, X, g)); zero = false; }
+            TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1 - 2));
+        }
+        curw = (cur == T) ? X : T;
+        TRY(launch_smooth2r(h, curw, zero ? nullptr : cur, b, g, C.b, C.g, c, l));
     } else {
         if (zero_init) TRY(zero_field(h, X, g));
         TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1));
+        if (cur != X && cur != T) {  // nu1 == 0 with a foreign initial iterate
+            TRY(copy_field(h, X, cur, g));
+            curw = X;
+        } else {
+            curw = const_cast<double *>(cur);
+        }
+        TRY(launch_restrict(h, C.b, C.g, curw, b, g, c, l));
     }
-    double *curw;
-    if (cur != X && cur != T) {  // nu1 == 0 with a foreign initial iterate
-        TRY(copy_field(h, X, cur, g));
-        curw = X;
-    } else {
-        curw = const_cast<double *>(cur);
-    }
-    Level &C = h->lev[l + 1];
-    TRY(launch_restrict(h, C.b, C.g, curw, b, g, c, l));
     if (l + 1 == h->tail_l0) {
         TRY(launch_tail(h, l + 1, m, C.b, nullptr, C.e));
     } else {
@@ -829,10 +855,14 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         A.out = nullptr;
         A.slot = h->red + SLOT_RES0;
         dim3 grd = stream2d_grid(h, A.yc);
+        if (M == 5) {   // two warps per strip (2 nodes each): 4 strips per CTA
+            const int strips = (h->n + f2d::SW_OUT - 1) / f2d::SW_OUT;
+            grd.x = (strips + 3) / 4;
+        }
         ++h->launches;
         int pe = prof_begin(h, PROF_RESID);
         const int fe = h->fe.kind;
-#define ISDC_RS(FE_, M_) f2d::k_resid_s<FE_, M_><<<grd, f2d::SW_NT, 0, h->s>>>(A)
+#define ISDC_RS(FE_, M_) f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1)><<<grd, f2d::SW_NT, 0, h->s>>>(A)
         if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
         else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
 #undef ISDC_RS
@@ -1117,6 +1147,10 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSmooth) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSmooth) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
         cudaFuncSetAttribute(f3d::k_smooth2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
@@ -1188,6 +1222,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
 
 isdc_status isdc_profile_enable(isdc_handle h, int on) {
     if (!h) return ISDC_ERR_INVALID_ARG;
+    if (on >= 16 && on < 16 + 8) { h->prof = on; return ISDC_OK; }   // one class only (16 + class)
     h->prof = on < 0 ? 0 : (on > 2 ? 2 : on);
     return ISDC_OK;
 }

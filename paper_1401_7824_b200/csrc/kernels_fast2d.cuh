@@ -16,7 +16,8 @@ namespace f2d {
 // (w & 1) of a band of rows (w >> 1); each lane rolls a 3-row register window down its column.
 // Optional: NORM -> ||b - S u||_inf over the tile (the SDC defect test of the incoming iterate).
 // ---------------------------------------------------------------------------------------------
-constexpr int TX = 64, TY = 32, NT = 256;
+constexpr int TX = 64, TY = 16, NT = 256;   // 16-row tiles: ~33 KB smem -> 6 CTAs / SM to overlap TMA and compute
+constexpr int SB1 = (TY + 2 + 3) / 4, SB2 = TY / 4;   // rows per warp band in sweep 1 / sweep 2
 constexpr int UW = TX + 4, UH = TY + 4;
 constexpr int BW = TX + 4, BH = TY + 2;
 constexpr int TW = TX + 2, TH = TY + 2;
@@ -25,7 +26,7 @@ constexpr int TW = TX + 2, TH = TY + 2;
 // read, the same expressions run on zeros).  MODE 2: u + P e first (fused bilinear prolongation
 // + correction): coarse box EW x EH at (x0/2 - 2, y0/2 - 2) by TMA (zero fill
 // = the coarse zero ring), correction applied to every in-domain point of the u box.
-constexpr int EW = 36, EH = 19;
+constexpr int EW = 36, EH = TY / 2 + 3;
 
 struct __align__(128) SmemSmooth {
     alignas(128) double u[UH][UW];
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
     // ---- sweep 1, main columns 0..63 of the t region (rows -1..32, 4 bands of 9 rows)
     {
         const int band = w >> 1, hh = w & 1;
-        const int rs = -1 + 9 * band, re = min(rs + 9, TY + 1);
+        const int rs = -1 + SB1 * band, re = min(rs + SB1, TY + 1);
         {
             const int x = lane + 32 * hh;          // tile column; u smem col x+2
             const int gx = x0 + x;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
     // ---- sweep 2 on the 64 x 32 tile (4 bands of 8 rows)
     {
         const int band = w >> 1, hh = w & 1;
-        const int rs = 8 * band, re = rs + 8;
+        const int rs = SB2 * band, re = rs + SB2;
         {
             const int x = lane + 32 * hh;          // t smem col x+1
             const int gx = x0 + x;
@@ -616,10 +617,15 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
 }
 
 // residual of nodes m = 1..M-1 in one pass: p_m = (u_m - u_0) [- sum qa_mj fE(u_j)], z_m = sum qb_mj u_j,
-// r~_m = B p_m - L z_m, per-node max into slot[m-1]
-template <int FE, int MM>
-__global__ void __launch_bounds__(SW_NT) k_resid_s(StreamArgs A) {
-    const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5);
+// r~_m = B p_m - L z_m, per-node max into slot[m-1].  The M-1 nodes are split over G = (M-1)/NMW
+// warps per strip (NMW nodes each; the extra loads of the same rows hit L1/L2), which halves the
+// register rings and doubles the resident warps.
+template <int FE, int MM, int NMW>
+__global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {
+    constexpr int G = (MM - 1) / NMW;
+    const int wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32 / G) + wid / G;
+    const int m0 = 1 + NMW * (wid % G);
     const int n = A.n;
     const int x = strip * SW_OUT - 1 + lane;
     if (strip * SW_OUT >= n) return;
@@ -627,10 +633,10 @@ __global__ void __launch_bounds__(SW_NT) k_resid_s(StreamArgs A) {
     const bool xin = x >= 0 && x < n, xout = lane >= 1 && lane <= SW_OUT && x < n;
     const BLConst c = A.bl;
     double L[3][MM + 4];
-    double pq[MM - 1][3], pr[MM - 1][3], zq[MM - 1][3], zr[MM - 1][3];
-    double rmax[MM - 1];
+    double pq[NMW][3], pr[NMW][3], zq[NMW][3], zr[NMW][3];
+    double rmax[NMW];
 #pragma unroll
-    for (int m = 0; m < MM - 1; ++m) rmax[m] = 0.0;
+    for (int m = 0; m < NMW; ++m) rmax[m] = 0.0;
     const int nit = y1 - y0 + 2;
     auto rowoff = [&](int y) { return (long long)y * A.pitch + x; };
     auto load = [&](int it, double (&dst)[MM + 4]) {
@@ -657,8 +663,13 @@ __global__ void __launch_bounds__(SW_NT) k_resid_s(StreamArgs A) {
             for (int j = 0; j < MM; ++j) fj[j] = g * A.ct[j];
         }
 #pragma unroll
-        for (int m = 1; m < MM; ++m) {
-            double diff = uj[m] - uj[0];
+        for (int mm = 0; mm < NMW; ++mm) {
+            const int m = m0 + mm;
+            double um = uj[0];
+#pragma unroll
+            for (int j = 1; j < MM; ++j)
+                if (j == m) um = uj[j];
+            double diff = um - uj[0];
             if (FE != 0) {
                 double fa = A.a[m][0] * fj[0];
 #pragma unroll
@@ -670,16 +681,16 @@ __global__ void __launch_bounds__(SW_NT) k_resid_s(StreamArgs A) {
             for (int j = 1; j < MM; ++j)
                 acc = acc + A.beta[m][j] * uj[j];
             const double pv = in ? diff : 0.0, zv = in ? acc : 0.0;
-            pq[m - 1][k] = pv; zq[m - 1][k] = zv;
-            pr[m - 1][k] = shfl_up1(pv) + shfl_dn1(pv);
-            zr[m - 1][k] = shfl_up1(zv) + shfl_dn1(zv);
+            pq[mm][k] = pv; zq[mm][k] = zv;
+            pr[mm][k] = shfl_up1(pv) + shfl_dn1(pv);
+            zr[mm][k] = shfl_up1(zv) + shfl_dn1(zv);
             if (it >= 2 && xout) {
-                const double fp = pr[m - 1][km1] + (pq[m - 1][km2] + pq[m - 1][k]);
-                const double fz = zr[m - 1][km1] + (zq[m - 1][km2] + zq[m - 1][k]);
-                const double ez = zr[m - 1][km2] + zr[m - 1][k];
-                const double Bp = c.kB0 * pq[m - 1][km1] + c.kB1 * fp;
-                const double Lz = (c.kL0 * zq[m - 1][km1] + c.kL1 * fz) + c.kL2 * ez;
-                rmax[m - 1] = amax(rmax[m - 1], fabs(Bp - Lz));
+                const double fp = pr[mm][km1] + (pq[mm][km2] + pq[mm][k]);
+                const double fz = zr[mm][km1] + (zq[mm][km2] + zq[mm][k]);
+                const double ez = zr[mm][km2] + zr[mm][k];
+                const double Bp = c.kB0 * pq[mm][km1] + c.kB1 * fp;
+                const double Lz = (c.kL0 * zq[mm][km1] + c.kL1 * fz) + c.kL2 * ez;
+                rmax[mm] = amax(rmax[mm], fabs(Bp - Lz));
             }
         }
     };
@@ -689,9 +700,131 @@ __global__ void __launch_bounds__(SW_NT) k_resid_s(StreamArgs A) {
         if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
     }
 #pragma unroll
-    for (int m = 0; m < MM - 1; ++m) {
-        unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(rmax[m]));
-        if (lane == 0 && v) atomicMax(A.slot + m, v);
+    for (int mm = 0; mm < NMW; ++mm) {
+        unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(rmax[mm]));
+        if (lane == 0 && v) atomicMax(A.slot + m0 - 1 + mm, v);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused pre-smoother + defect + full-weighting restriction: one pass reads
+// u, b and writes the smoothed iterate u'' (tile) and b_c = R(b - S u'') (coarse tile), 26 B per
+// fine point instead of 24 + 18.  Fine tile 58 x 32 at (x0, y0), coarse tile 29 x 16 at
+// (x0/2, y0/2).  Local regions (x, y relative to the tile origin):
+//   t   (sweep 1)  [-2, 60] x [-2, 34]      u'' (sweep 2)  [-1, 59] x [-1, 33]
+//   d   (defect)   [ 0, 58] x [ 0, 32]      u box [-4, 61] x [-3, 35],  b box [-2, 61] x [-2, 34]
+// u'' overwrites the u buffer after sweep 1, d overwrites the t buffer after sweep 2.
+// MODE 0: u from memory; MODE 1: u == 0 (nothing read).
+// ---------------------------------------------------------------------------------------------
+constexpr int FR_TX = 58, FR_TY = 16, FR_CX = 29, FR_CY = FR_TY / 2;
+constexpr int FR_UW = 66, FR_UH = FR_TY + 7, FR_UOX = -4, FR_UOY = -3;
+constexpr int FR_BW = 64, FR_BH = FR_TY + 5, FR_BOX = -2, FR_BOY = -2;
+constexpr int FR_TW = 64, FR_TH = FR_TY + 5, FR_TOX = -2, FR_TOY = -2;
+
+struct __align__(128) SmemSR {
+    alignas(128) double u[FR_UH][FR_UW];
+    alignas(128) double b[FR_BH][FR_BW];
+    alignas(128) double t[FR_TH][FR_TW];
+    uint64_t bar;
+};
+
+// one stencil phase over the region [xs, xs+w) x [ys, ys+h): 2 column chunks of 32 lanes x 4 row
+// bands, one (chunk, band) per warp, rolling a 3-row register window down each column.
+// src/dst are arrays with origins (sox, soy) / (dox, doy) and row lengths sw / dw.
+template <int KIND, int SW_, int DW_>
+__device__ __forceinline__ void fr_phase(const double *__restrict__ src, int sox, int soy, double *__restrict__ dst,
+                                         int dox, int doy, const double *__restrict__ B, int xs, int w, int ys,
+                                         int h, int x0, int y0, int n, const SCoef &c, double *__restrict__ gout,
+                                         int pitch) {
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int chunk = wp & 1, band = wp >> 1;
+    const int bh = (h + 3) / 4;
+    const int x = xs + 32 * chunk + lane;
+    const int r0 = ys + band * bh, r1 = min(r0 + bh, ys + h);
+    if (x >= xs + w || r0 >= r1) return;
+    const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
+    // row pointers advanced by one row per step (no per-access index arithmetic)
+    const double *sp = src + (r0 - 1 - soy) * SW_ + (x - sox);          // row y-1, column x
+    const double *bp = B + (r0 - FR_BOY) * FR_BW + (x - FR_BOX);
+    double *dp = dst + (r0 - doy) * DW_ + (x - dox);
+    double um = sp[0], rm = sp[-1] + sp[1];
+    sp += SW_;
+    double uc = sp[0], rc = sp[-1] + sp[1];
+    const int gx = x0 + x;
+    const bool xin = gx >= 0 && gx < n;
+    const bool xt = KIND == 1 && x >= 0 && x < FR_TX && xin;
+    double *gp = (KIND == 1) ? gout + (long long)(y0 + r0) * pitch + gx : nullptr;
+    int gy = y0 + r0;
+#pragma unroll 2
+    for (int y = r0; y < r1; ++y) {
+        sp += SW_;
+        const double up = sp[0], rp = sp[-1] + sp[1];
+        const double f = rc + (um + up);
+        const double e = rm + rp;
+        const double su = (c0 * uc + c1 * f) + c2 * e;
+        const double bv = *bp;
+        const bool in = xin && (unsigned)gy < (unsigned)n;
+        double v;
+        if (KIND == 2) v = bv - su;                                   // defect
+        else v = in ? uc + wd * (bv - su) : 0.0;                     // Jacobi (zero outside)
+        *dp = v;
+        if (KIND == 1 && xt && y >= 0 && y < FR_TY && gy < n) *gp = v;
+        um = uc; uc = up; rm = rc; rc = rp;
+        bp += FR_BW; dp += DW_; ++gy;
+        if (KIND == 1) gp += pitch;
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtensorMap tu,
+                                                 const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
+                                                 double *__restrict__ bc, int n, int pitch, int nc, int pitch_c,
+                                                 SCoef c) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SmemSR &S = *reinterpret_cast<SmemSR *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * FR_TX, y0 = blockIdx.y * FR_TY;
+    if (tid == 0) {
+        if (MODE != 1) tma_prefetch_desc(&tu);
+        tma_prefetch_desc(&tb);
+        mbar_init(&S.bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : FR_UW * FR_UH) + FR_BW * FR_BH) * 8);
+        if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 + FR_UOX, y0 + FR_UOY, &S.bar);
+        tma_load_2d(&S.b[0][0], &tb, x0 + FR_BOX, y0 + FR_BOY, &S.bar);
+    }
+    if (MODE == 1) {
+        for (int q = tid; q < FR_UW * FR_UH; q += NT) (&S.u[0][0])[q] = 0.0;
+        __syncthreads();
+    }
+    mbar_wait(&S.bar, 0);
+    const double *Bp = &S.b[0][0];
+    // sweep 1: u -> t on [-2, 60] x [-2, 34]
+    fr_phase<0, FR_UW, FR_TW>(&S.u[0][0], FR_UOX, FR_UOY, &S.t[0][0], FR_TOX, FR_TOY, Bp, -2, 63, -2, FR_TY + 5, x0, y0, n,
+                              c, nullptr, pitch);
+    __syncthreads();
+    // sweep 2: t -> u'' (into the u buffer) on [-1, 59] x [-1, 33]; the tile goes to global
+    fr_phase<1, FR_TW, FR_UW>(&S.t[0][0], FR_TOX, FR_TOY, &S.u[0][0], FR_UOX, FR_UOY, Bp, -1, 61, -1, FR_TY + 3, x0, y0, n,
+                              c, out, pitch);
+    __syncthreads();
+    // defect: d = b - S u'' (into the t buffer) on [0, 58] x [0, 32]
+    fr_phase<2, FR_UW, FR_TW>(&S.u[0][0], FR_UOX, FR_UOY, &S.t[0][0], FR_TOX, FR_TOY, Bp, 0, 59, 0, FR_TY + 1, x0, y0, n, c,
+                              nullptr, pitch);
+    __syncthreads();
+    // full weighting: coarse (I, J) <-> local fine (2I+1, 2J+1)
+    for (int p = tid; p < FR_CX * FR_CY; p += NT) {
+        const int I = p % FR_CX, J = p / FR_CX;
+        const int gI = x0 / 2 + I, gJ = y0 / 2 + J;
+        if (gI >= nc || gJ >= nc) continue;
+        const double *d0 = &S.t[2 * J - FR_TOY][2 * I + 1 - FR_TOX];   // row 2J (fine y = 2J), column 2I+1
+        const double *d1 = d0 + FR_TW, *d2 = d1 + FR_TW;
+        const double rd0 = d0[-1] + d0[1], rd1 = d1[-1] + d1[1], rd2 = d2[-1] + d2[1];
+        const double fd = rd1 + (d0[0] + d2[0]);
+        const double ed = rd0 + rd2;
+        bc[(long long)gJ * pitch_c + gI] = ((4.0 * d1[0] + 2.0 * fd) + ed) * 0.0625;
     }
 }
 

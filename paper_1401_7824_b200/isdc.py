@@ -102,6 +102,8 @@ EXPORTED = ["isdc_workspace_bytes", "isdc_create", "isdc_set_initial", "isdc_set
             "isdc_destroy", "isdc_last_error", "isdc_status_string", "isdc_profile_enable", "isdc_profile_reset",
             "isdc_profile_get"]
 
+PROFILE_CLASS_IDS = {"fine_smoother": 0, "fine_defect_restrict": 1, "fine_prolong_correct": 2, "rhs": 3,
+                     "residual": 4, "coarse_levels": 5}
 PROFILE_CLASSES = {0: "fine_smoother", 1: "fine_defect_restrict", 2: "fine_prolong_correct", 3: "rhs", 4: "residual",
                    5: "coarse_levels"}
 
@@ -264,7 +266,7 @@ class ISDC:
         return out
 
     def profile(self, level: int = 1):
-        """0 off, 1 time the fine-level smoother only (bench's timed region), 2 time every class."""
+        """0 off, 1 the fine-level kernel classes, 2 every class, 16 + c class c only (bench's timed region)."""
         self._check(self.L.isdc_profile_enable(self.h, int(level)))
 
     def profile_reset(self):
