@@ -43,7 +43,8 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--workload")
-    ap.add_argument("--smoother-regex", default="k_smooth2|k_up|k_down|k3_smooth")
+    ap.add_argument("--kernel-regex", default="k_smooth2")
+    ap.add_argument("--cls", default="fine_defect_restrict", help="bench.py profile class of the kernel")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.rep:
@@ -59,18 +60,19 @@ def main():
                 fields.append(f"{k}={r[i]} {units[i]}".strip())
             lines.append(name.split("(")[0] + " | " + " | ".join(fields))
             import re
-            if a.workload and traffic is None and re.search(a.smoother_regex, name):
+            if a.workload and re.search(a.kernel_regex, name):
                 rd = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
                 wr = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
                 grid = float(r[idx["launch__grid_size"]].replace(",", ""))
-                traffic = (rd + wr, grid, name.split("(")[0])
+                if traffic is None or grid > traffic[1]:      # largest grid = the fine level
+                    traffic = (rd + wr, grid, name.split("(")[0])
         with open(os.path.join(PROF, f"{a.tag}_kernels.txt"), "w") as f:
             f.write("\n".join(lines) + "\n")
         if a.workload and traffic:
             path = os.path.join(PROF, "ncu_traffic.json")
             d = json.load(open(path)) if os.path.exists(path) else {}
-            d[a.workload] = {"fine_smoother_bytes_per_launch": traffic[0], "kernel": traffic[2],
-                             "grid": traffic[1], "source": f"profiles/{a.tag}_kernels.txt (first matching launch, "
+            d[a.workload] = {"class": a.cls, "dram_bytes_per_launch": traffic[0], "kernel": traffic[2],
+                             "grid": traffic[1], "source": f"profiles/{a.tag}_kernels.txt (matching launch with the "
                                                            "largest grid = fine level)"}
             json.dump(d, open(path, "w"), indent=1)
     if a.launches:
@@ -78,9 +80,10 @@ def main():
         hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
         h = rows[hi]
         ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+        mi = h.index("Metric Name")
         agg = collections.defaultdict(lambda: [0, 0.0])
         for r in rows[hi + 1:]:
-            if len(r) <= vi:
+            if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
                 continue
             v = float(r[vi].replace(",", ""))
             v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
