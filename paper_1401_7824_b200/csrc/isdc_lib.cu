@@ -58,6 +58,7 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    bool fuse3d = false;       // ISDC_FUSE3D=1: fused 3D prolongation + smoother (slower so far)
     bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
     bool stream2d = true;      // ISDC_STREAM2D=0: the tile-based 2D RHS / residual kernels instead
     int smooth3d_rows = 4;     // ISDC_SMOOTH3D_ROWS: rows per thread of the 3D fused smoother (2 or 4)
@@ -320,19 +321,32 @@ int pick_chunk(const isdc_ctx *h, int tiles, int planes, int halo) {
     return best;
 }
 
+// e != nullptr: u + P e first (fused trilinear prolongation + correction)
 isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
-                              const SCoef &c, int level) {
+                              const SCoef &c, int level, const double *e = nullptr, const GridDesc *gc = nullptr) {
     const CUtensorMap *mu = tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1);
     const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, f3d::S_BH, 1);
-    if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    const CUtensorMap *me = e ? tmap(h, e, *gc, f3d::S_EW, f3d::S_EH, 1) : mb;
+    if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
-    int pe = prof_begin(h, level == 0 ? PROF_SMOOTH : PROF_COARSE);
+    const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
+    int pe = prof_begin(h, cls);
     int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + f3d::S_TY - 1) / f3d::S_TY;
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
-    if (h->smooth3d_rows == 4) f3d::k_smooth2<4><<<grd, 256, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
-    else f3d::k_smooth2<2><<<grd, 512, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
-    prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
+    if (e) {
+        if (h->smooth3d_rows == 4)
+            f3d::k_smooth2<4, true><<<grd, 256, f3d::S_SMEM_PRO, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+        else
+            f3d::k_smooth2<2, true><<<grd, 512, f3d::S_SMEM_PRO, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+    } else {
+        if (h->smooth3d_rows == 4)
+            f3d::k_smooth2<4, false><<<grd, 256, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+        else
+            f3d::k_smooth2<2, false><<<grd, 512, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+    }
+    // algorithmic bytes: read u, b (+ e / 8); write u''
+    prof_end(h, pe, cls, (24.0 + (e ? 1.0 : 0.0)) * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -673,6 +687,12 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
         // fused bilinear prolongation + correction + two sweeps (one pass)
         double *dst = (curw == T) ? X : T;
         TRY(launch_smooth2(h, dst, curw, b, g, c, nullptr, l, C.e, &C.g));
+        cu = dst;
+        TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2 - 2));
+    } else if (use_fast3d(h, l) && h->fuse3d && h->P.mg.nu2 >= 2) {
+        // fused trilinear prolongation + correction + two sweeps (one z-stream)
+        double *dst = (curw == T) ? X : T;
+        TRY(launch_smooth2_3d(h, dst, curw, b, g, c, l, C.e, &C.g));
         cu = dst;
         TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2 - 2));
     } else {
@@ -1130,6 +1150,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
+    if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;
@@ -1153,8 +1174,10 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSR) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
-        cudaFuncSetAttribute(f3d::k_smooth2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
+        cudaFuncSetAttribute(f3d::k_smooth2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
         cudaFuncSetAttribute(f3d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::R_SMEM);
         cudaFuncSetAttribute(f3d::k_fe_cd4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::FE_SMEM);
 #define ISDC_BL_ATTR(FE_, MODE_, RR_, NM_) \

@@ -747,32 +747,41 @@ __device__ __forceinline__ void fr_phase(const double *__restrict__ src, int sox
     const double *sp = src + (r0 - 1 - soy) * SW_ + (x - sox);          // row y-1, column x
     const double *bp = B + (r0 - FR_BOY) * FR_BW + (x - FR_BOX);
     double *dp = dst + (r0 - doy) * DW_ + (x - dox);
-    double um = sp[0], rm = sp[-1] + sp[1];
+    double qa = sp[0], ra = sp[-1] + sp[1];          // row y-1
     sp += SW_;
-    double uc = sp[0], rc = sp[-1] + sp[1];
+    double qb = sp[0], rb = sp[-1] + sp[1];          // row y
+    double qc, rc;
     const int gx = x0 + x;
     const bool xin = gx >= 0 && gx < n;
     const bool xt = KIND == 1 && x >= 0 && x < FR_TX && xin;
     double *gp = (KIND == 1) ? gout + (long long)(y0 + r0) * pitch + gx : nullptr;
-    int gy = y0 + r0;
-#pragma unroll 2
-    for (int y = r0; y < r1; ++y) {
-        sp += SW_;
-        const double up = sp[0], rp = sp[-1] + sp[1];
-        const double f = rc + (um + up);
-        const double e = rm + rp;
-        const double su = (c0 * uc + c1 * f) + c2 * e;
-        const double bv = *bp;
-        const bool in = xin && (unsigned)gy < (unsigned)n;
-        double v;
-        if (KIND == 2) v = bv - su;                                   // defect
-        else v = in ? uc + wd * (bv - su) : 0.0;                     // Jacobi (zero outside)
-        *dp = v;
-        if (KIND == 1 && xt && y >= 0 && y < FR_TY && gy < n) *gp = v;
-        um = uc; uc = up; rm = rc; rc = rp;
-        bp += FR_BW; dp += DW_; ++gy;
-        if (KIND == 1) gp += pitch;
+    int gy = y0 + r0, y = r0;
+    // one output row: window rows (QM, QC, QN) with x-pair sums (RM, RC, RN); QN/RN are loaded.
+    // The loop body runs three rows with rotating register roles, so no value is ever moved.
+#define ISDC_FR_ROW(QM, QC, QN, RM, RC, RN)                                                   \
+    {                                                                                         \
+        sp += SW_;                                                                            \
+        QN = sp[0]; RN = sp[-1] + sp[1];                                                      \
+        const double f = RC + (QM + QN);                                                      \
+        const double e = RM + RN;                                                             \
+        const double su = (c0 * QC + c1 * f) + c2 * e;                                        \
+        const double bv = *bp;                                                                \
+        double v;                                                                             \
+        if (KIND == 2) v = bv - su;                                  /* defect */             \
+        else v = (xin && (unsigned)gy < (unsigned)n) ? QC + wd * (bv - su) : 0.0;            \
+        *dp = v;                                                                              \
+        if (KIND == 1 && xt && y >= 0 && y < FR_TY && gy < n) *gp = v;                        \
+        bp += FR_BW; dp += DW_; ++gy; ++y;                                                    \
+        if (KIND == 1) gp += pitch;                                                           \
     }
+    while (y + 3 <= r1) {
+        ISDC_FR_ROW(qa, qb, qc, ra, rb, rc)
+        ISDC_FR_ROW(qb, qc, qa, rb, rc, ra)
+        ISDC_FR_ROW(qc, qa, qb, rc, ra, rb)
+    }
+    if (y < r1) ISDC_FR_ROW(qa, qb, qc, ra, rb, rc)
+    if (y < r1) ISDC_FR_ROW(qb, qc, qa, rb, rc, ra)
+#undef ISDC_FR_ROW
 }
 
 template <int MODE>
