@@ -66,7 +66,10 @@ typedef enum {
 
 typedef enum {
     ISDC_MODE_ISDC_FIXED = 0,  /* exactly L V-cycles per node solve                        */
-    ISDC_MODE_SDC_TOL = 1      /* V-cycles until ||b - S u|| <= inner_tol*max(1,||b||)  */
+    ISDC_MODE_SDC_TOL = 1,     /* V-cycles until ||b - S u|| <= inner_tol*max(1,||b||)  */
+    ISDC_MODE_ISDC_CAPPED = 2  /* the SDC_TOL test before every cycle, at most L cycles: the
+                                  reading of Table 1's ISDC counts below K~(M-1)L (P:82 vs
+                                  P:126-136, R10)                     */
 } isdc_mode;
 
 typedef struct {

@@ -465,7 +465,8 @@ typedef struct {
     int fe;
     double fe_a[3];
     const double *G;     /* forcing profile (FE_FORCING), n^d, else NULL */
-    int mode;            /* 0 = ISDC (exactly L cycles), 1 = SDC (cycles to inner tolerance) */
+    int mode;            /* 0 = ISDC (exactly L cycles), 1 = SDC (cycles to inner tolerance),
+                            2 = ISDC capped: cycles to inner tolerance, at most L (reading R10) */
     int L;
     double inner_tol;    /* SDC: stop when ||b - S u|| <= inner_tol * max(1, ||b||) */
     int inner_cap;
@@ -566,7 +567,9 @@ double ora_residual_state(const ora_problem *P, const double *tau, const double 
 
 /* One node solve: ISDC = exactly L V-cycles; SDC = cycle until the defect test
  * ||b - S u|| <= inner_tol*max(1,||b||) passes (tested before every cycle, so 0 cycles is
- * possible), at most inner_cap cycles.  Returns cycles used; *cap_hit set when the cap ended it. */
+ * possible), at most inner_cap cycles.  ISDC capped (mode 2, NEXT f1; the reading of Table 1's
+ * counts below K~(M-1)L, P:82 vs P:126-136, R10): the same test, at most L cycles.
+ * Returns cycles used; *cap_hit set when inner_cap ended an SDC solve. */
 static int node_solve(const ora_problem *P, double gamma, const double *b, double *u, int *cap_hit) {
     int d = P->dim, n = P->n;
     *cap_hit = 0;
@@ -575,11 +578,12 @@ static int node_solve(const ora_problem *P, double gamma, const double *b, doubl
         return P->L;
     }
     double thr = P->inner_tol * fmax(1.0, maxabs(b, npts(d, n)));
+    const int cap = (P->mode == 2) ? P->L : P->inner_cap;
     int cyc = 0;
     for (;;) {
         double dn = ora_defect_norm(d, n, gamma, b, u);
         if (dn <= thr) break;
-        if (cyc >= P->inner_cap) { *cap_hit = 1; break; }
+        if (cyc >= cap) { if (P->mode == 1) *cap_hit = 1; break; }
         vcycle_rec(d, n, gamma, P->nu1, P->nu2, P->omega, b, u);
         ++cyc;
     }

@@ -165,8 +165,11 @@ isdc_status validate(const isdc_problem *p) {
     if (p->fe == ISDC_FE_FORCING && !p->fe_field_dev) return ISDC_ERR_INVALID_ARG;
     if (p->mg.nu1 < 0 || p->mg.nu2 < 0 || p->mg.nu1 + p->mg.nu2 < 1) return ISDC_ERR_INVALID_ARG;
     if (!(p->mg.omega > 0)) return ISDC_ERR_INVALID_ARG;
-    if (p->solve.mode != ISDC_MODE_ISDC_FIXED && p->solve.mode != ISDC_MODE_SDC_TOL) return ISDC_ERR_INVALID_ARG;
-    if (p->solve.mode == ISDC_MODE_ISDC_FIXED && p->solve.L < 1) return ISDC_ERR_INVALID_ARG;
+    if (p->solve.mode != ISDC_MODE_ISDC_FIXED && p->solve.mode != ISDC_MODE_SDC_TOL &&
+        p->solve.mode != ISDC_MODE_ISDC_CAPPED)
+        return ISDC_ERR_INVALID_ARG;
+    if (p->solve.mode != ISDC_MODE_SDC_TOL && p->solve.L < 1) return ISDC_ERR_INVALID_ARG;
+    if (p->solve.mode == ISDC_MODE_ISDC_CAPPED && !(p->solve.inner_tol >= 0)) return ISDC_ERR_INVALID_ARG;
     if (p->solve.mode == ISDC_MODE_SDC_TOL && (p->solve.inner_cap < 0 || !(p->solve.inner_tol >= 0)))
         return ISDC_ERR_INVALID_ARG;
     if (p->solve.fixed_sweeps <= 0 && p->solve.max_sweeps < 1) return ISDC_ERR_INVALID_ARG;
@@ -955,7 +958,8 @@ isdc_status read_residual(isdc_ctx *h, double *per_node, double *maxn) {
     return ISDC_OK;
 }
 
-// node solve m: ISDC = exactly L cycles; SDC = cycles until the defect test passes
+// node solve m: ISDC = exactly L cycles; SDC = cycles until the defect test passes;
+// ISDC capped = the same test, at most L cycles (reading R10, NEXT f1)
 isdc_status node_solve(isdc_ctx *h, int m, double *X, const double *src, int *cycles, int *cap_hit) {
     const GridDesc &g = h->lev[0].g;
     const SCoef &c = h->lev[0].coef[m];
@@ -977,7 +981,8 @@ isdc_status node_solve(isdc_ctx *h, int m, double *X, const double *src, int *cy
         TRY(read_slots(h, SLOT_DEFECT, 1, &dn));
         if (!(dn == dn)) { h->err = "non-finite defect"; return ISDC_ERR_NONFINITE; }
         if (dn <= thr) break;
-        if (cyc >= h->P.solve.inner_cap) { *cap_hit = 1; break; }
+        const bool capped = h->P.solve.mode == ISDC_MODE_ISDC_CAPPED;
+        if (cyc >= (capped ? h->P.solve.L : h->P.solve.inner_cap)) { if (!capped) *cap_hit = 1; break; }
         TRY(vcycle(h, 0, m, X, h->T, h->Bf, cur));
         cur = nullptr;
         ++cyc;
@@ -1077,7 +1082,7 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
     for (int j = 0; j < M; ++j) Fold[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
     double **Fnew = h->Fs[nw];
     int caps = 0;
-    bool sdc = h->P.solve.mode == ISDC_MODE_SDC_TOL;
+    bool sdc = h->P.solve.mode != ISDC_MODE_ISDC_FIXED;   // needs ||b|| for the defect test
     for (int m = 0; m + 1 < M; ++m) {
         TRY(run_rhs(h, m, uold, unew[m], h->Bf, sdc, Fold, Fnew[m]));
         const double *src;

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libisdc.so")
 
 FE_NONE, FE_CUBIC, FE_FORCING, FE_ADVECTION = 0, 1, 2, 3
-MODE_ISDC, MODE_SDC = 0, 1
+MODE_ISDC, MODE_SDC, MODE_ISDC_CAPPED = 0, 1, 2
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "cuda error", 4: "non-finite value",
           5: "bad workspace"}
 

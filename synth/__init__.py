@@ -28,7 +28,7 @@ from typing import Optional
 import numpy as np
 
 FE_NONE, FE_CUBIC, FE_FORCING, FE_ADVECTION = 0, 1, 2, 3
-MODE_ISDC, MODE_SDC = 0, 1
+MODE_ISDC, MODE_SDC, MODE_ISDC_CAPPED = 0, 1, 2
 
 
 @dataclasses.dataclass

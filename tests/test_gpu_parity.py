@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import synth
-from synth import FE_ADVECTION, FE_CUBIC, FE_FORCING, FE_NONE, MODE_ISDC, MODE_SDC
+from synth import FE_ADVECTION, FE_CUBIC, FE_FORCING, FE_NONE, MODE_ISDC, MODE_ISDC_CAPPED, MODE_SDC
 
 pytestmark = pytest.mark.gpu
 
@@ -97,7 +97,8 @@ def test_rhs_and_residual_bitwise(gpu, ora, dim, fe):
 @pytest.mark.parametrize("dim,fe,mode,n", [(2, FE_NONE, MODE_ISDC, 127), (2, FE_CUBIC, MODE_SDC, 127),
                                            (2, FE_FORCING, MODE_ISDC, 127), (3, FE_ADVECTION, MODE_ISDC, 31),
                                            (3, FE_NONE, MODE_SDC, 31), (3, FE_NONE, MODE_ISDC, 63),
-                                           (3, FE_ADVECTION, MODE_ISDC, 63), (3, FE_CUBIC, MODE_SDC, 63)])
+                                           (3, FE_ADVECTION, MODE_ISDC, 63), (3, FE_CUBIC, MODE_SDC, 63),
+                                           (2, FE_FORCING, MODE_ISDC_CAPPED, 127), (3, FE_NONE, MODE_ISDC_CAPPED, 63)])
 def test_sweep_bitwise(gpu, ora, dim, fe, mode, n):
     M = 5 if fe != FE_NONE else 3
     cfg = synth.Config(0, dim, n, M, 0.01, 0.5, fe, fe_a=(1.0, 0.5, 0.25))
@@ -124,6 +125,7 @@ STEP_CASES = [
     (3, 0, 255, MODE_ISDC), (3, 0, 255, MODE_SDC),
     (4, 0, 31, MODE_ISDC), (4, 1, 31, MODE_ISDC), (4, 2, 31, MODE_ISDC),
     (5, 0, 31, MODE_ISDC),
+    (2, 0, 127, MODE_ISDC_CAPPED), (4, 0, 31, MODE_ISDC_CAPPED),
 ]
 
 

@@ -282,3 +282,30 @@ def test_config1_reference_behaviour(ora):
     assert si["vcycles"] == 32 and ss["vcycles"] > 32
     # residuals decrease overall and both end near the exact-solve value (~2e-2)
     assert si["res_hist"][-1] < si["res_hist"][0] and 1e-2 < si["res_hist"][-1] < 5e-2
+
+
+def test_isdc_capped_pins(ora):
+    """ISDC-capped node solves (NEXT f1, reading R10: Table 1's ISDC counts fall below K~(M-1)L,
+    P:82 vs P:126-136): the SDC defect test before every cycle, at most L cycles.
+    Pins: inner_tol = 0 reproduces fixed-L ISDC bit for bit; an infinite tolerance does no cycle
+    (the initial guesses u_{m+1}^k stay, so one sweep leaves the spread state unchanged); on the
+    paper's heat problem every node solve uses <= L cycles, never more in total than fixed-L ISDC,
+    and the step converges."""
+    from synth import MODE_ISDC_CAPPED
+    n = 31
+    u0 = synth.sine_mode(n, (1, 1))
+    cfg = Config(0, 2, n, 3, 0.001, 10.0, FE_NONE, sweep_tol=5e-8, max_sweeps=100)
+    u_fix, st_fix = ora.step(ora.Problem(cfg, mode=MODE_ISDC), u0, 0.0)
+    u_c0, st_c0 = ora.step(ora.Problem(dataclasses.replace(cfg, inner_tol=0.0), mode=MODE_ISDC_CAPPED), u0, 0.0)
+    assert np.array_equal(u_c0, u_fix) and np.array_equal(st_c0["res_hist"], st_fix["res_hist"])
+    assert st_c0["vcycles"] == st_fix["vcycles"]
+    prob_inf = ora.Problem(dataclasses.replace(cfg, inner_tol=1e300), mode=MODE_ISDC_CAPPED)
+    state, cyc = ora.sweep(prob_inf, 0.0, [u0] * cfg.M)
+    assert list(cyc) == [0] * (cfg.M - 1)
+    for j in range(cfg.M):
+        assert np.array_equal(state[j], u0)
+    u_c, st_c = ora.step(ora.Problem(cfg, mode=MODE_ISDC_CAPPED), u0, 0.0)
+    assert st_c["converged"]
+    assert np.all(st_c["node_cycles"] <= cfg.L)
+    assert st_c["vcycles"] <= st_c["sweeps"] * (cfg.M - 1) * cfg.L
+    assert np.abs(u_c - u_fix).max() < 1e-6 * np.abs(u_fix).max()
