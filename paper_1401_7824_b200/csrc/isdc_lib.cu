@@ -327,8 +327,8 @@ int pick_chunk(const isdc_ctx *h, int tiles, int planes, int halo) {
 // e != nullptr: u + P e first (fused trilinear prolongation + correction)
 isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                               const SCoef &c, int level, const double *e = nullptr, const GridDesc *gc = nullptr) {
-    const CUtensorMap *mu = tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1);
     const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, f3d::S_BH, 1);
+    const CUtensorMap *mu = in ? tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1) : mb;   // in == nullptr: zero iterate
     const CUtensorMap *me = e ? tmap(h, e, *gc, f3d::S_EW, f3d::S_EH, 1) : mb;
     if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
@@ -337,19 +337,18 @@ isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const 
     int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + f3d::S_TY - 1) / f3d::S_TY;
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
+#define ISDC_S3(SR_, MODE_, SM_) \
+    f3d::k_smooth2<SR_, MODE_><<<grd, 32 * (32 / SR_), SM_, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me)
     if (e) {
-        if (h->smooth3d_rows == 4)
-            f3d::k_smooth2<4, true><<<grd, 256, f3d::S_SMEM_PRO, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
-        else
-            f3d::k_smooth2<2, true><<<grd, 512, f3d::S_SMEM_PRO, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+        if (h->smooth3d_rows == 4) ISDC_S3(4, 2, f3d::S_SMEM_PRO); else ISDC_S3(2, 2, f3d::S_SMEM_PRO);
+    } else if (!in) {
+        if (h->smooth3d_rows == 4) ISDC_S3(4, 1, f3d::S_SMEM); else ISDC_S3(2, 1, f3d::S_SMEM);
     } else {
-        if (h->smooth3d_rows == 4)
-            f3d::k_smooth2<4, false><<<grd, 256, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
-        else
-            f3d::k_smooth2<2, false><<<grd, 512, f3d::S_SMEM, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+        if (h->smooth3d_rows == 4) ISDC_S3(4, 0, f3d::S_SMEM); else ISDC_S3(2, 0, f3d::S_SMEM);
     }
-    // algorithmic bytes: read u, b (+ e / 8); write u''
-    prof_end(h, pe, cls, (24.0 + (e ? 1.0 : 0.0)) * npts_of(h, g));
+#undef ISDC_S3
+    // algorithmic bytes: read u (unless zero), b (+ e / 8); write u''
+    prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 1.0 : 0.0)) * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -669,6 +668,13 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
         }
         curw = (cur == T) ? X : T;
         TRY(launch_smooth2r(h, curw, zero ? nullptr : cur, b, g, C.b, C.g, c, l));
+    } else if (zero_init && use_fast3d(h, l) && h->P.mg.nu1 >= 2) {
+        // 3D: the first two sweeps from the zero iterate neither store nor read it
+        TRY(launch_smooth2_3d(h, T, nullptr, b, g, c, l));
+        cur = T;
+        TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1 - 2));
+        curw = const_cast<double *>(cur);
+        TRY(launch_restrict(h, C.b, C.g, curw, b, g, c, l));
     } else {
         if (zero_init) TRY(zero_field(h, X, g));
         TRY(smooth(h, l, X, T, b, c, cur, h->P.mg.nu1));
@@ -1179,10 +1185,12 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSR) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
-        cudaFuncSetAttribute(f3d::k_smooth2<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
-        cudaFuncSetAttribute(f3d::k_smooth2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
+        cudaFuncSetAttribute(f3d::k_smooth2<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
+        cudaFuncSetAttribute(f3d::k_smooth2<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
         cudaFuncSetAttribute(f3d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::R_SMEM);
         cudaFuncSetAttribute(f3d::k_fe_cd4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::FE_SMEM);
 #define ISDC_BL_ATTR(FE_, MODE_, RR_, NM_) \

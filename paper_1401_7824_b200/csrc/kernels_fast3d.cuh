@@ -190,14 +190,17 @@ __device__ __forceinline__ void smooth_step2(const SmoothCtx<SR> &C, SmoothRegs<
 }
 
 // u box 34 x 34 at (x0-2, y0-2); b box 34 x 32 at (x0-2, y0-1); t plane 34 x 34 (pad ring).
-// SR rows per thread, 32 / SR warps (the region is always 32 x 32).  PRO: u + P e first (fused
-// trilinear prolongation + correction, te = coarse correction map with 20 x 18 x 1 boxes).
-template <int SR, bool PRO>
+// SR rows per thread, 32 / SR warps (the region is always 32 x 32).  MODE 0: u from memory;
+// MODE 1: u == 0 (first smoothing of a coarse correction: u is neither stored nor read, the
+// u stages stay zero); MODE 2: u + P e first (fused trilinear prolongation + correction, te =
+// coarse correction map with 20 x 18 x 1 boxes).
+template <int SR, int MODE>
 __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_constant__ CUtensorMap tu,
                                                                 const __grid_constant__ CUtensorMap tb,
                                                                 double *__restrict__ out, int n, int pitch,
                                                                 long long plane, SCoef c, int zc,
                                                                 const __grid_constant__ CUtensorMap te) {
+    constexpr bool PRO = MODE == 2, ZERO = MODE == 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
     SmoothCtx<SR> C;
@@ -219,8 +222,8 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
     double *Usw = reinterpret_cast<double *>(sm), *Bsw = reinterpret_cast<double *>(sm + S_NS * S_UPL);
     auto issue = [&](int it) {
         const int s = it % S_NS, p = z0 - 2 + it;
-        mbar_expect_tx(&bar[s], (S_UW * S_UH + S_BW * S_BH + (PRO ? 2 * S_EW * S_EH : 0)) * 8);
-        tma_load_3d(Usw + s * (S_UPL / 8), &tu, x0 - 2, y0 - 2, p, &bar[s]);
+        mbar_expect_tx(&bar[s], ((ZERO ? 0 : S_UW * S_UH) + S_BW * S_BH + (PRO ? 2 * S_EW * S_EH : 0)) * 8);
+        if (!ZERO) tma_load_3d(Usw + s * (S_UPL / 8), &tu, x0 - 2, y0 - 2, p, &bar[s]);
         tma_load_3d(Bsw + s * (S_BPL / 8), &tb, x0 - 2, y0 - 1, p - 1, &bar[s]);
         if (PRO) {   // coarse planes Za, Zb of fine plane p (Za = Zb for odd p)
             const int za = (p & 1) ? (p - 1) / 2 : p / 2 - 1, zb = (p & 1) ? za : p / 2;
@@ -234,6 +237,9 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
         for (int s = 0; s < S_NS; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
     }
+    if (ZERO)
+        for (int s = 0; s < S_NS; ++s)
+            for (int q = tid; q < S_UW * S_UH; q += blockDim.x) Usw[s * (S_UPL / 8) + q] = 0.0;
     __syncthreads();
     if (tid == 0)
         for (int it = 0; it < S_NS && it < nit; ++it) issue(it);
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
     {                                                                  \
         const int it = base + (K);                                     \
         if (it < nit) {                                                \
-            smooth_step<SR, K, PRO>(C, G, it, phase);                  \
+            smooth_step<SR, K, (MODE == 2)>(C, G, it, phase);          \
             __syncthreads();                                           \
             if (tid == 0 && it + S_NS < nit) issue(it + S_NS);         \
             smooth_step2<SR, K>(C, G, it);                             \
