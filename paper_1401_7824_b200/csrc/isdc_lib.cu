@@ -4,6 +4,7 @@
 // Eq. (5), node solves, residual P:87-89), L5 geometric multigrid (mg_vcycle), with the L4
 // stencils fused into every kernel.  All device work is stream-ordered on the handle's stream;
 // all device memory lives in the caller's workspace.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -406,9 +407,11 @@ template <int MODE>
 isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f3d::BLArgs A, int prof_cls,
                       double bytes) {
     const GridDesc &g = h->lev[0].g;
-    int rr = (nm == 1) ? 4 : 2, ns = 4;
+    // rings cost 14 * RR * NM doubles per thread: NM = 1 -> RR = 4, NM = 2 -> RR = 2, NM = 4 -> RR = 1
+    int rr = (nm == 1) ? 4 : (nm == 2 ? 2 : 1), ns = (nm == 4) ? 6 : 4;
     auto smem_of = [&](int r_, int ns_) {
-        return r_ == 4 ? f3d::BLShape<4>::smem(K, ns_, nm) : f3d::BLShape<2>::smem(K, ns_, nm);
+        return r_ == 4 ? f3d::BLShape<4>::smem(K, ns_, nm)
+                       : (r_ == 2 ? f3d::BLShape<2>::smem(K, ns_, nm) : f3d::BLShape<1>::smem(K, ns_, nm));
     };
     while (ns >= 2 && smem_of(rr, ns) > (size_t)kMaxDynSmem) --ns;
     if (rr == 4 && ns < 3) { rr = 2; ns = 4; while (ns >= 2 && smem_of(rr, ns) > (size_t)kMaxDynSmem) --ns; }
@@ -437,7 +440,8 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
         else ISDC_BL(3, RR_, NM_);                                             \
     } while (0)
     if (nm == 1) { if (rr == 4) ISDC_BL_FE(4, 1); else ISDC_BL_FE(2, 1); }
-    else ISDC_BL_FE(2, 2);
+    else if (nm == 2) ISDC_BL_FE(2, 2);
+    else ISDC_BL_FE(1, 4);
 #undef ISDC_BL_FE
 #undef ISDC_BL
     prof_end(h, pe, prof_cls, bytes);
@@ -856,9 +860,12 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         if (fe == 3) { A.iF0 = K; for (int j = 0; j < M; ++j) fields[K++] = F[j]; }
         A.M = M; A.dtm = A.gm = 0.0; A.out = nullptr;
         double dt = h->P.dt, nudt = h->P.nu * dt;
-        const int passes = (M - 1 + 1) / 2;   // two nodes per pass
-        for (int m0 = 1; m0 < M; m0 += 2) {
-            const int nm = (m0 + 1 < M) ? 2 : 1;
+        // two nodes per pass (RR = 2); the single-pass NM = 4 / RR = 1 variant measured slower
+        // (cfg 5: 8.7 ms vs 2 x 3.4 ms per residual: 208 registers, 8-row regions)
+        const int per = 2;
+        const int passes = (M - 1 + per - 1) / per;
+        for (int m0 = 1; m0 < M; m0 += per) {
+            const int nm = std::min(per, M - m0) == 3 ? 2 : std::min(per, M - m0);
             for (int k = 0; k < f3d::BL_MAXNM; ++k) A.slot[k] = nullptr;
             for (int k = 0; k < nm; ++k) {
                 const int m = m0 + k;
@@ -1198,7 +1205,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
 #define ISDC_BL_ATTR4(MODE_, RR_, NM_) \
         ISDC_BL_ATTR(0, MODE_, RR_, NM_) ISDC_BL_ATTR(1, MODE_, RR_, NM_) ISDC_BL_ATTR(2, MODE_, RR_, NM_) ISDC_BL_ATTR(3, MODE_, RR_, NM_)
         ISDC_BL_ATTR4(0, 4, 1) ISDC_BL_ATTR4(0, 2, 1) ISDC_BL_ATTR4(1, 4, 1) ISDC_BL_ATTR4(1, 2, 1) ISDC_BL_ATTR4(1, 2, 2)
-        ISDC_BL_ATTR4(0, 2, 2)
+        ISDC_BL_ATTR4(0, 2, 2) ISDC_BL_ATTR4(1, 1, 4)
 #undef ISDC_BL_ATTR4
 #undef ISDC_BL_ATTR
         int rs = 2 * (ISDC_MAXM - 1) * f2d::ZH * f2d::ZW * (int)sizeof(double);
