@@ -50,6 +50,8 @@ struct isdc_ctx {
     double *Gp = nullptr;      // forcing profile (pitched)
     double *Fs[2][ISDC_MAXM];  // stored f^E(u_j) per iterate set (3D CD4 fast path), Fs[*][0] shared
     double *FT = nullptr;      // f^E of the isdc_rhs staging buffer T
+    double *FA[ISDC_MAXM], *WB[ISDC_MAXM];   // RHS folds of the next sweep (3D CD4)
+    bool fold_valid[2] = {false, false};     // folds hold iterate set s
     double *Ginv = nullptr;    // (M-1) coarse inverses, P x P each
     unsigned long long *red = nullptr;  // reduction slots
     int step_index = 0;
@@ -59,6 +61,7 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
     bool fuse3d = false;       // ISDC_FUSE3D=1: fused 3D prolongation + smoother (slower so far)
     bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
     bool stream2d = true;      // ISDC_STREAM2D=0: the tile-based 2D RHS / residual kernels instead
@@ -71,7 +74,7 @@ struct isdc_ctx {
     cudaStream_t cap = nullptr;
     bool graphs = true;
     struct Graph { cudaGraphExec_t exec = nullptr; std::vector<Pending> events; long nkernels = 0; };
-    std::map<std::tuple<int, int, int>, Graph> sweep_graphs;
+    std::map<std::tuple<int, int, int, int>, Graph> sweep_graphs;
     bool capturing = false;
     // live kernel timing (isdc_profile_*)
     int prof = 0;               // 0 off, 1 fine smoother only, 2 every class
@@ -211,6 +214,10 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
             }
         double *ft = (double *)take(fe);
         if (h) h->FT = ft;
+        for (int q = 0; q + 1 < M; ++q) {
+            double *fa = (double *)take(fe), *wb = (double *)take(fe);
+            if (h) { h->FA[q] = fa; h->WB[q] = wb; }
+        }
     }
     // coarse levels
     int nl = 0;
@@ -382,6 +389,9 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
 bool need_F(const isdc_ctx *h) {
     return h->d == 3 && h->fe.kind == 3 && (use_fast3d(h, 0, 8) || use_fast3d(h, 0, 16));
 }
+// the residual passes store the next sweep's RHS folds (3D CD4 fast RHS and residual both on)
+bool folds_on(const isdc_ctx *h) { return need_F(h) && use_fast3d(h, 0, 8) && use_fast3d(h, 0, 16) && h->folds; }
+
 isdc_status launch_fe(isdc_ctx *h, double *F, const double *u) {
     if (!need_F(h)) return ISDC_OK;
     const GridDesc &g = h->lev[0].g;
@@ -746,7 +756,7 @@ dim3 stream2d_grid(const isdc_ctx *h, int &yc) {
 bool stream2d_ok(const isdc_ctx *h) { return fast2d_pointwise_fe(h) && (h->M == 3 || h->M == 5) && h->stream2d; }
 
 isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_m, double *bout, bool bnorm,
-                    double *const *Fold = nullptr, const double *Fnew = nullptr) {
+                    double *const *Fold = nullptr, const double *Fnew = nullptr, bool fold_ok = false) {
     if (stream2d_ok(h)) {
         f2d::StreamArgs A;
         const int M = h->M;
@@ -773,6 +783,28 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         LAUNCH_CHECK(h);
         return ISDC_OK;
     }
+    if (use_fast3d(h, 0, 8) && h->fe.kind == 3 && Fold && Fnew && fold_ok) {
+        // RHS from the folds stored by the previous sweep's residual pass (same expression trees)
+        const int M = h->M;
+        const double *fields[f3d::BL_MAXF];
+        f3d::BLArgs A;
+        int K = 0;
+        A.iuo1 = K; fields[K++] = uold[m + 1];
+        A.ifo = K; fields[K++] = Fold[m];
+        A.iun = K; fields[K++] = unew_m;
+        A.iFn = K; fields[K++] = Fnew;
+        A.iwb = K; fields[K++] = h->WB[m];
+        A.ifa = K; fields[K++] = h->FA[m];
+        A.iu0 = A.iuG = A.iF0 = 0; A.nfold = 0;
+        A.M = M; A.mnode[0] = m;
+        double dt = h->P.dt, nu = h->P.nu;
+        A.dtm = dt * h->dtau[m];
+        A.gm = nu * A.dtm;
+        A.out = bout;
+        for (int k = 0; k < f3d::BL_MAXNM; ++k) A.slot[k] = nullptr;
+        if (bnorm) { TRY(clear_slots(h, SLOT_BNORM, 1)); A.slot[0] = h->red + SLOT_BNORM; }
+        return launch_bl<2>(h, fields, K, 1, A, PROF_RHS, (M + 2) * 8.0 * npts_of(h, h->lev[0].g));
+    }
     if (use_fast3d(h, 0, 8) && (h->fe.kind != 3 || (Fold && Fnew))) {
         const int M = h->M, fe = h->fe.kind;
         const double *fields[f3d::BL_MAXF];
@@ -780,7 +812,7 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         int K = 0;
         A.iu0 = K; for (int j = 0; j < M; ++j) fields[K++] = uold[j];
         A.iun = K; fields[K++] = unew_m;
-        A.iuG = A.iF0 = A.iFn = 0;
+        A.iuG = A.iF0 = A.iFn = 0; A.nfold = 0;
         if (fe == 2) { A.iuG = K; fields[K++] = h->Gp; }
         if (fe == 3) { A.iF0 = K; for (int j = 0; j < M; ++j) fields[K++] = Fold[j]; A.iFn = K; fields[K++] = Fnew; }
         A.M = M; A.mnode[0] = m;
@@ -845,7 +877,8 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
 }
 
 // residual of node fields u[0..M-1]: enqueue the kernels (slots SLOT_RES0..), then read them
-isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = nullptr) {
+// write_folds: the residual passes also store the next sweep's RHS folds (3D CD4)
+isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = nullptr, bool write_folds = false) {
     const GridDesc &g = h->lev[0].g;
     int M = h->M;
     TRY(clear_slots(h, SLOT_RES0, M - 1));
@@ -855,9 +888,11 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         f3d::BLArgs A;
         int K = 0;
         A.iu0 = K; for (int j = 0; j < M; ++j) fields[K++] = u[j];
-        A.iun = A.iuG = A.iF0 = A.iFn = 0;
+        A.iun = A.iuG = A.iF0 = A.iFn = 0; A.nfold = 0;
         if (fe == 2) { A.iuG = K; fields[K++] = h->Gp; }
         if (fe == 3) { A.iF0 = K; for (int j = 0; j < M; ++j) fields[K++] = F[j]; }
+        const double dts = h->P.dt, nudts = h->P.nu * dts;
+        int qnext = 0;   // next RHS node whose folds are still to be written
         A.M = M; A.dtm = A.gm = 0.0; A.out = nullptr;
         double dt = h->P.dt, nudt = h->P.nu * dt;
         // two nodes per pass (RR = 2); the single-pass NM = 4 / RR = 1 variant measured slower
@@ -872,6 +907,19 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
                 A.mnode[k] = m;
                 for (int j = 0; j < M; ++j) { A.a[k][j] = dt * h->Q[m * M + j]; A.beta[k][j] = nudt * h->Q[m * M + j]; }
                 A.slot[k] = h->red + SLOT_RES0 + m - 1;
+            }
+            A.nfold = 0;
+            if (write_folds && fe == 3) {   // RHS nodes q = qnext .. (nm per pass, M - 1 in all)
+                for (int k = 0; k < nm && qnext + 1 < M; ++k, ++qnext) {
+                    A.qnode[k] = qnext;
+                    for (int j = 0; j < M; ++j) {
+                        A.sa[k][j] = dts * h->S[qnext * M + j];
+                        A.sb[k][j] = nudts * h->S[qnext * M + j];
+                    }
+                    A.fa_out[k] = h->FA[qnext];
+                    A.wb_out[k] = h->WB[qnext];
+                    A.nfold = k + 1;
+                }
             }
             // algorithmic bytes of the whole residual: M node fields (+G) once, spread over the passes
             TRY(launch_bl<1>(h, fields, K, nm, A, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g) / passes));
@@ -1006,8 +1054,8 @@ isdc_status node_solve(isdc_ctx *h, int m, double *X, const double *src, int *cy
 }
 
 isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double *maxn,
-                         double *const *F = nullptr) {
-    TRY(enqueue_residual(h, u, F));
+                         double *const *F = nullptr, bool write_folds = false) {
+    TRY(enqueue_residual(h, u, F, write_folds));
     return read_residual(h, per_node, maxn);
 }
 
@@ -1021,8 +1069,9 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
     double *Fold[ISDC_MAXM];
     for (int j = 0; j < M; ++j) Fold[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
     double **Fnew = h->Fs[nw];
+    const bool fold_ok = !h->spread && h->fold_valid[h->cur];
     for (int m = 0; m + 1 < M; ++m) {
-        TRY(run_rhs(h, m, uold, unew[m], h->Bf, false, Fold, Fnew[m]));
+        TRY(run_rhs(h, m, uold, unew[m], h->Bf, false, Fold, Fnew[m], fold_ok));
         const double *src;
         if (h->P.solve.guess == 1) { TRY(zero_field(h, unew[m + 1], h->lev[0].g)); src = nullptr; }
         else if (h->P.solve.guess == 2) src = unew[m];
@@ -1030,11 +1079,11 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
         for (int l = 0; l < h->P.solve.L; ++l) TRY(vcycle(h, 0, m, unew[m + 1], h->T, h->Bf, l == 0 ? src : nullptr));
         TRY(launch_fe(h, Fnew[m + 1], unew[m + 1]));
     }
-    return enqueue_residual(h, unew, Fnew);
+    return enqueue_residual(h, unew, Fnew, folds_on(h));
 }
 
 isdc_status graph_sweep(isdc_ctx *h) {
-    auto key = std::make_tuple(h->cur, h->spread ? 1 : 0, h->prof);
+    auto key = std::make_tuple(h->cur, h->spread ? 1 : 0, h->prof, h->fold_valid[h->cur] ? 1 : 0);
     auto it = h->sweep_graphs.find(key);
     if (it == h->sweep_graphs.end()) {
         if (!h->cap) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
@@ -1085,6 +1134,7 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
         if (cap_hits) *cap_hits = 0;
         h->cur = 1 - h->cur;
         h->spread = false;
+        h->fold_valid[h->cur] = folds_on(h);   // the residual stored the folds of the new iterate
         return read_residual(h, res_per_node, res_max);
     }
     double *uold[ISDC_MAXM];
@@ -1096,8 +1146,9 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
     double **Fnew = h->Fs[nw];
     int caps = 0;
     bool sdc = h->P.solve.mode != ISDC_MODE_ISDC_FIXED;   // needs ||b|| for the defect test
+    const bool fold_ok = !h->spread && h->fold_valid[h->cur];
     for (int m = 0; m + 1 < M; ++m) {
-        TRY(run_rhs(h, m, uold, unew[m], h->Bf, sdc, Fold, Fnew[m]));
+        TRY(run_rhs(h, m, uold, unew[m], h->Bf, sdc, Fold, Fnew[m], fold_ok));
         const double *src;
         const GridDesc &g = h->lev[0].g;
         if (h->P.solve.guess == 1) { TRY(zero_field(h, unew[m + 1], g)); src = nullptr; }
@@ -1112,7 +1163,8 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
     h->cur = nw;
     h->spread = false;
     if (cap_hits) *cap_hits = caps;
-    return run_residual(h, h->U[h->cur], res_per_node, res_max, h->Fs[h->cur]);
+    h->fold_valid[h->cur] = folds_on(h);
+    return run_residual(h, h->U[h->cur], res_per_node, res_max, h->Fs[h->cur], folds_on(h));
 }
 
 }  // namespace
@@ -1169,6 +1221,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
+    if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;
@@ -1205,7 +1258,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
 #define ISDC_BL_ATTR4(MODE_, RR_, NM_) \
         ISDC_BL_ATTR(0, MODE_, RR_, NM_) ISDC_BL_ATTR(1, MODE_, RR_, NM_) ISDC_BL_ATTR(2, MODE_, RR_, NM_) ISDC_BL_ATTR(3, MODE_, RR_, NM_)
         ISDC_BL_ATTR4(0, 4, 1) ISDC_BL_ATTR4(0, 2, 1) ISDC_BL_ATTR4(1, 4, 1) ISDC_BL_ATTR4(1, 2, 1) ISDC_BL_ATTR4(1, 2, 2)
-        ISDC_BL_ATTR4(0, 2, 2) ISDC_BL_ATTR4(1, 1, 4)
+        ISDC_BL_ATTR4(0, 2, 2) ISDC_BL_ATTR4(1, 1, 4) ISDC_BL_ATTR4(2, 4, 1) ISDC_BL_ATTR4(2, 2, 1)
 #undef ISDC_BL_ATTR4
 #undef ISDC_BL_ATTR
         int rs = 2 * (ISDC_MAXM - 1) * f2d::ZH * f2d::ZW * (int)sizeof(double);
@@ -1300,6 +1353,7 @@ isdc_status isdc_set_initial(isdc_handle h, const double *u0, int step_index) {
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyDeviceToDevice));
     TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
     h->cur = 0; h->spread = true; h->step_index = step_index;
+    h->fold_valid[0] = h->fold_valid[1] = false;
     return upload_ct(h);
 }
 
@@ -1308,6 +1362,7 @@ isdc_status isdc_set_initial_host(isdc_handle h, const double *u0, int step_inde
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyHostToDevice));
     TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
     h->cur = 0; h->spread = true; h->step_index = step_index;
+    h->fold_valid[0] = h->fold_valid[1] = false;
     return upload_ct(h);
 }
 
@@ -1318,6 +1373,7 @@ isdc_status isdc_set_state(isdc_handle h, const double *const *u, int step_index
         TRY(launch_fe(h, h->Fs[0][j], h->U[0][j]));
     }
     h->cur = 0; h->spread = false; h->step_index = step_index;
+    h->fold_valid[0] = h->fold_valid[1] = false;
     return upload_ct(h);
 }
 
@@ -1375,6 +1431,7 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     // u_0 <- u_M (Lobatto end node), next step starts from the spread state
     TRY(copy_field(h, h->U[0][0], h->U[h->cur][h->M - 1], h->lev[0].g));
     if (need_F(h)) TRY(copy_field(h, h->Fs[0][0], h->Fs[h->cur][h->M - 1], h->lev[0].g));
+    h->fold_valid[0] = h->fold_valid[1] = false;
     h->cur = 0;
     h->spread = true;
     h->step_index += 1;
@@ -1445,6 +1502,7 @@ isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold, const
     TRY(pitched_to_dense(h, b, h->Bf, cudaMemcpyDeviceToDevice));
     CUDA_TRY(h, cudaStreamSynchronize(h->s));
     h->spread = true;  // the staged data overwrote the iterate sets
+    h->fold_valid[0] = h->fold_valid[1] = false;
     return ISDC_OK;
 }
 

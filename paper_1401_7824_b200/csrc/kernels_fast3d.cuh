@@ -452,6 +452,13 @@ struct BLArgs {
     int mnode[BL_MAXNM];           // RHS: substep m (0-based); residual: the pass's nodes m (1..M-1)
     int iu0, iun, iuG, iF0, iFn;   // field slots: old/current u_j at iu0+j, u_m^{k+1} at iun, G at iuG,
                                    // stored F_j at iF0+j, F(u_m^{k+1}) at iFn
+    // FE == 4 (RHS from fold fields, CD4): slots of u_{m+1}^old, F_m^old, WB_m, FA_m
+    int iuo1, ifo, iwb, ifa;
+    // residual passes may also store the RHS folds of the next sweep:
+    // FA_q = fold_j (dt S_qj) F_j, WB_q = fold_j (nu dt S_qj) u_j, q = qnode[k], k < nfold
+    int nfold, qnode[BL_MAXNM];
+    double sa[BL_MAXNM][ISDC_MAXM], sb[BL_MAXNM][ISDC_MAXM];
+    double *fa_out[BL_MAXNM], *wb_out[BL_MAXNM];
     const double *ct;              // device cos(t_j)
     double dtm, gm;                // RHS: dt*dtau_m, nu*dt*dtau_m
     double a[BL_MAXNM][ISDC_MAXM], beta[BL_MAXNM][ISDC_MAXM];   // RHS: dt*S_mj, nu*dt*S_mj;
@@ -528,6 +535,9 @@ __device__ __forceinline__ void bl_point(const BLArgs &A, int k, const double *F
             }
             av = (un + A.dtm * (fn - fo)) + fa;
         }
+    } else if (MODE == 2) {   // RHS from stored folds (FE = CD4): the same expression trees
+        cv = fld(A.iwb) - A.gm * fld(A.iuo1);
+        av = (fld(A.iun) + A.dtm * (fld(A.iFn) - fld(A.ifo))) + fld(A.ifa);
     } else {           // residual node m: a = p, c = z
         double diff = fld(A.iu0 + m) - fld(A.iu0);
         if (FE != 0) {
@@ -565,6 +575,7 @@ __device__ __forceinline__ void bl_point(const BLArgs &A, int k, const double *F
 template <int FE, int MODE, int RR, int NM>
 __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
     using SH = BLShape<RR>;
+    constexpr bool RHS = MODE != 1;   // MODE 0: RHS, 1: residual, 2: RHS from stored folds
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const int K = A.K;
@@ -605,7 +616,7 @@ __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps map
     BLRegs<RR> G[NM];
 #pragma unroll
     for (int k = 0; k < NM; ++k) vmax[k] = 0.0;
-    double *orow = (MODE == 0) ? A.out + (long long)(z0 - 2) * A.plane + (long long)(y0 + ly0) * A.pitch + gx : nullptr;
+    double *orow = RHS ? A.out + (long long)(z0 - 2) * A.plane + (long long)(y0 + ly0) * A.pitch + gx : nullptr;
     auto step = [&](auto Kc, int it) {
         constexpr int Kk = decltype(Kc)::value;
         constexpr int i3 = Kk % 3, m3 = (Kk + 2) % 3, mm3 = (Kk + 1) % 3;
@@ -626,6 +637,26 @@ __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps map
                 Pa[po + r * SH::PW] = av;
                 Pa[SH::PPL / 8 + po + r * SH::PW] = cv;
             }
+            // residual pass: the next sweep's RHS folds at the tile points of this chunk's planes
+            if (MODE == 1 && FE == 3 && A.nfold > 0 && ((oks >> r) & 1u) && p >= z0 && p < z1) {
+                const double *Fr = F + o0 + r * SH::FW;
+                const int fpl = SH::FPL / 8;
+                const long long gofs = (long long)p * A.plane + (long long)(y0 + ly0 + r) * A.pitch + gx;
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    if (k >= A.nfold) break;
+                    double fa = A.sa[k][0] * Fr[A.iF0 * fpl];
+                    double wb = A.sb[k][0] * Fr[A.iu0 * fpl];
+#pragma unroll
+                    for (int j = 1; j < ISDC_MAXM; ++j)
+                        if (j < A.M) {
+                            fa = fa + A.sa[k][j] * Fr[(A.iF0 + j) * fpl];
+                            wb = wb + A.sb[k][j] * Fr[(A.iu0 + j) * fpl];
+                        }
+                    A.fa_out[k][gofs] = fa;
+                    A.wb_out[k][gofs] = wb;
+                }
+            }
         }
         __syncthreads();
         if (tid == 0 && it + ns < nit) issue(it + ns);
@@ -637,7 +668,7 @@ __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps map
             plane_partials<true, RR>(Pc, SH::PW, RR * w, lane, G[k].cq[i3], G[k].cf[i3], G[k].ce[i2]);
         }
         if (it >= 2) {   // output plane p-1
-            double *op = (MODE == 0) ? orow + (long long)it * A.plane : nullptr;
+            double *op = RHS ? orow + (long long)it * A.plane : nullptr;
 #pragma unroll
             for (int r = 0; r < RR; ++r) {
 #pragma unroll
@@ -648,9 +679,9 @@ __global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps map
                     const double ec_ = g.ce[m2][r] + (g.cf[mm3][r] + g.cf[i3][r]);
                     const double Ba = c.kB0 * g.aq[m3][r] + c.kB1 * fa_;
                     const double Lc = (c.kL0 * g.cq[m3][r] + c.kL1 * fc_) + c.kL2 * ec_;
-                    const double val = (MODE == 0) ? Ba + Lc : Ba - Lc;
+                    const double val = RHS ? Ba + Lc : Ba - Lc;
                     if ((oks >> r) & 1u) {
-                        if (MODE == 0) op[r * A.pitch] = val;
+                        if (RHS) op[r * A.pitch] = val;
                         vmax[k] = amax(vmax[k], fabs(val));
                     }
                 }
