@@ -61,6 +61,8 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
+    bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
     bool fuse3d = false;       // ISDC_FUSE3D=1: fused 3D prolongation + smoother (slower so far)
     bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
@@ -417,16 +419,25 @@ template <int MODE>
 isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f3d::BLArgs A, int prof_cls,
                       double bytes) {
     const GridDesc &g = h->lev[0].g;
-    // rings cost 14 * RR * NM doubles per thread: NM = 1 -> RR = 4, NM = 2 -> RR = 2, NM = 4 -> RR = 1
-    int rr = (nm == 1) ? 4 : (nm == 2 ? 2 : 1), ns = (nm == 4) ? 6 : 4;
+    // rings cost 14 * RR * NM doubles per thread: NM = 1 -> RR = 4, NM = 2 -> RR = 2 (or RR = 1 with
+    // 16 warps: the same 16-row region, twice the warps), NM = 4 -> RR = 1
+    const bool w16 = (nm == 2) && h->bl16;
+    const bool r16 = (nm == 1) && h->rhs16;   // RHS: 16 warps x 2 rows (same 32-row region as 8 x 4)
+    int rr = (nm == 1) ? (r16 ? 2 : 4) : (nm == 2 && !w16 ? 2 : 1), ns = (nm == 4) ? 6 : 4;
     auto smem_of = [&](int r_, int ns_) {
-        return r_ == 4 ? f3d::BLShape<4>::smem(K, ns_, nm)
-                       : (r_ == 2 ? f3d::BLShape<2>::smem(K, ns_, nm) : f3d::BLShape<1>::smem(K, ns_, nm));
+        return w16 ? f3d::BLShape<1, 16>::smem(K, ns_, nm) : r16 ? f3d::BLShape<2, 16>::smem(K, ns_, nm)
+                   : (r_ == 4 ? f3d::BLShape<4>::smem(K, ns_, nm)
+                              : (r_ == 2 ? f3d::BLShape<2>::smem(K, ns_, nm) : f3d::BLShape<1>::smem(K, ns_, nm)));
     };
     while (ns >= 2 && smem_of(rr, ns) > (size_t)kMaxDynSmem) --ns;
-    if (rr == 4 && ns < 3) { rr = 2; ns = 4; while (ns >= 2 && smem_of(rr, ns) > (size_t)kMaxDynSmem) --ns; }
+    bool r16b = r16;
+    if ((rr == 4 || r16) && ns < 3) {   // too many fields for a 32-row region: 8 warps x 2 rows
+        r16b = false; rr = 2; ns = 4;
+        auto sm8 = [&](int ns_) { return f3d::BLShape<2>::smem(K, ns_, nm); };
+        while (ns >= 2 && sm8(ns) > (size_t)kMaxDynSmem) --ns;
+    }
     if (ns < 2) { h->err = "too many fields for the 3D stream kernel"; return ISDC_ERR_UNSUPPORTED; }
-    int rh = f3d::NW * rr;
+    int rh = w16 ? 16 : (r16b ? 32 : f3d::NW * rr);
     f3d::BLMaps maps;
     for (int k = 0; k < K; ++k) {
         const CUtensorMap *mk = tmap(h, fields[k], g, f3d::RW + 2, rh, 1);
@@ -437,11 +448,13 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     int tx = (g.n + f3d::RW - 3) / (f3d::RW - 2), ty = (g.n + rh - 3) / (rh - 2);
     A.zc = pick_chunk(h, tx * ty, g.n, 2);
     dim3 grd(tx, ty, (g.n + A.zc - 1) / A.zc);
-    size_t sm = smem_of(rr, ns);
+    size_t sm = r16b ? f3d::BLShape<2, 16>::smem(K, ns, nm) : (r16 ? f3d::BLShape<2>::smem(K, ns, nm) : smem_of(rr, ns));
     ++h->launches;
     int pe = prof_begin(h, prof_cls);
     int fe = h->fe.kind;
 #define ISDC_BL(FE_, RR_, NM_) f3d::k_bl<FE_, MODE, RR_, NM_><<<grd, f3d::NT, sm, h->s>>>(maps, A, ns)
+#define ISDC_BL16(FE_) f3d::k_bl<FE_, MODE, 1, 2, 16><<<grd, 512, sm, h->s>>>(maps, A, ns)
+#define ISDC_RHS16(FE_) f3d::k_bl<FE_, MODE, 2, 1, 16><<<grd, 512, sm, h->s>>>(maps, A, ns)
 #define ISDC_BL_FE(RR_, NM_)                                                   \
     do {                                                                       \
         if (fe == 0) ISDC_BL(0, RR_, NM_);                                     \
@@ -449,10 +462,14 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
         else if (fe == 2) ISDC_BL(2, RR_, NM_);                                \
         else ISDC_BL(3, RR_, NM_);                                             \
     } while (0)
-    if (nm == 1) { if (rr == 4) ISDC_BL_FE(4, 1); else ISDC_BL_FE(2, 1); }
+    if (nm == 1 && r16b) { if (fe == 0) ISDC_RHS16(0); else if (fe == 1) ISDC_RHS16(1); else if (fe == 2) ISDC_RHS16(2); else ISDC_RHS16(3); }
+    else if (nm == 1) { if (rr == 4) ISDC_BL_FE(4, 1); else ISDC_BL_FE(2, 1); }
+    else if (w16) { if (fe == 0) ISDC_BL16(0); else if (fe == 1) ISDC_BL16(1); else if (fe == 2) ISDC_BL16(2); else ISDC_BL16(3); }
     else if (nm == 2) ISDC_BL_FE(2, 2);
     else ISDC_BL_FE(1, 4);
 #undef ISDC_BL_FE
+#undef ISDC_BL16
+#undef ISDC_RHS16
 #undef ISDC_BL
     prof_end(h, pe, prof_cls, bytes);
     LAUNCH_CHECK(h);
@@ -1222,6 +1239,8 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';
+    if (const char *b16 = getenv("ISDC_BL16")) h->bl16 = b16[0] != '0';
+    if (const char *r16 = getenv("ISDC_RHS16")) h->rhs16 = r16[0] != '0';
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;
@@ -1259,6 +1278,11 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         ISDC_BL_ATTR(0, MODE_, RR_, NM_) ISDC_BL_ATTR(1, MODE_, RR_, NM_) ISDC_BL_ATTR(2, MODE_, RR_, NM_) ISDC_BL_ATTR(3, MODE_, RR_, NM_)
         ISDC_BL_ATTR4(0, 4, 1) ISDC_BL_ATTR4(0, 2, 1) ISDC_BL_ATTR4(1, 4, 1) ISDC_BL_ATTR4(1, 2, 1) ISDC_BL_ATTR4(1, 2, 2)
         ISDC_BL_ATTR4(0, 2, 2) ISDC_BL_ATTR4(1, 1, 4) ISDC_BL_ATTR4(2, 4, 1) ISDC_BL_ATTR4(2, 2, 1)
+        for (auto kern : {f3d::k_bl<0, 1, 1, 2, 16>, f3d::k_bl<1, 1, 1, 2, 16>, f3d::k_bl<2, 1, 1, 2, 16>,
+                          f3d::k_bl<3, 1, 1, 2, 16>, f3d::k_bl<0, 0, 2, 1, 16>, f3d::k_bl<1, 0, 2, 1, 16>,
+                          f3d::k_bl<2, 0, 2, 1, 16>, f3d::k_bl<3, 0, 2, 1, 16>, f3d::k_bl<0, 2, 2, 1, 16>,
+                          f3d::k_bl<1, 2, 2, 1, 16>, f3d::k_bl<2, 2, 2, 1, 16>, f3d::k_bl<3, 2, 2, 1, 16>})
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
 #undef ISDC_BL_ATTR4
 #undef ISDC_BL_ATTR
         int rs = 2 * (ISDC_MAXM - 1) * f2d::ZH * f2d::ZW * (int)sizeof(double);

@@ -471,9 +471,9 @@ struct BLArgs {
     unsigned long long *slot[BL_MAXNM];   // max |out| per output (RHS: optional, residual: required)
 };
 
-template <int RR>
+template <int RR, int NWW = NW>
 struct BLShape {
-    static constexpr int RH = NW * RR;                 // region rows
+    static constexpr int RH = NWW * RR;                // region rows
     static constexpr int TX = RW - 2, TY = RH - 2;     // output tile
     static constexpr int FW = RW + 2, FH = RH;         // input box 34 x RH at (x0-2, y0-1)
     static constexpr int PW = RW + 2, PH = RH + 2;     // a / c planes with a pad ring
@@ -572,9 +572,10 @@ __device__ __forceinline__ void bl_point(const BLArgs &A, int k, const double *F
 }
 
 // NM outputs per pass (RHS: 1; residual: nodes per pass).  Registers: 14 * RR * NM doubles of rings.
-template <int FE, int MODE, int RR, int NM>
-__global__ void __launch_bounds__(NT, 1) k_bl(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
-    using SH = BLShape<RR>;
+// NWW warps (region rows NWW * RR).
+template <int FE, int MODE, int RR, int NM, int NWW = NW>
+__global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
+    using SH = BLShape<RR, NWW>;
     constexpr bool RHS = MODE != 1;   // MODE 0: RHS, 1: residual, 2: RHS from stored folds
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
