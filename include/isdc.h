@@ -104,6 +104,13 @@ typedef struct {
     const double *fe_field_dev;  /* FORCING: G, dense n^d device field (copied at create), else NULL */
     isdc_mg_opts mg;
     isdc_solve_opts solve;
+    /* Residual in the sweep test (NEXT f2): 0 = weighted ||r~|| = ||B_h r|| (R15);
+     * 1 = the paper's unweighted ||r|| = ||W^{-1} r~||, 2D only, W^{-1} applied by
+     * V-cycles on B_h from zero until ||r~ - B_h x|| <= w_tol*||r~|| (at most w_cap; R15b).
+     * The W-cycles are counted apart from the V-cycles. */
+    int residual_kind;
+    double w_tol;                /* 1e-6 */
+    int w_cap;                   /* 50   */
 } isdc_problem;
 
 /* Per-step statistics (Table 1 accounting; SPEC RunStats S:249-252). */
@@ -113,6 +120,7 @@ typedef struct {
     int cap_hits;        /* SDC node solves that stopped at inner_cap                           */
     int converged;       /* residual < sweep_tol reached (always 1 with fixed_sweeps)           */
     double final_residual;
+    long wcycles;        /* W-cycles of the unweighted residual (residual_kind 1)         */
 } isdc_step_stats;
 
 /* Bytes of device workspace a problem needs (fields, MG hierarchy, reductions, tables). */

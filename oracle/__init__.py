@@ -49,6 +49,7 @@ class OraProblem(C.Structure):
         ("mode", C.c_int), ("L", C.c_int), ("inner_tol", C.c_double), ("inner_cap", C.c_int),
         ("sweep_tol", C.c_double), ("max_sweeps", C.c_int), ("fixed_sweeps", C.c_int),
         ("nu1", C.c_int), ("nu2", C.c_int), ("omega", C.c_double), ("guess", C.c_int),
+        ("res_kind", C.c_int), ("w_tol", C.c_double), ("w_cap", C.c_int),
     ]
 
 
@@ -78,6 +79,7 @@ def _declare(L):
                            C.POINTER(C.c_long), _dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                            C.POINTER(C.c_int)]
     L.ora_num_threads.restype = C.c_int
+    L.ora_last_wcycles.restype = C.c_long
 
 
 def _p(a: np.ndarray):
@@ -174,7 +176,7 @@ def fe_eval(fe, u, a=(0.0, 0.0, 0.0), G=None, ct=1.0):
 class Problem:
     """Mirror of synth.Config plus run-time choices; holds the ctypes struct and keeps G alive."""
 
-    def __init__(self, cfg, G=None, mode=0, guess=0):
+    def __init__(self, cfg, G=None, mode=0, guess=0, res_kind=0, w_tol=1e-6, w_cap=50):
         self.cfg = cfg
         self.G = None if G is None else _c(G)
         self.s = OraProblem()
@@ -187,6 +189,7 @@ class Problem:
         s.mode, s.L, s.inner_tol, s.inner_cap = mode, cfg.L, cfg.inner_tol, cfg.inner_cap
         s.sweep_tol, s.max_sweeps, s.fixed_sweeps = cfg.sweep_tol, cfg.max_sweeps, cfg.fixed_sweeps
         s.nu1, s.nu2, s.omega, s.guess = cfg.nu1, cfg.nu2, cfg.omega, guess
+        s.res_kind, s.w_tol, s.w_cap = res_kind, w_tol, w_cap
 
 
 def _ptrs(fields):
@@ -236,7 +239,7 @@ def step(prob: Problem, u0, t_n):
     if rc:
         raise RuntimeError("ora_step failed")
     k = sw.value
-    return u, dict(sweeps=k, vcycles=vc.value, res_hist=hist[:k].copy(),
+    return u, dict(sweeps=k, vcycles=vc.value, res_hist=hist[:k].copy(), wcycles=lib().ora_last_wcycles(),
                    node_cycles=np.array(ncyc[: k * (cfg.M - 1)]).reshape(k, cfg.M - 1),
                    cap_hits=caps.value, converged=bool(conv.value), seconds=el)
 

@@ -476,7 +476,12 @@ typedef struct {
     int nu1, nu2;
     double omega;
     int guess;           /* 0 = u_{m+1}^k; 1 = zero; 2 = u_m^{k+1} (P:187-189 ablation) */
+    int res_kind;        /* 0 = weighted ||r~|| (reading R15); 1 = unweighted ||W^-1 r~|| (2D, NEXT f2) */
+    double w_tol;        /* res_kind 1: W-solve until ||r~ - W x|| <= w_tol * ||r~|| (reading R15b) */
+    int w_cap;           /* res_kind 1: at most w_cap W-cycles per node */
 } ora_problem;
+
+static long g_wcycles;   /* W-cycles of the last ora_step (not V-cycles: P:165) */
 
 /* Right-hand side of Eq. (5) for substep m (0-based: node m -> m+1), regrouped by linearity of
  * B_h and L_h (SURVEY §8(c1) "check by expansion"):
@@ -558,6 +563,22 @@ double ora_residual_state(const ora_problem *P, const double *tau, const double 
             r[p] = B_at(&c, pm, d, n, ii, jj, kk) - L_at(&c, zm, d, n, ii, jj, kk);
         }
         double nm = maxabs(r, NP);
+        if (P->res_kind == 1) {
+            /* unweighted residual: x = W^{-1} r~ by V(nu1,nu2)-cycles on
+             * S = B_h (gamma = 0, the same multigrid components) from x = 0, until
+             * ||r~ - B_h x|| <= w_tol*||r~|| (tested before every cycle), at most w_cap cycles;
+             * report ||x||.  W-cycles are counted apart from the V-cycles. */
+            double *x = calloc(NP, sizeof(double));
+            double thr = P->w_tol * nm;
+            for (int wc = 0;; ++wc) {
+                double dn = ora_defect_norm(d, n, 0.0, r, x);
+                if (dn <= thr || wc >= P->w_cap) break;
+                vcycle_rec(d, n, 0.0, P->nu1, P->nu2, P->omega, r, x);
+                ++g_wcycles;
+            }
+            nm = maxabs(x, NP);
+            free(x);
+        }
         if (per_node) per_node[m - 1] = nm;
         if (nm > best || isinf(nm)) best = nm;
     }
@@ -635,6 +656,7 @@ int ora_step(const ora_problem *P, double *u0, double t_n, int *sweeps, long *vc
     int k = 0, conv = 0, caps = 0;
     long vc = 0;
     int kmax = P->fixed_sweeps > 0 ? P->fixed_sweeps : P->max_sweeps;
+    g_wcycles = 0;
     while (k < kmax) {
         int cyc[32];
         caps += ora_sweep(P, tau, S, dtau, t_n, uold, unew, cyc);
@@ -652,6 +674,8 @@ int ora_step(const ora_problem *P, double *u0, double t_n, int *sweeps, long *vc
     if (cap_hits) *cap_hits = caps;
     return 0;
 }
+
+long ora_last_wcycles(void) { return g_wcycles; }
 
 /* Exposed for the per-operation parity tests: RHS of substep m and residual of a given state. */
 void ora_rhs(const ora_problem *P, double t_n, int m, double *const *uold, double *const *unew, double *b) {

@@ -51,6 +51,10 @@ struct isdc_ctx {
     double *Fs[2][ISDC_MAXM];  // stored f^E(u_j) per iterate set (3D CD4 fast path), Fs[*][0] shared
     double *FT = nullptr;      // f^E of the isdc_rhs staging buffer T
     double *FA[ISDC_MAXM], *WB[ISDC_MAXM];   // RHS folds of the next sweep (3D CD4)
+    double *RT[ISDC_MAXM];     // residual_kind 1: weighted residual fields r~_m (m = 1..M-1 at RT[m-1])
+    double *WX = nullptr;      // residual_kind 1: W-solve iterate
+    long wcyc = 0;             // W-cycles since the last step start
+    int wslot = 0;             // coefficient slot of gamma = 0 (W = B_h): M - 1
     bool fold_valid[2] = {false, false};     // folds hold iterate set s
     double *Ginv = nullptr;    // (M-1) coarse inverses, P x P each
     unsigned long long *red = nullptr;  // reduction slots
@@ -180,6 +184,9 @@ isdc_status validate(const isdc_problem *p) {
         return ISDC_ERR_INVALID_ARG;
     if (p->solve.fixed_sweeps <= 0 && p->solve.max_sweeps < 1) return ISDC_ERR_INVALID_ARG;
     if (p->solve.guess < 0 || p->solve.guess > 2) return ISDC_ERR_INVALID_ARG;
+    if (p->residual_kind < 0 || p->residual_kind > 1) return ISDC_ERR_INVALID_ARG;
+    if (p->residual_kind == 1 && (p->grid.dim != 2 || p->M > ISDC_MAXM - 1)) return ISDC_ERR_UNSUPPORTED;
+    if (p->residual_kind == 1 && (!(p->w_tol >= 0) || p->w_cap < 0)) return ISDC_ERR_INVALID_ARG;
     return ISDC_OK;
 }
 
@@ -234,8 +241,16 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
         double *t = (double *)take(el * sizeof(double));
         if (h) { h->lev[l].e = e; h->lev[l].b = b; h->lev[l].t = t; }
     }
+    if (p->residual_kind == 1) {
+        for (int m = 1; m < M; ++m) {
+            double *f = (double *)take(fe);
+            if (h) h->RT[m - 1] = f;
+        }
+        double *x = (double *)take(fe);
+        if (h) h->WX = x;
+    }
     int Pc = (d == 3) ? 27 : 9;
-    double *Gi = (double *)take((size_t)(M - 1) * Pc * Pc * sizeof(double));
+    double *Gi = (double *)take((size_t)M * Pc * Pc * sizeof(double));   // M-1 substeps + gamma = 0
     unsigned long long *red = (unsigned long long *)take(kRedSlots * sizeof(unsigned long long));
     double *ctd = (double *)take(ISDC_MAXM * sizeof(double));
     if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; }
@@ -787,6 +802,7 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         A.bl = h->bl;
         A.out = bout;
         A.slot = nullptr;
+        for (int j = 0; j < ISDC_MAXM; ++j) A.rt[j] = nullptr;
         if (bnorm) { TRY(clear_slots(h, SLOT_BNORM, 1)); A.slot = h->red + SLOT_BNORM; }
         dim3 grd = stream2d_grid(h, A.yc);
         ++h->launches;
@@ -955,6 +971,9 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         A.bl = h->bl;
         A.out = nullptr;
         A.slot = h->red + SLOT_RES0;
+        for (int j = 0; j < ISDC_MAXM; ++j) A.rt[j] = nullptr;
+        if (h->P.residual_kind == 1)
+            for (int m = 1; m < M; ++m) A.rt[m - 1] = h->RT[m - 1];
         dim3 grd = stream2d_grid(h, A.yc);
         if (M == 5) {   // two warps per strip (2 nodes each): 4 strips per CTA
             const int strips = (h->n + f2d::SW_OUT - 1) / f2d::SW_OUT;
@@ -971,7 +990,7 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         LAUNCH_CHECK(h);
         return ISDC_OK;
     }
-    if (fast2d_pointwise_fe(h)) {
+    if (fast2d_pointwise_fe(h) && h->P.residual_kind == 0) {   // tile kernel (no r~ field output)
         f2d::ResArgs A;
         for (int j = 0; j < M; ++j) A.u[j] = u[j];
         A.G = h->Gp; A.ct = h->ctdev; A.M = M; A.fe = h->fe.kind; A.n = h->n; A.pitch = g.pitch;
@@ -1009,10 +1028,12 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         h->launches += 2;
         if (h->d == 2) {
             k_pz<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
-            k_resid<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1);
+            k_resid<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1,
+                                                                 h->P.residual_kind == 1 ? h->RT[m - 1] : nullptr);
         } else {
             k_pz<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
-            k_resid<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1);
+            k_resid<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1,
+                                                                 nullptr);
         }
         LAUNCH_CHECK(h);
     }
@@ -1020,10 +1041,42 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
     return ISDC_OK;
 }
 
+isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double *b, const double *src,
+                   bool zero_init);
+
+// residual_kind 1 (NEXT f2): ||W^{-1} r~_m|| with W^{-1} applied by V-cycles on B_h (coefficient slot
+// wslot, gamma = 0) from zero until ||r~ - B_h x|| <= w_tol*||r~||, at most w_cap cycles (the same
+// test as the oracle, reading R15b); the W-cycles are counted in h->wcyc
+isdc_status unweighted_norms(isdc_ctx *h, double *norms) {
+    const GridDesc &g = h->lev[0].g;
+    const SCoef &c = h->lev[0].coef[h->wslot];
+    for (int m = 1; m < h->M; ++m) {
+        const double thr = h->P.w_tol * norms[m - 1];
+        TRY(zero_field(h, h->WX, g));
+        for (int wc = 0;; ++wc) {
+            TRY(clear_slots(h, SLOT_SCRATCH, 1));
+            TRY(launch_defect_norm(h, h->WX, h->RT[m - 1], g, c, h->red + SLOT_SCRATCH));
+            double dn;
+            TRY(read_slots(h, SLOT_SCRATCH, 1, &dn));
+            if (!(dn == dn)) { h->err = "non-finite W defect"; return ISDC_ERR_NONFINITE; }
+            if (dn <= thr || wc >= h->P.w_cap) break;
+            TRY(vcycle(h, 0, h->wslot, h->WX, h->T, h->RT[m - 1], nullptr, false));
+            ++h->wcyc;
+        }
+        TRY(clear_slots(h, SLOT_SCRATCH, 1));
+        ++h->launches;
+        k_norm<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->WX, g, h->red + SLOT_SCRATCH);
+        LAUNCH_CHECK(h);
+        TRY(read_slots(h, SLOT_SCRATCH, 1, &norms[m - 1]));
+    }
+    return ISDC_OK;
+}
+
 isdc_status read_residual(isdc_ctx *h, double *per_node, double *maxn) {
     int M = h->M;
     double tmp[ISDC_MAXM];
     TRY(read_slots(h, SLOT_RES0, M - 1, tmp));
+    if (h->P.residual_kind == 1) TRY(unweighted_norms(h, tmp));
     double mx = 0.0;
     bool bad = false;
     for (int m = 0; m < M - 1; ++m) {
@@ -1292,9 +1345,11 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         attrs = true;
     }
     int Pc = (h->d == 3) ? 27 : 9;
-    std::vector<double> Gi((size_t)(h->M - 1) * Pc * Pc);
-    for (int m = 0; m + 1 < h->M; ++m) {
-        double gamma = prob->nu * (prob->dt * h->dtau[m]);
+    std::vector<double> Gi((size_t)h->M * Pc * Pc);
+    h->wslot = h->M - 1;
+    const int nslots = h->M - 1 + (prob->residual_kind == 1 ? 1 : 0);
+    for (int m = 0; m < nslots; ++m) {
+        double gamma = (m == h->wslot) ? 0.0 : prob->nu * (prob->dt * h->dtau[m]);
         for (int l = 0; l < h->nlev; ++l) h->lev[l].coef[m] = make_scoef(h->d, h->lev[l].g.n, gamma, prob->mg.omega);
         const SCoef &cc = h->lev[h->nlev - 1].coef[m];
         if (isdc_coarse_inverse(h->d, cc.c0, cc.c1, cc.c2, Gi.data() + (size_t)m * Pc * Pc)) {
@@ -1310,7 +1365,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         for (int l = 0; l < h->nlev; ++l)
             if (h->lev[l].g.n <= tail_n) { h->tail_l0 = l; break; }
         if (h->tail_l0 >= 0) {
-            for (int m = 0; m + 1 < h->M; ++m) {
+            for (int m = 0; m < nslots; ++m) {
                 TailParams &T = h->tailp[m];
                 T.nlev = h->nlev - h->tail_l0;
                 for (int i = 0; i < T.nlev; ++i) {
@@ -1436,6 +1491,7 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     if (!h) return ISDC_ERR_INVALID_ARG;
     const isdc_solve_opts &o = h->P.solve;
     int kmax = o.fixed_sweeps > 0 ? o.fixed_sweeps : o.max_sweeps;
+    h->wcyc = 0;
     int k = 0, caps = 0, conv = 0;
     long vc = 0;
     double res = 0.0;
@@ -1463,6 +1519,7 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     if (stats) {
         stats->sweeps = k; stats->vcycles = vc; stats->cap_hits = caps; stats->converged = conv;
         stats->final_residual = res;
+        stats->wcycles = h->wcyc;
     }
     return ISDC_OK;
 }

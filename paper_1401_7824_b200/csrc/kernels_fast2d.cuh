@@ -507,6 +507,7 @@ struct StreamArgs {
     BLConst bl;
     double *out;                    // RHS b
     unsigned long long *slot;       // RHS: ||b|| (optional); residual: per-node slots slot[m-1]
+    double *rt[ISDC_MAXM];          // residual: r~_m fields at rt[m-1] (unweighted residual), or null
 };
 
 // fields loaded per row: u_0..u_{M-1}, [unew], [G], [u_{m+1}, u_m: L1 hits of the first M, loaded
@@ -690,7 +691,9 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {
                 const double ez = zr[mm][km2] + zr[mm][k];
                 const double Bp = c.kB0 * pq[mm][km1] + c.kB1 * fp;
                 const double Lz = (c.kL0 * zq[mm][km1] + c.kL1 * fz) + c.kL2 * ez;
-                rmax[mm] = amax(rmax[mm], fabs(Bp - Lz));
+                const double rv = Bp - Lz;
+                rmax[mm] = amax(rmax[mm], fabs(rv));
+                if (A.rt[m - 1]) A.rt[m - 1][rowoff(y - 1)] = rv;
             }
         }
     };

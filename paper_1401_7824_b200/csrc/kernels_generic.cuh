@@ -210,9 +210,12 @@ __global__ void k_pz(double *__restrict__ Pf, double *__restrict__ Zf, PZParams 
 // residual pass 2: r = B p - L z, ||r||_inf into *slot
 template <int D>
 __global__ void k_resid(const double *__restrict__ Pf, const double *__restrict__ Zf, GridDesc g, BLConst c,
-                        unsigned long long *slot) {
+                        unsigned long long *slot, double *__restrict__ out) {
     POINT_INDEX_OR_RETURN(g)
     double val = 0.0;
-    if (inside) val = apply_B<D>(c, Pf, g, i, j, k) - apply_L<D>(c, Zf, g, i, j, k);
+    if (inside) {
+        val = apply_B<D>(c, Pf, g, i, j, k) - apply_L<D>(c, Zf, g, i, j, k);
+        if (out) out[gidx(g, i, j, k)] = val;   // r~ field (unweighted residual)
+    }
     block_max_to(slot, fabs(val));
 }

@@ -45,12 +45,13 @@ class _Solve(C.Structure):
 class _Problem(C.Structure):
     _fields_ = [("grid", _Grid), ("M", C.c_int), ("nodes", C.c_int), ("dt", C.c_double), ("nu", C.c_double),
                 ("fe", C.c_int), ("fe_params", C.c_double * 3), ("fe_field_dev", C.c_void_p),
-                ("mg", _Mg), ("solve", _Solve)]
+                ("mg", _Mg), ("solve", _Solve), ("residual_kind", C.c_int), ("w_tol", C.c_double),
+                ("w_cap", C.c_int)]
 
 
 class _Stats(C.Structure):
     _fields_ = [("sweeps", C.c_int), ("vcycles", C.c_long), ("cap_hits", C.c_int), ("converged", C.c_int),
-                ("final_residual", C.c_double)]
+                ("final_residual", C.c_double), ("wcycles", C.c_long)]
 
 
 _lib = None
@@ -119,6 +120,7 @@ class ISDC:
                  fe_a=(0.0, 0.0, 0.0), G: Optional[torch.Tensor] = None, mode: int = MODE_ISDC, L: int = 2,
                  inner_tol: float = 1e-12, inner_cap: int = 50, sweep_tol: float = 1e-10, max_sweeps: int = 200,
                  fixed_sweeps: int = 0, nu1: int = 2, nu2: int = 2, omega: float = 0.8, guess: int = 0,
+                 residual_kind: int = 0, w_tol: float = 1e-6, w_cap: int = 50,
                  device: Optional[torch.device] = None, stream: Optional[torch.cuda.Stream] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ISDC needs a CUDA device (no CPU fallback)")
@@ -140,6 +142,7 @@ class ISDC:
         s = p.solve
         s.mode, s.L, s.inner_tol, s.inner_cap = mode, L, inner_tol, inner_cap
         s.sweep_tol, s.max_sweeps, s.fixed_sweeps, s.guess = sweep_tol, max_sweeps, fixed_sweeps, guess
+        p.residual_kind, p.w_tol, p.w_cap = residual_kind, w_tol, w_cap
         self.p = p
         self.dim, self.n, self.M = dim, n, M
         self.kmax = fixed_sweeps if fixed_sweeps > 0 else max_sweeps
@@ -214,7 +217,7 @@ class ISDC:
         self._check(self.L.isdc_step(self.h, C.byref(st), _np_ptr(hist), ncyc))
         k = st.sweeps
         return dict(sweeps=k, vcycles=st.vcycles, cap_hits=st.cap_hits, converged=bool(st.converged),
-                    final_residual=st.final_residual, res_hist=hist[:k].copy(),
+                    final_residual=st.final_residual, res_hist=hist[:k].copy(), wcycles=st.wcycles,
                     node_cycles=np.array(ncyc[: k * (self.M - 1)]).reshape(k, self.M - 1))
 
     def run(self, nsteps: int):

@@ -183,3 +183,21 @@ def test_errors(gpu):
         gpu.ISDC(2, 63, 3, -0.01, 1.0)         # dt <= 0
     with pytest.raises(gpu.IsdcError):
         gpu.ISDC(2, 63, 3, 0.01, 1.0, fe=FE_FORCING, G=None) if False else gpu.ISDC(2, 63, 3, 0.01, 1.0, L=0)
+
+
+# ------------------------------------------------------------ unweighted residual (NEXT f2)
+@pytest.mark.parametrize("cid,n,mode", [(1, 63, MODE_ISDC), (2, 127, MODE_ISDC), (3, 255, MODE_ISDC),
+                                        (1, 63, MODE_SDC), (2, 255, MODE_ISDC_CAPPED)])
+def test_unweighted_residual_steps_bitwise(gpu, ora, cid, n, mode):
+    """residual_kind 1: ||W^{-1} r~|| with W^{-1} by V-cycles on B_h -- every
+    residual, count (sweeps, V-cycles, W-cycles) and the solution equal the oracle's bits."""
+    cfg, u0, G = synth.problem_inputs(cid, 0, n)
+    h = make(gpu, cfg, G, mode=mode, residual_kind=1, w_tol=1e-6, w_cap=50)
+    prob = ora.Problem(cfg, G, mode=mode, res_kind=1, w_tol=1e-6, w_cap=50)
+    h.set_initial(torch.from_numpy(u0).cuda(), 0)
+    st = h.step()
+    u_ref, st_ref = ora.step(prob, u0, 0.0)
+    assert st["sweeps"] == st_ref["sweeps"] and st["vcycles"] == st_ref["vcycles"]
+    assert st["wcycles"] == st_ref["wcycles"] and st["wcycles"] > 0
+    assert np.array_equal(st["res_hist"], st_ref["res_hist"])
+    assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)

@@ -309,3 +309,34 @@ def test_isdc_capped_pins(ora):
     assert np.all(st_c["node_cycles"] <= cfg.L)
     assert st_c["vcycles"] <= st_c["sweeps"] * (cfg.M - 1) * cfg.L
     assert np.abs(u_c - u_fix).max() < 1e-6 * np.abs(u_fix).max()
+
+
+def test_unweighted_residual_pins(ora):
+    """NEXT f2: the paper's unweighted residual r = W^{-1} r~, W^{-1} applied by
+    V-cycles on B_h (gamma = 0), 2D.  Pins: on a single discrete sine mode r~ is an eigenvector
+    of W = B_h, so ||r|| = ||r~|| / lambda_B (closed form, within the W-solve tolerance); zero at
+    the collocation solution; for random states ||r~|| <= ||r|| <= 3 ||r~|| (||B_h||_inf = 1,
+    ||B_h^{-1}||_inf <= 3 in 2D); the W-cycles are counted apart."""
+    n, M, dt, nu, ks = 31, 3, 0.01, 1.0, (2, 3)
+    cfg = Config(0, 2, n, M, dt, nu, FE_NONE)
+    phi = synth.sine_mode(n, ks)
+    lL, lB = sym(ks, n)
+    state = [1.0 * phi, 0.7 * phi, 0.2 * phi]
+    rw, per_w = ora.residual(ora.Problem(cfg), 0.0, state)
+    ru, per_u = ora.residual(ora.Problem(cfg, res_kind=1, w_tol=1e-10), 0.0, state)
+    assert rw > 1e-3
+    assert np.allclose(per_u, per_w / lB, rtol=1e-8, atol=0)
+    tau, Q, S, dtau = ora.tables(M)
+    coll = np.linalg.solve(np.eye(M) - dt * nu * lL / lB * Q, np.ones(M))
+    r0, _ = ora.residual(ora.Problem(cfg, res_kind=1), 0.0, [c * phi for c in coll])
+    assert r0 < 1e-12
+    rng = np.random.default_rng(5)
+    rand = [rng.standard_normal((n, n)) for _ in range(M)]
+    rw, per_w = ora.residual(ora.Problem(cfg), 0.0, rand)
+    ru, per_u = ora.residual(ora.Problem(cfg, res_kind=1, w_tol=1e-10), 0.0, rand)
+    assert np.all(per_w <= per_u * (1 + 1e-8)) and np.all(per_u <= 3 * per_w * (1 + 1e-8))
+    u0 = synth.sine_mode(n, (1, 1))
+    c2 = Config(0, 2, n, M, 0.001, 10.0, FE_NONE, sweep_tol=5e-8, max_sweeps=50)
+    _, st = ora.step(ora.Problem(c2, mode=MODE_SDC, res_kind=1), u0, 0.0)
+    assert st["converged"] and st["wcycles"] > 0
+    assert st["vcycles"] == ora.step(ora.Problem(c2, mode=MODE_SDC), u0, 0.0)[1]["vcycles"]
