@@ -133,6 +133,19 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def replica_seed(seed, rank):
+    """Replicas only: rank r solves its own independent problem, seed + r."""
+    return seed + rank
+
+
+def aggregate_ranks(el_ms, steps, world, reduce_max):
+    """Whole-job throughput of N independent replicas: every rank ran `steps` steps in `el_ms`
+    device milliseconds; the job time is the max over ranks (reduce_max: all-reduce MAX of one
+    float).  Returns (max_ms, steps/s of all ranks)."""
+    el_max = float(reduce_max(float(el_ms)))
+    return el_max, world * steps / (el_max / 1e3)
+
+
 def cpu_baseline(cfg, u0, G, mode, sweeps_per_step, reps=1):
     """Time the oracle (as it stands) on this host: `reps` full-size sweeps + residual."""
     import oracle
@@ -209,7 +222,7 @@ def main():
             dist.barrier()
 
     mode = synth.MODE_SDC if a.mode == "sdc" else synth.MODE_ISDC
-    cfg, u0, G = synth.problem_inputs(a.config, a.seed + rank)
+    cfg, u0, G = synth.problem_inputs(a.config, replica_seed(a.seed, rank))
     h = pk.ISDC.from_config(cfg, None if G is None else torch.from_numpy(G), mode=mode)
     u0_dev = torch.from_numpy(u0).cuda()
     P = cfg.n ** cfg.dim
@@ -239,14 +252,16 @@ def main():
     launches = h.launches - l0
     el_ms = ev0.elapsed_time(ev1)
     barrier()
-    t = torch.tensor([el_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    el_max = float(t.item())
 
+    def reduce_max(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    el_max, steps_per_s = aggregate_ranks(el_ms, a.steps, world, reduce_max)
     sweeps = sum(s["sweeps"] for s in stats)
     vcyc = sum(s["vcycles"] for s in stats)
-    steps_per_s = world * a.steps / (el_max / 1e3)
     vcyc_per_s = world * vcyc / (el_max / 1e3)
     peak, peak_kind = peaks()
 
