@@ -982,7 +982,11 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         ++h->launches;
         int pe = prof_begin(h, PROF_RESID);
         const int fe = h->fe.kind;
-#define ISDC_RS(FE_, M_) f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1)><<<grd, f2d::SW_NT, 0, h->s>>>(A)
+#define ISDC_RS(FE_, M_)                                                                                \
+    do {                                                                                                \
+        if (h->P.residual_kind == 1) f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), true><<<grd, f2d::SW_NT, 0, h->s>>>(A); \
+        else f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), false><<<grd, f2d::SW_NT, 0, h->s>>>(A);                       \
+    } while (0)
         if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
         else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
 #undef ISDC_RS

@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
 // r~_m = B p_m - L z_m, per-node max into slot[m-1].  The M-1 nodes are split over G = (M-1)/NMW
 // warps per strip (NMW nodes each; the extra loads of the same rows hit L1/L2), which halves the
 // register rings and doubles the resident warps.
-template <int FE, int MM, int NMW>
+template <int FE, int MM, int NMW, bool WRT = false>   // WRT: also store the r~_m fields (unweighted residual)
 __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {
     constexpr int G = (MM - 1) / NMW;
     const int wid = threadIdx.x >> 5;
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {
                 const double Lz = (c.kL0 * zq[mm][km1] + c.kL1 * fz) + c.kL2 * ez;
                 const double rv = Bp - Lz;
                 rmax[mm] = amax(rmax[mm], fabs(rv));
-                if (A.rt[m - 1]) A.rt[m - 1][rowoff(y - 1)] = rv;
+                if (WRT) A.rt[m - 1][rowoff(y - 1)] = rv;
             }
         }
     };
