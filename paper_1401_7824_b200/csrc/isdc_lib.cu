@@ -65,6 +65,7 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    int tail2d = 31;           // ISDC_TAIL2D: largest 2D level handled by the single-CTA tail (31 measured best)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
@@ -1298,6 +1299,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';
     if (const char *b16 = getenv("ISDC_BL16")) h->bl16 = b16[0] != '0';
     if (const char *r16 = getenv("ISDC_RHS16")) h->rhs16 = r16[0] != '0';
+    if (const char *t2 = getenv("ISDC_TAIL2D")) h->tail2d = atoi(t2);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;
@@ -1365,7 +1367,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     h->graphs = !(eg && eg[0] == '1');
     // single-CTA tail: levels n <= 63 (2D) / 15 (3D) in shared memory
     if (h->fast) {
-        int tail_n = (h->d == 2) ? 63 : 15;
+        int tail_n = (h->d == 2) ? h->tail2d : 15;   // ISDC_TAIL2D: largest 2D level in the tail
         for (int l = 0; l < h->nlev; ++l)
             if (h->lev[l].g.n <= tail_n) { h->tail_l0 = l; break; }
         if (h->tail_l0 >= 0) {
