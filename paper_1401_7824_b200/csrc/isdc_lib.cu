@@ -65,6 +65,7 @@ struct isdc_ctx {
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    int tail3d = 15;           // ISDC_TAIL3D: largest 3D level handled by the tail (fast kernels above)
     int tail2d = 31;           // ISDC_TAIL2D: largest 2D level handled by the single-CTA tail (31 measured best)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
@@ -331,7 +332,7 @@ const CUtensorMap *tmap(isdc_ctx *h, const double *base, const GridDesc &g, int 
 
 bool use_fast2d(const isdc_ctx *h, int level) { return h->fast && h->d == 2 && h->lev[level].g.n >= 63; }
 bool use_fast3d(const isdc_ctx *h, int level, int kind = 1) {
-    return h->fast && h->d == 3 && h->lev[level].g.n >= 31 && (h->fast3d_mask & kind);
+    return h->fast && h->d == 3 && h->lev[level].g.n > h->tail3d && (h->fast3d_mask & kind);
 }
 
 // z-chunk length for a z-streaming 3D kernel with `tiles` xy tiles over `planes` output planes, one
@@ -1300,6 +1301,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *b16 = getenv("ISDC_BL16")) h->bl16 = b16[0] != '0';
     if (const char *r16 = getenv("ISDC_RHS16")) h->rhs16 = r16[0] != '0';
     if (const char *t2 = getenv("ISDC_TAIL2D")) h->tail2d = atoi(t2);
+    if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
         int dev = 0, nsm = 0;
@@ -1367,7 +1369,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     h->graphs = !(eg && eg[0] == '1');
     // single-CTA tail: levels n <= 63 (2D) / 15 (3D) in shared memory
     if (h->fast) {
-        int tail_n = (h->d == 2) ? h->tail2d : 15;   // ISDC_TAIL2D: largest 2D level in the tail
+        int tail_n = (h->d == 2) ? h->tail2d : h->tail3d;   // ISDC_TAIL2D / ISDC_TAIL3D
         for (int l = 0; l < h->nlev; ++l)
             if (h->lev[l].g.n <= tail_n) { h->tail_l0 = l; break; }
         if (h->tail_l0 >= 0) {
