@@ -11,6 +11,7 @@
 #include <map>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../../include/isdc.h"
@@ -67,6 +68,9 @@ struct isdc_ctx {
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
     int tail3d = 15;           // ISDC_TAIL3D: largest 3D level handled by the tail (fast kernels above)
     int tail2d = 31;           // ISDC_TAIL2D: largest 2D level handled by the single-CTA tail (31 measured best)
+    bool pdl = false;          // ISDC_PDL=1: programmatic dependent launch (measured neutral with the implicit
+                               // trigger, slower with an early trigger)
+    cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
@@ -111,6 +115,8 @@ struct isdc_ctx {
 #define LAUNCH_CHECK(h)                                                                      \
     do {                                                                                     \
         cudaError_t _e = cudaGetLastError();                                                 \
+        if (_e == cudaSuccess) _e = (h)->kl_err;                                             \
+        (h)->kl_err = cudaSuccess;                                                           \
         if (_e != cudaSuccess) {                                                             \
             (h)->err = std::string("kernel launch: ") + cudaGetErrorString(_e);             \
             return ISDC_ERR_CUDA;                                                            \
@@ -118,6 +124,37 @@ struct isdc_ctx {
     } while (0)
 
 namespace {
+
+// Kernel launch with programmatic dependent launch (PDL): the kernel may start while its stream
+// predecessor drains; every kernel waits (griddepcontrol.wait, common.cuh) before touching global
+// memory, so only its launch latency and shared-memory prologue overlap.  Captured into the
+// CUDA graphs as programmatic dependency edges.  Usage: kl(h, kernel, grid, block, smem)(args...).
+template <typename... KA>
+struct KLaunch {
+    isdc_ctx *h;
+    void (*k)(KA...);
+    dim3 g, b;
+    size_t sm;
+    template <typename... A>
+    void operator()(A &&...a) const {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = g;
+        cfg.blockDim = b;
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = h->s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k, std::forward<A>(a)...);
+        if (e != cudaSuccess && h->kl_err == cudaSuccess) h->kl_err = e;
+    }
+};
+template <typename... KA>
+KLaunch<KA...> kl(isdc_ctx *h, void (*k)(KA...), dim3 g, dim3 b, size_t sm) {
+    return KLaunch<KA...>{h, k, g, b, sm};
+}
 
 constexpr size_t kAlign = 256;
 constexpr int kRedSlots = 64;
@@ -365,7 +402,7 @@ isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const 
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
 #define ISDC_S3(SR_, MODE_, SM_) \
-    f3d::k_smooth2<SR_, MODE_><<<grd, 32 * (32 / SR_), SM_, h->s>>>(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me)
+    kl(h, f3d::k_smooth2<SR_, MODE_>, grd, 32 * (32 / SR_), SM_)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me)
     if (e) {
         if (h->smooth3d_rows == 4) ISDC_S3(4, 2, f3d::S_SMEM_PRO); else ISDC_S3(2, 2, f3d::S_SMEM_PRO);
     } else if (!in) {
@@ -394,10 +431,10 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + f2d::TY - 1) / f2d::TY);
     size_t sm = sizeof(f2d::SmemSmooth) + 128;
-    if (norm_slot) f2d::k_smooth2<true, 0><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
-    else if (e) f2d::k_smooth2<false, 2><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    else if (!in) f2d::k_smooth2<false, 1><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    else f2d::k_smooth2<false, 0><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    if (norm_slot) kl(h, f2d::k_smooth2<true, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
+    else if (e) kl(h, f2d::k_smooth2<false, 2>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    else if (!in) kl(h, f2d::k_smooth2<false, 1>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    else kl(h, f2d::k_smooth2<false, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
     // algorithmic bytes: read u (unless zero), b (+ e / 4); write u''
     prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 2.0 : 0.0)) * npts_of(h, g));
     LAUNCH_CHECK(h);
@@ -421,7 +458,7 @@ isdc_status launch_fe(isdc_ctx *h, double *F, const double *u) {
     int tx = (g.n + f3d::RW - 1) / f3d::RW, ty = (g.n + f3d::RH - 1) / f3d::RH;
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
-    f3d::k_fe_cd4<<<grd, f3d::NT, f3d::FE_SMEM, h->s>>>(*mu, F, g.n, g.pitch, g.plane, h->fe.kx, h->fe.ky, h->fe.kz, zc);
+    kl(h, f3d::k_fe_cd4, grd, f3d::NT, f3d::FE_SMEM)(*mu, F, g.n, g.pitch, g.plane, h->fe.kx, h->fe.ky, h->fe.kz, zc);
     prof_end(h, pe, PROF_RHS, 0.0);   // implementation traffic, not in the algorithmic bytes
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -469,9 +506,9 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     ++h->launches;
     int pe = prof_begin(h, prof_cls);
     int fe = h->fe.kind;
-#define ISDC_BL(FE_, RR_, NM_) f3d::k_bl<FE_, MODE, RR_, NM_><<<grd, f3d::NT, sm, h->s>>>(maps, A, ns)
-#define ISDC_BL16(FE_) f3d::k_bl<FE_, MODE, 1, 2, 16><<<grd, 512, sm, h->s>>>(maps, A, ns)
-#define ISDC_RHS16(FE_) f3d::k_bl<FE_, MODE, 2, 1, 16><<<grd, 512, sm, h->s>>>(maps, A, ns)
+#define ISDC_BL(FE_, RR_, NM_) kl(h, f3d::k_bl<FE_, MODE, RR_, NM_>, grd, f3d::NT, sm)(maps, A, ns)
+#define ISDC_BL16(FE_) kl(h, f3d::k_bl<FE_, MODE, 1, 2, 16>, grd, 512, sm)(maps, A, ns)
+#define ISDC_RHS16(FE_) kl(h, f3d::k_bl<FE_, MODE, 2, 1, 16>, grd, 512, sm)(maps, A, ns)
 #define ISDC_BL_FE(RR_, NM_)                                                   \
     do {                                                                       \
         if (fe == 0) ISDC_BL(0, RR_, NM_);                                     \
@@ -504,8 +541,8 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::FR_TX - 1) / f2d::FR_TX, (g.n + f2d::FR_TY - 1) / f2d::FR_TY);
     size_t sm = sizeof(f2d::SmemSR) + 128;
-    if (in) f2d::k_smooth2r<0><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    else f2d::k_smooth2r<1><<<grd, f2d::NT, sm, h->s>>>(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    if (in) kl(h, f2d::k_smooth2r<0>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    else kl(h, f2d::k_smooth2r<1>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
     // algorithmic bytes: read u (unless zero), b; write u'', b_c
     prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + 2.0) * npts_of(h, g));
     LAUNCH_CHECK(h);
@@ -516,8 +553,8 @@ isdc_status launch_jacobi(isdc_ctx *h, double *out, const double *in, const doub
                           const SCoef &c, int level) {
     ++h->launches;
     int pe = prof_begin(h, level == 0 ? PROF_SMOOTH : PROF_COARSE);
-    if (h->d == 2) k_jacobi<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
-    else k_jacobi<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(out, in, b, g, c);
+    if (h->d == 2) kl(h, k_jacobi<2>, point_grid<2>(g, kBlk), kBlk, 0)(out, in, b, g, c);
+    else kl(h, k_jacobi<3>, point_grid<3>(g, kBlk), kBlk, 0)(out, in, b, g, c);
     prof_end(h, pe, level == 0 ? PROF_SMOOTH : PROF_COARSE, 24.0 * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -526,8 +563,8 @@ isdc_status launch_jacobi(isdc_ctx *h, double *out, const double *in, const doub
 isdc_status launch_defect_norm(isdc_ctx *h, const double *u, const double *b, const GridDesc &g, const SCoef &c,
                                unsigned long long *slot) {
     ++h->launches;
-    if (h->d == 2) k_defect_norm<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(u, b, g, c, slot);
-    else k_defect_norm<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(u, b, g, c, slot);
+    if (h->d == 2) kl(h, k_defect_norm<2>, point_grid<2>(g, kBlk), kBlk, 0)(u, b, g, c, slot);
+    else kl(h, k_defect_norm<3>, point_grid<3>(g, kBlk), kBlk, 0)(u, b, g, c, slot);
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
@@ -541,7 +578,7 @@ isdc_status launch_restrict(isdc_ctx *h, double *bc, const GridDesc &gc, const d
         const CUtensorMap *mb = tmap(h, b, gf, f2d::RBW, f2d::RBH);
         if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
         dim3 grd((gc.n + f2d::RCX - 1) / f2d::RCX, (gc.n + f2d::RCY - 1) / f2d::RCY);
-        f2d::k_restrict<<<grd, f2d::RNT, sizeof(f2d::SmemRestrict) + 128, h->s>>>(*mu, *mb, bc, gf.n, gc.n,
+        kl(h, f2d::k_restrict, grd, f2d::RNT, sizeof(f2d::SmemRestrict) + 128)(*mu, *mb, bc, gf.n, gc.n,
                                                                                      gc.pitch, c);
     } else if (use_fast3d(h, level, 2)) {
         const CUtensorMap *mu = tmap(h, u, gf, f3d::R_UW, f3d::R_UH, 1);
@@ -550,9 +587,9 @@ isdc_status launch_restrict(isdc_ctx *h, double *bc, const GridDesc &gc, const d
         int tx = (gc.n + f3d::R_CX - 1) / f3d::R_CX, ty = (gc.n + f3d::R_CY - 1) / f3d::R_CY;
         int kc = pick_chunk(h, tx * ty, gc.n, 2);
         dim3 grd(tx, ty, (gc.n + kc - 1) / kc);
-        f3d::k_restrict<<<grd, f3d::NT, f3d::R_SMEM, h->s>>>(*mu, *mb, bc, gf.n, gc.n, gc.pitch, gc.plane, c, kc);
-    } else if (h->d == 2) k_restrict_defect<2><<<point_grid<2>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
-    else k_restrict_defect<3><<<point_grid<3>(gc, kBlk), kBlk, 0, h->s>>>(bc, gc, u, b, gf, c);
+        kl(h, f3d::k_restrict, grd, f3d::NT, f3d::R_SMEM)(*mu, *mb, bc, gf.n, gc.n, gc.pitch, gc.plane, c, kc);
+    } else if (h->d == 2) kl(h, k_restrict_defect<2>, point_grid<2>(gc, kBlk), kBlk, 0)(bc, gc, u, b, gf, c);
+    else kl(h, k_restrict_defect<3>, point_grid<3>(gc, kBlk), kBlk, 0)(bc, gc, u, b, gf, c);
     prof_end(h, pe, level == 0 ? PROF_RESTRICT : PROF_COARSE, 16.0 * npts_of(h, gf) + 8.0 * npts_of(h, gc));
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -564,12 +601,12 @@ isdc_status launch_prolong(isdc_ctx *h, double *u, const GridDesc &gf, const dou
     int pe = prof_begin(h, level == 0 ? PROF_PROLONG : PROF_COARSE);
     if (use_fast2d(h, level)) {
         dim3 grd(((gf.n + 1) / 2 + 255) / 256, gf.n);
-        f2d::k_prolong<<<grd, 256, 0, h->s>>>(u, gf.n, gf.pitch, e, gc.n, gc.pitch);
+        kl(h, f2d::k_prolong, grd, 256, 0)(u, gf.n, gf.pitch, e, gc.n, gc.pitch);
     } else if (use_fast3d(h, level, 4)) {
         dim3 grd(((gf.n + 1) / 2 + 255) / 256, gf.n, gf.n);
-        f3d::k_prolong<<<grd, 256, 0, h->s>>>(u, gf.n, gf.pitch, gf.plane, e, gc.n, gc.pitch, gc.plane);
-    } else if (h->d == 2) k_prolong_add<2><<<point_grid<2>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
-    else k_prolong_add<3><<<point_grid<3>(gf, kBlk), kBlk, 0, h->s>>>(u, gf, e, gc);
+        kl(h, f3d::k_prolong, grd, 256, 0)(u, gf.n, gf.pitch, gf.plane, e, gc.n, gc.pitch, gc.plane);
+    } else if (h->d == 2) kl(h, k_prolong_add<2>, point_grid<2>(gf, kBlk), kBlk, 0)(u, gf, e, gc);
+    else kl(h, k_prolong_add<3>, point_grid<3>(gf, kBlk), kBlk, 0)(u, gf, e, gc);
     prof_end(h, pe, level == 0 ? PROF_PROLONG : PROF_COARSE, 16.0 * npts_of(h, gf) + 8.0 * npts_of(h, gc));
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -580,8 +617,8 @@ isdc_status launch_coarse(isdc_ctx *h, double *u, const double *b, const GridDes
     int Pc = (h->d == 3) ? 27 : 9;
     const double *Gi = h->Ginv + (size_t)m * Pc * Pc;
     int pe = prof_begin(h, PROF_COARSE);
-    if (h->d == 2) k_coarse_solve<2><<<1, 32, 0, h->s>>>(u, b, g, Gi);
-    else k_coarse_solve<3><<<1, 32, 0, h->s>>>(u, b, g, Gi);
+    if (h->d == 2) kl(h, k_coarse_solve<2>, 1, 32, 0)(u, b, g, Gi);
+    else kl(h, k_coarse_solve<3>, 1, 32, 0)(u, b, g, Gi);
     prof_end(h, pe, PROF_COARSE, 16.0 * Pc);
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -678,8 +715,8 @@ isdc_status tail_dispatch(isdc_ctx *h, const TailParams &P, bool attr_only = fal
             : cudaFuncSetAttribute(k_tail<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem);
         return e == cudaSuccess ? ISDC_OK : ISDC_ERR_CUDA;
     }
-    if (h->d == 2) k_tail<2><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
-    else k_tail<3><<<1, TAIL_THREADS, h->tail_smem, h->s>>>(P);
+    if (h->d == 2) kl(h, k_tail<2>, 1, TAIL_THREADS, h->tail_smem)(P);
+    else kl(h, k_tail<3>, 1, TAIL_THREADS, h->tail_smem)(P);
     return ISDC_OK;
 }
 
@@ -810,7 +847,7 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         ++h->launches;
         int pe = prof_begin(h, PROF_RHS);
         const int fe = h->fe.kind;
-#define ISDC_RS(FE_, M_) f2d::k_rhs_s<FE_, M_><<<grd, f2d::SW_NT, 0, h->s>>>(A)
+#define ISDC_RS(FE_, M_) kl(h, f2d::k_rhs_s<FE_, M_>, grd, f2d::SW_NT, 0)(A)
         if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
         else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
 #undef ISDC_RS
@@ -883,9 +920,9 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         dim3 grd((g.n + f2d::QX - 1) / f2d::QX, (g.n + f2d::QY - 1) / f2d::QY);
         ++h->launches;
         int pe = prof_begin(h, PROF_RHS);
-        if (A.fe == 0) f2d::k_rhs<0><<<grd, f2d::QNT, 0, h->s>>>(A, bout, slot);
-        else if (A.fe == 1) f2d::k_rhs<1><<<grd, f2d::QNT, 0, h->s>>>(A, bout, slot);
-        else f2d::k_rhs<2><<<grd, f2d::QNT, 0, h->s>>>(A, bout, slot);
+        if (A.fe == 0) kl(h, f2d::k_rhs<0>, grd, f2d::QNT, 0)(A, bout, slot);
+        else if (A.fe == 1) kl(h, f2d::k_rhs<1>, grd, f2d::QNT, 0)(A, bout, slot);
+        else kl(h, f2d::k_rhs<2>, grd, f2d::QNT, 0)(A, bout, slot);
         prof_end(h, pe, PROF_RHS, (h->M + 2 + (h->fe.kind == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
         LAUNCH_CHECK(h);
         return ISDC_OK;
@@ -895,8 +932,8 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
     const GridDesc &g = h->lev[0].g;
     ++h->launches;
     int pe = prof_begin(h, PROF_RHS);
-    if (h->d == 2) k_vw<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
-    else k_vw<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
+    if (h->d == 2) kl(h, k_vw<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->V, h->W, P);
+    else kl(h, k_vw<3>, point_grid<3>(g, kBlk), kBlk, 0)(h->V, h->W, P);
     LAUNCH_CHECK(h);
     unsigned long long *slot = nullptr;
     if (bnorm) {
@@ -904,8 +941,8 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         slot = h->red + SLOT_BNORM;
     }
     ++h->launches;
-    if (h->d == 2) k_bvw<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(bout, h->V, h->W, g, h->bl, slot);
-    else k_bvw<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(bout, h->V, h->W, g, h->bl, slot);
+    if (h->d == 2) kl(h, k_bvw<2>, point_grid<2>(g, kBlk), kBlk, 0)(bout, h->V, h->W, g, h->bl, slot);
+    else kl(h, k_bvw<3>, point_grid<3>(g, kBlk), kBlk, 0)(bout, h->V, h->W, g, h->bl, slot);
     prof_end(h, pe, PROF_RHS, (h->M + 2 + (h->fe.kind == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -986,8 +1023,8 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         const int fe = h->fe.kind;
 #define ISDC_RS(FE_, M_)                                                                                \
     do {                                                                                                \
-        if (h->P.residual_kind == 1) f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), true><<<grd, f2d::SW_NT, 0, h->s>>>(A); \
-        else f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), false><<<grd, f2d::SW_NT, 0, h->s>>>(A);                       \
+        if (h->P.residual_kind == 1) kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), true>, grd, f2d::SW_NT, 0)(A); \
+        else kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), false>, grd, f2d::SW_NT, 0)(A);                       \
     } while (0)
         if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
         else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
@@ -1011,9 +1048,9 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         dim3 grd((g.n + f2d::ZX - 1) / f2d::ZX, (g.n + f2d::ZY - 1) / f2d::ZY);
         ++h->launches;
         int pe = prof_begin(h, PROF_RESID);
-        if (A.fe == 0) f2d::k_resid<0><<<grd, f2d::ZNT, sm, h->s>>>(A, h->red + SLOT_RES0);
-        else if (A.fe == 1) f2d::k_resid<1><<<grd, f2d::ZNT, sm, h->s>>>(A, h->red + SLOT_RES0);
-        else f2d::k_resid<2><<<grd, f2d::ZNT, sm, h->s>>>(A, h->red + SLOT_RES0);
+        if (A.fe == 0) kl(h, f2d::k_resid<0>, grd, f2d::ZNT, sm)(A, h->red + SLOT_RES0);
+        else if (A.fe == 1) kl(h, f2d::k_resid<1>, grd, f2d::ZNT, sm)(A, h->red + SLOT_RES0);
+        else kl(h, f2d::k_resid<2>, grd, f2d::ZNT, sm)(A, h->red + SLOT_RES0);
         prof_end(h, pe, PROF_RESID, (M + (h->fe.kind == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
         LAUNCH_CHECK(h);
         return ISDC_OK;
@@ -1033,12 +1070,12 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         P.g = g;
         h->launches += 2;
         if (h->d == 2) {
-            k_pz<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
-            k_resid<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1,
+            kl(h, k_pz<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->V, h->W, P);
+            kl(h, k_resid<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1,
                                                                  h->P.residual_kind == 1 ? h->RT[m - 1] : nullptr);
         } else {
-            k_pz<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, P);
-            k_resid<3><<<point_grid<3>(g, kBlk), kBlk, 0, h->s>>>(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1,
+            kl(h, k_pz<3>, point_grid<3>(g, kBlk), kBlk, 0)(h->V, h->W, P);
+            kl(h, k_resid<3>, point_grid<3>(g, kBlk), kBlk, 0)(h->V, h->W, g, h->bl, h->red + SLOT_RES0 + m - 1,
                                                                  nullptr);
         }
         LAUNCH_CHECK(h);
@@ -1071,7 +1108,7 @@ isdc_status unweighted_norms(isdc_ctx *h, double *norms) {
         }
         TRY(clear_slots(h, SLOT_SCRATCH, 1));
         ++h->launches;
-        k_norm<2><<<point_grid<2>(g, kBlk), kBlk, 0, h->s>>>(h->WX, g, h->red + SLOT_SCRATCH);
+        kl(h, k_norm<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->WX, g, h->red + SLOT_SCRATCH);
         LAUNCH_CHECK(h);
         TRY(read_slots(h, SLOT_SCRATCH, 1, &norms[m - 1]));
     }
@@ -1301,6 +1338,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *b16 = getenv("ISDC_BL16")) h->bl16 = b16[0] != '0';
     if (const char *r16 = getenv("ISDC_RHS16")) h->rhs16 = r16[0] != '0';
     if (const char *t2 = getenv("ISDC_TAIL2D")) h->tail2d = atoi(t2);
+    if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {

@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
                                                 const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
                                                 int n, int pitch, SCoef c, unsigned long long *slot,
                                                 const __grid_constant__ CUtensorMap te) {
+    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemSmooth &S = *reinterpret_cast<SmemSmooth *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();   // only shared-memory setup above
     if (tid == 0) {
         mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : UW * UH) + BW * BH + (MODE == 2 ? EW * EH : 0)) * 8);
         if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 - 2, y0 - 2, &S.bar);
@@ -177,6 +179,7 @@ struct __align__(128) SmemRestrict {
 __global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtensorMap tu,
                                                   const __grid_constant__ CUtensorMap tb, double *__restrict__ bc,
                                                   int nf, int nc, int pitch_c, SCoef c) {
+    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemRestrict &S = *reinterpret_cast<SmemRestrict *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     const int tid = threadIdx.x;
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtens
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();   // only shared-memory setup above
     if (tid == 0) {
         mbar_expect_tx(&S.bar, (RUW * RUH + RBW * RBH) * 8);
         tma_load_2d(&S.u[0][0], &tu, fx0 - 2, fy0 - 1, &S.bar);
@@ -246,6 +250,8 @@ __global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtens
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf, int pitch_f,
                                                  const double *__restrict__ e, int nc, int pitch_c) {
+    pdl_launch();
+    pdl_wait();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;   // column pair
     const int y = blockIdx.y;
     const int x = 2 * t;
@@ -306,6 +312,8 @@ struct RhsArgs {
 
 template <int FE>
 __global__ void __launch_bounds__(QNT) k_rhs(RhsArgs A, double *__restrict__ bout, unsigned long long *slot) {
+    pdl_launch();
+    pdl_wait();
     __shared__ double vs[QH][QW];
     __shared__ double ws[QH][QW];
     const int tid = threadIdx.x;
@@ -404,6 +412,8 @@ struct ResArgs {
 
 template <int FE>
 __global__ void __launch_bounds__(ZNT) k_resid(ResArgs A, unsigned long long *slots) {
+    pdl_launch();
+    pdl_wait();
     extern __shared__ __align__(16) double zsm[];
     const int M = A.M;
     double *ps = zsm;                                  // [M-1][ZH][ZW]
@@ -568,6 +578,8 @@ __device__ __forceinline__ void rhs_row(const StreamArgs &A, const double (&L)[M
 
 template <int FE, int MM>
 __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
+    pdl_launch();
+    pdl_wait();
     const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5);
     const int n = A.n;
     const int x = strip * SW_OUT - 1 + lane;
@@ -623,6 +635,8 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
 // register rings and doubles the resident warps.
 template <int FE, int MM, int NMW, bool WRT = false>   // WRT: also store the r~_m fields (unweighted residual)
 __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {
+    pdl_launch();
+    pdl_wait();
     constexpr int G = (MM - 1) / NMW;
     const int wid = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32 / G) + wid / G;
@@ -792,6 +806,7 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
                                                  const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
                                                  double *__restrict__ bc, int n, int pitch, int nc, int pitch_c,
                                                  SCoef c) {
+    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemSR &S = *reinterpret_cast<SmemSR *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     const int tid = threadIdx.x;
@@ -803,6 +818,7 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();   // only shared-memory setup above
     if (tid == 0) {
         mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : FR_UW * FR_UH) + FR_BW * FR_BH) * 8);
         if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 + FR_UOX, y0 + FR_UOY, &S.bar);

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
                                                                 double *__restrict__ out, int n, int pitch,
                                                                 long long plane, SCoef c, int zc,
                                                                 const __grid_constant__ CUtensorMap te) {
+    pdl_launch();
     constexpr bool PRO = MODE == 2, ZERO = MODE == 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
         for (int s = 0; s < S_NS; ++s)
             for (int q = tid; q < S_UW * S_UH; q += blockDim.x) Usw[s * (S_UPL / 8) + q] = 0.0;
     __syncthreads();
+    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < S_NS && it < nit; ++it) issue(it);
 
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
                                                     const __grid_constant__ CUtensorMap tb,
                                                     double *__restrict__ bc, int nf, int nc, int pitch_c,
                                                     long long plane_c, SCoef c, int kc) {
+    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
     double *Us = reinterpret_cast<double *>(sm);
@@ -323,6 +326,7 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < R_NS && it < nit; ++it) issue(it);
 
@@ -391,6 +395,8 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
 __global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf, int pitch_f, long long plane_f,
                                                  const double *__restrict__ e, int nc, int pitch_c,
                                                  long long plane_c) {
+    pdl_launch();
+    pdl_wait();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y, z = blockIdx.z;
     const int x = 2 * t;
@@ -575,6 +581,7 @@ __device__ __forceinline__ void bl_point(const BLArgs &A, int k, const double *F
 // NWW warps (region rows NWW * RR).
 template <int FE, int MODE, int RR, int NM, int NWW = NW>
 __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
+    pdl_launch();
     using SH = BLShape<RR, NWW>;
     constexpr bool RHS = MODE != 1;   // MODE 0: RHS, 1: residual, 2: RHS from stored folds
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -599,6 +606,7 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < ns && it < nit; ++it) issue(it);
 
@@ -715,6 +723,7 @@ constexpr size_t FE_SMEM = (size_t)FE_NS * FE_PL + 8 * FE_NS + 128;
 __global__ void __launch_bounds__(NT, 1) k_fe_cd4(const __grid_constant__ CUtensorMap tu, double *__restrict__ Fout,
                                                   int n, int pitch, long long plane, double kx, double ky,
                                                   double kz, int zc) {
+    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     double *Us = reinterpret_cast<double *>(sm);
@@ -733,6 +742,7 @@ __global__ void __launch_bounds__(NT, 1) k_fe_cd4(const __grid_constant__ CUtens
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < FE_NS && it < nit; ++it) issue(it);
     const int gx = x0 + lane;
