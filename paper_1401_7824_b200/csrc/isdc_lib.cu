@@ -71,6 +71,7 @@ struct isdc_ctx {
     bool pdl = false;          // ISDC_PDL=1: programmatic dependent launch (measured neutral with the implicit
                                // trigger, slower with an early trigger)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
+    bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
@@ -533,6 +534,19 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
 // fused pre-smoother (2 sweeps) + defect + full weighting, 2D; in == nullptr: zero iterate
 isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                             double *bc, const GridDesc &gc, const SCoef &c, int level) {
+    if (h->sr_stream) {   // warp-strip streaming variant (no shared memory)
+        ++h->launches;
+        const int cls = level == 0 ? PROF_RESTRICT : PROF_COARSE;
+        int pe = prof_begin(h, cls);
+        const int strips = (g.n + f2d::SR_OUT - 1) / f2d::SR_OUT;
+        const int yc = g.n >= 1023 ? 64 : 32;
+        dim3 grd((strips + f2d::SW_NT / 32 - 1) / (f2d::SW_NT / 32), (g.n + yc - 1) / yc);
+        if (in) kl(h, f2d::k_sr_s<0>, grd, f2d::SW_NT, 0)(in, b, out, bc, g.n, g.pitch, gc.n, gc.pitch, c, yc);
+        else kl(h, f2d::k_sr_s<1>, grd, f2d::SW_NT, 0)(in, b, out, bc, g.n, g.pitch, gc.n, gc.pitch, c, yc);
+        prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + 2.0) * npts_of(h, g));
+        LAUNCH_CHECK(h);
+        return ISDC_OK;
+    }
     const CUtensorMap *mb = tmap(h, b, g, f2d::FR_BW, f2d::FR_BH);
     const CUtensorMap *mu = in ? tmap(h, in, g, f2d::FR_UW, f2d::FR_UH) : mb;
     if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
@@ -1339,6 +1353,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *r16 = getenv("ISDC_RHS16")) h->rhs16 = r16[0] != '0';
     if (const char *t2 = getenv("ISDC_TAIL2D")) h->tail2d = atoi(t2);
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
+    if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
     {
