@@ -78,7 +78,7 @@ struct isdc_ctx {
     bool fuse3d = false;       // ISDC_FUSE3D=1: fused 3D prolongation + smoother (slower so far)
     bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
     bool stream2d = true;      // ISDC_STREAM2D=0: the tile-based 2D RHS / residual kernels instead
-    int smooth3d_rows = 4;     // ISDC_SMOOTH3D_ROWS: rows per thread of the 3D fused smoother (2 or 4)
+    int smooth3d_rows = 0;     // ISDC_SMOOTH3D_ROWS: rows per thread of the 3D fused smoother (2, 3, 4; 0 = auto)
     int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
     TailParams tailp[ISDC_MAXM];
@@ -389,33 +389,44 @@ int pick_chunk(const isdc_ctx *h, int tiles, int planes, int halo) {
     return best;
 }
 
-// e != nullptr: u + P e first (fused trilinear prolongation + correction)
-isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
-                              const SCoef &c, int level, const double *e = nullptr, const GridDesc *gc = nullptr) {
-    const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, f3d::S_BH, 1);
-    const CUtensorMap *mu = in ? tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1) : mb;   // in == nullptr: zero iterate
+// e != nullptr: u + P e first (fused trilinear prolongation + correction); in == nullptr:
+// zero iterate.  Shape (rows per thread SR x warps): 4 x 8 (32-row region, default), 2 x 16, 3 x 12.
+template <int SR, int NWW>
+isdc_status launch_smooth2_3d_t(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
+                                const SCoef &c, int level, const double *e, const GridDesc *gc) {
+    using Z = f3d::SS<SR * NWW>;
+    const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, Z::BH, 1);
+    const CUtensorMap *mu = in ? tmap(h, in, g, f3d::S_UW, Z::UH, 1) : mb;
     const CUtensorMap *me = e ? tmap(h, e, *gc, f3d::S_EW, f3d::S_EH, 1) : mb;
     if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
     const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
     int pe = prof_begin(h, cls);
-    int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + f3d::S_TY - 1) / f3d::S_TY;
+    int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + Z::TY - 1) / Z::TY;
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
-#define ISDC_S3(SR_, MODE_, SM_) \
-    kl(h, f3d::k_smooth2<SR_, MODE_>, grd, 32 * (32 / SR_), SM_)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me)
-    if (e) {
-        if (h->smooth3d_rows == 4) ISDC_S3(4, 2, f3d::S_SMEM_PRO); else ISDC_S3(2, 2, f3d::S_SMEM_PRO);
-    } else if (!in) {
-        if (h->smooth3d_rows == 4) ISDC_S3(4, 1, f3d::S_SMEM); else ISDC_S3(2, 1, f3d::S_SMEM);
-    } else {
-        if (h->smooth3d_rows == 4) ISDC_S3(4, 0, f3d::S_SMEM); else ISDC_S3(2, 0, f3d::S_SMEM);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(f3d::k_smooth2<SR, 0, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<SR, 1, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM);
+        cudaFuncSetAttribute(f3d::k_smooth2<SR, 2, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM_PRO);
+        attr = true;
     }
-#undef ISDC_S3
+    if (e) kl(h, f3d::k_smooth2<SR, 2, NWW>, grd, 32 * NWW, Z::SMEM_PRO)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+    else if (!in) kl(h, f3d::k_smooth2<SR, 1, NWW>, grd, 32 * NWW, Z::SMEM)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
+    else kl(h, f3d::k_smooth2<SR, 0, NWW>, grd, 32 * NWW, Z::SMEM)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
     // algorithmic bytes: read u (unless zero), b (+ e / 8); write u''
     prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 1.0 : 0.0)) * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
+}
+isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
+                              const SCoef &c, int level, const double *e = nullptr, const GridDesc *gc = nullptr) {
+    // auto: 3 x 12 warps up to 255^3 (measured 1.5 % faster on config 4), 4 x 8 above (config 5)
+    const int rows = h->smooth3d_rows ? h->smooth3d_rows : (g.n <= 255 ? 3 : 4);
+    if (rows == 2) return launch_smooth2_3d_t<2, 16>(h, out, in, b, g, c, level, e, gc);
+    if (rows == 3) return launch_smooth2_3d_t<3, 12>(h, out, in, b, g, c, level, e, gc);
+    return launch_smooth2_3d_t<4, 8>(h, out, in, b, g, c, level, e, gc);
 }
 
 // two fused Jacobi sweeps on the fine 2D level
@@ -1355,7 +1366,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
     if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
-    if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) h->smooth3d_rows = atoi(sr) == 2 ? 2 : 4;
+    if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) { int v = atoi(sr); h->smooth3d_rows = (v == 2 || v == 3 || v == 4) ? v : 0; }
     {
         int dev = 0, nsm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -1378,12 +1389,6 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSR) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
-        cudaFuncSetAttribute(f3d::k_smooth2<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
-        cudaFuncSetAttribute(f3d::k_smooth2<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::S_SMEM_PRO);
         cudaFuncSetAttribute(f3d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::R_SMEM);
         cudaFuncSetAttribute(f3d::k_fe_cd4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::FE_SMEM);
 #define ISDC_BL_ATTR(FE_, MODE_, RR_, NM_) \

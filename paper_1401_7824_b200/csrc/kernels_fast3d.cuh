@@ -72,6 +72,17 @@ constexpr int S_EPL = a128(S_EW * S_EH * 8);
 constexpr int S_EOFF = S_NS * (S_UPL + S_BPL) + 2 * S_TPL + 128;   // after the mbarriers
 constexpr size_t S_SMEM_PRO = (size_t)S_EOFF + (size_t)S_NS * 2 * S_EPL + 128;
 
+// region-height-dependent sizes of the fused smoother (region RHR = SR x warps rows; the constants
+// above are the 32-row case)
+template <int RHR>
+struct SS {
+    static constexpr int TY = RHR - 2, UH = RHR + 2, BH = RHR, TH = RHR + 2;
+    static constexpr int UPL = a128(S_UW * UH * 8), BPL = a128(S_BW * BH * 8), TPL = a128(S_TW * TH * 8);
+    static constexpr size_t SMEM = (size_t)S_NS * (UPL + BPL) + 2 * TPL + 8 * S_NS + 128;
+    static constexpr int EOFF = S_NS * (UPL + BPL) + 2 * TPL + 128;
+    static constexpr size_t SMEM_PRO = (size_t)EOFF + (size_t)S_NS * 2 * S_EPL + 128;
+};
+
 // Register state of one thread (SR owned points).  Rings are indexed by the iteration that
 // produced the value (mod 3 for centre/face sums, mod 2 for edge sums and b), so after unrolling
 // the z loop by 6 every index is a compile-time constant and no value is ever moved.
@@ -101,7 +112,7 @@ struct SmoothCtx {
 // (rows w, w + nwarps, ...), lane = box column (plus lanes 0-1 for columns 32-33); the column
 // quantities are per-lane constants, the row quantities per-row constants.
 __device__ __noinline__ void prolong_plane(double *U, const double *Ea, const double *Eb, int p, int n, int x0, int y0,
-                                           int ex0, int ey0) {
+                                           int ex0, int ey0, int uh) {
     // out of line: the z loop is unrolled by 6, an inlined copy per step overflows the i-cache
     if ((unsigned)p >= (unsigned)n) return;
     const bool ze = !(p & 1);
@@ -116,7 +127,7 @@ __device__ __noinline__ void prolong_plane(double *U, const double *Ea, const do
         const bool xe = !(gx & 1);
         const int xa = (xe ? gx / 2 - 1 : (gx - 1) / 2) - ex0;
         const double wx = xe ? 0.5 : 1.0;
-        for (int ly = threadIdx.x >> 5; ly < S_UH; ly += nw) {
+        for (int ly = threadIdx.x >> 5; ly < uh; ly += nw) {
             const int gy = y0 - 2 + ly;
             if ((unsigned)gy >= (unsigned)n) continue;
             const bool ye = !(gy & 1);
@@ -136,24 +147,25 @@ __device__ __noinline__ void prolong_plane(double *U, const double *Ea, const do
     }
 }
 
-template <int SR, int K, bool PRO>   // K = it % 6 = it % S_NS (the z loop is unrolled by 6 from it = 0)
+template <int SR, int K, bool PRO, int RHR>   // K = it % 6 = it % S_NS (the z loop is unrolled by 6 from it = 0)
 __device__ __forceinline__ void smooth_step(const SmoothCtx<SR> &C, SmoothRegs<SR> &G, int it, uint32_t phase) {
+    using Z = SS<RHR>;
     static_assert(S_NS == 6, "stage index = K");
     constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3;   // it, it-1, it-2 (mod 3)
     constexpr int i2 = K % 2, m2 = (K + 1) % 2;                       // it, it-1 (mod 2)
     constexpr int s = K;
     mbar_wait(&C.bar[s], phase);
     if (PRO) {
-        prolong_plane(const_cast<double *>(C.Us + s * (S_UPL / 8)), C.Es + (2 * s) * (S_EPL / 8),
-                      C.Es + (2 * s + 1) * (S_EPL / 8), C.z0 - 2 + it, C.n, C.x0, C.y0, C.ex0, C.ey0);
+        prolong_plane(const_cast<double *>(C.Us + s * (Z::UPL / 8)), C.Es + (2 * s) * (S_EPL / 8),
+                      C.Es + (2 * s + 1) * (S_EPL / 8), C.z0 - 2 + it, C.n, C.x0, C.y0, C.ex0, C.ey0, Z::UH);
         __syncthreads();
     }
-    plane_partials<true, SR>(C.Us + s * (S_UPL / 8), S_UW, C.row0, C.lane, G.q[i3], G.f[i3], G.e[i2]);
-    double *T = C.Ts + i2 * (S_TPL / 8);
+    plane_partials<true, SR>(C.Us + s * (Z::UPL / 8), S_UW, C.row0, C.lane, G.q[i3], G.f[i3], G.e[i2]);
+    double *T = C.Ts + i2 * (Z::TPL / 8);
     if (it >= 2) {   // sweep 1 at plane gz = p-1 on the 32 x 32 region
         const int gz = C.z0 - 3 + it;
         const unsigned in = ((unsigned)gz < (unsigned)C.n) ? C.inxy : 0u;
-        const double *Bp = C.Bs + s * (S_BPL / 8) + C.row0 * S_BW + C.lane + 1;
+        const double *Bp = C.Bs + s * (Z::BPL / 8) + C.row0 * S_BW + C.lane + 1;
         double *Tp = T + (C.row0 + 1) * S_TW + C.lane + 1;
 #pragma unroll
         for (int r = 0; r < SR; ++r) {
@@ -168,12 +180,13 @@ __device__ __forceinline__ void smooth_step(const SmoothCtx<SR> &C, SmoothRegs<S
     }
 }
 
-template <int SR, int K>
+template <int SR, int K, int RHR>
 __device__ __forceinline__ void smooth_step2(const SmoothCtx<SR> &C, SmoothRegs<SR> &G, int it) {
+    using Z = SS<RHR>;
     constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3;
     constexpr int i2 = K % 2, m2 = (K + 1) % 2;
     if (it < 2) return;
-    const double *T = C.Ts + i2 * (S_TPL / 8);
+    const double *T = C.Ts + i2 * (Z::TPL / 8);
     plane_partials<true, SR>(T, S_TW, C.row0, C.lane, G.tq[i3], G.tf[i3], G.te[i2]);
     if (it >= 4) {   // sweep 2 at plane p-2 = z0 - 4 + it on the 30 x 30 tile
         double *op = C.optr + (long long)it * C.plane;
@@ -194,38 +207,40 @@ __device__ __forceinline__ void smooth_step2(const SmoothCtx<SR> &C, SmoothRegs<
 // MODE 1: u == 0 (first smoothing of a coarse correction: u is neither stored nor read, the
 // u stages stay zero); MODE 2: u + P e first (fused trilinear prolongation + correction, te =
 // coarse correction map with 20 x 18 x 1 boxes).
-template <int SR, int MODE>
-__global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_constant__ CUtensorMap tu,
+template <int SR, int MODE, int NWW = 32 / SR>
+__global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__ CUtensorMap tu,
                                                                 const __grid_constant__ CUtensorMap tb,
                                                                 double *__restrict__ out, int n, int pitch,
                                                                 long long plane, SCoef c, int zc,
                                                                 const __grid_constant__ CUtensorMap te) {
     pdl_launch();
     constexpr bool PRO = MODE == 2, ZERO = MODE == 1;
+    constexpr int RHR = SR * NWW;   // region rows
+    using Z = SS<RHR>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
     SmoothCtx<SR> C;
     C.Us = reinterpret_cast<const double *>(sm);
-    C.Bs = reinterpret_cast<const double *>(sm + S_NS * S_UPL);
-    C.Ts = reinterpret_cast<double *>(sm + S_NS * (S_UPL + S_BPL));
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S_NS * (S_UPL + S_BPL) + 2 * S_TPL);
-    double *Esw = reinterpret_cast<double *>(sm + S_EOFF);
+    C.Bs = reinterpret_cast<const double *>(sm + S_NS * Z::UPL);
+    C.Ts = reinterpret_cast<double *>(sm + S_NS * (Z::UPL + Z::BPL));
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S_NS * (Z::UPL + Z::BPL) + 2 * Z::TPL);
+    double *Esw = reinterpret_cast<double *>(sm + Z::EOFF);
     C.bar = bar;
     C.Es = Esw;
     const int tid = threadIdx.x;
     C.lane = tid & 31;
     C.row0 = SR * (tid >> 5);
-    const int x0 = blockIdx.x * S_TX, y0 = blockIdx.y * S_TY;
+    const int x0 = blockIdx.x * S_TX, y0 = blockIdx.y * Z::TY;
     const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, n);
     const int nit = z1 - z0 + 4;
     C.z0 = z0; C.n = n; C.pitch = pitch; C.plane = plane;
     C.x0 = x0; C.y0 = y0; C.ex0 = (x0 / 2 - 2) & ~1; C.ey0 = y0 / 2 - 2;
-    double *Usw = reinterpret_cast<double *>(sm), *Bsw = reinterpret_cast<double *>(sm + S_NS * S_UPL);
+    double *Usw = reinterpret_cast<double *>(sm), *Bsw = reinterpret_cast<double *>(sm + S_NS * Z::UPL);
     auto issue = [&](int it) {
         const int s = it % S_NS, p = z0 - 2 + it;
-        mbar_expect_tx(&bar[s], ((ZERO ? 0 : S_UW * S_UH) + S_BW * S_BH + (PRO ? 2 * S_EW * S_EH : 0)) * 8);
-        if (!ZERO) tma_load_3d(Usw + s * (S_UPL / 8), &tu, x0 - 2, y0 - 2, p, &bar[s]);
-        tma_load_3d(Bsw + s * (S_BPL / 8), &tb, x0 - 2, y0 - 1, p - 1, &bar[s]);
+        mbar_expect_tx(&bar[s], ((ZERO ? 0 : S_UW * Z::UH) + S_BW * Z::BH + (PRO ? 2 * S_EW * S_EH : 0)) * 8);
+        if (!ZERO) tma_load_3d(Usw + s * (Z::UPL / 8), &tu, x0 - 2, y0 - 2, p, &bar[s]);
+        tma_load_3d(Bsw + s * (Z::BPL / 8), &tb, x0 - 2, y0 - 1, p - 1, &bar[s]);
         if (PRO) {   // coarse planes Za, Zb of fine plane p (Za = Zb for odd p)
             const int za = (p & 1) ? (p - 1) / 2 : p / 2 - 1, zb = (p & 1) ? za : p / 2;
             tma_load_3d(Esw + (2 * s) * (S_EPL / 8), &te, C.ex0, C.ey0, za, &bar[s]);
@@ -240,7 +255,7 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
     }
     if (ZERO)
         for (int s = 0; s < S_NS; ++s)
-            for (int q = tid; q < S_UW * S_UH; q += blockDim.x) Usw[s * (S_UPL / 8) + q] = 0.0;
+            for (int q = tid; q < S_UW * Z::UH; q += blockDim.x) Usw[s * (Z::UPL / 8) + q] = 0.0;
     __syncthreads();
     pdl_wait();   // only shared-memory setup above
     if (tid == 0)
@@ -256,7 +271,7 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
     for (int r = 0; r < SR; ++r) {
         const int ly = ly0 + r, gy = y0 + ly;
         if (xin && gy >= 0 && gy < n) C.inxy |= 1u << r;
-        if (xout && ly >= 0 && ly < S_TY && gy < n) C.oks |= 1u << r;
+        if (xout && ly >= 0 && ly < Z::TY && gy < n) C.oks |= 1u << r;
     }
     C.optr = out + (long long)(z0 - 4) * plane + (long long)(y0 + ly0) * pitch + gx;
     SmoothRegs<SR> G;
@@ -268,10 +283,10 @@ __global__ void __launch_bounds__(32 * (RH / SR), 1) k_smooth2(const __grid_cons
     {                                                                  \
         const int it = base + (K);                                     \
         if (it < nit) {                                                \
-            smooth_step<SR, K, (MODE == 2)>(C, G, it, phase);          \
+            smooth_step<SR, K, (MODE == 2), RHR>(C, G, it, phase);    \
             __syncthreads();                                           \
             if (tid == 0 && it + S_NS < nit) issue(it + S_NS);         \
-            smooth_step2<SR, K>(C, G, it);                             \
+            smooth_step2<SR, K, RHR>(C, G, it);                       \
         }                                                              \
     }
     for (int base = 0; base < nit; base += 6) {
