@@ -49,7 +49,7 @@ class OraProblem(C.Structure):
         ("mode", C.c_int), ("L", C.c_int), ("inner_tol", C.c_double), ("inner_cap", C.c_int),
         ("sweep_tol", C.c_double), ("max_sweeps", C.c_int), ("fixed_sweeps", C.c_int),
         ("nu1", C.c_int), ("nu2", C.c_int), ("omega", C.c_double), ("guess", C.c_int),
-        ("res_kind", C.c_int), ("w_tol", C.c_double), ("w_cap", C.c_int),
+        ("res_kind", C.c_int), ("w_tol", C.c_double), ("w_cap", C.c_int), ("bc", C.c_int),
     ]
 
 
@@ -80,6 +80,9 @@ def _declare(L):
                            C.POINTER(C.c_int)]
     L.ora_num_threads.restype = C.c_int
     L.ora_last_wcycles.restype = C.c_long
+    L.ora_set_bc.argtypes = [C.c_int]
+    L.ora_weno5.argtypes = [C.c_double] * 5
+    L.ora_weno5.restype = C.c_double
 
 
 def _p(a: np.ndarray):
@@ -107,67 +110,78 @@ def tables(M: int):
     return tau, Q, S, dtau
 
 
-def apply_B(u):
+def _bc(periodic):
+    """Select the grid kind of the next oracle call (isdc_oracle.c header: Dirichlet / periodic)."""
+    lib().ora_set_bc(1 if periodic else 0)
+    return lib()
+
+
+def weno5(v0, v1, v2, v3, v4):
+    """WENO5-JS face value from five cell values (isdc_oracle.c weno5, reading R31)."""
+    return lib().ora_weno5(float(v0), float(v1), float(v2), float(v3), float(v4))
+
+
+def apply_B(u, periodic=False):
     u = _c(u); out = np.empty_like(u)
-    lib().ora_apply_B(u.ndim, u.shape[0], _p(u), _p(out)); return out
+    _bc(periodic).ora_apply_B(u.ndim, u.shape[0], _p(u), _p(out)); return out
 
 
-def apply_L(u):
+def apply_L(u, periodic=False):
     u = _c(u); out = np.empty_like(u)
-    lib().ora_apply_L(u.ndim, u.shape[0], _p(u), _p(out)); return out
+    _bc(periodic).ora_apply_L(u.ndim, u.shape[0], _p(u), _p(out)); return out
 
 
-def apply_S(u, gamma):
+def apply_S(u, gamma, periodic=False):
     u = _c(u); out = np.empty_like(u)
-    lib().ora_apply_S(u.ndim, u.shape[0], gamma, _p(u), _p(out)); return out
+    _bc(periodic).ora_apply_S(u.ndim, u.shape[0], gamma, _p(u), _p(out)); return out
 
 
-def level_coefs(dim, n, gamma, omega=0.8):
+def level_coefs(dim, n, gamma, omega=0.8, periodic=False):
     c = np.zeros(4)
-    lib().ora_level_coefs(dim, n, gamma, omega, _p(c)); return c
+    _bc(periodic).ora_level_coefs(dim, n, gamma, omega, _p(c)); return c
 
 
-def jacobi(b, u, gamma, sweeps=1, omega=0.8):
+def jacobi(b, u, gamma, sweeps=1, omega=0.8, periodic=False):
     b = _c(b); u = _c(u).copy()
-    lib().ora_jacobi(u.ndim, u.shape[0], gamma, omega, sweeps, _p(b), _p(u)); return u
+    _bc(periodic).ora_jacobi(u.ndim, u.shape[0], gamma, omega, sweeps, _p(b), _p(u)); return u
 
 
-def defect_norm(b, u, gamma):
+def defect_norm(b, u, gamma, periodic=False):
     b = _c(b); u = _c(u)
-    return lib().ora_defect_norm(u.ndim, u.shape[0], gamma, _p(b), _p(u))
+    return _bc(periodic).ora_defect_norm(u.ndim, u.shape[0], gamma, _p(b), _p(u))
 
 
-def restrict(d):
-    d = _c(d); nc = (d.shape[0] - 1) // 2
+def restrict(d, periodic=False):
+    d = _c(d); nc = d.shape[0] // 2 if periodic else (d.shape[0] - 1) // 2
     out = np.zeros((nc,) * d.ndim)
-    lib().ora_restrict(d.ndim, d.shape[0], _p(d), _p(out)); return out
+    _bc(periodic).ora_restrict(d.ndim, d.shape[0], _p(d), _p(out)); return out
 
 
-def prolong_add(ec, uf):
+def prolong_add(ec, uf, periodic=False):
     ec = _c(ec); uf = _c(uf).copy()
-    lib().ora_prolong_add(ec.ndim, ec.shape[0], _p(ec), _p(uf)); return uf
+    _bc(periodic).ora_prolong_add(ec.ndim, ec.shape[0], _p(ec), _p(uf)); return uf
 
 
-def coarse_inverse(dim, gamma, omega=0.8):
-    P = 9 if dim == 2 else 27
+def coarse_inverse(dim, gamma, omega=0.8, periodic=False):
+    P = (4 if periodic else 3) ** dim
     G = np.zeros((P, P))
-    if lib().ora_coarse_inverse(dim, gamma, omega, _p(G)):
+    if _bc(periodic).ora_coarse_inverse(dim, gamma, omega, _p(G)):
         raise ValueError("singular")
     return G
 
 
-def vcycle(b, u, gamma, nu1=2, nu2=2, omega=0.8, cycles=1):
+def vcycle(b, u, gamma, nu1=2, nu2=2, omega=0.8, cycles=1, periodic=False):
     b = _c(b); u = _c(u).copy()
     for _ in range(cycles):
-        lib().ora_vcycle(u.ndim, u.shape[0], gamma, nu1, nu2, omega, _p(b), _p(u))
+        _bc(periodic).ora_vcycle(u.ndim, u.shape[0], gamma, nu1, nu2, omega, _p(b), _p(u))
     return u
 
 
-def fe_eval(fe, u, a=(0.0, 0.0, 0.0), G=None, ct=1.0):
+def fe_eval(fe, u, a=(0.0, 0.0, 0.0), G=None, ct=1.0, periodic=False):
     u = _c(u); out = np.empty_like(u)
     av = np.array(a, dtype=np.float64)
     Gp = _p(_c(G)) if G is not None else None
-    lib().ora_fe_eval(fe, u.ndim, u.shape[0], _p(av), Gp, ct, _p(u), _p(out)); return out
+    _bc(periodic).ora_fe_eval(fe, u.ndim, u.shape[0], _p(av), Gp, ct, _p(u), _p(out)); return out
 
 
 # ---------------------------------------------------------------------------------------------
@@ -190,6 +204,7 @@ class Problem:
         s.sweep_tol, s.max_sweeps, s.fixed_sweeps = cfg.sweep_tol, cfg.max_sweeps, cfg.fixed_sweeps
         s.nu1, s.nu2, s.omega, s.guess = cfg.nu1, cfg.nu2, cfg.omega, guess
         s.res_kind, s.w_tol, s.w_cap = res_kind, w_tol, w_cap
+        s.bc = getattr(cfg, "bc", 0)
 
 
 def _ptrs(fields):

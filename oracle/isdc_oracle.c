@@ -12,8 +12,12 @@
  * Compile: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC ... -lquadmath
  * (no FMA contraction: every a*b+c below is a rounded multiply followed by a rounded add).
  *
- * Layout: dense fp64 arrays, n^d interior points, x fastest: idx = i + n*(j + n*k).
- * Homogeneous Dirichlet data: every value outside 0..n-1 reads as 0.
+ * Layout: dense fp64 arrays, n^d points, x fastest: idx = i + n*(j + n*k).
+ * Boundary kinds (g_per, set per call by ora_set_bc / from ora_problem.bc):
+ *   Dirichlet (default): n = 2^p - 1 interior points of [0,1]^d, h = 1/(n+1); every value outside
+ *     0..n-1 reads as 0 (homogeneous data).
+ *   Periodic (NEXT f3, Burgers P:106-112): n = 2^p points x_i = -1 + i h of [-1,1)^d, h = 2/n;
+ *     indices wrap modulo n ("periodic boundary conditions"; reading R31).
  *
  * Pins (tests/test_oracle_*.py): every function below is pinned by a closed form, an invariant,
  * a special case or brute force, except where a header comment says "parity unpinned".
@@ -119,7 +123,23 @@ int ora_tables(int M, double *tau, double *Q, double *S, double *dtau) {
 /* ------------------------------------------------------------------------------------------ */
 /* Grid access                                                                                 */
 /* ------------------------------------------------------------------------------------------ */
+static int g_per = 0;    /* 1: periodic grid (see the header); read-only inside parallel regions */
+void ora_set_bc(int periodic) { g_per = periodic ? 1 : 0; }
+int ora_get_bc(void) { return g_per; }
+
+/* one wrap suffices: stencil offsets are at most 3 and n >= 4 */
+static inline int wrap(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+/* 1/h: Dirichlet N = n+1; periodic n/2 (both exact powers of two) */
+static inline double inv_h(int n) { return g_per ? (double)n * 0.5 : (double)(n + 1); }
+/* next coarser level and the coarsest one (exact dense solve) */
+static inline int coarser(int n) { return g_per ? n / 2 : (n - 1) / 2; }
+static inline int coarsest(void) { return g_per ? 4 : 3; }
+
 static inline double at(const double *u, int d, int n, int i, int j, int k) {
+    if (g_per) {
+        i = wrap(i, n); j = wrap(j, n);
+        if (d == 3) k = wrap(k, n);
+    }
     if (i < 0 || j < 0 || i >= n || j >= n) return 0.0;
     if (d == 3) {
         if (k < 0 || k >= n) return 0.0;
@@ -159,7 +179,7 @@ static inline double edges(const double *q, int d, int n, int i, int j, int k) {
 /* Compact (Mehrstellen) pair, P:68-72 and SPEC S:144 (2D); 3D: standard 19-point pair.        */
 /*   2D: L_h = 1/(6h^2)[1 4 1; 4 -20 4; 1 4 1],  B_h = 1/12[0 1 0; 1 8 1; 0 1 0]               */
 /*   3D: L_h = 1/(6h^2)(centre -24, faces 2, edges 1),  B_h = 1/12(centre 6, faces 1)          */
-/* Constants (host, binary64, in this order): N2 = N*N;                                        */
+/* Constants (host, binary64, in this order): N = 1/h (inv_h), N2 = N*N;                     */
 /*   2D kB0 = 8/12, kB1 = 1/12, kL0 = (-20*N2)/6, kL1 = (4*N2)/6, kL2 = N2/6                   */
 /*   3D kB0 = 6/12, kB1 = 1/12, kL0 = (-24*N2)/6, kL1 = (2*N2)/6, kL2 = N2/6                   */
 /*   B q = kB0*q + kB1*faces;   L q = (kL0*q + kL1*faces) + kL2*edges                          */
@@ -168,7 +188,7 @@ typedef struct { double kB0, kB1, kL0, kL1, kL2; } bl_consts;
 
 static bl_consts make_bl(int d, int n) {
     bl_consts c;
-    double N = (double)(n + 1), N2 = N * N;
+    double N = inv_h(n), N2 = N * N;
     if (d == 2) {
         c.kB0 = 8.0 / 12.0; c.kB1 = 1.0 / 12.0;
         c.kL0 = (-20.0 * N2) / 6.0; c.kL1 = (4.0 * N2) / 6.0; c.kL2 = N2 / 6.0;
@@ -204,7 +224,7 @@ void ora_apply_L(int d, int n, const double *q, double *out) {
 
 /* ------------------------------------------------------------------------------------------ */
 /* Node-system operator S_l = B_h - gamma L_h on level l ("W - dt_m A", A = nu L_h),      */
-/* rediscretised with h_l = 1/N_l.  g = gamma*(N_l*N_l) (exact: N_l^2 is a power of two).      */
+/* rediscretised with h_l = 1/N_l (N_l = inv_h).  g = gamma*(N_l*N_l) (N_l^2 a power of two).  */
 /*   2D: c0 = (8 + 40g)/12, c1 = (1 - 8g)/12, c2 = (-2g)/12                                    */
 /*   3D: c0 = (6 + 48g)/12, c1 = (1 - 4g)/12, c2 = (-2g)/12                                    */
 /*   S u = (c0*u + c1*faces) + c2*edges ;  weighted Jacobi: u + wd*(b - S u), wd = omega/c0    */
@@ -213,7 +233,7 @@ typedef struct { double c0, c1, c2, wd; } s_coef;
 
 static s_coef make_s(int d, int n, double gamma, double omega) {
     s_coef s;
-    double N = (double)(n + 1);
+    double N = inv_h(n);
     double g = gamma * (N * N);
     if (d == 2) {
         s.c0 = (8.0 + 40.0 * g) / 12.0; s.c1 = (1.0 - 8.0 * g) / 12.0; s.c2 = (-2.0 * g) / 12.0;
@@ -282,14 +302,15 @@ double ora_defect_norm(int d, int n, double gamma, const double *b, const double
     return m;
 }
 
-/* Full-weighting restriction: coarse (I,J[,K]) <-> fine 2I+1.
+/* Full-weighting restriction: coarse (I,J[,K]) <-> fine 2I+1
+ * (Dirichlet) or fine 2I (periodic, the coarse grid keeps the even points of x_i = -1 + i h).
  *   2D: bc = ((4*d + 2*faces) + edges) * 0.0625
  *   3D: bc = ((8*d + 4*faces) + (2*edges + corners)) * 0.015625,
  *       corners = e(k-1) + e(k+1)  (8 corners of the 27-point cube)                           */
 void ora_restrict(int d, int nf, const double *df, double *bc) {
-    int nc = (nf - 1) / 2;
+    int nc = coarser(nf), o = g_per ? 0 : 1;
     FOR_POINTS(d, nc) {
-        int x = 2 * ii + 1, y = 2 * jj + 1, z = (d == 3) ? 2 * kk + 1 : 0;
+        int x = 2 * ii + o, y = 2 * jj + o, z = (d == 3) ? 2 * kk + o : 0;
         double c = at(df, d, nf, x, y, z);
         double fa = faces(df, d, nf, x, y, z), ed = edges(df, d, nf, x, y, z);
         double v;
@@ -303,19 +324,28 @@ void ora_restrict(int d, int nf, const double *df, double *bc) {
     }
 }
 
-/* Bi/trilinear prolongation + correction: u += P e.  Per axis: odd fine index x -> coarse
- * (x-1)/2 (weight 1); even x -> coarse pair (x/2-1, x/2) summed (a + b), weight 1/2; pairs are
- * summed x innermost, then y, then z; the sum is scaled once by 0.5^(#even axes).            */
+/* Bi/trilinear prolongation + correction: u += P e.  Per axis (Dirichlet): odd fine index x ->
+ * coarse (x-1)/2 (weight 1); even x -> coarse pair (x/2-1, x/2) summed (a + b), weight 1/2.
+ * Periodic: even x -> coarse x/2; odd x -> pair ((x-1)/2, (x+1)/2 mod nc), weight 1/2.  Pairs are
+ * summed x innermost, then y, then z; the sum is scaled once by 0.5^(#paired axes).          */
+static void prolong_axis(int x, int *xs, int *nx, double *w) {
+    if (g_per) {
+        if (x & 1) { xs[0] = (x - 1) / 2; xs[1] = (x + 1) / 2; *nx = 2; *w *= 0.5; }
+        else { xs[0] = x / 2; *nx = 1; }
+    } else {
+        if (x & 1) { xs[0] = (x - 1) / 2; *nx = 1; }
+        else { xs[0] = x / 2 - 1; xs[1] = x / 2; *nx = 2; *w *= 0.5; }
+    }
+}
 void ora_prolong_add(int d, int nc, const double *ec, double *uf) {
-    int nf = 2 * nc + 1;
+    int nf = g_per ? 2 * nc : 2 * nc + 1;
     FOR_POINTS(d, nf) {
         int xs[2], ys[2], zs[2], nx, ny, nz;
         double w = 1.0;
-        if (ii & 1) { xs[0] = (ii - 1) / 2; nx = 1; } else { xs[0] = ii / 2 - 1; xs[1] = ii / 2; nx = 2; w *= 0.5; }
-        if (jj & 1) { ys[0] = (jj - 1) / 2; ny = 1; } else { ys[0] = jj / 2 - 1; ys[1] = jj / 2; ny = 2; w *= 0.5; }
+        prolong_axis(ii, xs, &nx, &w);
+        prolong_axis(jj, ys, &ny, &w);
         if (d == 2) { zs[0] = 0; nz = 1; }
-        else if (kk & 1) { zs[0] = (kk - 1) / 2; nz = 1; }
-        else { zs[0] = kk / 2 - 1; zs[1] = kk / 2; nz = 2; w *= 0.5; }
+        else prolong_axis(kk, zs, &nz, &w);
         double sz = 0.0;
         for (int c = 0; c < nz; ++c) {
             double sy = 0.0;
@@ -331,20 +361,23 @@ void ora_prolong_add(int d, int nc, const double *ec, double *uf) {
     }
 }
 
-/* Coarsest level n = 3: exact solve with the inverse of the 9x9 / 27x27 matrix of S, built from
- * the binary64 coefficients (c0,c1,c2) and inverted by Gauss-Jordan elimination with partial
- * pivoting in binary128, rounded once (reading R12).  e_i = sum_j Ginv_ij b_j,
- * accumulated left to right over ascending j starting from Ginv_i0*b_0. */
+/* Coarsest level (Dirichlet n = 3; periodic n = 4): exact solve with the inverse of the P x P
+ * matrix of S (P = n^d), built from the binary64 coefficients (c0,c1,c2) and inverted by
+ * Gauss-Jordan elimination with partial pivoting in binary128, rounded once (DESIGN.md reading
+ * R12; periodic: neighbour distances taken modulo n).  e_i = sum_j Ginv_ij b_j, accumulated left
+ * to right over ascending j starting from Ginv_i0*b_0. */
+#define ORA_PMAX 64
 int ora_coarse_inverse(int d, double gamma, double omega, double *Ginv) {
-    int n = 3, P = (d == 3) ? 27 : 9;
+    int n = coarsest(), P = (d == 3) ? n * n * n : n * n;
     s_coef s = make_s(d, n, gamma, omega);
-    qf A[27][54];
+    qf (*A)[2 * ORA_PMAX] = malloc(sizeof(qf) * ORA_PMAX * 2 * ORA_PMAX);
     for (int r = 0; r < P; ++r) for (int c = 0; c < 2 * P; ++c) A[r][c] = 0;
     for (int r = 0; r < P; ++r) {
-        int ri = r % 3, rj = (r / 3) % 3, rk = r / 9;
+        int ri = r % n, rj = (r / n) % n, rk = r / (n * n);
         for (int c = 0; c < P; ++c) {
-            int ci = c % 3, cj = (c / 3) % 3, ck = c / 9;
+            int ci = c % n, cj = (c / n) % n, ck = c / (n * n);
             int di = abs(ri - ci), dj = abs(rj - cj), dk = abs(rk - ck);
+            if (g_per) { if (n - di < di) di = n - di; if (n - dj < dj) dj = n - dj; if (n - dk < dk) dk = n - dk; }
             if (di > 1 || dj > 1 || dk > 1) continue;
             int nd = di + dj + dk;
             double v = (nd == 0) ? s.c0 : (nd == 1) ? s.c1 : (nd == 2) ? s.c2 : 0.0;
@@ -355,7 +388,7 @@ int ora_coarse_inverse(int d, double gamma, double omega, double *Ginv) {
     for (int c = 0; c < P; ++c) {
         int piv = c;
         for (int r = c + 1; r < P; ++r) if (fabsq(A[r][c]) > fabsq(A[piv][c])) piv = r;
-        if (A[piv][c] == 0) return -1;
+        if (A[piv][c] == 0) { free(A); return -1; }
         if (piv != c) for (int k = 0; k < 2 * P; ++k) { qf t = A[c][k]; A[c][k] = A[piv][k]; A[piv][k] = t; }
         qf inv = 1 / A[c][c];
         for (int k = 0; k < 2 * P; ++k) A[c][k] *= inv;
@@ -366,6 +399,7 @@ int ora_coarse_inverse(int d, double gamma, double omega, double *Ginv) {
         }
     }
     for (int r = 0; r < P; ++r) for (int c = 0; c < P; ++c) Ginv[r * P + c] = (double)A[r][P + c];
+    free(A);
     return 0;
 }
 static void coarse_apply(int P, const double *Ginv, const double *b, double *e) {
@@ -380,18 +414,18 @@ static void coarse_apply(int P, const double *Ginv, const double *b, double *e) 
 /* Geometric multigrid V(nu1,nu2) cycle on S_l ("V-cycles"; components per B:configs[1] */
 /* and DESIGN.md R11-R14): nu1 weighted-Jacobi sweeps; d = b - S u; b_c = R d; e_c = V(0,b_c)  */
 /* on level l+1 (correction scheme, zero initial guess, same gamma); u += P e_c; nu2 sweeps.   */
-/* On n = 3 the cycle is the exact solve.                                                      */
+/* On the coarsest level (n = 3, periodic 4) the cycle is the exact solve.                   */
 /* ------------------------------------------------------------------------------------------ */
 static void vcycle_rec(int d, int n, double gamma, int nu1, int nu2, double omega,
                        const double *b, double *u) {
     size_t P = npts(d, n);
-    if (n == 3) {
+    if (n == coarsest()) {
         /* one-entry cache of the coarse inverse (the oracle is single-threaded at this level) */
-        static double Ginv[27 * 27], cg = -1.0, co = -1.0;
-        static int cd = 0;
-        if (cd != d || cg != gamma || co != omega) {
+        static double Ginv[ORA_PMAX * ORA_PMAX], cg = -1.0, co = -1.0;
+        static int cd = 0, cp = -1;
+        if (cd != d || cg != gamma || co != omega || cp != g_per) {
             ora_coarse_inverse(d, gamma, omega, Ginv);
-            cd = d; cg = gamma; co = omega;
+            cd = d; cg = gamma; co = omega; cp = g_per;
         }
         coarse_apply((int)P, Ginv, b, u);
         return;
@@ -400,7 +434,7 @@ static void vcycle_rec(int d, int n, double gamma, int nu1, int nu2, double omeg
     double *t = malloc(P * sizeof(double));
     for (int it = 0; it < nu1; ++it) { jacobi(&s, d, n, b, u, t); memcpy(u, t, P * sizeof(double)); }
     defect(&s, d, n, b, u, t);
-    int nc = (n - 1) / 2;
+    int nc = coarser(n);
     size_t Pc = npts(d, nc);
     double *bc = malloc(Pc * sizeof(double)), *ec = calloc(Pc, sizeof(double));
     ora_restrict(d, n, t, bc);
@@ -419,13 +453,64 @@ void ora_vcycle(int d, int n, double gamma, int nu1, int nu2, double omega, cons
 /*   FORCING: G*ct (ct = cos(t_j), host scalar);                                               */
 /*   ADVECTION (CD4, zero ghosts): dx = (8*(u(x+1)-u(x-1)) - (u(x+2)-u(x-2)))*kx, kx=(a_x*N)/12,*/
 /*   f = -((dx + dy) + dz)   (2D: -(dx + dy))                                                   */
+/*   BURGERS (periodic; "5th order WENO"; reading R31): f = -(u u_x + u u_y)    */
+/*     in conservation form -sum_a d_a(u^2/2), WENO5-JS reconstruction of Lax-Friedrichs split  */
+/*     fluxes (below).                                                                         */
 /* ------------------------------------------------------------------------------------------ */
-enum { FE_NONE = 0, FE_CUBIC = 1, FE_FORCING = 2, FE_ADVECTION = 3 };
+enum { FE_NONE = 0, FE_CUBIC = 1, FE_FORCING = 2, FE_ADVECTION = 3, FE_BURGERS = 4 };
+
+/* WENO5 reconstruction (Jiang & Shu 1996; restated, reading R31) of the value at the face between
+ * v2 and v3 from the five cell values v0..v4 (upwind side v0..v2):
+ *   candidate stencils  p0 = (2v0 - 7v1 + 11v2)/6,  p1 = (-v1 + 5v2 + 2v3)/6,  p2 = (2v2 + 5v3 - v4)/6
+ *   smoothness          b_k = 13/12 s_k^2 + 1/4 t_k^2   with
+ *                       s0 = v0 - 2v1 + v2, t0 = v0 - 4v1 + 3v2;  s1 = v1 - 2v2 + v3, t1 = v1 - v3;
+ *                       s2 = v2 - 2v3 + v4, t2 = 3v2 - 4v3 + v4
+ *   weights             a_k = d_k / (eps + b_k)^2,  d = (0.1, 0.6, 0.3),  eps = 1e-6
+ *   value               (a0 p0 + a1 p1 + a2 p2) / (a0 + a1 + a2)
+ * Canonical trees: exactly as written below (left to right, divisions by 6 and by the weight sum
+ * are IEEE divisions, 13/12 is the binary64 constant 13.0/12.0). */
+static double weno5(double v0, double v1, double v2, double v3, double v4) {
+    const double eps = 1e-6, c13 = 13.0 / 12.0;
+    double p0 = ((2.0 * v0 - 7.0 * v1) + 11.0 * v2) / 6.0;
+    double p1 = ((5.0 * v2 - v1) + 2.0 * v3) / 6.0;
+    double p2 = ((2.0 * v2 + 5.0 * v3) - v4) / 6.0;
+    double s0 = (v0 - 2.0 * v1) + v2, t0 = (v0 - 4.0 * v1) + 3.0 * v2;
+    double s1 = (v1 - 2.0 * v2) + v3, t1 = v1 - v3;
+    double s2 = (v2 - 2.0 * v3) + v4, t2 = (3.0 * v2 - 4.0 * v3) + v4;
+    double b0 = c13 * (s0 * s0) + 0.25 * (t0 * t0);
+    double b1 = c13 * (s1 * s1) + 0.25 * (t1 * t1);
+    double b2 = c13 * (s2 * s2) + 0.25 * (t2 * t2);
+    double e0 = eps + b0, e1 = eps + b1, e2 = eps + b2;
+    double a0 = 0.1 / (e0 * e0), a1 = 0.6 / (e1 * e1), a2 = 0.3 / (e2 * e2);
+    return ((a0 * p0 + a1 * p1) + a2 * p2) / ((a0 + a1) + a2);
+}
+double ora_weno5(double v0, double v1, double v2, double v3, double v4) { return weno5(v0, v1, v2, v3, v4); }
+
+/* Lax-Friedrichs split fluxes of f(u) = u^2/2 with the global speed alpha = max|u| of the field
+ * being evaluated: f+- = (q +- alpha u) * 0.5, q = (u*u)*0.5. */
+static inline double split_flux(double x, double alpha, int plus) {
+    double q = (x * x) * 0.5, a = alpha * x;
+    return plus ? (q + a) * 0.5 : (q - a) * 0.5;
+}
+/* numerical flux through the face between point s and s+1 of axis ax (0 x, 1 y, 2 z):
+ *   F = weno5(f+(s-2), f+(s-1), f+(s), f+(s+1), f+(s+2)) + weno5(f-(s+3), f-(s+2), f-(s+1), f-(s), f-(s-1)) */
+static double burgers_face(const double *u, int d, int n, int i, int j, int k, int ax, double alpha) {
+    int di = (ax == 0), dj = (ax == 1), dk = (ax == 2);
+    double fp[5], fm[5];
+    for (int s = 0; s < 5; ++s) {
+        int o = s - 2;       /* f+ at s-2 .. s+2 */
+        fp[s] = split_flux(at(u, d, n, i + o * di, j + o * dj, k + o * dk), alpha, 1);
+        int q = 3 - s;       /* f- at s+3 .. s-1 */
+        fm[s] = split_flux(at(u, d, n, i + q * di, j + q * dj, k + q * dk), alpha, 0);
+    }
+    return weno5(fp[0], fp[1], fp[2], fp[3], fp[4]) + weno5(fm[0], fm[1], fm[2], fm[3], fm[4]);
+}
 
 static void fe_eval(int fe, int d, int n, const double *a, const double *G, double ct,
                     const double *u, double *out) {
-    double N = (double)(n + 1);
+    double N = inv_h(n);
     double kx = (a[0] * N) / 12.0, ky = (a[1] * N) / 12.0, kz = (a[2] * N) / 12.0;
+    double alpha = (fe == FE_BURGERS) ? maxabs(u, npts(d, n)) : 0.0;
     FOR_POINTS(d, n) {
         size_t p = IDX(d, n);
         double v = 0.0;
@@ -447,6 +532,15 @@ static void fe_eval(int fe, int d, int n, const double *a, const double *G, doub
             } else {
                 v = -(dx + dy);
             }
+        } else if (fe == FE_BURGERS) {
+            /* f = -(((Fx(i) - Fx(i-1)) + (Fy(j) - Fy(j-1))) [+ (Fz(k) - Fz(k-1))]) * (1/h)) */
+            int i = ii, j = jj, k = kk;
+            double gx = burgers_face(u, d, n, i, j, k, 0, alpha) - burgers_face(u, d, n, i - 1, j, k, 0, alpha);
+            double gy = burgers_face(u, d, n, i, j, k, 1, alpha) - burgers_face(u, d, n, i, j - 1, k, 1, alpha);
+            double sum = gx + gy;
+            if (d == 3)
+                sum = sum + (burgers_face(u, d, n, i, j, k, 2, alpha) - burgers_face(u, d, n, i, j, k - 1, 2, alpha));
+            v = -(sum * N);
         }
         out[p] = v;
     }
@@ -479,6 +573,7 @@ typedef struct {
     int res_kind;        /* 0 = weighted ||r~|| (reading R15); 1 = unweighted ||W^-1 r~|| (2D, NEXT f2) */
     double w_tol;        /* res_kind 1: W-solve until ||r~ - W x|| <= w_tol * ||r~|| (reading R15b) */
     int w_cap;           /* res_kind 1: at most w_cap W-cycles per node */
+    int bc;              /* 0 = homogeneous Dirichlet on [0,1]^d; 1 = periodic on [-1,1)^d (NEXT f3) */
 } ora_problem;
 
 static long g_wcycles;   /* W-cycles of the last ora_step (not V-cycles: P:165) */
@@ -642,6 +737,7 @@ int ora_sweep(const ora_problem *P, const double *tau, const double *S, const do
  * = cycles of node solve m in sweep k+1.  Returns 0, or -1 on bad tables. */
 int ora_step(const ora_problem *P, double *u0, double t_n, int *sweeps, long *vcycles,
              double *res_hist, int *node_cycles, int *cap_hits, int *converged) {
+    ora_set_bc(P->bc);
     int d = P->dim, n = P->n, M = P->M;
     size_t NP = npts(d, n);
     double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
@@ -679,6 +775,7 @@ long ora_last_wcycles(void) { return g_wcycles; }
 
 /* Exposed for the per-operation parity tests: RHS of substep m and residual of a given state. */
 void ora_rhs(const ora_problem *P, double t_n, int m, double *const *uold, double *const *unew, double *b) {
+    ora_set_bc(P->bc);
     int M = P->M;
     size_t NP = npts(P->dim, P->n);
     double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
@@ -689,11 +786,13 @@ void ora_rhs(const ora_problem *P, double t_n, int m, double *const *uold, doubl
     free(v); free(w); free(f1); free(f2);
 }
 double ora_residual(const ora_problem *P, double t_n, double *const *u, double *per_node) {
+    ora_set_bc(P->bc);
     double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
     ora_tables(P->M, tau, Q, S, dtau);
     return ora_residual_state(P, tau, Q, t_n, u, per_node);
 }
 int ora_sweep_state(const ora_problem *P, double t_n, double *const *uold, double *const *unew, int *cycles) {
+    ora_set_bc(P->bc);
     double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
     ora_tables(P->M, tau, Q, S, dtau);
     return ora_sweep(P, tau, S, dtau, t_n, uold, unew, cycles);

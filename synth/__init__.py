@@ -14,9 +14,13 @@ cfg   draws (numpy ``default_rng(seed)``, PCG64; integers first, then amplitudes
 3     kl = integers(1, 65, (64, 2)); a = 0.1*standard_normal(64);   G = sin(2πx) sin(2πy)
 4     kln = integers(1, 9, (16, 3)); a = standard_normal(16)        u0 = Σ a sin sin sin
 5     c = uniform(0.3, 0.7, 3);      u0 = exp(-|x-c|^2 / 0.01)       (Gaussian blob)
+B     (NEXT f3, viscous Burgers P:106-112, periodic [-1,1)^2): seed 0: u0 = exp(-|x|^2/sigma^2),
+      sigma = 0.1 (x read as the vector (x, y)); seed s > 0: c = uniform(-0.5, 0.5, 2),
+      A = uniform(0.5, 1.5); u0 = A exp(-|x-c|^2/sigma^2)
 ====  ==========================================================================================
 
 Grid: n interior points per direction, N = n + 1 = 2^p, x_i = i / N for i = 1..n (h = 1/N).
+Periodic grids (Burgers): n = 2^p points x_i = -1 + i h, i = 0..n-1, h = 2/n.
 Arrays are C-contiguous, shape (n, n) or (n, n, n), x fastest (index [z, y, x]).
 """
 from __future__ import annotations
@@ -27,8 +31,9 @@ from typing import Optional
 
 import numpy as np
 
-FE_NONE, FE_CUBIC, FE_FORCING, FE_ADVECTION = 0, 1, 2, 3
+FE_NONE, FE_CUBIC, FE_FORCING, FE_ADVECTION, FE_BURGERS = 0, 1, 2, 3, 4
 MODE_ISDC, MODE_SDC, MODE_ISDC_CAPPED = 0, 1, 2
+BC_DIRICHLET, BC_PERIODIC = 0, 1
 
 
 @dataclasses.dataclass
@@ -54,6 +59,7 @@ class Config:
     nu1: int = 2
     nu2: int = 2
     omega: float = 0.8
+    bc: int = BC_DIRICHLET
 
 
 # SURVEY.md §8 per-config table; stop rules per the DESIGN.md readings (c2 items 19, 25, 26).
@@ -144,3 +150,35 @@ def problem_inputs(cid: int, seed: int = 0, n: Optional[int] = None):
     u0 = initial_condition(cid, seed, nn)
     G = forcing_field(nn, cfg.dim) if cfg.fe == FE_FORCING else None
     return cfg, u0, G
+
+
+# ------------------------------------------------------------------ viscous Burgers (NEXT f3)
+def grid_x_periodic(n: int) -> np.ndarray:
+    """Periodic coordinates x_i = -1 + i h, h = 2/n, i = 0..n-1 (exact: n is a power of two)."""
+    if n < 4 or n & (n - 1):
+        raise ValueError(f"periodic n must be a power of two >= 4, got n={n}")
+    return -1.0 + np.arange(n, dtype=np.float64) * (2.0 / float(n))
+
+
+def burgers_config(nu: float, M: int, n: int = 128, dt: float = 0.001, **kw) -> Config:
+    """Table 1b problem: 2D viscous Burgers on [-1,1)^2, periodic, IMEX
+    with WENO5 advection; h = 1/64 (n = 128, reading R30), dt = 0.001, one step, L = 2,
+    residual tolerance 5e-8."""
+    base = dict(steps=1, sweep_tol=5e-8, max_sweeps=100, bc=BC_PERIODIC)
+    base.update(kw)
+    return Config(0, 2, n, M, dt, float(nu), FE_BURGERS, **base)
+
+
+def burgers_initial(n: int, seed: int = 0, sigma: float = 0.1, dim: int = 2) -> np.ndarray:
+    """u0 = A exp(-|x - c|^2 / sigma^2) on the periodic grid (seed 0: A = 1, c = 0)."""
+    x = grid_x_periodic(n)
+    if seed == 0:
+        c, A = np.zeros(dim), 1.0
+    else:
+        rng = np.random.default_rng(seed)
+        c = rng.uniform(-0.5, 0.5, dim)
+        A = rng.uniform(0.5, 1.5)
+    g = [np.exp(-((x - c[a]) ** 2) / (sigma * sigma)) for a in range(dim)]
+    if dim == 2:
+        return A * np.multiply.outer(g[1], g[0])
+    return A * np.multiply.outer(np.multiply.outer(g[2], g[1]), g[0])
