@@ -13,10 +13,12 @@
  *
  * Conventions shared by every call
  *  - Grid: d in {2,3}; n interior points per direction with n + 1 = 2^p (p >= 2); h = 1/(n+1);
- *    homogeneous Dirichlet data on the unit square/cube.
+ *    homogeneous Dirichlet data on the unit square/cube.  Periodic grids (grid.bc =
+ *    ISDC_BC_PERIODIC, NEXT f3, Burgers P:106-112): n = 2^p points (p >= 2) x_i = -1 + i h of
+ *    [-1,1)^d, h = 2/n, wrap-around neighbours (readings R30, R31).
  *  - Field layout at the boundary: dense fp64, n^d values, C-contiguous with x fastest
  *    (index i + n*(j + n*k)) -- a torch tensor of shape (n,n) or (n,n,n).  Internally the library
- *    keeps pitched copies (row pitch n+1 doubles) inside the caller's workspace.
+ *    keeps pitched copies (row pitch n+1 doubles; periodic: n) inside the caller's workspace.
  *  - Ownership: the caller owns every buffer passed in (device fields, host arrays, the
  *    workspace).  The library never calls cudaMalloc; it owns only the handle, host-side tables
  *    and CUDA graphs.  Pointers named *_dev are device pointers, *_host are host pointers.
@@ -61,8 +63,16 @@ typedef enum {
     ISDC_FE_NONE = 0,          /* f^E == 0: implicit SDC, Eq. (3)                                 */
     ISDC_FE_CUBIC = 1,         /* f^E(u) = u - u^3 (Allen-Cahn type, config 2)                    */
     ISDC_FE_FORCING = 2,       /* f^E(x,t) = G(x) cos(t), G given as a field (config 3)           */
-    ISDC_FE_ADVECTION_CD4 = 3  /* f^E(u) = -a . grad u, 4th-order central differences (config 5) */
+    ISDC_FE_ADVECTION_CD4 = 3, /* f^E(u) = -a . grad u, 4th-order central differences (config 5) */
+    ISDC_FE_BURGERS_WENO5 = 4  /* f^E(u) = -(u u_x + u u_y [+ u u_z]) = -sum_a d_a(u^2/2): WENO5-JS on
+                                  Lax-Friedrichs split fluxes, alpha = max|u| of the evaluated field
+                                  (R31).  Periodic grids only.          */
 } isdc_fe_kind;
+
+typedef enum {
+    ISDC_BC_DIRICHLET = 0,     /* homogeneous Dirichlet on [0,1]^d, n = 2^p - 1 interior points  */
+    ISDC_BC_PERIODIC = 1       /* periodic on [-1,1)^d, n = 2^p points (NEXT f3)                  */
+} isdc_bc;
 
 typedef enum {
     ISDC_MODE_ISDC_FIXED = 0,  /* exactly L V-cycles per node solve                        */
@@ -74,8 +84,9 @@ typedef enum {
 
 typedef struct {
     int dim;          /* 2 or 3                                                                  */
-    int n;            /* interior points per direction, n = 2^p - 1, p >= 2                      */
-    int coarsest_n;   /* must be 3 (exact 3^d solve on the coarsest level)                       */
+    int n;            /* points per direction: Dirichlet n = 2^p - 1 (interior), periodic n = 2^p, p >= 2 */
+    int coarsest_n;   /* 0 or the coarsest level: 3 (Dirichlet, exact 3^d solve), 4 (periodic, 4^d) */
+    int bc;           /* isdc_bc                                                                 */
 } isdc_grid;
 
 typedef struct {

@@ -64,6 +64,8 @@ struct isdc_ctx {
     bool fast = true;          // use the tuned fine-level kernels
     std::map<std::tuple<const void *, int, int, int>, CUtensorMap> tmaps;  // TMA descriptors by (buffer, box)
     double *ctdev = nullptr;   // device cos(t_n + dt*tau_j), refreshed when the step index changes
+    bool per = false;          // periodic grid (NEXT f3): generic kernels on every level
+    unsigned long long *alpha = nullptr;   // Burgers: max|u| slots, [0,M) uold_j, [8,8+M) unew_m, [16,16+M) residual u_j
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
     int tail3d = 15;           // ISDC_TAIL3D: largest 3D level handled by the tail (fast kernels above)
@@ -165,21 +167,29 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 bool pow2m1(int n) { return n >= 3 && ((n + 1) & n) == 0; }
 
-GridDesc make_grid(int d, int n) {
+bool pow2(int n) { return n >= 4 && (n & (n - 1)) == 0; }
+// 1/h: Dirichlet N = n+1 on [0,1]; periodic n/2 on [-1,1) (both powers of two, exact)
+double inv_h(int n, bool per) { return per ? (double)n * 0.5 : (double)(n + 1); }
+int coarser(int n, bool per) { return per ? n / 2 : (n - 1) / 2; }
+int coarsest(bool per) { return per ? 4 : 3; }
+
+GridDesc make_grid(int d, int n, bool per) {
     GridDesc g;
     g.n = n;
-    g.pitch = n + 1;
-    g.plane = (d == 3) ? (long long)n * (n + 1) : 0;
+    g.pitch = per ? n : n + 1;
+    g.plane = (d == 3) ? (long long)n * g.pitch : 0;
+    g.per = per ? 1 : 0;
     return g;
 }
-size_t field_elems(int d, int n) {
-    return (d == 3) ? (size_t)n * n * (n + 1) : (size_t)n * (n + 1);
+size_t field_elems(int d, int n, bool per) {
+    size_t pitch = per ? (size_t)n : (size_t)n + 1;
+    return (d == 3) ? (size_t)n * n * pitch : (size_t)n * pitch;
 }
 
-SCoef make_scoef(int d, int n, double gamma, double omega) {
+SCoef make_scoef(int d, int n, double gamma, double omega, bool per) {
     // DESIGN.md §4.2 (same expressions, same order as the paper-derived definition)
     SCoef c;
-    double N = (double)(n + 1);
+    double N = inv_h(n, per);
     double g = gamma * (N * N);
     if (d == 2) {
         c.c0 = (8.0 + 40.0 * g) / 12.0; c.c1 = (1.0 - 8.0 * g) / 12.0; c.c2 = (-2.0 * g) / 12.0;
@@ -190,9 +200,9 @@ SCoef make_scoef(int d, int n, double gamma, double omega) {
     return c;
 }
 
-BLConst make_bl(int d, int n) {
+BLConst make_bl(int d, int n, bool per) {
     BLConst c;
-    double N = (double)(n + 1), N2 = N * N;
+    double N = inv_h(n, per), N2 = N * N;
     if (d == 2) {
         c.kB0 = 8.0 / 12.0; c.kB1 = 1.0 / 12.0;
         c.kL0 = (-20.0 * N2) / 6.0; c.kL1 = (4.0 * N2) / 6.0; c.kL2 = N2 / 6.0;
@@ -206,12 +216,15 @@ BLConst make_bl(int d, int n) {
 isdc_status validate(const isdc_problem *p) {
     if (!p) return ISDC_ERR_INVALID_ARG;
     if (p->grid.dim != 2 && p->grid.dim != 3) return ISDC_ERR_INVALID_ARG;
-    if (!pow2m1(p->grid.n)) return ISDC_ERR_INVALID_ARG;
-    if (p->grid.coarsest_n != 3 && p->grid.coarsest_n != 0) return ISDC_ERR_INVALID_ARG;
+    if (p->grid.bc != ISDC_BC_DIRICHLET && p->grid.bc != ISDC_BC_PERIODIC) return ISDC_ERR_INVALID_ARG;
+    const bool per = p->grid.bc == ISDC_BC_PERIODIC;
+    if (per ? !pow2(p->grid.n) : !pow2m1(p->grid.n)) return ISDC_ERR_INVALID_ARG;
+    if (p->grid.coarsest_n != coarsest(per) && p->grid.coarsest_n != 0) return ISDC_ERR_INVALID_ARG;
+    if (p->fe == ISDC_FE_BURGERS_WENO5 && !per) return ISDC_ERR_UNSUPPORTED;   // WENO5 needs the periodic ghosts
     if (!(p->dt > 0) || !(p->nu > 0)) return ISDC_ERR_INVALID_ARG;
     if (p->nodes != ISDC_NODES_GAUSS_LOBATTO) return ISDC_ERR_UNSUPPORTED;
     if (p->M < 2 || p->M > ISDC_MAXM) return ISDC_ERR_UNSUPPORTED;
-    if (p->fe < ISDC_FE_NONE || p->fe > ISDC_FE_ADVECTION_CD4) return ISDC_ERR_INVALID_ARG;
+    if (p->fe < ISDC_FE_NONE || p->fe > ISDC_FE_BURGERS_WENO5) return ISDC_ERR_INVALID_ARG;
     if (p->fe == ISDC_FE_FORCING && !p->fe_field_dev) return ISDC_ERR_INVALID_ARG;
     if (p->mg.nu1 < 0 || p->mg.nu2 < 0 || p->mg.nu1 + p->mg.nu2 < 1) return ISDC_ERR_INVALID_ARG;
     if (!(p->mg.omega > 0)) return ISDC_ERR_INVALID_ARG;
@@ -233,13 +246,14 @@ isdc_status validate(const isdc_problem *p) {
 // workspace layout; when base == nullptr only sizes are computed
 size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     int d = p->grid.dim, n = p->grid.n, M = p->M;
+    const bool per = p->grid.bc == ISDC_BC_PERIODIC;
     size_t off = 0;
     auto take = [&](size_t bytes) -> char * {
         char *r = base ? base + off : nullptr;
         off += align_up(bytes);
         return r;
     };
-    size_t fe = field_elems(d, n) * sizeof(double);
+    size_t fe = field_elems(d, n, per) * sizeof(double);
     // iterate sets: U[0][0] == U[1][0] (the u_0 buffer)
     double *u0 = (double *)take(fe);
     if (h) { h->U[0][0] = h->U[1][0] = u0; }
@@ -270,11 +284,11 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     }
     // coarse levels
     int nl = 0;
-    for (int m = n; m >= 3; m = (m - 1) / 2) ++nl;
+    for (int m = n; m >= coarsest(per); m = coarser(m, per)) ++nl;
     if (h) h->lev.assign(nl, Level());
-    for (int l = 0, m = n; l < nl; ++l, m = (m - 1) / 2) {
-        size_t el = field_elems(d, m);
-        if (h) { h->lev[l].g = make_grid(d, m); h->lev[l].elems = el; }
+    for (int l = 0, m = n; l < nl; ++l, m = coarser(m, per)) {
+        size_t el = field_elems(d, m, per);
+        if (h) { h->lev[l].g = make_grid(d, m, per); h->lev[l].elems = el; }
         if (l == 0) continue;
         double *e = (double *)take(el * sizeof(double));
         double *b = (double *)take(el * sizeof(double));
@@ -289,11 +303,12 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
         double *x = (double *)take(fe);
         if (h) h->WX = x;
     }
-    int Pc = (d == 3) ? 27 : 9;
+    const int cn = coarsest(per), Pc = (d == 3) ? cn * cn * cn : cn * cn;
     double *Gi = (double *)take((size_t)M * Pc * Pc * sizeof(double));   // M-1 substeps + gamma = 0
     unsigned long long *red = (unsigned long long *)take(kRedSlots * sizeof(unsigned long long));
     double *ctd = (double *)take(ISDC_MAXM * sizeof(double));
-    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; }
+    unsigned long long *al = (unsigned long long *)take(3 * ISDC_MAXM * sizeof(unsigned long long));
+    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; }
     return off;
 }
 
@@ -639,24 +654,24 @@ isdc_status launch_prolong(isdc_ctx *h, double *u, const GridDesc &gf, const dou
 
 isdc_status launch_coarse(isdc_ctx *h, double *u, const double *b, const GridDesc &g, int m) {
     ++h->launches;
-    int Pc = (h->d == 3) ? 27 : 9;
+    const int Pc = (h->d == 3) ? g.n * g.n * g.n : g.n * g.n;
     const double *Gi = h->Ginv + (size_t)m * Pc * Pc;
     int pe = prof_begin(h, PROF_COARSE);
-    if (h->d == 2) kl(h, k_coarse_solve<2>, 1, 32, 0)(u, b, g, Gi);
-    else kl(h, k_coarse_solve<3>, 1, 32, 0)(u, b, g, Gi);
+    if (h->d == 2) kl(h, k_coarse_solve<2>, 1, Pc > 32 ? 64 : 32, 0)(u, b, g, Gi);
+    else kl(h, k_coarse_solve<3>, 1, Pc > 32 ? 64 : 32, 0)(u, b, g, Gi);
     prof_end(h, pe, PROF_COARSE, 16.0 * Pc);
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
 
 isdc_status copy_field(isdc_ctx *h, double *dst, const double *src, const GridDesc &g) {
-    size_t bytes = field_elems(h->d, g.n) * sizeof(double);
+    size_t bytes = field_elems(h->d, g.n, g.per != 0) * sizeof(double);
     CUDA_TRY(h, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, h->s));
     return ISDC_OK;
 }
 
 isdc_status zero_field(isdc_ctx *h, double *dst, const GridDesc &g) {
-    size_t bytes = field_elems(h->d, g.n) * sizeof(double);
+    size_t bytes = field_elems(h->d, g.n, g.per != 0) * sizeof(double);
     CUDA_TRY(h, cudaMemsetAsync(dst, 0, bytes, h->s));
     return ISDC_OK;
 }
@@ -763,7 +778,7 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
     Level &L = h->lev[l];
     const GridDesc &g = L.g;
     if (l == h->tail_l0) return launch_tail(h, l, m, b, zero_init ? nullptr : (src ? src : X), X);
-    if (g.n == 3) return launch_coarse(h, X, b, g, m);
+    if (l == h->nlev - 1) return launch_coarse(h, X, b, g, m);   // n = 3 (periodic: 4)
     const SCoef &c = L.coef[m];
     const double *cur = src ? src : X;
     Level &C = h->lev[l + 1];
@@ -835,8 +850,24 @@ void fill_vw(isdc_ctx *h, VWParams &P, int m, double *const *uold, const double 
         P.beta[j] = nudt * h->S[m * h->M + j];
     }
     P.ct = h->ctdev;
+    P.ctn = h->ctdev + m;
+    if (h->fe.kind == ISDC_FE_BURGERS_WENO5) {   // alpha = max|u| of each evaluated field (launch_alpha)
+        P.ct = (const double *)h->alpha;
+        P.ctn = (const double *)(h->alpha + ISDC_MAXM + m);
+    }
     P.fe = h->fe;
     P.g = h->lev[0].g;
+}
+
+// Burgers (R31): alpha = max|u| of `field` into alpha slot `slot` (bits of a non-negative double)
+isdc_status launch_alpha(isdc_ctx *h, const double *field, int slot) {
+    const GridDesc &g = h->lev[0].g;
+    CUDA_TRY(h, cudaMemsetAsync(h->alpha + slot, 0, sizeof(unsigned long long), h->s));
+    ++h->launches;
+    if (h->d == 2) kl(h, k_norm<2>, point_grid<2>(g, kBlk), kBlk, 0)(field, g, h->alpha + slot);
+    else kl(h, k_norm<3>, point_grid<3>(g, kBlk), kBlk, 0)(field, g, h->alpha + slot);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
 }
 
 bool fast2d_pointwise_fe(const isdc_ctx *h) { return h->fast && h->d == 2 && h->fe.kind <= 2 && h->n >= 63; }
@@ -852,7 +883,8 @@ dim3 stream2d_grid(const isdc_ctx *h, int &yc) {
 bool stream2d_ok(const isdc_ctx *h) { return fast2d_pointwise_fe(h) && (h->M == 3 || h->M == 5) && h->stream2d; }
 
 isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_m, double *bout, bool bnorm,
-                    double *const *Fold = nullptr, const double *Fnew = nullptr, bool fold_ok = false) {
+                    double *const *Fold = nullptr, const double *Fnew = nullptr, bool fold_ok = false,
+                    bool fresh_old = false) {
     if (stream2d_ok(h)) {
         f2d::StreamArgs A;
         const int M = h->M;
@@ -955,8 +987,14 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
     VWParams P;
     fill_vw(h, P, m, uold, unew_m);
     const GridDesc &g = h->lev[0].g;
-    ++h->launches;
     int pe = prof_begin(h, PROF_RHS);
+    if (h->fe.kind == ISDC_FE_BURGERS_WENO5) {
+        // uold is fixed for the whole sweep: its speeds are measured at substep 0 (or on request)
+        if (m == 0 || fresh_old)
+            for (int j = 0; j < h->M; ++j) TRY(launch_alpha(h, uold[j], j));
+        TRY(launch_alpha(h, unew_m, ISDC_MAXM + m));
+    }
+    ++h->launches;
     if (h->d == 2) kl(h, k_vw<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->V, h->W, P);
     else kl(h, k_vw<3>, point_grid<3>(g, kBlk), kBlk, 0)(h->V, h->W, P);
     LAUNCH_CHECK(h);
@@ -1082,6 +1120,8 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
     }
     double dt = h->P.dt, nudt = h->P.nu * dt;
     int pe = prof_begin(h, PROF_RESID);
+    if (h->fe.kind == ISDC_FE_BURGERS_WENO5)
+        for (int j = 0; j < M; ++j) TRY(launch_alpha(h, u[j], 2 * ISDC_MAXM + j));
     for (int m = 1; m < M; ++m) {
         PZParams P;
         P.M = M; P.m = m;
@@ -1090,7 +1130,7 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             P.qa[j] = dt * h->Q[m * M + j];
             P.qb[j] = nudt * h->Q[m * M + j];
         }
-        P.ct = h->ctdev;
+        P.ct = (h->fe.kind == ISDC_FE_BURGERS_WENO5) ? (const double *)(h->alpha + 2 * ISDC_MAXM) : h->ctdev;
         P.fe = h->fe;
         P.g = g;
         h->launches += 2;
@@ -1343,17 +1383,19 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     h->P = *prob;
     h->s = (cudaStream_t)stream;
     h->d = prob->grid.dim; h->n = prob->grid.n; h->N = h->n + 1; h->M = prob->M;
+    h->per = prob->grid.bc == ISDC_BC_PERIODIC;
     layout(h, prob, (char *)ws);
     if (isdc_build_tables(h->M, h->tau, h->Q, h->S, h->dtau)) { delete h; return ISDC_ERR_UNSUPPORTED; }
-    h->bl = make_bl(h->d, h->n);
+    h->bl = make_bl(h->d, h->n, h->per);
     h->fe.kind = (int)prob->fe;
-    double N = (double)h->N;
+    double N = inv_h(h->n, h->per);
+    h->fe.kh = N;
     h->fe.kx = (prob->fe_params[0] * N) / 12.0;
     h->fe.ky = (prob->fe_params[1] * N) / 12.0;
     h->fe.kz = (prob->fe_params[2] * N) / 12.0;
     h->fe.G = h->Gp;
     const char *env = getenv("ISDC_GENERIC_KERNELS");
-    h->fast = !(env && env[0] == '1');
+    h->fast = !(env && env[0] == '1') && !h->per;   // the tuned kernels assume Dirichlet zeros
     if (h->fast && !tma_encoder()) h->fast = false;
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
@@ -1410,15 +1452,16 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         cudaFuncSetAttribute(f2d::k_resid<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
         attrs = true;
     }
-    int Pc = (h->d == 3) ? 27 : 9;
+    const int cn = coarsest(h->per), Pc = (h->d == 3) ? cn * cn * cn : cn * cn;
     std::vector<double> Gi((size_t)h->M * Pc * Pc);
     h->wslot = h->M - 1;
     const int nslots = h->M - 1 + (prob->residual_kind == 1 ? 1 : 0);
     for (int m = 0; m < nslots; ++m) {
         double gamma = (m == h->wslot) ? 0.0 : prob->nu * (prob->dt * h->dtau[m]);
-        for (int l = 0; l < h->nlev; ++l) h->lev[l].coef[m] = make_scoef(h->d, h->lev[l].g.n, gamma, prob->mg.omega);
+        for (int l = 0; l < h->nlev; ++l)
+            h->lev[l].coef[m] = make_scoef(h->d, h->lev[l].g.n, gamma, prob->mg.omega, h->per);
         const SCoef &cc = h->lev[h->nlev - 1].coef[m];
-        if (isdc_coarse_inverse(h->d, cc.c0, cc.c1, cc.c2, Gi.data() + (size_t)m * Pc * Pc)) {
+        if (isdc_coarse_inverse(h->d, cn, h->per ? 1 : 0, cc.c0, cc.c1, cc.c2, Gi.data() + (size_t)m * Pc * Pc)) {
             delete h;
             return ISDC_ERR_INVALID_ARG;
         }
@@ -1645,7 +1688,7 @@ isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold, const
         TRY(launch_fe(h, Fo[j], uo[j]));
     }
     TRY(launch_fe(h, h->Fs[0][1], h->U[0][1]));
-    TRY(run_rhs(h, node_m, uo, h->U[0][1], h->Bf, false, Fo, h->Fs[0][1]));
+    TRY(run_rhs(h, node_m, uo, h->U[0][1], h->Bf, false, Fo, h->Fs[0][1], false, true));
     TRY(pitched_to_dense(h, b, h->Bf, cudaMemcpyDeviceToDevice));
     CUDA_TRY(h, cudaStreamSynchronize(h->s));
     h->spread = true;  // the staged data overwrote the iterate sets

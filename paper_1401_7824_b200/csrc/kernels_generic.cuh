@@ -12,7 +12,8 @@ struct VWParams {                 // RHS of Eq. (5) for substep m (DESIGN.md §4
     double dtm, gm;               // dt*dtau_m, nu*dtm
     double a[ISDC_MAXM];          // dt*S_{m,j}
     double beta[ISDC_MAXM];       // (nu*dt)*S_{m,j}
-    const double *ct;             // device: cos(t_n + dt*tau_j), j = 0..M-1
+    const double *ct;             // device: cos(t_n + dt*tau_j), j = 0..M-1 (Burgers: alpha of uold_j)
+    const double *ctn;            // the same for unew_m (&ct[m]; Burgers: alpha of unew_m)
     FeDesc fe;
     GridDesc g;
 };
@@ -22,7 +23,7 @@ struct PZParams {                 // residual of node m
     int M, m;
     double qa[ISDC_MAXM];         // dt*Q_{m,j}
     double qb[ISDC_MAXM];         // (nu*dt)*Q_{m,j}
-    const double *ct;             // device: cos(t_n + dt*tau_j)
+    const double *ct;             // device: cos(t_n + dt*tau_j) (Burgers: alpha of u_j)
     FeDesc fe;
     GridDesc g;
 };
@@ -72,10 +73,15 @@ __global__ void k_norm(const double *__restrict__ q, GridDesc g, unsigned long l
 template <int D>
 __device__ __forceinline__ double defect_at(const SCoef &c, const double *u, const double *b, const GridDesc &g,
                                             int i, int j, int k) {
+    if (g.per) {   // periodic: the fine neighbours of coarse point 0 wrap around
+        i = wrapn(i, g.n); j = wrapn(j, g.n);
+        if (D == 3) k = wrapn(k, g.n);
+    }
     return b[gidx(g, i, j, k)] - apply_S<D>(c, u, g, i, j, k);
 }
 
-// full weighting of the fine defect d = b - S u: coarse (I,J,K) <-> fine (2I+1, 2J+1, 2K+1)
+// full weighting of the fine defect d = b - S u: coarse (I,J,K) <-> fine (2I+1, 2J+1, 2K+1);
+// periodic grids: fine (2I, 2J, 2K)
 template <int D>
 __global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const double *__restrict__ u,
                                   const double *__restrict__ b, GridDesc gf, SCoef c) {
@@ -85,7 +91,8 @@ __global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const do
     int J = blockIdx.y * blockDim.y + threadIdx.y;
     int K = (D == 3) ? (int)blockIdx.z : 0;
     if (I >= gc.n || J >= gc.n) return;
-    int x = 2 * I + 1, y = 2 * J + 1, z = (D == 3) ? 2 * K + 1 : 0;
+    const int o = gf.per ? 0 : 1;
+    int x = 2 * I + o, y = 2 * J + o, z = (D == 3) ? 2 * K + o : 0;
     if (D == 2) {
         double d[3][3];
 #pragma unroll
@@ -117,7 +124,17 @@ __global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const do
     }
 }
 
-// bi/trilinear prolongation + correction u += P e
+// bi/trilinear prolongation + correction u += P e.  Per axis, Dirichlet: an even
+// fine index takes the coarse pair (x/2-1, x/2), an odd one (x-1)/2; periodic: an odd fine index
+// takes the pair ((x-1)/2, (x+1)/2 mod nc), an even one x/2.
+__device__ __forceinline__ bool prolong_axis(int x, bool per, int &a, int &b) {
+    // pair iff (x + per) is even; first member (x - 1 + per) >> 1 (arithmetic shift: -1 at x = 0)
+    bool pair = ((x + (per ? 1 : 0)) & 1) == 0;
+    a = (x - (per ? 0 : 1)) >> 1;
+    b = a + 1;
+    if (!pair) a = b = (per ? x >> 1 : (x - 1) >> 1);
+    return pair;
+}
 template <int D>
 __global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double *__restrict__ e, GridDesc gc) {
     pdl_launch();
@@ -125,13 +142,13 @@ __global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double 
     POINT_INDEX_OR_RETURN(gf)
     if (!inside) return;
     int xa, xb, ya, yb, za = 0, zb = 0;
-    bool xe = !(i & 1), ye = !(j & 1), ze = (D == 3) && !(k & 1);
+    const bool per = gf.per != 0;
+    bool xe = prolong_axis(i, per, xa, xb), ye = prolong_axis(j, per, ya, yb);
+    bool ze = (D == 3) && prolong_axis(k, per, za, zb);
     double w = 1.0;
-    if (xe) { xa = i / 2 - 1; xb = i / 2; w *= 0.5; } else { xa = xb = (i - 1) / 2; }
-    if (ye) { ya = j / 2 - 1; yb = j / 2; w *= 0.5; } else { ya = yb = (j - 1) / 2; }
-    if (D == 3) {
-        if (ze) { za = k / 2 - 1; zb = k / 2; w *= 0.5; } else { za = zb = (k - 1) / 2; }
-    }
+    if (xe) w *= 0.5;
+    if (ye) w *= 0.5;
+    if (ze) w *= 0.5;
     double sz = 0.0;
     for (int cz = 0; cz < ((D == 3 && ze) ? 2 : 1); ++cz) {
         int Z = cz ? zb : za;
@@ -148,21 +165,21 @@ __global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double 
     u[p] = u[p] + sz * w;
 }
 
-// coarsest level (n = 3): u = Ginv b, accumulated over ascending j
+// coarsest level (n = 3; periodic n = 4): u = Ginv b, accumulated over ascending j
 template <int D>
 __global__ void k_coarse_solve(double *__restrict__ u, const double *__restrict__ b, GridDesc g,
                                const double *__restrict__ Ginv) {
     pdl_launch();
     pdl_wait();
-    constexpr int P = (D == 3) ? 27 : 9;
-    __shared__ double bs[27];
+    const int n = g.n, P = (D == 3) ? n * n * n : n * n;
+    __shared__ double bs[64];
     int t = threadIdx.x;
-    if (t < P) bs[t] = b[gidx(g, t % 3, (t / 3) % 3, D == 3 ? t / 9 : 0)];
+    if (t < P) bs[t] = b[gidx(g, t % n, (t / n) % n, D == 3 ? t / (n * n) : 0)];
     __syncthreads();
     if (t < P) {
         double acc = Ginv[t * P] * bs[0];
         for (int jj = 1; jj < P; ++jj) acc = acc + Ginv[t * P + jj] * bs[jj];
-        u[gidx(g, t % 3, (t / 3) % 3, D == 3 ? t / 9 : 0)] = acc;
+        u[gidx(g, t % n, (t / n) % n, D == 3 ? t / (n * n) : 0)] = acc;
     }
 }
 
@@ -183,7 +200,7 @@ __global__ void k_vw(double *__restrict__ V, double *__restrict__ W, VWParams P)
     } else {
         double fa = P.a[0] * fe_at<D>(P.fe, P.uold[0], g, i, j, k, P.ct[0]);
         for (int jj = 1; jj < P.M; ++jj) fa = fa + P.a[jj] * fe_at<D>(P.fe, P.uold[jj], g, i, j, k, P.ct[jj]);
-        double fn = fe_at<D>(P.fe, P.unew_m, g, i, j, k, P.ct[P.m]);
+        double fn = fe_at<D>(P.fe, P.unew_m, g, i, j, k, *P.ctn);
         double fo = fe_at<D>(P.fe, P.uold[P.m], g, i, j, k, P.ct[P.m]);
         V[p] = (P.unew_m[p] + P.dtm * (fn - fo)) + fa;
     }

@@ -14,6 +14,7 @@
 #include <quadmath.h>
 #include <cstring>
 #include <cmath>
+#include <vector>
 
 #include "tables.h"
 
@@ -105,16 +106,22 @@ int isdc_build_tables(int M, double *tau, double *Q, double *S, double *dtau) {
     return 0;
 }
 
-// Coarsest level (n = 3): matrix entries are the binary64 coefficients c0 (centre), c1 (face
-// neighbours), c2 (edge neighbours; 2D: diagonal neighbours); zero otherwise.
-int isdc_coarse_inverse(int dim, double c0, double c1, double c2, double *Ginv) {
-    const int P = (dim == 3) ? 27 : 9;
-    q128 A[27 * 27], Lc[27 * 27];
+// Coarsest level (n = 3; periodic n = 4): matrix entries are the binary64 coefficients c0 (centre),
+// c1 (face neighbours), c2 (edge neighbours; 2D: diagonal neighbours); zero otherwise.  Periodic
+// grids measure neighbour distances modulo n.
+int isdc_coarse_inverse(int dim, int n, int periodic, double c0, double c1, double c2, double *Ginv) {
+    if (n < 2 || n > 4) return -2;
+    const int P = (dim == 3) ? n * n * n : n * n;
+    std::vector<q128> A((size_t)P * P), Lc((size_t)P * P), y(P);
+    auto dist = [&](int a, int b) {
+        int d = std::abs(a - b);
+        return (periodic && n - d < d) ? n - d : d;
+    };
     for (int r = 0; r < P; ++r) {
-        int rx = r % 3, ry = (r / 3) % 3, rz = r / 9;
+        int rx = r % n, ry = (r / n) % n, rz = r / (n * n);
         for (int c = 0; c < P; ++c) {
-            int cx = c % 3, cy = (c / 3) % 3, cz = c / 9;
-            int dx = std::abs(rx - cx), dy = std::abs(ry - cy), dz = std::abs(rz - cz);
+            int cx = c % n, cy = (c / n) % n, cz = c / (n * n);
+            int dx = dist(rx, cx), dy = dist(ry, cy), dz = dist(rz, cz);
             double v = 0.0;
             if (dx <= 1 && dy <= 1 && dz <= 1) {
                 int hops = dx + dy + dz;
@@ -137,7 +144,6 @@ int isdc_coarse_inverse(int dim, double c0, double c1, double c2, double *Ginv) 
         }
     }
     for (int c = 0; c < P; ++c) {
-        q128 y[27];
         for (int i = 0; i < P; ++i) {                 // Lc y = e_c
             q128 t = (i == c) ? 1 : 0;
             for (int k = 0; k < i; ++k) t -= Lc[i * P + k] * y[k];

@@ -16,7 +16,8 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libisdc.so")
 
-FE_NONE, FE_CUBIC, FE_FORCING, FE_ADVECTION = 0, 1, 2, 3
+FE_NONE, FE_CUBIC, FE_FORCING, FE_ADVECTION, FE_BURGERS = 0, 1, 2, 3, 4
+BC_DIRICHLET, BC_PERIODIC = 0, 1
 MODE_ISDC, MODE_SDC, MODE_ISDC_CAPPED = 0, 1, 2
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "cuda error", 4: "non-finite value",
           5: "bad workspace"}
@@ -29,7 +30,7 @@ class IsdcError(RuntimeError):
 
 
 class _Grid(C.Structure):
-    _fields_ = [("dim", C.c_int), ("n", C.c_int), ("coarsest_n", C.c_int)]
+    _fields_ = [("dim", C.c_int), ("n", C.c_int), ("coarsest_n", C.c_int), ("bc", C.c_int)]
 
 
 class _Mg(C.Structure):
@@ -92,7 +93,7 @@ def lib():
         L.isdc_profile_reset.argtypes = [_vp]
         L.isdc_profile_get.argtypes = [_vp, C.c_int, _dp, C.POINTER(C.c_long), _dp]
         L.isdc_build_tables.argtypes = [C.c_int, _dp, _dp, _dp, _dp]
-        L.isdc_coarse_inverse.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, _dp]
+        L.isdc_coarse_inverse.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _dp]
         _lib = L
     return _lib
 
@@ -120,7 +121,7 @@ class ISDC:
                  fe_a=(0.0, 0.0, 0.0), G: Optional[torch.Tensor] = None, mode: int = MODE_ISDC, L: int = 2,
                  inner_tol: float = 1e-12, inner_cap: int = 50, sweep_tol: float = 1e-10, max_sweeps: int = 200,
                  fixed_sweeps: int = 0, nu1: int = 2, nu2: int = 2, omega: float = 0.8, guess: int = 0,
-                 residual_kind: int = 0, w_tol: float = 1e-6, w_cap: int = 50,
+                 residual_kind: int = 0, w_tol: float = 1e-6, w_cap: int = 50, bc: int = BC_DIRICHLET,
                  device: Optional[torch.device] = None, stream: Optional[torch.cuda.Stream] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ISDC needs a CUDA device (no CPU fallback)")
@@ -128,7 +129,7 @@ class ISDC:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         p = _Problem()
-        p.grid.dim, p.grid.n, p.grid.coarsest_n = dim, n, 3
+        p.grid.dim, p.grid.n, p.grid.coarsest_n, p.grid.bc = dim, n, 0, bc
         p.M, p.nodes, p.dt, p.nu, p.fe = M, 0, dt, nu, fe
         for i in range(3):
             p.fe_params[i] = fe_a[i]
@@ -160,7 +161,7 @@ class ISDC:
         return cls(cfg.dim, cfg.n, cfg.M, cfg.dt, cfg.nu, cfg.fe, cfg.fe_a, G, mode=mode, L=cfg.L,
                    inner_tol=cfg.inner_tol, inner_cap=cfg.inner_cap, sweep_tol=cfg.sweep_tol,
                    max_sweeps=cfg.max_sweeps, fixed_sweeps=cfg.fixed_sweeps, nu1=cfg.nu1, nu2=cfg.nu2,
-                   omega=cfg.omega, **kw)
+                   omega=cfg.omega, bc=getattr(cfg, "bc", BC_DIRICHLET), **kw)
 
     # ------------------------------------------------------------------ plumbing
     def _check(self, st):

@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(L):
 def test_workspace_and_validation_without_gpu(L):
     from paper_1401_7824_b200.isdc import _Problem
     p = _Problem()
-    p.grid.dim, p.grid.n, p.grid.coarsest_n = 2, 63, 3
+    p.grid.dim, p.grid.n, p.grid.coarsest_n, p.grid.bc = 2, 63, 3, 0
     p.M, p.dt, p.nu = 3, 0.01, 1.0
     p.mg.nu1 = p.mg.nu2 = 2
     p.mg.omega = 0.8
@@ -59,6 +59,18 @@ def test_workspace_and_validation_without_gpu(L):
     q = _Problem.from_buffer_copy(p)
     q.fe = 2  # forcing without a field
     assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == 1
+    # periodic grids (NEXT f3): n = 2^p points, coarsest 4; WENO5 Burgers only on periodic grids
+    q = _Problem.from_buffer_copy(p)
+    q.fe = 4
+    assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == 2
+    q.grid.bc, q.grid.n, q.grid.coarsest_n = 1, 128, 0
+    assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == 0
+    assert nb.value >= (2 * 3 - 1 + 4) * 128 * 128 * 8
+    for n, cn, code in [(127, 0, 1), (96, 0, 1), (128, 3, 1), (128, 4, 0), (4, 0, 0)]:
+        q.grid.n, q.grid.coarsest_n = n, cn
+        assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == code, (n, cn)
+    q.grid.bc = 2
+    assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == 1
     # create refuses a missing / too-small workspace before touching the device
     h = C.c_void_p()
     assert L.isdc_create(C.byref(p), None, 0, None, C.byref(h)) == 5
@@ -74,12 +86,13 @@ def test_library_tables_equal_oracle_bits(L, ora, M):
     assert np.array_equal(S, oS.ravel()) and np.array_equal(dtau, od)
 
 
-@pytest.mark.parametrize("dim", [2, 3])
-def test_library_coarse_inverse_equals_oracle_bits(L, ora, dim):
+@pytest.mark.parametrize("dim,periodic", [(2, False), (3, False), (2, True), (3, True)])
+def test_library_coarse_inverse_equals_oracle_bits(L, ora, dim, periodic):
     dp = C.POINTER(C.c_double)
-    P = 9 if dim == 2 else 27
+    n = 4 if periodic else 3
+    P = n ** dim
     for g in [0.0, 1e-5, 3e-3, 0.0172, 0.5]:
-        c = ora.level_coefs(dim, 3, g)
+        c = ora.level_coefs(dim, n, g, periodic=periodic)
         Gi = np.zeros(P * P)
-        assert L.isdc_coarse_inverse(dim, c[0], c[1], c[2], Gi.ctypes.data_as(dp)) == 0
-        assert np.array_equal(Gi, ora.coarse_inverse(dim, g).ravel())
+        assert L.isdc_coarse_inverse(dim, n, int(periodic), c[0], c[1], c[2], Gi.ctypes.data_as(dp)) == 0
+        assert np.array_equal(Gi, ora.coarse_inverse(dim, g, periodic=periodic).ravel())
