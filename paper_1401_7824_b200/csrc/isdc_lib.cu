@@ -19,6 +19,7 @@
 #include "kernels_fast2d.cuh"
 #include "kernels_fast3d.cuh"
 #include "kernels_tail.cuh"
+#include "kernels_ptail.cuh"
 #include "tables.h"
 
 namespace {
@@ -85,6 +86,9 @@ struct isdc_ctx {
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
     TailParams tailp[ISDC_MAXM];
     size_t tail_smem = 0;
+    int ptail_l0 = -1;         // periodic grids: first level of the single-CTA periodic tail (ISDC_PTAIL=0: none)
+    PTailParams ptailp[ISDC_MAXM];
+    size_t ptail_smem = 0;
     // CUDA graphs of whole ISDC sweeps, keyed by (cur, spread, profiling)
     cudaStream_t cap = nullptr;
     bool graphs = true;
@@ -267,7 +271,7 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     if (h) { h->T = T; h->Bf = Bf; h->V = V; h->W = W; h->Gp = Gp; }
     // stored f^E fields for the 3D CD4 fast path: shared F_0, two sets of M-1, staging scratch
     if (h) { for (int s_ = 0; s_ < 2; ++s_) for (int j = 0; j < ISDC_MAXM; ++j) h->Fs[s_][j] = nullptr; }
-    if (d == 3 && p->fe == ISDC_FE_ADVECTION_CD4) {
+    if ((d == 3 && p->fe == ISDC_FE_ADVECTION_CD4) || p->fe == ISDC_FE_BURGERS_WENO5) {
         double *f0 = (double *)take(fe);
         if (h) h->Fs[0][0] = h->Fs[1][0] = f0;
         for (int s_ = 0; s_ < 2; ++s_)
@@ -470,14 +474,32 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
 
 // f^E(u) (CD4 advection) into a stored field (3D fast path), DESIGN.md §6.11
 bool need_F(const isdc_ctx *h) {
+    // stored f^E(u_j) fields: 3D CD4 fast kernels; Burgers always (each WENO5 f^E is evaluated
+    // once per new node field instead of (M+2)(M-1) + M(M-1) times per sweep)
+    if (h->fe.kind == ISDC_FE_BURGERS_WENO5) return true;
     return h->d == 3 && h->fe.kind == 3 && (use_fast3d(h, 0, 8) || use_fast3d(h, 0, 16));
 }
 // the residual passes store the next sweep's RHS folds (3D CD4 fast RHS and residual both on)
 bool folds_on(const isdc_ctx *h) { return need_F(h) && use_fast3d(h, 0, 8) && use_fast3d(h, 0, 16) && h->folds; }
 
+isdc_status launch_alpha(isdc_ctx *h, const double *field, int slot);
+
 isdc_status launch_fe(isdc_ctx *h, double *F, const double *u) {
     if (!need_F(h)) return ISDC_OK;
     const GridDesc &g = h->lev[0].g;
+    if (h->fe.kind == ISDC_FE_BURGERS_WENO5) {
+        // generic stored f^E (Burgers): alpha = max|u| first (reading R31), then every point
+        const int slot = 3 * ISDC_MAXM - 1;
+        isdc_status sa = launch_alpha(h, u, slot);
+        if (sa != ISDC_OK) return sa;
+        ++h->launches;
+        int pe = prof_begin(h, PROF_RHS);
+        if (h->d == 2) kl(h, k_fe<2>, point_grid<2>(g, kBlk), kBlk, 0)(F, u, g, h->fe, h->alpha + slot);
+        else kl(h, k_fe<3>, point_grid<3>(g, kBlk), kBlk, 0)(F, u, g, h->fe, h->alpha + slot);
+        prof_end(h, pe, PROF_RHS, 0.0);
+        LAUNCH_CHECK(h);
+        return ISDC_OK;
+    }
     const CUtensorMap *mu = tmap(h, u, g, f3d::FE_W, f3d::FE_H, 1);
     if (!mu) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
@@ -772,11 +794,24 @@ isdc_status launch_tail(isdc_ctx *h, int l, int m, const double *b, const double
     return ISDC_OK;
 }
 
+isdc_status launch_ptail(isdc_ctx *h, int l, int m, const double *b, const double *u_in, double *u_out) {
+    PTailParams P = h->ptailp[m];
+    P.b_in = b; P.u_in = u_in; P.u_out = u_out;
+    ++h->launches;
+    int pe = prof_begin(h, l == 0 ? PROF_SMOOTH : PROF_COARSE);
+    if (h->d == 2) kl(h, k_ptail<2>, 1, PTAIL_THREADS, h->ptail_smem)(P);
+    else kl(h, k_ptail<3>, 1, PTAIL_THREADS, h->ptail_smem)(P);
+    prof_end(h, pe, l == 0 ? PROF_SMOOTH : PROF_COARSE, 16.0 * npts_of(h, h->lev[l].g));
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
 // zero_init: the iterate is zero (coarse-grid correction); X need not hold zeros
 isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double *b, const double *src,
                    bool zero_init = false) {
     Level &L = h->lev[l];
     const GridDesc &g = L.g;
+    if (l == h->ptail_l0) return launch_ptail(h, l, m, b, zero_init ? nullptr : (src ? src : X), X);
     if (l == h->tail_l0) return launch_tail(h, l, m, b, zero_init ? nullptr : (src ? src : X), X);
     if (l == h->nlev - 1) return launch_coarse(h, X, b, g, m);   // n = 3 (periodic: 4)
     const SCoef &c = L.coef[m];
@@ -857,6 +892,8 @@ void fill_vw(isdc_ctx *h, VWParams &P, int m, double *const *uold, const double 
     }
     P.fe = h->fe;
     P.g = h->lev[0].g;
+    for (int j = 0; j < ISDC_MAXM; ++j) P.F[j] = nullptr;
+    P.Fn = nullptr;
 }
 
 // Burgers (R31): alpha = max|u| of `field` into alpha slot `slot` (bits of a non-negative double)
@@ -988,7 +1025,10 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
     fill_vw(h, P, m, uold, unew_m);
     const GridDesc &g = h->lev[0].g;
     int pe = prof_begin(h, PROF_RHS);
-    if (h->fe.kind == ISDC_FE_BURGERS_WENO5) {
+    if (need_F(h) && Fold && Fnew) {
+        for (int j = 0; j < h->M; ++j) P.F[j] = Fold[j];
+        P.Fn = Fnew;
+    } else if (h->fe.kind == ISDC_FE_BURGERS_WENO5) {
         // uold is fixed for the whole sweep: its speeds are measured at substep 0 (or on request)
         if (m == 0 || fresh_old)
             for (int j = 0; j < h->M; ++j) TRY(launch_alpha(h, uold[j], j));
@@ -1120,7 +1160,8 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
     }
     double dt = h->P.dt, nudt = h->P.nu * dt;
     int pe = prof_begin(h, PROF_RESID);
-    if (h->fe.kind == ISDC_FE_BURGERS_WENO5)
+    const bool useF = need_F(h) && F;
+    if (h->fe.kind == ISDC_FE_BURGERS_WENO5 && !useF)
         for (int j = 0; j < M; ++j) TRY(launch_alpha(h, u[j], 2 * ISDC_MAXM + j));
     for (int m = 1; m < M; ++m) {
         PZParams P;
@@ -1131,6 +1172,7 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             P.qb[j] = nudt * h->Q[m * M + j];
         }
         P.ct = (h->fe.kind == ISDC_FE_BURGERS_WENO5) ? (const double *)(h->alpha + 2 * ISDC_MAXM) : h->ctdev;
+        for (int j = 0; j < ISDC_MAXM; ++j) P.F[j] = (useF && j < M) ? F[j] : nullptr;
         P.fe = h->fe;
         P.g = g;
         h->launches += 2;
@@ -1487,6 +1529,33 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
             }
             h->tail_smem = (h->d == 2) ? tail_smem_bytes<2>(h->tailp[0]) : tail_smem_bytes<3>(h->tailp[0]);
             if (h->tailp[0].nlev > TAIL_MAX_LEVELS || tail_dispatch(h, h->tailp[0], true) != ISDC_OK) h->tail_l0 = -1;
+        }
+    }
+    // periodic grids: levels n <= 64 (2D) / 16 (3D) in one single-CTA launch (kernels_ptail.cuh)
+    const char *ept = getenv("ISDC_PTAIL");
+    if (h->per && !(ept && ept[0] == '0')) {
+        const int lim = (h->d == 2) ? 64 : 16;
+        for (int l = 0; l < h->nlev; ++l)
+            if (h->lev[l].g.n <= lim) { h->ptail_l0 = l; break; }
+        if (h->ptail_l0 >= 0 && h->nlev - h->ptail_l0 >= 2 && h->nlev - h->ptail_l0 <= PTAIL_MAX_LEVELS) {
+            for (int m = 0; m < nslots; ++m) {
+                PTailParams &T = h->ptailp[m];
+                T.nlev = h->nlev - h->ptail_l0;
+                for (int i = 0; i < T.nlev; ++i) {
+                    T.n[i] = h->lev[h->ptail_l0 + i].g.n;
+                    T.c[i] = h->lev[h->ptail_l0 + i].coef[m];
+                }
+                T.nu1 = prob->mg.nu1; T.nu2 = prob->mg.nu2;
+                T.Ginv = h->Ginv + (size_t)m * Pc * Pc;
+                T.b_in = nullptr; T.u_in = nullptr; T.u_out = nullptr;
+            }
+            h->ptail_smem = (h->d == 2) ? ptail_smem_bytes<2>(h->ptailp[0]) : ptail_smem_bytes<3>(h->ptailp[0]);
+            cudaError_t ea = (h->d == 2)
+                ? cudaFuncSetAttribute(k_ptail<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ptail_smem)
+                : cudaFuncSetAttribute(k_ptail<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ptail_smem);
+            if (ea != cudaSuccess || h->ptail_smem > kMaxDynSmem) { cudaGetLastError(); h->ptail_l0 = -1; }
+        } else {
+            h->ptail_l0 = -1;   // a single level: the coarse solve alone
         }
     }
     cudaError_t e = cudaMemcpyAsync(h->Ginv, Gi.data(), Gi.size() * sizeof(double), cudaMemcpyHostToDevice, h->s);

@@ -14,6 +14,8 @@ struct VWParams {                 // RHS of Eq. (5) for substep m (DESIGN.md §4
     double beta[ISDC_MAXM];       // (nu*dt)*S_{m,j}
     const double *ct;             // device: cos(t_n + dt*tau_j), j = 0..M-1 (Burgers: alpha of uold_j)
     const double *ctn;            // the same for unew_m (&ct[m]; Burgers: alpha of unew_m)
+    const double *F[ISDC_MAXM];   // stored f^E(uold_j), or F[0] == null: evaluate f^E here
+    const double *Fn;             // stored f^E(unew_m)
     FeDesc fe;
     GridDesc g;
 };
@@ -24,6 +26,7 @@ struct PZParams {                 // residual of node m
     double qa[ISDC_MAXM];         // dt*Q_{m,j}
     double qb[ISDC_MAXM];         // (nu*dt)*Q_{m,j}
     const double *ct;             // device: cos(t_n + dt*tau_j) (Burgers: alpha of u_j)
+    const double *F[ISDC_MAXM];   // stored f^E(u_j), or F[0] == null: evaluate f^E here
     FeDesc fe;
     GridDesc g;
 };
@@ -81,16 +84,10 @@ __device__ __forceinline__ double defect_at(const SCoef &c, const double *u, con
 }
 
 // full weighting of the fine defect d = b - S u: coarse (I,J,K) <-> fine (2I+1, 2J+1, 2K+1);
-// periodic grids: fine (2I, 2J, 2K)
+// periodic grids: fine (2I, 2J, 2K).  The value at one coarse point (shared with the periodic tail).
 template <int D>
-__global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const double *__restrict__ u,
-                                  const double *__restrict__ b, GridDesc gf, SCoef c) {
-    pdl_launch();
-    pdl_wait();
-    int I = blockIdx.x * blockDim.x + threadIdx.x;
-    int J = blockIdx.y * blockDim.y + threadIdx.y;
-    int K = (D == 3) ? (int)blockIdx.z : 0;
-    if (I >= gc.n || J >= gc.n) return;
+__device__ __forceinline__ double fw_defect(const SCoef &c, const double *u, const double *b, const GridDesc &gf,
+                                            int I, int J, int K) {
     const int o = gf.per ? 0 : 1;
     int x = 2 * I + o, y = 2 * J + o, z = (D == 3) ? 2 * K + o : 0;
     if (D == 2) {
@@ -102,7 +99,7 @@ __global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const do
         double rd0 = d[0][0] + d[0][2], rd1 = d[1][0] + d[1][2], rd2 = d[2][0] + d[2][2];
         double fd = rd1 + (d[0][1] + d[2][1]);
         double ed = rd0 + rd2;
-        bc[gidx(gc, I, J, 0)] = ((4.0 * d[1][1] + 2.0 * fd) + ed) * 0.0625;
+        return ((4.0 * d[1][1] + 2.0 * fd) + ed) * 0.0625;
     } else {
         double fd[3], ed[3], dc[3];
 #pragma unroll
@@ -120,8 +117,19 @@ __global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const do
         double F = fd[1] + (dc[0] + dc[2]);
         double E = ed[1] + (fd[0] + fd[2]);
         double C = ed[0] + ed[2];
-        bc[gidx(gc, I, J, K)] = ((8.0 * dc[1] + 4.0 * F) + (2.0 * E + C)) * 0.015625;
+        return ((8.0 * dc[1] + 4.0 * F) + (2.0 * E + C)) * 0.015625;
     }
+}
+template <int D>
+__global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const double *__restrict__ u,
+                                  const double *__restrict__ b, GridDesc gf, SCoef c) {
+    pdl_launch();
+    pdl_wait();
+    int I = blockIdx.x * blockDim.x + threadIdx.x;
+    int J = blockIdx.y * blockDim.y + threadIdx.y;
+    int K = (D == 3) ? (int)blockIdx.z : 0;
+    if (I >= gc.n || J >= gc.n) return;
+    bc[gidx(gc, I, J, K)] = fw_defect<D>(c, u, b, gf, I, J, K);
 }
 
 // bi/trilinear prolongation + correction u += P e.  Per axis, Dirichlet: an even
@@ -135,12 +143,10 @@ __device__ __forceinline__ bool prolong_axis(int x, bool per, int &a, int &b) {
     if (!pair) a = b = (per ? x >> 1 : (x - 1) >> 1);
     return pair;
 }
+// the correction (P e)(i,j,k) at one fine point (shared with the periodic tail)
 template <int D>
-__global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double *__restrict__ e, GridDesc gc) {
-    pdl_launch();
-    pdl_wait();
-    POINT_INDEX_OR_RETURN(gf)
-    if (!inside) return;
+__device__ __forceinline__ double prolong_val(const double *e, const GridDesc &gc, const GridDesc &gf, int i, int j,
+                                              int k) {
     int xa, xb, ya, yb, za = 0, zb = 0;
     const bool per = gf.per != 0;
     bool xe = prolong_axis(i, per, xa, xb), ye = prolong_axis(j, per, ya, yb);
@@ -161,8 +167,16 @@ __global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double 
         }
         sz = cz ? sz + sy : sy;
     }
+    return sz * w;
+}
+template <int D>
+__global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double *__restrict__ e, GridDesc gc) {
+    pdl_launch();
+    pdl_wait();
+    POINT_INDEX_OR_RETURN(gf)
+    if (!inside) return;
     long long p = gidx(gf, i, j, k);
-    u[p] = u[p] + sz * w;
+    u[p] = u[p] + prolong_val<D>(e, gc, gf, i, j, k);
 }
 
 // coarsest level (n = 3; periodic n = 4): u = Ginv b, accumulated over ascending j
@@ -197,6 +211,10 @@ __global__ void k_vw(double *__restrict__ V, double *__restrict__ W, VWParams P)
     W[p] = acc - P.gm * P.uold[P.m + 1][p];
     if (P.fe.kind == 0) {
         V[p] = P.unew_m[p];
+    } else if (P.F[0]) {            // the same tree on stored f^E values
+        double fa = P.a[0] * P.F[0][p];
+        for (int jj = 1; jj < P.M; ++jj) fa = fa + P.a[jj] * P.F[jj][p];
+        V[p] = (P.unew_m[p] + P.dtm * (P.Fn[p] - P.F[P.m][p])) + fa;
     } else {
         double fa = P.a[0] * fe_at<D>(P.fe, P.uold[0], g, i, j, k, P.ct[0]);
         for (int jj = 1; jj < P.M; ++jj) fa = fa + P.a[jj] * fe_at<D>(P.fe, P.uold[jj], g, i, j, k, P.ct[jj]);
@@ -231,7 +249,11 @@ __global__ void k_pz(double *__restrict__ Pf, double *__restrict__ Zf, PZParams 
     if (!inside) return;
     long long p = gidx(g, i, j, k);
     double diff = P.u[P.m][p] - P.u[0][p];
-    if (P.fe.kind != 0) {
+    if (P.fe.kind != 0 && P.F[0]) {
+        double fa = P.qa[0] * P.F[0][p];
+        for (int jj = 1; jj < P.M; ++jj) fa = fa + P.qa[jj] * P.F[jj][p];
+        diff = diff - fa;
+    } else if (P.fe.kind != 0) {
         double fa = P.qa[0] * fe_at<D>(P.fe, P.u[0], g, i, j, k, P.ct[0]);
         for (int jj = 1; jj < P.M; ++jj) fa = fa + P.qa[jj] * fe_at<D>(P.fe, P.u[jj], g, i, j, k, P.ct[jj]);
         diff = diff - fa;
@@ -255,4 +277,16 @@ __global__ void k_resid(const double *__restrict__ Pf, const double *__restrict_
         if (out) out[gidx(g, i, j, k)] = val;   // r~ field (unweighted residual)
     }
     block_max_to(slot, fabs(val));
+}
+
+// f^E(u) into a stored field (generic; Burgers: aux = the alpha slot of u, else cos t unused)
+template <int D>
+__global__ void k_fe(double *__restrict__ F, const double *__restrict__ u, GridDesc g, FeDesc fe,
+                     const unsigned long long *aux) {
+    pdl_launch();
+    pdl_wait();
+    POINT_INDEX_OR_RETURN(g)
+    if (!inside) return;
+    const double a = __longlong_as_double((long long)*aux);
+    F[gidx(g, i, j, k)] = fe_at<D>(fe, u, g, i, j, k, a);
 }
