@@ -68,16 +68,28 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
     if (MODE == 2) {
         // u += P e on the u box (fine (x0-2+lx, y0-2+ly)); local coarse index of the pair / single
         // coarse neighbour: even lx -> (lx/2, lx/2+1), odd lx -> (lx+1)/2 (same for rows)
-        for (int q = tid; q < UW * UH; q += NT) {
-            const int lx = q % UW, ly = q / UW;
+        // Column pairs (lx, lx+1), lx = 2k even: the even point takes the coarse pair (k, k+1),
+        // the odd one coarse k+1, so one row of e serves both; 16-byte u accesses.  Same trees
+        // as the per-point form: sx(r) = e[r][xa] (+ e[r][xa+1]); sz = sx(ya) (+ sx(ya+1)).
+        constexpr int PW = UW / 2;
+        for (int q = tid; q < PW * UH; q += NT) {
+            const int ly = q / PW, k = q - ly * PW, lx = 2 * k;
             const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
-            if (gx < 0 || gx >= n || gy < 0 || gy >= n) continue;
-            const bool xe = !(lx & 1), ye = !(ly & 1);
-            const int xa = xe ? lx / 2 : (lx + 1) / 2, ya = ye ? ly / 2 : (ly + 1) / 2;
-            auto sx = [&](int r) { return xe ? S.e[r][xa] + S.e[r][xa + 1] : S.e[r][xa]; };
-            const double sz = ye ? sx(ya) + sx(ya + 1) : sx(ya);
-            const double w = xe ? (ye ? 0.25 : 0.5) : (ye ? 0.5 : 1.0);
-            S.u[ly][lx] = S.u[ly][lx] + sz * w;
+            if (gy < 0 || gy >= n || gx + 1 < 0 || gx >= n) continue;
+            const bool ye = !(ly & 1);
+            const int ya = ye ? ly / 2 : (ly + 1) / 2;
+            const double ea0 = S.e[ya][k], ea1 = S.e[ya][k + 1];
+            double sze = ea0 + ea1, szo = ea1, we = 0.5, wo = 1.0;
+            if (ye) {
+                const double eb0 = S.e[ya + 1][k], eb1 = S.e[ya + 1][k + 1];
+                sze = sze + (eb0 + eb1);
+                szo = szo + eb1;
+                we = 0.25; wo = 0.5;
+            }
+            double2 v = *reinterpret_cast<const double2 *>(&S.u[ly][lx]);
+            if (gx >= 0) v.x = v.x + sze * we;
+            if (gx + 1 < n) v.y = v.y + szo * wo;
+            *reinterpret_cast<double2 *>(&S.u[ly][lx]) = v;
         }
         __syncthreads();
     }
@@ -801,6 +813,45 @@ __device__ __forceinline__ void fr_phase(const double *__restrict__ src, int sox
 #undef ISDC_FR_ROW
 }
 
+// Same trees as the generic defect (apply_S) and fw_defect: rd = d(x-1) + d(x+1);
+// fd = rd1 + (d0 + d2); ed = rd0 + rd2; b_c = ((4 d1 + 2 fd) + ed) * 0.0625.
+__device__ __forceinline__ void fr_defect_fw(const SmemSR &S, int x0, int y0, int nc, int pitch_c, const SCoef &c,
+                                             double *__restrict__ bc) {
+    static_assert(FR_TY == 16 && NT == 256 && FR_TX == 58, "4 bands x 4 fine rows, 2 column chunks");
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int chunk = wp & 1, band = wp >> 1;
+    const int x = 30 * chunk + lane, r0 = 4 * band;
+    const double c0 = c.c0, c1 = c.c1, c2 = c.c2;
+    const double *sp = &S.u[r0 - 1 - FR_UOY][x - FR_UOX];
+    const double *bp = &S.b[r0 - FR_BOY][x - FR_BOX];
+    double qm = sp[0], rm = sp[-1] + sp[1];
+    sp += FR_UW;
+    double qc = sp[0], rc = sp[-1] + sp[1];
+    const bool xo = (x & 1) && (chunk ? x >= 31 : x <= 29) && x <= 57;
+    const int gI = x0 / 2 + (x - 1) / 2;
+    double D0 = 0.0, R0 = 0.0, D1 = 0.0, R1 = 0.0;
+#pragma unroll
+    for (int yy = 0; yy < 5; ++yy) {
+        sp += FR_UW;
+        const double qn = sp[0], rn = sp[-1] + sp[1];
+        const double f = rc + (qm + qn);
+        const double e = rm + rn;
+        const double su = (c0 * qc + c1 * f) + c2 * e;
+        const double d = bp[yy * FR_BW] - su;
+        const double rd = __shfl_up_sync(0xffffffffu, d, 1) + __shfl_down_sync(0xffffffffu, d, 1);
+        if (yy == 2 || yy == 4) {          // rows r0 + yy - 2, -1, yy: coarse row J = (r0 + yy - 2) / 2
+            const int gJ = y0 / 2 + (r0 + yy - 2) / 2;
+            if (xo && gI < nc && gJ < nc) {
+                const double fd = R1 + (D0 + d);
+                const double ed = R0 + rd;
+                bc[(long long)gJ * pitch_c + gI] = ((4.0 * D1 + 2.0 * fd) + ed) * 0.0625;
+            }
+        }
+        D0 = D1; R0 = R1; D1 = d; R1 = rd;
+        qm = qc; rm = rc; qc = qn; rc = rn;
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtensorMap tu,
                                                  const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
@@ -838,22 +889,11 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
     fr_phase<1, FR_TW, FR_UW>(&S.t[0][0], FR_TOX, FR_TOY, &S.u[0][0], FR_UOX, FR_UOY, Bp, -1, 61, -1, FR_TY + 3, x0, y0, n,
                               c, out, pitch);
     __syncthreads();
-    // defect: d = b - S u'' (into the t buffer) on [0, 58] x [0, 32]
-    fr_phase<2, FR_UW, FR_TW>(&S.u[0][0], FR_UOX, FR_UOY, &S.t[0][0], FR_TOX, FR_TOY, Bp, 0, 59, 0, FR_TY + 1, x0, y0, n, c,
-                              nullptr, pitch);
-    __syncthreads();
-    // full weighting: coarse (I, J) <-> local fine (2I+1, 2J+1)
-    for (int p = tid; p < FR_CX * FR_CY; p += NT) {
-        const int I = p % FR_CX, J = p / FR_CX;
-        const int gI = x0 / 2 + I, gJ = y0 / 2 + J;
-        if (gI >= nc || gJ >= nc) continue;
-        const double *d0 = &S.t[2 * J - FR_TOY][2 * I + 1 - FR_TOX];   // row 2J (fine y = 2J), column 2I+1
-        const double *d1 = d0 + FR_TW, *d2 = d1 + FR_TW;
-        const double rd0 = d0[-1] + d0[1], rd1 = d1[-1] + d1[1], rd2 = d2[-1] + d2[1];
-        const double fd = rd1 + (d0[0] + d2[0]);
-        const double ed = rd0 + rd2;
-        bc[(long long)gJ * pitch_c + gI] = ((4.0 * d1[0] + 2.0 * fd) + ed) * 0.0625;
-    }
+    // defect d = b - S u'' and full weighting in registers (no smem round trip): warp (chunk,
+    // band) computes d on local columns [30*chunk, 30*chunk + 32) and rows 4*band .. 4*band + 4,
+    // takes the x-pair sums d(x-1) + d(x+1) by shuffles and emits the coarse points of fine rows
+    // 4*band + 1 and 4*band + 3 at its odd columns (chunk 0: 1..29, chunk 1: 31..57).
+    fr_defect_fw(S, x0, y0, nc, pitch_c, c, bc);
 }
 
 // ---------------------------------------------------------------------------------------------
