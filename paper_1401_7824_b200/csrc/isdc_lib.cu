@@ -52,7 +52,7 @@ struct isdc_ctx {
     double *Gp = nullptr;      // forcing profile (pitched)
     double *Fs[2][ISDC_MAXM];  // stored f^E(u_j) per iterate set (3D CD4 fast path), Fs[*][0] shared
     double *FT = nullptr;      // f^E of the isdc_rhs staging buffer T
-    double *FA[ISDC_MAXM], *WB[ISDC_MAXM];   // RHS folds of the next sweep (3D CD4)
+    double *FA[ISDC_MAXM] = {}, *WB[ISDC_MAXM] = {};   // RHS folds of the next sweep
     double *RT[ISDC_MAXM];     // residual_kind 1: weighted residual fields r~_m (m = 1..M-1 at RT[m-1])
     double *WX = nullptr;      // residual_kind 1: W-solve iterate
     long wcyc = 0;             // W-cycles since the last step start
@@ -286,6 +286,14 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
             if (h) { h->FA[q] = fa; h->WB[q] = wb; }
         }
     }
+    // RHS folds w_q (2D streaming path, forcing / no f^E): M-1 fields
+    if (d == 2 && !per && n >= 63 && (M == 3 || M == 5) &&
+        (p->fe == ISDC_FE_NONE || p->fe == ISDC_FE_FORCING) && p->residual_kind == 0) {
+        for (int q = 0; q + 1 < M; ++q) {
+            double *wb = (double *)take(fe);
+            if (h) { h->WB[q] = wb; h->FA[q] = nullptr; }
+        }
+    }
     // coarse levels
     int nl = 0;
     for (int m = n; m >= coarsest(per); m = coarser(m, per)) ++nl;
@@ -480,7 +488,15 @@ bool need_F(const isdc_ctx *h) {
     return h->d == 3 && h->fe.kind == 3 && (use_fast3d(h, 0, 8) || use_fast3d(h, 0, 16));
 }
 // the residual passes store the next sweep's RHS folds (3D CD4 fast RHS and residual both on)
-bool folds_on(const isdc_ctx *h) { return need_F(h) && use_fast3d(h, 0, 8) && use_fast3d(h, 0, 16) && h->folds; }
+bool stream2d_ok(const isdc_ctx *h);
+// 2D: the streaming residual stores w_q for the streaming RHS (f^E none / forcing, weighted residual)
+bool folds2d_on(const isdc_ctx *h) {
+    return h->folds && h->d == 2 && stream2d_ok(h) && (h->fe.kind == 0 || h->fe.kind == 2) &&
+           h->P.residual_kind == 0 && h->WB[0] != nullptr;
+}
+bool folds_on(const isdc_ctx *h) {
+    return (need_F(h) && use_fast3d(h, 0, 8) && use_fast3d(h, 0, 16) && h->folds) || folds2d_on(h);
+}
 
 isdc_status launch_alpha(isdc_ctx *h, const double *field, int slot);
 
@@ -941,11 +957,19 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         ++h->launches;
         int pe = prof_begin(h, PROF_RHS);
         const int fe = h->fe.kind;
+        const bool fold = fold_ok && folds2d_on(h);
+        A.wfold = fold ? h->WB[m] : nullptr;
 #define ISDC_RS(FE_, M_) kl(h, f2d::k_rhs_s<FE_, M_>, grd, f2d::SW_NT, 0)(A)
-        if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
+#define ISDC_RSF(FE_, M_) kl(h, f2d::k_rhs_s<FE_, M_, true>, grd, f2d::SW_NT, 0)(A)
+        if (fold) {
+            if (M == 3) { if (fe == 0) ISDC_RSF(0, 3); else ISDC_RSF(2, 3); }
+            else { if (fe == 0) ISDC_RSF(0, 5); else ISDC_RSF(2, 5); }
+        } else if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
         else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
 #undef ISDC_RS
-        prof_end(h, pe, PROF_RHS, (M + 2 + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, h->lev[0].g));
+#undef ISDC_RSF
+        // algorithmic bytes: the node fields read (folds: w_m, unew [, G]) and b written
+        prof_end(h, pe, PROF_RHS, ((fold ? 3 : M + 2) + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, h->lev[0].g));
         LAUNCH_CHECK(h);
         return ISDC_OK;
     }
@@ -1116,6 +1140,18 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         for (int j = 0; j < ISDC_MAXM; ++j) A.rt[j] = nullptr;
         if (h->P.residual_kind == 1)
             for (int m = 1; m < M; ++m) A.rt[m - 1] = h->RT[m - 1];
+        const bool wfo = write_folds && folds2d_on(h);
+        A.wfold = nullptr;
+        for (int q = 0; q < ISDC_MAXM; ++q) A.wf[q] = nullptr;
+        if (wfo) {
+            const double nu = h->P.nu;
+            for (int q = 0; q + 1 < M; ++q) {
+                for (int j = 0; j < M; ++j) A.fb[q][j] = nudt * h->S[q * M + j];
+                const double dtm = dt * h->dtau[q];
+                A.fgm[q] = nu * dtm;
+                A.wf[q] = h->WB[q];
+            }
+        }
         dim3 grd = stream2d_grid(h, A.yc);
         if (M == 5) {   // two warps per strip (2 nodes each): 4 strips per CTA
             const int strips = (h->n + f2d::SW_OUT - 1) / f2d::SW_OUT;
@@ -1129,9 +1165,15 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         if (h->P.residual_kind == 1) kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), true>, grd, f2d::SW_NT, 0)(A); \
         else kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), false>, grd, f2d::SW_NT, 0)(A);                       \
     } while (0)
-        if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
+#define ISDC_RSW(FE_, M_) kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), false, true>, grd, f2d::SW_NT, 0)(A)
+        if (wfo) {
+            if (M == 3) { if (fe == 0) ISDC_RSW(0, 3); else ISDC_RSW(2, 3); }
+            else { if (fe == 0) ISDC_RSW(0, 5); else ISDC_RSW(2, 5); }
+        } else if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
         else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
 #undef ISDC_RS
+#undef ISDC_RSW
+        // algorithmic bytes: the node fields (+G) read; the folds are implementation traffic
         prof_end(h, pe, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
         LAUNCH_CHECK(h);
         return ISDC_OK;

@@ -530,6 +530,12 @@ struct StreamArgs {
     double *out;                    // RHS b
     unsigned long long *slot;       // RHS: ||b|| (optional); residual: per-node slots slot[m-1]
     double *rt[ISDC_MAXM];          // residual: r~_m fields at rt[m-1] (unweighted residual), or null
+    // RHS folds of the next sweep: the residual pass also stores
+    // w_q = sum_j (nu dt S_qj) u_j - (nu dt dtau_q) u_{q+1} for q = 0..M-2 at wf[q]; the RHS of
+    // substep q then reads w_q instead of the M node fields
+    double fb[ISDC_MAXM][ISDC_MAXM], fgm[ISDC_MAXM];
+    double *wf[ISDC_MAXM];
+    const double *wfold;            // RHS from folds: w_m
 };
 
 // fields loaded per row: u_0..u_{M-1}, [unew], [G], [u_{m+1}, u_m: L1 hits of the first M, loaded
@@ -539,6 +545,12 @@ template <int MODE, int FE, int MM>
 __device__ __forceinline__ void stream_load(const StreamArgs &A, long long off, bool in, double (&L)[MM + 4]) {
 #pragma unroll
     for (int j = 0; j < MM; ++j) L[j] = in ? __ldcs(A.u[j] + off) : 0.0;
+    if (MODE == 2) {               // RHS from folds: w_m, unew [, G]
+        L[0] = in ? __ldcs(A.wfold + off) : 0.0;
+        L[MM + SL_UN] = in ? __ldcs(A.unew + off) : 0.0;
+        if (FE == 2) L[MM + SL_G] = in ? __ldg(A.G + off) : 0.0;
+        return;
+    }
     if (MODE == 0) {
         L[MM + SL_UN] = in ? __ldcs(A.unew + off) : 0.0;
         L[MM + SL_UO1] = in ? __ldg(A.u[A.m + 1] + off) : 0.0;
@@ -549,6 +561,28 @@ __device__ __forceinline__ void stream_load(const StreamArgs &A, long long off, 
 
 template <int FE>
 __device__ __forceinline__ double fe_of(double u) { return u - (u * u) * u; }   // FE == 1
+
+// v, w of substep m from the stored fold w_m (same trees as rhs_row, w read instead of formed)
+template <int FE, int MM>
+__device__ __forceinline__ void rhs_row_fold(const StreamArgs &A, const double (&L)[MM + 4], bool in, double &v,
+                                             double &w) {
+    static_assert(FE == 0 || FE == 2, "folds carry w only: f^E must be pointwise in x (none / forcing)");
+    const int m = A.m;
+    w = L[0];
+    const double un = L[MM + SL_UN];
+    if (FE == 0) {
+        v = un;
+    } else {
+        const double g = L[MM + SL_G];
+        double fa = A.a[0][0] * (g * A.ct[0]);
+#pragma unroll
+        for (int j = 1; j < MM; ++j)
+            fa = fa + A.a[0][j] * (g * A.ct[j]);
+        const double fn = g * A.ct[m], fo = g * A.ct[m];
+        v = (un + A.dtm * (fn - fo)) + fa;
+    }
+    if (!in) { v = 0.0; w = 0.0; }
+}
 
 template <int FE, int MM>
 __device__ __forceinline__ void rhs_row(const StreamArgs &A, const double (&L)[MM + 4], bool in, double &v, double &w) {
@@ -588,7 +622,7 @@ __device__ __forceinline__ void rhs_row(const StreamArgs &A, const double (&L)[M
     if (!in) { v = 0.0; w = 0.0; }
 }
 
-template <int FE, int MM>
+template <int FE, int MM, bool FOLD = false>
 __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
     pdl_launch();
     pdl_wait();
@@ -606,7 +640,7 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
     auto rowoff = [&](int y) { return (long long)y * A.pitch + x; };
     auto load = [&](int it, double (&dst)[MM + 4]) {
         const int y = y0 - 1 + it;
-        stream_load<0, FE, MM>(A, rowoff(y), xin && y >= 0 && y < n && it < nit, dst);
+        stream_load<FOLD ? 2 : 0, FE, MM>(A, rowoff(y), xin && y >= 0 && y < n && it < nit, dst);
     };
     load(0, L[0]);
     load(1, L[1]);
@@ -617,7 +651,8 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
         const int y = y0 - 1 + it;
         const bool in = xin && y >= 0 && y < n;
         double v, w;
-        rhs_row<FE, MM>(A, L[k], in, v, w);
+        if constexpr (FOLD) rhs_row_fold<FE, MM>(A, L[k], in, v, w);
+        else rhs_row<FE, MM>(A, L[k], in, v, w);
         vq[k] = v; wq[k] = w;
         vr[k] = shfl_up1(v) + shfl_dn1(v);
         wr[k] = shfl_up1(w) + shfl_dn1(w);
@@ -645,8 +680,8 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
 // r~_m = B p_m - L z_m, per-node max into slot[m-1].  The M-1 nodes are split over G = (M-1)/NMW
 // warps per strip (NMW nodes each; the extra loads of the same rows hit L1/L2), which halves the
 // register rings and doubles the resident warps.
-template <int FE, int MM, int NMW, bool WRT = false>   // WRT: also store the r~_m fields (unweighted residual)
-__global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {
+template <int FE, int MM, int NMW, bool WRT = false, bool WF = false>   // WRT: also store the r~_m fields (unweighted
+__global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {              // residual); WF: the next sweep's RHS folds
     pdl_launch();
     pdl_wait();
     constexpr int G = (MM - 1) / NMW;
@@ -688,6 +723,18 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {
             const double g = L[k][MM + SL_G];
 #pragma unroll
             for (int j = 0; j < MM; ++j) fj[j] = g * A.ct[j];
+        }
+        if (WF && in && xout && y >= y0 && y < y1) {
+            // this warp's folds q in [m0 - 1, m0 - 1 + NMW): w_q = sum_j fb_qj u_j - fgm_q u_{q+1}
+            // (q unrolled over all folds and selected per warp, so every index is compile-time)
+#pragma unroll
+            for (int q = 0; q + 1 < MM; ++q) {
+                if (q < m0 - 1 || q >= m0 - 1 + NMW) continue;
+                double acc = A.fb[q][0] * uj[0];
+#pragma unroll
+                for (int j = 1; j < MM; ++j) acc = acc + A.fb[q][j] * uj[j];
+                __stcs(A.wf[q] + rowoff(y), acc - A.fgm[q] * uj[q + 1]);   // read again only by the next sweep
+            }
         }
 #pragma unroll
         for (int mm = 0; mm < NMW; ++mm) {
