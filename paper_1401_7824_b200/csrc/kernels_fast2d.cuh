@@ -96,33 +96,43 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
 
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
     double dmax = 0.0;
-    // ---- sweep 1, main columns 0..63 of the t region (rows -1..32, 4 bands of 9 rows)
+    // ---- sweep 1, main columns 0..63 of the t region (rows -1..TY, 4 bands of SB1 rows).  Row
+    // pointers and three rotating register roles per 3-row step: no index arithmetic and no
+    // register moves per row (the loop is issue-bound).
     {
         const int band = w >> 1, hh = w & 1;
         const int rs = -1 + SB1 * band, re = min(rs + SB1, TY + 1);
-        {
-            const int x = lane + 32 * hh;          // tile column; u smem col x+2
-            const int gx = x0 + x;
-            const bool xin = gx < n;
-            double um = S.u[rs + 1][x + 2];         // row rs-1
-            double rm = S.u[rs + 1][x + 1] + S.u[rs + 1][x + 3];
-            double uc = S.u[rs + 2][x + 2];         // row rs
-            double rc = S.u[rs + 2][x + 1] + S.u[rs + 2][x + 3];
-            for (int y = rs; y < re; ++y) {
-                double up = S.u[y + 3][x + 2];
-                double rp = S.u[y + 3][x + 1] + S.u[y + 3][x + 3];
-                double f = rc + (um + up);
-                double e = rm + rp;
-                double su = (c0 * uc + c1 * f) + c2 * e;
-                int gy = y0 + y;
-                bool in = xin && gy >= 0 && gy < n;
-                double bv = S.b[y + 1][x + 2];
-                double d = bv - su;
-                if (NORM && in && y >= 0 && y < TY) dmax = amax(dmax, fabs(d));
-                S.t[y + 1][x + 1] = in ? uc + wd * d : 0.0;
-                um = uc; uc = up; rm = rc; rc = rp;
-            }
+        const int x = lane + 32 * hh;              // tile column; u smem col x+2
+        const bool xin = x0 + x < n;
+        const double *sp = &S.u[rs + 1][x + 2];    // row rs-1
+        double qa = sp[0], ra = sp[-1] + sp[1];
+        sp += UW;
+        double qb = sp[0], rb = sp[-1] + sp[1];    // row rs
+        double qc, rc;
+        const double *bp = &S.b[rs + 1][x + 2];
+        double *tp = &S.t[rs + 1][x + 1];
+        int y = rs, gy = y0 + rs;
+#define ISDC_S1_ROW(QM, QC, QN, RM, RC, RN)                                                  \
+        {                                                                                    \
+            sp += UW;                                                                        \
+            QN = sp[0]; RN = sp[-1] + sp[1];                                                 \
+            const double f = RC + (QM + QN);                                                 \
+            const double e = RM + RN;                                                        \
+            const double su = (c0 * QC + c1 * f) + c2 * e;                                   \
+            const bool in = xin && (unsigned)gy < (unsigned)n;                               \
+            const double d = *bp - su;                                                       \
+            if (NORM && in && y >= 0 && y < TY) dmax = amax(dmax, fabs(d));                 \
+            *tp = in ? QC + wd * d : 0.0;                                                    \
+            bp += BW; tp += TW; ++y; ++gy;                                                   \
         }
+        while (y + 3 <= re) {
+            ISDC_S1_ROW(qa, qb, qc, ra, rb, rc)
+            ISDC_S1_ROW(qb, qc, qa, rb, rc, ra)
+            ISDC_S1_ROW(qc, qa, qb, rc, ra, rb)
+        }
+        if (y < re) ISDC_S1_ROW(qa, qb, qc, ra, rb, rc)
+        if (y < re) ISDC_S1_ROW(qb, qc, qa, rb, rc, ra)
+#undef ISDC_S1_ROW
     }
     // ---- sweep 1, halo columns -1 and 64 (rows -1..32): 68 points, direct 9-point reads
     if (tid < 2 * TH) {
@@ -145,29 +155,39 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
     }
     if (NORM) block_max_to(slot, dmax);  // contains a __syncthreads
     __syncthreads();
-    // ---- sweep 2 on the 64 x 32 tile (4 bands of 8 rows)
+    // ---- sweep 2 on the 64 x TY tile (4 bands of SB2 rows), same row-pointer / rotating form
     {
         const int band = w >> 1, hh = w & 1;
         const int rs = SB2 * band, re = rs + SB2;
-        {
-            const int x = lane + 32 * hh;          // t smem col x+1
-            const int gx = x0 + x;
-            double tm = S.t[rs][x + 1];             // row rs-1
-            double rm = S.t[rs][x] + S.t[rs][x + 2];
-            double tc = S.t[rs + 1][x + 1];
-            double rc = S.t[rs + 1][x] + S.t[rs + 1][x + 2];
-            for (int y = rs; y < re; ++y) {
-                double tp = S.t[y + 2][x + 1];
-                double rp = S.t[y + 2][x] + S.t[y + 2][x + 2];
-                double f = rc + (tm + tp);
-                double e = rm + rp;
-                double su = (c0 * tc + c1 * f) + c2 * e;
-                double v = tc + wd * (S.b[y + 1][x + 2] - su);
-                int gy = y0 + y;
-                if (gx < n && gy < n) out[(long long)gy * pitch + gx] = v;
-                tm = tc; tc = tp; rm = rc; rc = rp;
-            }
+        const int x = lane + 32 * hh;              // t smem col x+1
+        const int gx = x0 + x;
+        const double *sp = &S.t[rs][x + 1];        // row rs-1
+        double qa = sp[0], ra = sp[-1] + sp[1];
+        sp += TW;
+        double qb = sp[0], rb = sp[-1] + sp[1];    // row rs
+        double qc, rc;
+        const double *bp = &S.b[rs + 1][x + 2];
+        double *gp = out + (long long)(y0 + rs) * pitch + gx;
+        int gy = y0 + rs, y = rs;
+#define ISDC_S2_ROW(QM, QC, QN, RM, RC, RN)                                                  \
+        {                                                                                    \
+            sp += TW;                                                                        \
+            QN = sp[0]; RN = sp[-1] + sp[1];                                                 \
+            const double f = RC + (QM + QN);                                                 \
+            const double e = RM + RN;                                                        \
+            const double su = (c0 * QC + c1 * f) + c2 * e;                                   \
+            const double v = QC + wd * (*bp - su);                                           \
+            if (gx < n && gy < n) *gp = v;                                                   \
+            bp += BW; gp += pitch; ++gy; ++y;                                                \
         }
+        while (y + 3 <= re) {
+            ISDC_S2_ROW(qa, qb, qc, ra, rb, rc)
+            ISDC_S2_ROW(qb, qc, qa, rb, rc, ra)
+            ISDC_S2_ROW(qc, qa, qb, rc, ra, rb)
+        }
+        if (y < re) ISDC_S2_ROW(qa, qb, qc, ra, rb, rc)
+        if (y < re) ISDC_S2_ROW(qb, qc, qa, rb, rc, ra)
+#undef ISDC_S2_ROW
     }
 }
 
