@@ -74,7 +74,8 @@ struct isdc_ctx {
     bool pdl = false;          // ISDC_PDL=1: programmatic dependent launch (measured neutral with the implicit
                                // trigger, slower with an early trigger)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
-    bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
+    bool sr_stream = false;
+    int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using 32-row k_smooth2r tiles    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
@@ -611,16 +612,25 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
         LAUNCH_CHECK(h);
         return ISDC_OK;
     }
-    const CUtensorMap *mb = tmap(h, b, g, f2d::FR_BW, f2d::FR_BH);
-    const CUtensorMap *mu = in ? tmap(h, in, g, f2d::FR_UW, f2d::FR_UH) : mb;
+    // 32-row tiles on the large levels, 16-row tiles where more CTAs matter (ISDC_SR_TY32_MIN)
+    const bool t32 = g.n >= h->sr_ty32_min;
+    const int TY = t32 ? 32 : 16;
+    const CUtensorMap *mb = tmap(h, b, g, f2d::FR_BW, TY + 5);
+    const CUtensorMap *mu = in ? tmap(h, in, g, f2d::FR_UW, TY + 7) : mb;
     if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
     const int cls = level == 0 ? PROF_RESTRICT : PROF_COARSE;
     int pe = prof_begin(h, cls);
-    dim3 grd((g.n + f2d::FR_TX - 1) / f2d::FR_TX, (g.n + f2d::FR_TY - 1) / f2d::FR_TY);
-    size_t sm = sizeof(f2d::SmemSR) + 128;
-    if (in) kl(h, f2d::k_smooth2r<0>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    else kl(h, f2d::k_smooth2r<1>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    dim3 grd((g.n + f2d::FR_TX - 1) / f2d::FR_TX, (g.n + TY - 1) / TY);
+    if (t32) {
+        size_t sm = sizeof(f2d::SmemSR<32>) + 128;
+        if (in) kl(h, f2d::k_smooth2r<0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+        else kl(h, f2d::k_smooth2r<1, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    } else {
+        size_t sm = sizeof(f2d::SmemSR<16>) + 128;
+        if (in) kl(h, f2d::k_smooth2r<0, 16>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+        else kl(h, f2d::k_smooth2r<1, 16>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    }
     // algorithmic bytes: read u (unless zero), b; write u'', b_c
     prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + 2.0) * npts_of(h, g));
     LAUNCH_CHECK(h);
@@ -1491,6 +1501,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *t2 = getenv("ISDC_TAIL2D")) h->tail2d = atoi(t2);
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
     if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
+    if (const char *st = getenv("ISDC_SR_TY32_MIN")) h->sr_ty32_min = atoi(st);
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) { int v = atoi(sr); h->smooth3d_rows = (v == 2 || v == 3 || v == 4) ? v : 0; }
     {
@@ -1509,10 +1520,14 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSmooth) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSmooth) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<16>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<16>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<0, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<32>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<32>) + 128);
         cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemRestrict) + 128);
         cudaFuncSetAttribute(f3d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::R_SMEM);

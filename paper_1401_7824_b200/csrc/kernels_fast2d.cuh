@@ -812,22 +812,28 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {           
 // u'' overwrites the u buffer after sweep 1, d overwrites the t buffer after sweep 2.
 // MODE 0: u from memory; MODE 1: u == 0 (nothing read).
 // ---------------------------------------------------------------------------------------------
-constexpr int FR_TX = 58, FR_TY = 16, FR_CX = 29, FR_CY = FR_TY / 2;
-constexpr int FR_UW = 66, FR_UH = FR_TY + 7, FR_UOX = -4, FR_UOY = -3;
-constexpr int FR_BW = 64, FR_BH = FR_TY + 5, FR_BOX = -2, FR_BOY = -2;
-constexpr int FR_TW = 64, FR_TH = FR_TY + 5, FR_TOX = -2, FR_TOY = -2;
+// Tile height TY (rows): 32 on the large levels (half the band-start loads per output of 16-row
+// tiles; ~58 KB -> 3 CTAs/SM), 16 on the small ones (more CTAs).  FR_TY16 / FR_TY32 below.
+constexpr int FR_TX = 58, FR_CX = 29;
+constexpr int FR_UW = 66, FR_UOX = -4, FR_UOY = -3;
+constexpr int FR_BW = 64, FR_BOX = -2, FR_BOY = -2;
+constexpr int FR_TW = 64, FR_TOX = -2, FR_TOY = -2;
+template <int TY> struct SRT {
+    static constexpr int UH = TY + 7, BH = TY + 5, TH = TY + 5, CY = TY / 2;
+};
 
+template <int TY>
 struct __align__(128) SmemSR {
-    alignas(128) double u[FR_UH][FR_UW];
-    alignas(128) double b[FR_BH][FR_BW];
-    alignas(128) double t[FR_TH][FR_TW];
+    alignas(128) double u[SRT<TY>::UH][FR_UW];
+    alignas(128) double b[SRT<TY>::BH][FR_BW];
+    alignas(128) double t[SRT<TY>::TH][FR_TW];
     uint64_t bar;
 };
 
 // one stencil phase over the region [xs, xs+w) x [ys, ys+h): 2 column chunks of 32 lanes x 4 row
 // bands, one (chunk, band) per warp, rolling a 3-row register window down each column.
 // src/dst are arrays with origins (sox, soy) / (dox, doy) and row lengths sw / dw.
-template <int KIND, int SW_, int DW_>
+template <int KIND, int SW_, int DW_, int FR_TY>
 __device__ __forceinline__ void fr_phase(const double *__restrict__ src, int sox, int soy, double *__restrict__ dst,
                                          int dox, int doy, const double *__restrict__ B, int xs, int w, int ys,
                                          int h, int x0, int y0, int n, const SCoef &c, double *__restrict__ gout,
@@ -882,12 +888,14 @@ __device__ __forceinline__ void fr_phase(const double *__restrict__ src, int sox
 
 // Same trees as the generic defect (apply_S) and fw_defect: rd = d(x-1) + d(x+1);
 // fd = rd1 + (d0 + d2); ed = rd0 + rd2; b_c = ((4 d1 + 2 fd) + ed) * 0.0625.
-__device__ __forceinline__ void fr_defect_fw(const SmemSR &S, int x0, int y0, int nc, int pitch_c, const SCoef &c,
+template <int FR_TY>
+__device__ __forceinline__ void fr_defect_fw(const SmemSR<FR_TY> &S, int x0, int y0, int nc, int pitch_c, const SCoef &c,
                                              double *__restrict__ bc) {
-    static_assert(FR_TY == 16 && NT == 256 && FR_TX == 58, "4 bands x 4 fine rows, 2 column chunks");
+    constexpr int BR = FR_TY / 4;   // fine rows per band (even)
+    static_assert(FR_TY % 8 == 0 && NT == 256 && FR_TX == 58, "4 bands x BR fine rows, 2 column chunks");
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int chunk = wp & 1, band = wp >> 1;
-    const int x = 30 * chunk + lane, r0 = 4 * band;
+    const int x = 30 * chunk + lane, r0 = BR * band;
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2;
     const double *sp = &S.u[r0 - 1 - FR_UOY][x - FR_UOX];
     const double *bp = &S.b[r0 - FR_BOY][x - FR_BOX];
@@ -898,7 +906,7 @@ __device__ __forceinline__ void fr_defect_fw(const SmemSR &S, int x0, int y0, in
     const int gI = x0 / 2 + (x - 1) / 2;
     double D0 = 0.0, R0 = 0.0, D1 = 0.0, R1 = 0.0;
 #pragma unroll
-    for (int yy = 0; yy < 5; ++yy) {
+    for (int yy = 0; yy <= BR; ++yy) {
         sp += FR_UW;
         const double qn = sp[0], rn = sp[-1] + sp[1];
         const double f = rc + (qm + qn);
@@ -906,7 +914,7 @@ __device__ __forceinline__ void fr_defect_fw(const SmemSR &S, int x0, int y0, in
         const double su = (c0 * qc + c1 * f) + c2 * e;
         const double d = bp[yy * FR_BW] - su;
         const double rd = __shfl_up_sync(0xffffffffu, d, 1) + __shfl_down_sync(0xffffffffu, d, 1);
-        if (yy == 2 || yy == 4) {          // rows r0 + yy - 2, -1, yy: coarse row J = (r0 + yy - 2) / 2
+        if (yy >= 2 && !(yy & 1)) {        // rows r0 + yy - 2, -1, yy: coarse row J = (r0 + yy - 2) / 2
             const int gJ = y0 / 2 + (r0 + yy - 2) / 2;
             if (xo && gI < nc && gJ < nc) {
                 const double fd = R1 + (D0 + d);
@@ -919,14 +927,15 @@ __device__ __forceinline__ void fr_defect_fw(const SmemSR &S, int x0, int y0, in
     }
 }
 
-template <int MODE>
+template <int MODE, int FR_TY = 16>
 __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtensorMap tu,
                                                  const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
                                                  double *__restrict__ bc, int n, int pitch, int nc, int pitch_c,
                                                  SCoef c) {
     pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    SmemSR &S = *reinterpret_cast<SmemSR *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+    using SR = SRT<FR_TY>;
+    SmemSR<FR_TY> &S = *reinterpret_cast<SmemSR<FR_TY> *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * FR_TX, y0 = blockIdx.y * FR_TY;
     if (tid == 0) {
@@ -938,22 +947,22 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
     __syncthreads();
     pdl_wait();   // only shared-memory setup above
     if (tid == 0) {
-        mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : FR_UW * FR_UH) + FR_BW * FR_BH) * 8);
+        mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : FR_UW * SR::UH) + FR_BW * SR::BH) * 8);
         if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 + FR_UOX, y0 + FR_UOY, &S.bar);
         tma_load_2d(&S.b[0][0], &tb, x0 + FR_BOX, y0 + FR_BOY, &S.bar);
     }
     if (MODE == 1) {
-        for (int q = tid; q < FR_UW * FR_UH; q += NT) (&S.u[0][0])[q] = 0.0;
+        for (int q = tid; q < FR_UW * SR::UH; q += NT) (&S.u[0][0])[q] = 0.0;
         __syncthreads();
     }
     mbar_wait(&S.bar, 0);
     const double *Bp = &S.b[0][0];
     // sweep 1: u -> t on [-2, 60] x [-2, 34]
-    fr_phase<0, FR_UW, FR_TW>(&S.u[0][0], FR_UOX, FR_UOY, &S.t[0][0], FR_TOX, FR_TOY, Bp, -2, 63, -2, FR_TY + 5, x0, y0, n,
+    fr_phase<0, FR_UW, FR_TW, FR_TY>(&S.u[0][0], FR_UOX, FR_UOY, &S.t[0][0], FR_TOX, FR_TOY, Bp, -2, 63, -2, FR_TY + 5, x0, y0, n,
                               c, nullptr, pitch);
     __syncthreads();
     // sweep 2: t -> u'' (into the u buffer) on [-1, 59] x [-1, 33]; the tile goes to global
-    fr_phase<1, FR_TW, FR_UW>(&S.t[0][0], FR_TOX, FR_TOY, &S.u[0][0], FR_UOX, FR_UOY, Bp, -1, 61, -1, FR_TY + 3, x0, y0, n,
+    fr_phase<1, FR_TW, FR_UW, FR_TY>(&S.t[0][0], FR_TOX, FR_TOY, &S.u[0][0], FR_UOX, FR_UOY, Bp, -1, 61, -1, FR_TY + 3, x0, y0, n,
                               c, out, pitch);
     __syncthreads();
     // defect d = b - S u'' and full weighting in registers (no smem round trip): warp (chunk,
