@@ -75,7 +75,8 @@ struct isdc_ctx {
                                // trigger, slower with an early trigger)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
     bool sr_stream = false;
-    int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using 32-row k_smooth2r tiles    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
+    int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using 32-row k_smooth2r tiles
+    int sm_ty32_min = 1 << 30; // ISDC_SM_TY32_MIN: smallest level n using 32-row k_smooth2 tiles (off: 48.4 vs 46.8 ms, cfg 3)    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
@@ -462,19 +463,30 @@ isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const 
 isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                            const SCoef &c, unsigned long long *norm_slot, int level, const double *e = nullptr,
                            const GridDesc *gc = nullptr) {
-    const CUtensorMap *mb = tmap(h, b, g, f2d::BW, f2d::BH);
-    const CUtensorMap *mu = in ? tmap(h, in, g, f2d::UW, f2d::UH) : mb;
-    const CUtensorMap *me = e ? tmap(h, e, *gc, f2d::EW, f2d::EH) : mb;
+    // 32-row tiles on the large levels (ISDC_SM_TY32_MIN), 16-row tiles below
+    const bool t32 = g.n >= h->sm_ty32_min;
+    const int TY = t32 ? 32 : 16;
+    const CUtensorMap *mb = tmap(h, b, g, f2d::BW, TY + 2);
+    const CUtensorMap *mu = in ? tmap(h, in, g, f2d::UW, TY + 4) : mb;
+    const CUtensorMap *me = e ? tmap(h, e, *gc, f2d::EW, TY / 2 + 3) : mb;
     if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
     const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
     int pe = prof_begin(h, cls);
-    dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + f2d::TY - 1) / f2d::TY);
-    size_t sm = sizeof(f2d::SmemSmooth) + 128;
-    if (norm_slot) kl(h, f2d::k_smooth2<true, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
-    else if (e) kl(h, f2d::k_smooth2<false, 2>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    else if (!in) kl(h, f2d::k_smooth2<false, 1>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    else kl(h, f2d::k_smooth2<false, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + TY - 1) / TY);
+    if (t32) {
+        size_t sm = sizeof(f2d::SmemSmoothT<32>) + 128;
+        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
+        else if (e) kl(h, f2d::k_smooth2<false, 2, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else if (!in) kl(h, f2d::k_smooth2<false, 1, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else kl(h, f2d::k_smooth2<false, 0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    } else {
+        size_t sm = sizeof(f2d::SmemSmooth) + 128;
+        if (norm_slot) kl(h, f2d::k_smooth2<true, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
+        else if (e) kl(h, f2d::k_smooth2<false, 2>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else if (!in) kl(h, f2d::k_smooth2<false, 1>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else kl(h, f2d::k_smooth2<false, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    }
     // algorithmic bytes: read u (unless zero), b (+ e / 4); write u''
     prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 2.0 : 0.0)) * npts_of(h, g));
     LAUNCH_CHECK(h);
@@ -1502,6 +1514,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
     if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
     if (const char *st = getenv("ISDC_SR_TY32_MIN")) h->sr_ty32_min = atoi(st);
+    if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) { int v = atoi(sr); h->smooth3d_rows = (v == 2 || v == 3 || v == 4) ? v : 0; }
     {
@@ -1520,6 +1533,10 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSmooth) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSmooth) + 128);
+        for (auto kern : {f2d::k_smooth2<true, 0, 32>, f2d::k_smooth2<false, 0, 32>, f2d::k_smooth2<false, 1, 32>,
+                          f2d::k_smooth2<false, 2, 32>})
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(f2d::SmemSmoothT<32>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSR<16>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -28,22 +28,28 @@ constexpr int TW = TX + 2, TH = TY + 2;
 // = the coarse zero ring), correction applied to every in-domain point of the u box.
 constexpr int EW = 36, EH = TY / 2 + 3;
 
-struct __align__(128) SmemSmooth {
-    alignas(128) double u[UH][UW];
-    alignas(128) double b[BH][BW];
-    alignas(128) double t[TH][TW];
-    alignas(128) double e[EH][EW];
+// tile height as a parameter: TY_ = 16 (above) or 32 on the large levels (fewer band starts)
+template <int TY_>
+struct __align__(128) SmemSmoothT {
+    alignas(128) double u[TY_ + 4][UW];
+    alignas(128) double b[TY_ + 2][BW];
+    alignas(128) double t[TY_ + 2][TW];
+    alignas(128) double e[TY_ / 2 + 3][EW];
     uint64_t bar;
 };
+using SmemSmooth = SmemSmoothT<TY>;
 
-template <bool NORM, int MODE = 0>
+template <bool NORM, int MODE = 0, int TY_ = 16>
 __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensorMap tu,
                                                 const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
                                                 int n, int pitch, SCoef c, unsigned long long *slot,
                                                 const __grid_constant__ CUtensorMap te) {
     pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    SmemSmooth &S = *reinterpret_cast<SmemSmooth *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    // the tile-height dependent sizes (shadow the 16-row namespace constants)
+    constexpr int TY = TY_, SB1 = (TY + 2 + 3) / 4, SB2 = TY / 4, UH = TY + 4, BH = TY + 2, TH = TY + 2;
+    constexpr int EH = TY / 2 + 3;
+    SmemSmoothT<TY_> &S = *reinterpret_cast<SmemSmoothT<TY_> *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     if (tid == 0) {

@@ -1,3 +1,3 @@
 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_table1.py -x -q -k "not cfg5" 2>&1 | tail -3 > gpurun_out/par.log
-for t in 2047 1023 4095; do ISDC_SR_TY32_MIN=$t python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3_$t.json 2>/dev/null; done
+for t in 2047 100000; do ISDC_SM_TY32_MIN=$t python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3_$t.json 2>/dev/null; done
 python bench.py --config 2 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b2.json 2>gpurun_out/b2.err
