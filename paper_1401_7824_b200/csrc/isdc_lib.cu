@@ -74,9 +74,9 @@ struct isdc_ctx {
     bool pdl = false;          // ISDC_PDL=1: programmatic dependent launch (measured neutral with the implicit
                                // trigger, slower with an early trigger)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
-    bool sr_stream = false;
+    bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using 32-row k_smooth2r tiles
-    int sm_ty32_min = 1 << 30; // ISDC_SM_TY32_MIN: smallest level n using 32-row k_smooth2 tiles (off: 48.4 vs 46.8 ms, cfg 3)    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
+    int sm_ty32_min = 1 << 30; // ISDC_SM_TY32_MIN: the same for k_smooth2 (off: 48.4 vs 46.8 ms per cfg-3 step)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
