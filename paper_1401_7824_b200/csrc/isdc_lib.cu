@@ -75,6 +75,7 @@ struct isdc_ctx {
                                // trigger, slower with an early trigger)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
     bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
+    int res_nmw = 2;           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using 32-row k_smooth2r tiles
     int sm_ty32_min = 1 << 30; // ISDC_SM_TY32_MIN: the same for k_smooth2 (off: 48.4 vs 46.8 ms per cfg-3 step)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
@@ -1175,24 +1176,29 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             }
         }
         dim3 grd = stream2d_grid(h, A.yc);
-        if (M == 5) {   // two warps per strip (2 nodes each): 4 strips per CTA
+        if (M == 5) {   // ISDC_RES_NMW nodes per warp (2: 4 strips per CTA; 1: 2 strips per CTA)
             const int strips = (h->n + f2d::SW_OUT - 1) / f2d::SW_OUT;
-            grd.x = (strips + 3) / 4;
+            grd.x = h->res_nmw == 1 ? (strips + 1) / 2 : (strips + 3) / 4;
         }
         ++h->launches;
         int pe = prof_begin(h, PROF_RESID);
         const int fe = h->fe.kind;
 #define ISDC_RS(FE_, M_)                                                                                \
     do {                                                                                                \
-        if (h->P.residual_kind == 1) kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), true>, grd, f2d::SW_NT, 0)(A); \
-        else kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), false>, grd, f2d::SW_NT, 0)(A);                       \
+        if (h->P.residual_kind == 1) kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? RNMW : M_ - 1), true>, grd, f2d::SW_NT, 0)(A); \
+        else kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? RNMW : M_ - 1), false>, grd, f2d::SW_NT, 0)(A);                       \
     } while (0)
-#define ISDC_RSW(FE_, M_) kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? 2 : M_ - 1), false, true>, grd, f2d::SW_NT, 0)(A)
-        if (wfo) {
-            if (M == 3) { if (fe == 0) ISDC_RSW(0, 3); else ISDC_RSW(2, 3); }
-            else { if (fe == 0) ISDC_RSW(0, 5); else ISDC_RSW(2, 5); }
-        } else if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
-        else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
+#define ISDC_RSW(FE_, M_) kl(h, f2d::k_resid_s<FE_, M_, (M_ == 5 ? RNMW : M_ - 1), false, true>, grd, f2d::SW_NT, 0)(A)
+        auto dispatch = [&](auto NMWc) {
+            constexpr int RNMW = decltype(NMWc)::value;
+            if (wfo) {
+                if (M == 3) { if (fe == 0) ISDC_RSW(0, 3); else ISDC_RSW(2, 3); }
+                else { if (fe == 0) ISDC_RSW(0, 5); else ISDC_RSW(2, 5); }
+            } else if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
+            else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
+        };
+        if (h->res_nmw == 1) dispatch(std::integral_constant<int, 1>{});
+        else dispatch(std::integral_constant<int, 2>{});
 #undef ISDC_RS
 #undef ISDC_RSW
         // algorithmic bytes: the node fields (+G) read; the folds are implementation traffic
@@ -1514,6 +1520,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
     if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
     if (const char *st = getenv("ISDC_SR_TY32_MIN")) h->sr_ty32_min = atoi(st);
+    if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
     if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) { int v = atoi(sr); h->smooth3d_rows = (v == 2 || v == 3 || v == 4) ? v : 0; }

@@ -707,19 +707,22 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
 // warps per strip (NMW nodes each; the extra loads of the same rows hit L1/L2), which halves the
 // register rings and doubles the resident warps.
 template <int FE, int MM, int NMW, bool WRT = false, bool WF = false>   // WRT: also store the r~_m fields (unweighted
-__global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {              // residual); WF: the next sweep's RHS folds
+__global__ void __launch_bounds__(SW_NT, NMW == 1 ? 3 : 2) k_resid_s(StreamArgs A) {              // residual); WF: the next sweep's RHS folds
     pdl_launch();
     pdl_wait();
     constexpr int G = (MM - 1) / NMW;
     const int wid = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32 / G) + wid / G;
-    const int m0 = 1 + NMW * (wid % G);
     const int n = A.n;
     const int x = strip * SW_OUT - 1 + lane;
     if (strip * SW_OUT >= n) return;
     const int y0 = blockIdx.y * A.yc, y1 = min(y0 + A.yc, n);
     const bool xin = x >= 0 && x < n, xout = lane >= 1 && lane <= SW_OUT && x < n;
     const BLConst c = A.bl;
+    // the warp's node group (role) is a compile-time constant inside `run`, so every node / fold
+    // index below is an immediate (coefficients straight from the constant bank, no selects)
+    auto run = [&](auto ROLE) {
+    constexpr int m0 = 1 + NMW * decltype(ROLE)::value;
     double L[3][MM + 4];
     double pq[NMW][3], pr[NMW][3], zq[NMW][3], zr[NMW][3];
     double rmax[NMW];
@@ -755,7 +758,7 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {           
             // (q unrolled over all folds and selected per warp, so every index is compile-time)
 #pragma unroll
             for (int q = 0; q + 1 < MM; ++q) {
-                if (q < m0 - 1 || q >= m0 - 1 + NMW) continue;
+                if (q < m0 - 1 || q >= m0 - 1 + NMW) continue;   // compile-time
                 double acc = A.fb[q][0] * uj[0];
 #pragma unroll
                 for (int j = 1; j < MM; ++j) acc = acc + A.fb[q][j] * uj[j];
@@ -806,6 +809,12 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {           
         unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(rmax[mm]));
         if (lane == 0 && v) atomicMax(A.slot + m0 - 1 + mm, v);
     }
+    };
+    const int role = wid % G;
+    if (role == 0) run(std::integral_constant<int, 0>{});
+    if constexpr (G > 1) { if (role == 1) run(std::integral_constant<int, 1>{}); }
+    if constexpr (G > 2) { if (role == 2) run(std::integral_constant<int, 2>{}); }
+    if constexpr (G > 3) { if (role == 3) run(std::integral_constant<int, 3>{}); }
 }
 
 // ---------------------------------------------------------------------------------------------

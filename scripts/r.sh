@@ -1,3 +1,4 @@
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_table1.py -x -q -k "not cfg5" 2>&1 | tail -3 > gpurun_out/par.log
-for t in 2047 100000; do ISDC_SM_TY32_MIN=$t python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3_$t.json 2>/dev/null; done
-python bench.py --config 2 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b2.json 2>gpurun_out/b2.err
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "not cfg5" 2>&1 | tail -3 > gpurun_out/par.log
+ISDC_RES_NMW=1 python -m pytest tests/test_gpu_fullsize.py -x -q -k "cfg3" 2>&1 | tail -2 >> gpurun_out/par.log
+python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3.json 2>gpurun_out/b3.err
+ISDC_RES_NMW=1 python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3_n1.json 2>gpurun_out/b3.err
