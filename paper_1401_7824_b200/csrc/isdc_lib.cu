@@ -76,7 +76,8 @@ struct isdc_ctx {
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
     bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
     int res_nmw = 2;           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
-    int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using 32-row k_smooth2r tiles
+    int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
+    int sr_ty = 32;            // ISDC_SR_TY: their height (24 or 32)
     int sm_ty32_min = 1 << 30; // ISDC_SM_TY32_MIN: the same for k_smooth2 (off: 48.4 vs 46.8 ms per cfg-3 step)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
@@ -627,7 +628,7 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
     }
     // 32-row tiles on the large levels, 16-row tiles where more CTAs matter (ISDC_SR_TY32_MIN)
     const bool t32 = g.n >= h->sr_ty32_min;
-    const int TY = t32 ? 32 : 16;
+    const int TY = t32 ? h->sr_ty : 16;
     const CUtensorMap *mb = tmap(h, b, g, f2d::FR_BW, TY + 5);
     const CUtensorMap *mu = in ? tmap(h, in, g, f2d::FR_UW, TY + 7) : mb;
     if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
@@ -635,10 +636,14 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
     const int cls = level == 0 ? PROF_RESTRICT : PROF_COARSE;
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::FR_TX - 1) / f2d::FR_TX, (g.n + TY - 1) / TY);
-    if (t32) {
+    if (TY == 32) {
         size_t sm = sizeof(f2d::SmemSR<32>) + 128;
         if (in) kl(h, f2d::k_smooth2r<0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
         else kl(h, f2d::k_smooth2r<1, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    } else if (TY == 24) {
+        size_t sm = sizeof(f2d::SmemSR<24>) + 128;
+        if (in) kl(h, f2d::k_smooth2r<0, 24>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+        else kl(h, f2d::k_smooth2r<1, 24>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
     } else {
         size_t sm = sizeof(f2d::SmemSR<16>) + 128;
         if (in) kl(h, f2d::k_smooth2r<0, 16>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
@@ -1520,6 +1525,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
     if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
     if (const char *st = getenv("ISDC_SR_TY32_MIN")) h->sr_ty32_min = atoi(st);
+    if (const char *st = getenv("ISDC_SR_TY")) h->sr_ty = atoi(st) == 24 ? 24 : 32;
     if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
     if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
@@ -1548,6 +1554,10 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSR<16>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSR<16>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<0, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<24>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<1, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<24>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<0, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSR<32>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,

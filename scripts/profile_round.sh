@@ -7,7 +7,7 @@ B3="python bench.py --config 3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 B5="python bench.py --config 5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 $B3 > gpurun_out/prof_${TAG}_cfg3_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -s 2000 -c 400 --csv --log-file gpurun_out/prof_${TAG}_cfg3_launches.csv $B3 > /dev/null 2>&1 && \
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_smooth2r<.int.0>" -s 2 -c 1 -o gpurun_out/prof_${TAG}_cfg3 $B3 > gpurun_out/prof_${TAG}_cfg3_ncu.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_smooth2r<.int.0," -s 2 -c 1 -o gpurun_out/prof_${TAG}_cfg3 $B3 > gpurun_out/prof_${TAG}_cfg3_ncu.log 2>&1
 echo "cfg3 rc=$?" >> gpurun_out/prof_${TAG}_rc.log
 $B5 > gpurun_out/prof_${TAG}_cfg5_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv --log-file gpurun_out/prof_${TAG}_cfg5_launches.csv $B5 > /dev/null 2>&1 && \
