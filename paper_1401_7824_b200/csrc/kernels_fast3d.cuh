@@ -592,6 +592,47 @@ __device__ __forceinline__ void bl_point(const BLArgs &A, int k, const double *F
     }
 }
 
+// Residual pass at one point (MODE 1, f^E none or stored CD4): every node field u_j and F_j is read
+// from the stage ONCE and streamed, in ascending j, into the left folds of all NM nodes and of the
+// next sweep's RHS folds -- the same trees as bl_point + the fold code (each accumulator is
+// c_0 x_0, then acc + c_j x_j for j = 1..M-1), with M loads per field instead of one per use.
+template <int FE, int NM>
+__device__ __forceinline__ void bl_resid_point(const BLArgs &A, const double *F, int fpl, int o, bool folds,
+                                               double (&av)[NM], double (&cv)[NM], double (&fo)[NM],
+                                               double (&wo)[NM]) {
+    const int M = A.M;
+    const double u0 = F[A.iu0 * fpl + o];
+    const double f0 = (FE == 3) ? F[A.iF0 * fpl + o] : 0.0;
+    double um[NM], fa[NM];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+        um[k] = u0;
+        if (FE == 3) fa[k] = A.a[k][0] * f0;
+        cv[k] = A.beta[k][0] * u0;
+        if (FE == 3 && folds) { fo[k] = A.sa[k][0] * f0; wo[k] = A.sb[k][0] * u0; }
+    }
+#pragma unroll
+    for (int j = 1; j < ISDC_MAXM; ++j) {
+        if (j < M) {
+            const double uj = F[(A.iu0 + j) * fpl + o];
+            const double Fj = (FE == 3) ? F[(A.iF0 + j) * fpl + o] : 0.0;
+#pragma unroll
+            for (int k = 0; k < NM; ++k) {
+                if (j == A.mnode[k]) um[k] = uj;
+                if (FE == 3) fa[k] = fa[k] + A.a[k][j] * Fj;
+                cv[k] = cv[k] + A.beta[k][j] * uj;
+                if (FE == 3 && folds) { fo[k] = fo[k] + A.sa[k][j] * Fj; wo[k] = wo[k] + A.sb[k][j] * uj; }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+        double diff = um[k] - u0;
+        if (FE == 3) diff = diff - fa[k];
+        av[k] = diff;
+    }
+}
+
 // NM outputs per pass (RHS: 1; residual: nodes per pass).  Registers: 14 * RR * NM doubles of rings.
 // NWW warps (region rows NWW * RR).
 template <int FE, int MODE, int RR, int NM, int NWW = NW>
@@ -653,6 +694,33 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
         const int po = (RR * w + 1) * SH::PW + lane + 1;
 #pragma unroll
         for (int r = 0; r < RR; ++r) {
+            if constexpr (MODE == 1 && (FE == 0 || FE == 3)) {
+                // residual: one read of every stage field per point (bl_resid_point)
+                double av[NM], cv[NM], fo[NM], wo[NM];
+                const bool folds = FE == 3 && A.nfold > 0;
+                if ((in >> r) & 1u) {
+                    bl_resid_point<FE, NM>(A, F, SH::FPL / 8, o0 + r * SH::FW, folds, av, cv, fo, wo);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NM; ++k) { av[k] = 0.0; cv[k] = 0.0; }
+                }
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    double *Pa = Ps + ((i2 * NM + k) * 2) * (SH::PPL / 8);
+                    Pa[po + r * SH::PW] = av[k];
+                    Pa[SH::PPL / 8 + po + r * SH::PW] = cv[k];
+                }
+                if (folds && ((oks >> r) & 1u) && p >= z0 && p < z1) {
+                    const long long gofs = (long long)p * A.plane + (long long)(y0 + ly0 + r) * A.pitch + gx;
+#pragma unroll
+                    for (int k = 0; k < NM; ++k) {
+                        if (k >= A.nfold) break;
+                        A.fa_out[k][gofs] = fo[k];
+                        A.wb_out[k][gofs] = wo[k];
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < NM; ++k) {
                 double av = 0.0, cv = 0.0;

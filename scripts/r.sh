@@ -1,3 +1,3 @@
-ISDC_SM_TY32_MIN=2047 ISDC_SM_TY=24 python -m pytest tests/test_gpu_fullsize.py -x -q -k "cfg3" 2>&1 | tail -2 > gpurun_out/par.log
-ISDC_SM_TY32_MIN=2047 ISDC_SM_TY=24 python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3_24.json 2>/dev/null
-python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3_16.json 2>/dev/null
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -3 > gpurun_out/par.log
+python bench.py --config 5 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b5.json 2>gpurun_out/b5.err
+python bench.py --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b4.json 2>gpurun_out/b4.err
