@@ -22,6 +22,40 @@
 #include "kernels_ptail.cuh"
 #include "tables.h"
 
+// Device-side node-solve loop of the SDC / capped-ISDC modes (one CUDA graph per sweep): the
+// defect test of node_solve runs in k_sdc_test, which drives a conditional WHILE node.
+struct SdcCtl {
+    double thr[ISDC_MAXM];   // inner_tol * max(1, ||b||) per node
+    int cyc[ISDC_MAXM];      // V-cycles done
+    int cap[ISDC_MAXM];      // SDC: the inner cap ended the solve
+    int err;                 // a defect came out NaN
+};
+__global__ void k_sdc_init(SdcCtl *ctl, int m, const unsigned long long *bslot, double inner_tol) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        const double bn = __longlong_as_double((long long)*bslot);
+        ctl->thr[m] = inner_tol * fmax(1.0, bn);   // the host expression of node_solve
+        ctl->cyc[m] = 0;
+        ctl->cap[m] = 0;
+        if (m == 0) ctl->err = 0;
+    }
+}
+// one test before every cycle (node_solve): stop when dn <= thr, or at the cap; clears the slot
+__global__ void k_sdc_test(SdcCtl *ctl, int m, unsigned long long *dslot, int capc, int sdc,
+                           cudaGraphConditionalHandle hnd) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        const double dn = __longlong_as_double((long long)*dslot);
+        unsigned go = 0;
+        if (!(dn == dn)) ctl->err = 1;
+        else if (dn <= ctl->thr[m]) go = 0;
+        else if (ctl->cyc[m] >= capc) { if (sdc) ctl->cap[m] = 1; }
+        else { go = 1; ctl->cyc[m] += 1; }
+        *dslot = 0ull;
+        cudaGraphSetConditional(hnd, go);
+    }
+}
+
 namespace {
 
 struct Level {
@@ -96,8 +130,16 @@ struct isdc_ctx {
     size_t ptail_smem = 0;
     // CUDA graphs of whole ISDC sweeps, keyed by (cur, spread, profiling)
     cudaStream_t cap = nullptr;
+    cudaStream_t cap2 = nullptr;   // capture stream of conditional-node bodies (device SDC loop)
+    struct SdcCtl *ctl = nullptr;  // device SDC loop state (workspace)
+    bool dev_sdc = true;           // ISDC_DEVICE_SDC=0: SDC / capped node solves tested on the host
     bool graphs = true;
-    struct Graph { cudaGraphExec_t exec = nullptr; std::vector<Pending> events; long nkernels = 0; };
+    struct Graph {
+        cudaGraphExec_t exec = nullptr; std::vector<Pending> events; long nkernels = 0;
+        long body[ISDC_MAXM] = {};   // kernels of one conditional-body pass per node (tested sweeps)
+    };
+    long body_kernels[ISDC_MAXM] = {};   // filled while a tested sweep is captured
+    long last_body[ISDC_MAXM] = {};      // of the graph launched last
     std::map<std::tuple<int, int, int, int>, Graph> sweep_graphs;
     bool capturing = false;
     // live kernel timing (isdc_profile_*)
@@ -112,6 +154,7 @@ struct isdc_ctx {
             if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
         for (auto e : evpool) cudaEventDestroy(e);
         if (cap) cudaStreamDestroy(cap);
+        if (cap2) cudaStreamDestroy(cap2);
     }
 };
 
@@ -325,7 +368,8 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     unsigned long long *red = (unsigned long long *)take(kRedSlots * sizeof(unsigned long long));
     double *ctd = (double *)take(ISDC_MAXM * sizeof(double));
     unsigned long long *al = (unsigned long long *)take(3 * ISDC_MAXM * sizeof(unsigned long long));
-    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; }
+    SdcCtl *ctl = (SdcCtl *)take(sizeof(SdcCtl));
+    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; h->ctl = ctl; }
     return off;
 }
 
@@ -1384,6 +1428,80 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
     return enqueue_residual(h, unew, Fnew, folds_on(h));
 }
 
+// all device work of one SDC / capped-ISDC sweep for capture into a CUDA graph: the node solves
+// loop on the device (conditional WHILE node per node, k_sdc_test before every cycle); the same
+// arithmetic as node_solve (the initial guess is copied into X first, so every cycle runs in place)
+isdc_status enqueue_tested_sweep(isdc_ctx *h) {
+    int M = h->M;
+    double *uold[ISDC_MAXM];
+    int nw = 1 - h->cur;
+    for (int j = 0; j < M; ++j) uold[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
+    double **unew = h->U[nw];
+    double *Fold[ISDC_MAXM];
+    for (int j = 0; j < M; ++j) Fold[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
+    double **Fnew = h->Fs[nw];
+    const bool fold_ok = !h->spread && h->fold_valid[h->cur];
+    const bool capped = h->P.solve.mode == ISDC_MODE_ISDC_CAPPED;
+    const int capc = capped ? h->P.solve.L : h->P.solve.inner_cap;
+    const GridDesc &g = h->lev[0].g;
+    if (!h->cap2) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap2, cudaStreamNonBlocking));
+    for (int m = 0; m + 1 < M; ++m) {
+        double *X = unew[m + 1];
+        TRY(run_rhs(h, m, uold, unew[m], h->Bf, true, Fold, Fnew[m], fold_ok));
+        if (h->P.solve.guess == 1) TRY(zero_field(h, X, g));
+        else TRY(copy_field(h, X, h->P.solve.guess == 2 ? unew[m] : uold[m + 1], g));
+        ++h->launches;
+        kl(h, k_sdc_init, 1, 32, 0)(h->ctl, m, (const unsigned long long *)(h->red + SLOT_BNORM), h->P.solve.inner_tol);
+        LAUNCH_CHECK(h);
+        TRY(clear_slots(h, SLOT_DEFECT, 1));
+        TRY(launch_defect_norm(h, X, h->Bf, g, h->lev[0].coef[m], h->red + SLOT_DEFECT));
+        // the conditional handle belongs to the graph being captured
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t ndeps = 0;
+        CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs, nullptr, &cg, &deps, &ndeps));
+        cudaGraphConditionalHandle hnd;
+        CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hnd, cg, 0, 0));
+        ++h->launches;
+        kl(h, k_sdc_test, 1, 32, 0)(h->ctl, m, h->red + SLOT_DEFECT, capc, capped ? 0 : 1, hnd);
+        LAUNCH_CHECK(h);
+        CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs, nullptr, &cg, &deps, &ndeps));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hnd;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cn;
+        CUDA_TRY(h, cudaGraphAddNode(&cn, cg, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CUDA_TRY(h, cudaStreamUpdateCaptureDependencies(h->s, &cn, 1, cudaStreamSetCaptureDependencies));
+        // body: one cycle in place, then the next test
+        cudaStream_t outer = h->s;
+        CUDA_TRY(h, cudaStreamBeginCaptureToGraph(h->cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        h->s = h->cap2;
+        const long lb = h->launches;
+        isdc_status st = vcycle(h, 0, m, X, h->T, h->Bf, nullptr);
+        if (st == ISDC_OK) st = launch_defect_norm(h, X, h->Bf, g, h->lev[0].coef[m], h->red + SLOT_DEFECT);
+        if (st == ISDC_OK) {
+            ++h->launches;
+            kl(h, k_sdc_test, 1, 32, 0)(h->ctl, m, h->red + SLOT_DEFECT, capc, capped ? 0 : 1, hnd);
+            cudaError_t le = cudaGetLastError();
+            if (le == cudaSuccess) le = h->kl_err;
+            h->kl_err = cudaSuccess;
+            if (le != cudaSuccess) { h->err = std::string("kernel launch: ") + cudaGetErrorString(le); st = ISDC_ERR_CUDA; }
+        }
+        h->body_kernels[m] = h->launches - lb;
+        cudaGraph_t bo = nullptr;
+        cudaError_t ee = cudaStreamEndCapture(h->cap2, &bo);
+        h->s = outer;
+        if (st != ISDC_OK) return st;
+        CUDA_TRY(h, ee);
+        TRY(launch_fe(h, Fnew[m + 1], X));
+    }
+    return enqueue_residual(h, unew, Fnew, folds_on(h));
+}
+
 isdc_status graph_sweep(isdc_ctx *h) {
     auto key = std::make_tuple(h->cur, h->spread ? 1 : 0, h->prof, h->fold_valid[h->cur] ? 1 : 0);
     auto it = h->sweep_graphs.find(key);
@@ -1395,7 +1513,8 @@ isdc_status graph_sweep(isdc_ctx *h) {
         h->s = h->cap;
         h->capturing = true;
         cudaError_t e = cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal);
-        isdc_status st = (e == cudaSuccess) ? enqueue_isdc_sweep(h) : ISDC_ERR_CUDA;
+        const bool tested = h->P.solve.mode != ISDC_MODE_ISDC_FIXED;
+        isdc_status st = (e == cudaSuccess) ? (tested ? enqueue_tested_sweep(h) : enqueue_isdc_sweep(h)) : ISDC_ERR_CUDA;
         cudaGraph_t g = nullptr;
         cudaError_t e2 = cudaStreamEndCapture(h->cap, &g);
         h->capturing = false;
@@ -1407,6 +1526,7 @@ isdc_status graph_sweep(isdc_ctx *h) {
         }
         isdc_ctx::Graph G;
         G.nkernels = h->launches - l0;
+        for (int q = 0; q < ISDC_MAXM; ++q) G.body[q] = h->body_kernels[q];
         h->launches = l0;   // capture is not execution
         G.events.assign(h->pend.begin() + pend0, h->pend.end());
         h->pend.resize(pend0);
@@ -1415,7 +1535,8 @@ isdc_status graph_sweep(isdc_ctx *h) {
         it = h->sweep_graphs.emplace(key, G).first;
     }
     CUDA_TRY(h, cudaGraphLaunch(it->second.exec, h->s));
-    h->launches += it->second.nkernels;
+    h->launches += it->second.nkernels;   // tested sweeps add the extra body passes once the counts are read
+    for (int q = 0; q < ISDC_MAXM; ++q) h->last_body[q] = it->second.body[q];
     if (h->prof) {  // the graph's event pairs hold this launch's timings
         CUDA_TRY(h, cudaStreamSynchronize(h->s));
         for (auto &p : it->second.events) {
@@ -1437,6 +1558,25 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
         h->cur = 1 - h->cur;
         h->spread = false;
         h->fold_valid[h->cur] = folds_on(h);   // the residual stored the folds of the new iterate
+        return read_residual(h, res_per_node, res_max);
+    }
+    if (h->graphs && h->dev_sdc && h->prof == 0) {
+        // SDC / capped ISDC: node-solve tests on the device inside the sweep graph
+        TRY(graph_sweep(h));
+        SdcCtl ctl;
+        CUDA_TRY(h, cudaMemcpyAsync(&ctl, h->ctl, sizeof(SdcCtl), cudaMemcpyDeviceToHost, h->s));
+        CUDA_TRY(h, cudaStreamSynchronize(h->s));
+        if (ctl.err) { h->err = "non-finite defect"; return ISDC_ERR_NONFINITE; }
+        int caps = 0;
+        for (int m = 0; m + 1 < M; ++m) {
+            if (cycles) cycles[m] = ctl.cyc[m];
+            caps += ctl.cap[m];
+            h->launches += (long)(ctl.cyc[m] - 1) * h->last_body[m];   // the capture counted one pass
+        }
+        if (cap_hits) *cap_hits = caps;
+        h->cur = 1 - h->cur;
+        h->spread = false;
+        h->fold_valid[h->cur] = folds_on(h);
         return read_residual(h, res_per_node, res_max);
     }
     double *uold[ISDC_MAXM];
@@ -1611,6 +1751,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
             return ISDC_ERR_INVALID_ARG;
         }
     }
+    if (const char *ds = getenv("ISDC_DEVICE_SDC")) h->dev_sdc = ds[0] != '0';
     const char *eg = getenv("ISDC_NO_GRAPHS");
     h->graphs = !(eg && eg[0] == '1');
     // single-CTA tail: levels n <= 63 (2D) / 15 (3D) in shared memory
