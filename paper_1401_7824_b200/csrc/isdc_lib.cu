@@ -760,7 +760,7 @@ isdc_status launch_prolong(isdc_ctx *h, double *u, const GridDesc &gf, const dou
         dim3 grd(((gf.n + 1) / 2 + 255) / 256, gf.n);
         kl(h, f2d::k_prolong, grd, 256, 0)(u, gf.n, gf.pitch, e, gc.n, gc.pitch);
     } else if (use_fast3d(h, level, 4)) {
-        dim3 grd(((gf.n + 1) / 2 + 255) / 256, gf.n, gf.n);
+        dim3 grd(((gf.n + 1) / 2 + 255) / 256, (gf.n + 1) / 2, gf.n);   // two rows per thread
         kl(h, f3d::k_prolong, grd, 256, 0)(u, gf.n, gf.pitch, gf.plane, e, gc.n, gc.pitch, gc.plane);
     } else if (h->d == 2) kl(h, k_prolong_add<2>, point_grid<2>(gf, kBlk), kBlk, 0)(u, gf, e, gc);
     else kl(h, k_prolong_add<3>, point_grid<3>(gf, kBlk), kBlk, 0)(u, gf, e, gc);

@@ -412,8 +412,10 @@ __global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf,
                                                  long long plane_c) {
     pdl_launch();
     pdl_wait();
+    // two fine rows (y0, y0 + 1) per thread: both 16-byte u loads are issued before either update
+    // (memory-level parallelism); the per-point expressions are unchanged
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y, z = blockIdx.z;
+    const int y0 = 2 * blockIdx.y, z = blockIdx.z;
     const int x = 2 * t;
     if (x >= nf) return;
     auto E = [&](int X, int Y, int Z) -> double {
@@ -421,35 +423,53 @@ __global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf,
                    ? __ldg(e + (long long)Z * plane_c + (long long)Y * pitch_c + X)
                    : 0.0;
     };
-    const bool ye = !(y & 1), ze = !(z & 1);
-    const int Ya = ye ? y / 2 - 1 : (y - 1) / 2, Yb = y / 2;
+    const bool ze = !(z & 1);
     const int Za = ze ? z / 2 - 1 : (z - 1) / 2, Zb = z / 2;
-    auto sy = [&](int Z, double &se, double &so) {
-        double sea = E(t - 1, Ya, Z) + E(t, Ya, Z), soa = E(t, Ya, Z);
-        if (ye) {
-            double seb = E(t - 1, Yb, Z) + E(t, Yb, Z), sob = E(t, Yb, Z);
-            se = sea + seb; so = soa + sob;
-        } else {
-            se = sea; so = soa;
+    const bool pair = x + 1 < nf;
+    double2 v[2];
+    double *row[2];
+    bool rin[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int y = y0 + q;
+        rin[q] = y < nf;
+        row[q] = u + (long long)z * plane_f + (long long)y * pitch_f;
+        if (rin[q]) {
+            if (pair) v[q] = *reinterpret_cast<const double2 *>(row[q] + x);
+            else v[q].x = row[q][x];
         }
-    };
-    double se, so;
-    sy(Za, se, so);
-    if (ze) {
-        double se2, so2;
-        sy(Zb, se2, so2);
-        se = se + se2; so = so + so2;
     }
-    double w = (ye ? 0.5 : 1.0) * (ze ? 0.5 : 1.0);
-    double we = w * 0.5;   // the even column also averages in x
-    double *row = u + (long long)z * plane_f + (long long)y * pitch_f;
-    if (x + 1 < nf) {
-        double2 v = *reinterpret_cast<double2 *>(row + x);
-        v.x = v.x + se * we;
-        v.y = v.y + so * w;
-        *reinterpret_cast<double2 *>(row + x) = v;
-    } else {
-        row[x] = row[x] + se * we;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (!rin[q]) continue;
+        const int y = y0 + q;
+        const bool ye = !(y & 1);
+        const int Ya = ye ? y / 2 - 1 : (y - 1) / 2, Yb = y / 2;
+        auto sy = [&](int Z, double &se, double &so) {
+            double sea = E(t - 1, Ya, Z) + E(t, Ya, Z), soa = E(t, Ya, Z);
+            if (ye) {
+                double seb = E(t - 1, Yb, Z) + E(t, Yb, Z), sob = E(t, Yb, Z);
+                se = sea + seb; so = soa + sob;
+            } else {
+                se = sea; so = soa;
+            }
+        };
+        double se, so;
+        sy(Za, se, so);
+        if (ze) {
+            double se2, so2;
+            sy(Zb, se2, so2);
+            se = se + se2; so = so + so2;
+        }
+        double w = (ye ? 0.5 : 1.0) * (ze ? 0.5 : 1.0);
+        double we = w * 0.5;   // the even column also averages in x
+        if (pair) {
+            v[q].x = v[q].x + se * we;
+            v[q].y = v[q].y + so * w;
+            *reinterpret_cast<double2 *>(row[q] + x) = v[q];
+        } else {
+            row[q][x] = v[q].x + se * we;
+        }
     }
 }
 

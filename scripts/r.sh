@@ -1,1 +1,3 @@
-for r in 2 3 4; do ISDC_SMOOTH3D_ROWS=$r python bench.py --config 5 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b5_r$r.json 2>/dev/null; done
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -2 > gpurun_out/par.log
+python bench.py --config 5 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b5.json 2>gpurun_out/b5.err
+python bench.py --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b4.json 2>gpurun_out/b4.err
