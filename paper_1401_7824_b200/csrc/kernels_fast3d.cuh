@@ -354,28 +354,29 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
     const int dx = 2 * ci + 1, dy = 2 * cj + 1;
     double fdl = 0, edl = 0, dcl = 0, fdm = 0, edm = 0, dcm = 0;   // partials at planes 2K (lower), 2K+1 (mid)
 
-    double qa[R], qb[R], fa[R], fb[R], eb[R];
+    // register rings (plane it at slot it % 3 for q, f and it % 2 for e); the z loop is unrolled by
+    // 6 so every slot index is a compile-time constant and no ring value is moved
+    double qr[3][R], fr[3][R], er[2][R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) qa[r] = qb[r] = fa[r] = fb[r] = eb[r] = 0.0;
-    for (int it = 0; it < nit; ++it) {
+    for (int r = 0; r < R; ++r) { qr[0][r] = qr[1][r] = qr[2][r] = fr[0][r] = fr[1][r] = fr[2][r] = er[0][r] = er[1][r] = 0.0; }
+    auto step = [&](auto Kc, int it) {
+        constexpr int KK = decltype(Kc)::value;
+        constexpr int i3 = KK % 3, m3 = (KK + 2) % 3, mm3 = (KK + 1) % 3, i2 = KK % 2, m2 = (KK + 1) % 2;
         const int s = it % R_NS;
         mbar_wait(&bar[s], (it / R_NS) & 1);
-        double qn[R], fn[R], en[R];
-        plane_partials<true>(Us + s * (R_UPL / 8), R_UW, R * w, lane + 1, qn, fn, en);
+        plane_partials<true>(Us + s * (R_UPL / 8), R_UW, R * w, lane + 1, qr[i3], fr[i3], er[i2]);
         const bool dd = it >= 2;     // defect at fine plane p-1
-        double *D = Ds + (it & 1) * (R_DPL / 8);
+        double *D = Ds + (KK & 1) * (R_DPL / 8);   // == it & 1 (the unrolled base is a multiple of 6)
         if (dd) {
             const double *Bp = Bs + s * (R_BPL / 8);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const double faces = fb[r] + (qa[r] + qn[r]);
-                const double edges = eb[r] + (fa[r] + fn[r]);
-                const double su = (c0 * qb[r] + c1 * faces) + c2 * edges;
+                const double faces = fr[m3][r] + (qr[mm3][r] + qr[i3][r]);
+                const double edges = er[m2][r] + (fr[mm3][r] + fr[i3][r]);
+                const double su = (c0 * qr[m3][r] + c1 * faces) + c2 * edges;
                 D[(R * w + r) * R_DW + lane] = Bp[(R * w + r) * R_BW + lane] - su;
             }
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r) { qa[r] = qb[r]; qb[r] = qn[r]; fa[r] = fb[r]; fb[r] = fn[r]; eb[r] = en[r]; }
         __syncthreads();
         if (tid == 0 && it + R_NS < nit) issue(it + R_NS);
         if (dd && crole) {
@@ -399,6 +400,14 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
                 fdl = fd; edl = ed; dcl = dc;
             }
         }
+    };
+    for (int base = 0; base < nit; base += 6) {
+        step(std::integral_constant<int, 0>{}, base);
+        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
+        if (base + 3 < nit) step(std::integral_constant<int, 3>{}, base + 3);
+        if (base + 4 < nit) step(std::integral_constant<int, 4>{}, base + 4);
+        if (base + 5 < nit) step(std::integral_constant<int, 5>{}, base + 5);
     }
 }
 
