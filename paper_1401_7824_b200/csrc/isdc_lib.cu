@@ -1058,7 +1058,7 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         const double *fields[f3d::BL_MAXF];
         f3d::BLArgs A;
         int K = 0;
-        A.iuo1 = K; fields[K++] = uold[m + 1];
+        A.iuo1 = 0;   // the stored fold already holds - gamma_m u_{m+1}^k (bl_resid_point)
         A.ifo = K; fields[K++] = Fold[m];
         A.iun = K; fields[K++] = unew_m;
         A.iFn = K; fields[K++] = Fnew;
@@ -1194,6 +1194,7 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
                         A.sa[k][j] = dts * h->S[qnext * M + j];
                         A.sb[k][j] = nudts * h->S[qnext * M + j];
                     }
+                    A.fgm[k] = h->P.nu * (h->P.dt * h->dtau[qnext]);   // the RHS's gamma_q = nu * dtm
                     A.fa_out[k] = h->FA[qnext];
                     A.wb_out[k] = h->WB[qnext];
                     A.nfold = k + 1;

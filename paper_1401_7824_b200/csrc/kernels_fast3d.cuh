@@ -508,6 +508,7 @@ struct BLArgs {
     // FA_q = fold_j (dt S_qj) F_j, WB_q = fold_j (nu dt S_qj) u_j, q = qnode[k], k < nfold
     int nfold, qnode[BL_MAXNM];
     double sa[BL_MAXNM][ISDC_MAXM], sb[BL_MAXNM][ISDC_MAXM];
+    double fgm[BL_MAXNM];          // gamma_q: WB_q stores fold_j (nu dt S_qj) u_j - gamma_q u_{q+1}
     double *fa_out[BL_MAXNM], *wb_out[BL_MAXNM];
     const double *ct;              // device cos(t_j)
     double dtm, gm;                // RHS: dt*dtau_m, nu*dt*dtau_m
@@ -586,7 +587,7 @@ __device__ __forceinline__ void bl_point(const BLArgs &A, int k, const double *F
             av = (un + A.dtm * (fn - fo)) + fa;
         }
     } else if (MODE == 2) {   // RHS from stored folds (FE = CD4): the same expression trees
-        cv = fld(A.iwb) - A.gm * fld(A.iuo1);
+        cv = fld(A.iwb);          // = fold - gamma_m u_{m+1}^k, formed by the residual pass
         av = (fld(A.iun) + A.dtm * (fld(A.iFn) - fld(A.ifo))) + fld(A.ifa);
     } else {           // residual node m: a = p, c = z
         double diff = fld(A.iu0 + m) - fld(A.iu0);
@@ -632,10 +633,11 @@ __device__ __forceinline__ void bl_resid_point(const BLArgs &A, const double *F,
     const int M = A.M;
     const double u0 = F[A.iu0 * fpl + o];
     const double f0 = (FE == 3) ? F[A.iF0 * fpl + o] : 0.0;
-    double um[NM], fa[NM];
+    double um[NM], fa[NM], uq1[NM];
 #pragma unroll
     for (int k = 0; k < NM; ++k) {
         um[k] = u0;
+        uq1[k] = u0;
         if (FE == 3) fa[k] = A.a[k][0] * f0;
         cv[k] = A.beta[k][0] * u0;
         if (FE == 3 && folds) { fo[k] = A.sa[k][0] * f0; wo[k] = A.sb[k][0] * u0; }
@@ -648,6 +650,7 @@ __device__ __forceinline__ void bl_resid_point(const BLArgs &A, const double *F,
 #pragma unroll
             for (int k = 0; k < NM; ++k) {
                 if (j == A.mnode[k]) um[k] = uj;
+                if (j == A.qnode[k] + 1) uq1[k] = uj;
                 if (FE == 3) fa[k] = fa[k] + A.a[k][j] * Fj;
                 cv[k] = cv[k] + A.beta[k][j] * uj;
                 if (FE == 3 && folds) { fo[k] = fo[k] + A.sa[k][j] * Fj; wo[k] = wo[k] + A.sb[k][j] * uj; }
@@ -659,6 +662,7 @@ __device__ __forceinline__ void bl_resid_point(const BLArgs &A, const double *F,
         double diff = um[k] - u0;
         if (FE == 3) diff = diff - fa[k];
         av[k] = diff;
+        if (FE == 3 && folds) wo[k] = wo[k] - A.fgm[k] * uq1[k];   // the RHS's w = acc - gamma u_{m+1}
     }
 }
 
