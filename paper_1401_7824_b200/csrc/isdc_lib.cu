@@ -113,7 +113,9 @@ struct isdc_ctx {
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
     int sr_ty = 32;            // ISDC_SR_TY: their height (24 or 32)
     int sm_ty32_min = 2047;    // ISDC_SM_TY32_MIN: the same for k_smooth2
-    int sm_ty = 24;            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
+    int sm_ty = 24;
+    int small_n = 511;         // ISDC_SMALL_N: levels n <= small_n use the short tiles below (more CTAs)
+    int sr_ty_small = 8, sm_ty_small = 8;   // ISDC_SR_TY_SMALL / ISDC_SM_TY_SMALL (8 or 16)            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
@@ -512,7 +514,7 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
                            const GridDesc *gc = nullptr) {
     // 32-row tiles on the large levels (ISDC_SM_TY32_MIN), 16-row tiles below
     const bool t32 = g.n >= h->sm_ty32_min;
-    const int TY = t32 ? h->sm_ty : 16;
+    const int TY = t32 ? h->sm_ty : (g.n <= h->small_n ? h->sm_ty_small : 16);
     const CUtensorMap *mb = tmap(h, b, g, f2d::BW, TY + 2);
     const CUtensorMap *mu = in ? tmap(h, in, g, f2d::UW, TY + 4) : mb;
     const CUtensorMap *me = e ? tmap(h, e, *gc, f2d::EW, TY / 2 + 3) : mb;
@@ -521,7 +523,13 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
     const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + TY - 1) / TY);
-    if (TY == 24) {
+    if (TY == 8) {
+        size_t sm = sizeof(f2d::SmemSmoothT<8>) + 128;
+        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
+        else if (e) kl(h, f2d::k_smooth2<false, 2, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else if (!in) kl(h, f2d::k_smooth2<false, 1, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else kl(h, f2d::k_smooth2<false, 0, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    } else if (TY == 24) {
         size_t sm = sizeof(f2d::SmemSmoothT<24>) + 128;
         if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 24>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
         else if (e) kl(h, f2d::k_smooth2<false, 2, 24>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
@@ -679,7 +687,7 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
     }
     // 32-row tiles on the large levels, 16-row tiles where more CTAs matter (ISDC_SR_TY32_MIN)
     const bool t32 = g.n >= h->sr_ty32_min;
-    const int TY = t32 ? h->sr_ty : 16;
+    const int TY = t32 ? h->sr_ty : (g.n <= h->small_n ? h->sr_ty_small : 16);
     const CUtensorMap *mb = tmap(h, b, g, f2d::FR_BW, TY + 5);
     const CUtensorMap *mu = in ? tmap(h, in, g, f2d::FR_UW, TY + 7) : mb;
     if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
@@ -691,6 +699,10 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
         size_t sm = sizeof(f2d::SmemSR<32>) + 128;
         if (in) kl(h, f2d::k_smooth2r<0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
         else kl(h, f2d::k_smooth2r<1, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    } else if (TY == 8) {
+        size_t sm = sizeof(f2d::SmemSR<8>) + 128;
+        if (in) kl(h, f2d::k_smooth2r<0, 8>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+        else kl(h, f2d::k_smooth2r<1, 8>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
     } else if (TY == 24) {
         size_t sm = sizeof(f2d::SmemSR<24>) + 128;
         if (in) kl(h, f2d::k_smooth2r<0, 24>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
@@ -1677,6 +1689,9 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
     if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
     if (const char *st = getenv("ISDC_SM_TY")) h->sm_ty = atoi(st) == 24 ? 24 : 32;
+    if (const char *st = getenv("ISDC_SMALL_N")) h->small_n = atoi(st);
+    if (const char *st = getenv("ISDC_SR_TY_SMALL")) h->sr_ty_small = atoi(st) == 8 ? 8 : 16;
+    if (const char *st = getenv("ISDC_SM_TY_SMALL")) h->sm_ty_small = atoi(st) == 8 ? 8 : 16;
     if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
     if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) { int v = atoi(sr); h->smooth3d_rows = (v == 2 || v == 3 || v == 4) ? v : 0; }
     {
