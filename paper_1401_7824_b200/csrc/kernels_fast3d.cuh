@@ -762,26 +762,6 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
                 Pa[po + r * SH::PW] = av;
                 Pa[SH::PPL / 8 + po + r * SH::PW] = cv;
             }
-            // residual pass: the next sweep's RHS folds at the tile points of this chunk's planes
-            if (MODE == 1 && FE == 3 && A.nfold > 0 && ((oks >> r) & 1u) && p >= z0 && p < z1) {
-                const double *Fr = F + o0 + r * SH::FW;
-                const int fpl = SH::FPL / 8;
-                const long long gofs = (long long)p * A.plane + (long long)(y0 + ly0 + r) * A.pitch + gx;
-#pragma unroll
-                for (int k = 0; k < NM; ++k) {
-                    if (k >= A.nfold) break;
-                    double fa = A.sa[k][0] * Fr[A.iF0 * fpl];
-                    double wb = A.sb[k][0] * Fr[A.iu0 * fpl];
-#pragma unroll
-                    for (int j = 1; j < ISDC_MAXM; ++j)
-                        if (j < A.M) {
-                            fa = fa + A.sa[k][j] * Fr[(A.iF0 + j) * fpl];
-                            wb = wb + A.sb[k][j] * Fr[(A.iu0 + j) * fpl];
-                        }
-                    A.fa_out[k][gofs] = fa;
-                    A.wb_out[k][gofs] = wb;
-                }
-            }
         }
         __syncthreads();
         if (tid == 0 && it + ns < nit) issue(it + ns);
