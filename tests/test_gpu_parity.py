@@ -201,3 +201,24 @@ def test_unweighted_residual_steps_bitwise(gpu, ora, cid, n, mode):
     assert st["wcycles"] == st_ref["wcycles"] and st["wcycles"] > 0
     assert np.array_equal(st["res_hist"], st_ref["res_hist"])
     assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)
+
+
+# ------------------------------------------------ alternative execution paths (same bits)
+@pytest.mark.parametrize("env,mode", [({"ISDC_DEVICE_SDC": "0"}, MODE_SDC), ({"ISDC_DEVICE_SDC": "0"}, MODE_ISDC_CAPPED),
+                                      ({"ISDC_NO_GRAPHS": "1"}, MODE_ISDC), ({"ISDC_NO_GRAPHS": "1"}, MODE_SDC),
+                                      ({"ISDC_GENERIC_KERNELS": "1"}, MODE_ISDC), ({"ISDC_FOLDS": "0"}, MODE_ISDC)])
+def test_execution_paths_bitwise(gpu, ora, monkeypatch, env, mode):
+    """Host-side node-solve tests, un-captured sweeps, the generic kernels and the fold-free RHS
+    produce the oracle's bits too (the environment is read when the handle is created)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for cid, n in ((2, 127), (4, 31)):
+        cfg, u0, G = synth.problem_inputs(cid, 0, n)
+        h = make(gpu, cfg, G, mode=mode)
+        h.set_initial(torch.from_numpy(u0).cuda(), 0)
+        st = h.step()
+        u_ref, st_ref = ora.step(ora.Problem(cfg, G, mode=mode), u0, 0.0)
+        assert st["sweeps"] == st_ref["sweeps"] and st["vcycles"] == st_ref["vcycles"]
+        assert np.array_equal(st["node_cycles"], st_ref["node_cycles"])
+        assert np.array_equal(st["res_hist"], st_ref["res_hist"])
+        assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)
