@@ -29,6 +29,8 @@ struct SdcCtl {
     int cyc[ISDC_MAXM];      // V-cycles done
     int cap[ISDC_MAXM];      // SDC: the inner cap ended the solve
     int err;                 // a defect came out NaN
+    double wthr[ISDC_MAXM];  // residual_kind 1: w_tol * ||r~_m|| per residual node
+    int wcn[ISDC_MAXM];      // W-cycles per residual node
 };
 __global__ void k_sdc_init(SdcCtl *ctl, int m, const unsigned long long *bslot, double inner_tol) {
     pdl_wait();
@@ -51,6 +53,27 @@ __global__ void k_sdc_test(SdcCtl *ctl, int m, unsigned long long *dslot, int ca
         else if (dn <= ctl->thr[m]) go = 0;
         else if (ctl->cyc[m] >= capc) { if (sdc) ctl->cap[m] = 1; }
         else { go = 1; ctl->cyc[m] += 1; }
+        *dslot = 0ull;
+        cudaGraphSetConditional(hnd, go);
+    }
+}
+
+// residual_kind 1 (NEXT f2) on the device: the W-solve of unweighted_norms, one node m at a time
+__global__ void k_w_init(SdcCtl *ctl, int m, const unsigned long long *rslot, double w_tol) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        ctl->wthr[m] = w_tol * __longlong_as_double((long long)*rslot);   // the host expression
+        ctl->wcn[m] = 0;
+        if (m == 1) ctl->err = 0;
+    }
+}
+__global__ void k_w_test(SdcCtl *ctl, int m, unsigned long long *dslot, int wcap, cudaGraphConditionalHandle hnd) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        const double dn = __longlong_as_double((long long)*dslot);
+        unsigned go = 0;
+        if (!(dn == dn)) ctl->err = 1;
+        else if (!(dn <= ctl->wthr[m]) && ctl->wcn[m] < wcap) { go = 1; ctl->wcn[m] += 1; }
         *dslot = 0ull;
         cudaGraphSetConditional(hnd, go);
     }
@@ -139,9 +162,12 @@ struct isdc_ctx {
     struct Graph {
         cudaGraphExec_t exec = nullptr; std::vector<Pending> events; long nkernels = 0;
         long body[ISDC_MAXM] = {};   // kernels of one conditional-body pass per node (tested sweeps)
+        long wbody[ISDC_MAXM] = {};  // ... and per residual node of the device W-solve
     };
     long body_kernels[ISDC_MAXM] = {};   // filled while a tested sweep is captured
+    long wbody_kernels[ISDC_MAXM] = {};  // kernels of one W-solve loop pass per residual node
     long last_body[ISDC_MAXM] = {};      // of the graph launched last
+    long last_wbody[ISDC_MAXM] = {};
     std::map<std::tuple<int, int, int, int>, Graph> sweep_graphs;
     bool capturing = false;
     // live kernel timing (isdc_profile_*)
@@ -215,7 +241,7 @@ KLaunch<KA...> kl(isdc_ctx *h, void (*k)(KA...), dim3 g, dim3 b, size_t sm) {
 
 constexpr size_t kAlign = 256;
 constexpr int kRedSlots = 64;
-enum { SLOT_DEFECT = 0, SLOT_BNORM = 1, SLOT_RES0 = 8, SLOT_SCRATCH = 32 };
+enum { SLOT_DEFECT = 0, SLOT_BNORM = 1, SLOT_RES0 = 8, SLOT_UW0 = 16, SLOT_SCRATCH = 32, SLOT_WDEF = 33 };
 
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -1361,11 +1387,12 @@ isdc_status unweighted_norms(isdc_ctx *h, double *norms) {
     return ISDC_OK;
 }
 
-isdc_status read_residual(isdc_ctx *h, double *per_node, double *maxn) {
+// dev_w: the unweighted norms were formed on the device (enqueue_wsolve) into SLOT_UW0..
+isdc_status read_residual(isdc_ctx *h, double *per_node, double *maxn, bool dev_w = false) {
     int M = h->M;
     double tmp[ISDC_MAXM];
-    TRY(read_slots(h, SLOT_RES0, M - 1, tmp));
-    if (h->P.residual_kind == 1) TRY(unweighted_norms(h, tmp));
+    TRY(read_slots(h, dev_w ? SLOT_UW0 : SLOT_RES0, M - 1, tmp));
+    if (h->P.residual_kind == 1 && !dev_w) TRY(unweighted_norms(h, tmp));
     double mx = 0.0;
     bool bad = false;
     for (int m = 0; m < M - 1; ++m) {
@@ -1418,6 +1445,9 @@ isdc_status run_residual(isdc_ctx *h, double *const *u, double *per_node, double
     return read_residual(h, per_node, maxn);
 }
 
+isdc_status enqueue_wsolve(isdc_ctx *h);
+bool dev_wsolve(const isdc_ctx *h);
+
 // all device work of one ISDC-mode sweep (no host synchronisation): RHS, L cycles per node, residual
 isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
     int M = h->M;
@@ -1438,8 +1468,86 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
         for (int l = 0; l < h->P.solve.L; ++l) TRY(vcycle(h, 0, m, unew[m + 1], h->T, h->Bf, l == 0 ? src : nullptr));
         TRY(launch_fe(h, Fnew[m + 1], unew[m + 1]));
     }
-    return enqueue_residual(h, unew, Fnew, folds_on(h));
+    TRY(enqueue_residual(h, unew, Fnew, folds_on(h)));
+    if (h->capturing && dev_wsolve(h)) TRY(enqueue_wsolve(h));
+    return ISDC_OK;
 }
+
+// Insert a conditional WHILE node into the graph being captured on h->s: `test` (a kernel launch
+// taking the handle) is enqueued first and sets the condition; `body` is captured into the loop
+// body on h->cap2 and must end with the same test.  Used by the device-side node-solve and W-solve
+// loops.
+template <typename TestF, typename BodyF>
+isdc_status capture_while(isdc_ctx *h, TestF test, BodyF body) {
+    if (!h->cap2) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap2, cudaStreamNonBlocking));
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t ndeps = 0;
+    CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs, nullptr, &cg, &deps, &ndeps));
+    cudaGraphConditionalHandle hnd;
+    CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hnd, cg, 0, 0));
+    TRY(test(hnd));
+    CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hnd;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CUDA_TRY(h, cudaGraphAddNode(&cn, cg, deps, ndeps, &cp));
+    cudaGraph_t bg = cp.conditional.phGraph_out[0];
+    CUDA_TRY(h, cudaStreamUpdateCaptureDependencies(h->s, &cn, 1, cudaStreamSetCaptureDependencies));
+    cudaStream_t outer = h->s;
+    CUDA_TRY(h, cudaStreamBeginCaptureToGraph(h->cap2, bg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    h->s = h->cap2;
+    isdc_status st = body(hnd);
+    cudaGraph_t bo = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(h->cap2, &bo);
+    h->s = outer;
+    if (st != ISDC_OK) return st;
+    CUDA_TRY(h, ee);
+    return ISDC_OK;
+}
+
+// residual_kind 1 on the device (enqueued after the residual kernels, which wrote r~_m into RT):
+// per node the W-solve of unweighted_norms as a conditional loop, then ||x|| into SLOT_UW0 + m - 1
+isdc_status enqueue_wsolve(isdc_ctx *h) {
+    const GridDesc &g = h->lev[0].g;
+    const SCoef &c = h->lev[0].coef[h->wslot];
+    for (int m = 1; m < h->M; ++m) {
+        TRY(zero_field(h, h->WX, g));
+        ++h->launches;
+        kl(h, k_w_init, 1, 32, 0)(h->ctl, m, (const unsigned long long *)(h->red + SLOT_RES0 + m - 1), h->P.w_tol);
+        LAUNCH_CHECK(h);
+        TRY(clear_slots(h, SLOT_WDEF, 1));
+        TRY(launch_defect_norm(h, h->WX, h->RT[m - 1], g, c, h->red + SLOT_WDEF));
+        auto test = [&](cudaGraphConditionalHandle hnd) -> isdc_status {
+            ++h->launches;
+            kl(h, k_w_test, 1, 32, 0)(h->ctl, m, h->red + SLOT_WDEF, h->P.w_cap, hnd);
+            LAUNCH_CHECK(h);
+            return ISDC_OK;
+        };
+        const long lb0 = h->launches;
+        long lb1 = 0;
+        TRY(capture_while(h, test, [&](cudaGraphConditionalHandle hnd) -> isdc_status {
+            const long lb = h->launches;
+            TRY(vcycle(h, 0, h->wslot, h->WX, h->T, h->RT[m - 1], nullptr));
+            TRY(launch_defect_norm(h, h->WX, h->RT[m - 1], g, c, h->red + SLOT_WDEF));
+            TRY(test(hnd));
+            lb1 = h->launches - lb;
+            return ISDC_OK;
+        }));
+        (void)lb0;
+        h->wbody_kernels[m] = lb1;
+        TRY(clear_slots(h, SLOT_UW0 + m - 1, 1));
+        ++h->launches;
+        kl(h, k_norm<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->WX, g, h->red + SLOT_UW0 + m - 1);
+        LAUNCH_CHECK(h);
+    }
+    return ISDC_OK;
+}
+bool dev_wsolve(const isdc_ctx *h) { return h->P.residual_kind == 1 && h->dev_sdc && h->graphs && h->prof == 0; }
 
 // all device work of one SDC / capped-ISDC sweep for capture into a CUDA graph: the node solves
 // loop on the device (conditional WHILE node per node, k_sdc_test before every cycle); the same
@@ -1512,7 +1620,9 @@ isdc_status enqueue_tested_sweep(isdc_ctx *h) {
         CUDA_TRY(h, ee);
         TRY(launch_fe(h, Fnew[m + 1], X));
     }
-    return enqueue_residual(h, unew, Fnew, folds_on(h));
+    TRY(enqueue_residual(h, unew, Fnew, folds_on(h)));
+    if (dev_wsolve(h)) TRY(enqueue_wsolve(h));
+    return ISDC_OK;
 }
 
 isdc_status graph_sweep(isdc_ctx *h) {
@@ -1539,7 +1649,7 @@ isdc_status graph_sweep(isdc_ctx *h) {
         }
         isdc_ctx::Graph G;
         G.nkernels = h->launches - l0;
-        for (int q = 0; q < ISDC_MAXM; ++q) G.body[q] = h->body_kernels[q];
+        for (int q = 0; q < ISDC_MAXM; ++q) { G.body[q] = h->body_kernels[q]; G.wbody[q] = h->wbody_kernels[q]; }
         h->launches = l0;   // capture is not execution
         G.events.assign(h->pend.begin() + pend0, h->pend.end());
         h->pend.resize(pend0);
@@ -1549,7 +1659,7 @@ isdc_status graph_sweep(isdc_ctx *h) {
     }
     CUDA_TRY(h, cudaGraphLaunch(it->second.exec, h->s));
     h->launches += it->second.nkernels;   // tested sweeps add the extra body passes once the counts are read
-    for (int q = 0; q < ISDC_MAXM; ++q) h->last_body[q] = it->second.body[q];
+    for (int q = 0; q < ISDC_MAXM; ++q) { h->last_body[q] = it->second.body[q]; h->last_wbody[q] = it->second.wbody[q]; }
     if (h->prof) {  // the graph's event pairs hold this launch's timings
         CUDA_TRY(h, cudaStreamSynchronize(h->s));
         for (auto &p : it->second.events) {
@@ -1557,6 +1667,19 @@ isdc_status graph_sweep(isdc_ctx *h) {
             cudaEventElapsedTime(&ms, h->evpool[p.a], h->evpool[p.b]);
             h->prof_ms[p.cls] += ms; h->prof_cnt[p.cls] += 1; h->prof_bytes[p.cls] += p.bytes;
         }
+    }
+    return ISDC_OK;
+}
+
+// the device W-solve's counters (W-cycles per residual node; launches of the extra loop passes)
+isdc_status read_wcycles(isdc_ctx *h) {
+    SdcCtl ctl;
+    CUDA_TRY(h, cudaMemcpyAsync(&ctl, h->ctl, sizeof(SdcCtl), cudaMemcpyDeviceToHost, h->s));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    if (ctl.err) { h->err = "non-finite W defect"; return ISDC_ERR_NONFINITE; }
+    for (int m = 1; m < h->M; ++m) {
+        h->wcyc += ctl.wcn[m];
+        h->launches += (long)(ctl.wcn[m] - 1) * h->last_wbody[m];
     }
     return ISDC_OK;
 }
@@ -1571,6 +1694,10 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
         h->cur = 1 - h->cur;
         h->spread = false;
         h->fold_valid[h->cur] = folds_on(h);   // the residual stored the folds of the new iterate
+        if (h->graphs && dev_wsolve(h)) {
+            TRY(read_wcycles(h));
+            return read_residual(h, res_per_node, res_max, true);
+        }
         return read_residual(h, res_per_node, res_max);
     }
     if (h->graphs && h->dev_sdc && h->prof == 0) {
@@ -1590,6 +1717,13 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
         h->cur = 1 - h->cur;
         h->spread = false;
         h->fold_valid[h->cur] = folds_on(h);
+        if (dev_wsolve(h)) {
+            for (int m = 1; m < M; ++m) {
+                h->wcyc += ctl.wcn[m];
+                h->launches += (long)(ctl.wcn[m] - 1) * h->last_wbody[m];
+            }
+            return read_residual(h, res_per_node, res_max, true);
+        }
         return read_residual(h, res_per_node, res_max);
     }
     double *uold[ISDC_MAXM];
@@ -1819,6 +1953,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         }
     }
     cudaError_t e = cudaMemcpyAsync(h->Ginv, Gi.data(), Gi.size() * sizeof(double), cudaMemcpyHostToDevice, h->s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->ctl, 0, sizeof(SdcCtl), h->s);   // the workspace is not zeroed
     if (e == cudaSuccess && h->Gp) {
         // the pad column of every pitched field is never read; copy G into the pitched layout
         const GridDesc &g = h->lev[0].g;
