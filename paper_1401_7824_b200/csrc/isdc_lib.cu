@@ -140,7 +140,8 @@ struct isdc_ctx {
     int small_n = 511;         // ISDC_SMALL_N: levels n <= small_n use the short tiles below (more CTAs)
     int sr_ty_small = 8, sm_ty_small = 8;   // ISDC_SR_TY_SMALL / ISDC_SM_TY_SMALL (8 or 16)            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
-    bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
+    bool bl16 = true;
+    bool bl_nm4 = false;       // ISDC_BL_NM4=1: 3D residual in one pass (4 nodes, 12 warps x 1 row)          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
     bool fuse3d = false;       // ISDC_FUSE3D=1: fused 3D prolongation + smoother (slower so far)
     bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
@@ -641,10 +642,11 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     // rings cost 14 * RR * NM doubles per thread: NM = 1 -> RR = 4, NM = 2 -> RR = 2 (or RR = 1 with
     // 16 warps: the same 16-row region, twice the warps), NM = 4 -> RR = 1
     const bool w16 = (nm == 2) && h->bl16;
+    const bool w12 = (nm == 4) && h->bl_nm4;   // 12 warps x 1 row: 170 registers for the 4 nodes' rings
     const bool r16 = (nm == 1) && h->rhs16;   // RHS: 16 warps x 2 rows (same 32-row region as 8 x 4)
     int rr = (nm == 1) ? (r16 ? 2 : 4) : (nm == 2 && !w16 ? 2 : 1), ns = (nm == 4) ? 6 : 4;
     auto smem_of = [&](int r_, int ns_) {
-        return w16 ? f3d::BLShape<1, 16>::smem(K, ns_, nm) : r16 ? f3d::BLShape<2, 16>::smem(K, ns_, nm)
+        return w12 ? f3d::BLShape<1, 12>::smem(K, ns_, nm) : w16 ? f3d::BLShape<1, 16>::smem(K, ns_, nm) : r16 ? f3d::BLShape<2, 16>::smem(K, ns_, nm)
                    : (r_ == 4 ? f3d::BLShape<4>::smem(K, ns_, nm)
                               : (r_ == 2 ? f3d::BLShape<2>::smem(K, ns_, nm) : f3d::BLShape<1>::smem(K, ns_, nm)));
     };
@@ -656,7 +658,7 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
         while (ns >= 2 && sm8(ns) > (size_t)kMaxDynSmem) --ns;
     }
     if (ns < 2) { h->err = "too many fields for the 3D stream kernel"; return ISDC_ERR_UNSUPPORTED; }
-    int rh = w16 ? 16 : (r16b ? 32 : f3d::NW * rr);
+    int rh = w12 ? 12 : (w16 ? 16 : (r16b ? 32 : f3d::NW * rr));
     f3d::BLMaps maps;
     for (int k = 0; k < K; ++k) {
         const CUtensorMap *mk = tmap(h, fields[k], g, f3d::RW + 2, rh, 1);
@@ -673,6 +675,7 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     int fe = h->fe.kind;
 #define ISDC_BL(FE_, RR_, NM_) kl(h, f3d::k_bl<FE_, MODE, RR_, NM_>, grd, f3d::NT, sm)(maps, A, ns)
 #define ISDC_BL16(FE_) kl(h, f3d::k_bl<FE_, MODE, 1, 2, 16>, grd, 512, sm)(maps, A, ns)
+#define ISDC_BL12(FE_) kl(h, f3d::k_bl<FE_, MODE, 1, 4, 12>, grd, 384, sm)(maps, A, ns)
 #define ISDC_RHS16(FE_) kl(h, f3d::k_bl<FE_, MODE, 2, 1, 16>, grd, 512, sm)(maps, A, ns)
 #define ISDC_BL_FE(RR_, NM_)                                                   \
     do {                                                                       \
@@ -685,9 +688,11 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     else if (nm == 1) { if (rr == 4) ISDC_BL_FE(4, 1); else ISDC_BL_FE(2, 1); }
     else if (w16) { if (fe == 0) ISDC_BL16(0); else if (fe == 1) ISDC_BL16(1); else if (fe == 2) ISDC_BL16(2); else ISDC_BL16(3); }
     else if (nm == 2) ISDC_BL_FE(2, 2);
+    else if (w12) { if (fe == 0) ISDC_BL12(0); else if (fe == 1) ISDC_BL12(1); else if (fe == 2) ISDC_BL12(2); else ISDC_BL12(3); }
     else ISDC_BL_FE(1, 4);
 #undef ISDC_BL_FE
 #undef ISDC_BL16
+#undef ISDC_BL12
 #undef ISDC_RHS16
 #undef ISDC_BL
     prof_end(h, pe, prof_cls, bytes);
@@ -1213,7 +1218,7 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         double dt = h->P.dt, nudt = h->P.nu * dt;
         // two nodes per pass (RR = 2); the single-pass NM = 4 / RR = 1 variant measured slower
         // (cfg 5: 8.7 ms vs 2 x 3.4 ms per residual: 208 registers, 8-row regions)
-        const int per = 2;
+        const int per = h->bl_nm4 ? 4 : 2;   // ISDC_BL_NM4=1: all four nodes in one pass (12 warps x 1 row)
         const int passes = (M - 1 + per - 1) / per;
         for (int m0 = 1; m0 < M; m0 += per) {
             const int nm = std::min(per, M - m0) == 3 ? 2 : std::min(per, M - m0);
@@ -1814,6 +1819,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';
     if (const char *b16 = getenv("ISDC_BL16")) h->bl16 = b16[0] != '0';
+    if (const char *b4 = getenv("ISDC_BL_NM4")) h->bl_nm4 = b4[0] != '0';
     if (const char *r16 = getenv("ISDC_RHS16")) h->rhs16 = r16[0] != '0';
     if (const char *t2 = getenv("ISDC_TAIL2D")) h->tail2d = atoi(t2);
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
@@ -1874,7 +1880,9 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         ISDC_BL_ATTR(0, MODE_, RR_, NM_) ISDC_BL_ATTR(1, MODE_, RR_, NM_) ISDC_BL_ATTR(2, MODE_, RR_, NM_) ISDC_BL_ATTR(3, MODE_, RR_, NM_)
         ISDC_BL_ATTR4(0, 4, 1) ISDC_BL_ATTR4(0, 2, 1) ISDC_BL_ATTR4(1, 4, 1) ISDC_BL_ATTR4(1, 2, 1) ISDC_BL_ATTR4(1, 2, 2)
         ISDC_BL_ATTR4(0, 2, 2) ISDC_BL_ATTR4(1, 1, 4) ISDC_BL_ATTR4(2, 4, 1) ISDC_BL_ATTR4(2, 2, 1)
-        for (auto kern : {f3d::k_bl<0, 1, 1, 2, 16>, f3d::k_bl<1, 1, 1, 2, 16>, f3d::k_bl<2, 1, 1, 2, 16>,
+        for (auto kern : {f3d::k_bl<0, 1, 1, 4, 12>, f3d::k_bl<1, 1, 1, 4, 12>, f3d::k_bl<2, 1, 1, 4, 12>,
+                          f3d::k_bl<3, 1, 1, 4, 12>,
+                          f3d::k_bl<0, 1, 1, 2, 16>, f3d::k_bl<1, 1, 1, 2, 16>, f3d::k_bl<2, 1, 1, 2, 16>,
                           f3d::k_bl<3, 1, 1, 2, 16>, f3d::k_bl<0, 0, 2, 1, 16>, f3d::k_bl<1, 0, 2, 1, 16>,
                           f3d::k_bl<2, 0, 2, 1, 16>, f3d::k_bl<3, 0, 2, 1, 16>, f3d::k_bl<0, 2, 2, 1, 16>,
                           f3d::k_bl<1, 2, 2, 1, 16>, f3d::k_bl<2, 2, 2, 1, 16>, f3d::k_bl<3, 2, 2, 1, 16>})
