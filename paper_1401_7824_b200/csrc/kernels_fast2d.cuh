@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
 // warps per strip (NMW nodes each; the extra loads of the same rows hit L1/L2), which halves the
 // register rings and doubles the resident warps.
 template <int FE, int MM, int NMW, bool WRT = false, bool WF = false>   // WRT: also store the r~_m fields (unweighted
-__global__ void __launch_bounds__(SW_NT, NMW == 1 ? 3 : 2) k_resid_s(StreamArgs A) {              // residual); WF: the next sweep's RHS folds
+__global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {              // residual); WF: the next sweep's RHS folds
     pdl_launch();
     pdl_wait();
     constexpr int G = (MM - 1) / NMW;
