@@ -10,10 +10,11 @@ namespace f2d {
 
 // ---------------------------------------------------------------------------------------------
 // Fused two-sweep weighted Jacobi (one HBM pass: read u, b; write u''), DESIGN.md §6.1.
-// Tile: 64 x 32 outputs per CTA, 256 threads (8 warps).  Smem: u box 68x36 at (x0-2, y0-2),
-// b box 68x34 at (x0-2, y0-1) (TMA, zero fill outside the domain), t = first sweep on the
-// 66x34 region at (x0-1, y0-1) (zero outside the domain).  Warp w owns the 32-column half
-// (w & 1) of a band of rows (w >> 1); each lane rolls a 3-row register window down its column.
+// Tile: 64 x TY outputs per CTA (TY = 16 by default; 24 / 8 on big / small levels, the TY_
+// template), 256 threads (8 warps).  Smem: u box 68 x (TY+4) at (x0-2, y0-2), b box 68 x (TY+2)
+// at (x0-2, y0-1) (TMA, zero fill outside the domain), t = first sweep on the 66 x (TY+2) region
+// at (x0-1, y0-1) (zero outside the domain).  Warp w owns the 32-column half (w & 1) of a band of
+// rows (w >> 1); each lane rolls a 3-row register window down its column.
 // Optional: NORM -> ||b - S u||_inf over the tile (the SDC defect test of the incoming iterate).
 // ---------------------------------------------------------------------------------------------
 constexpr int TX = 64, TY = 16, NT = 256;   // 16-row tiles: ~33 KB smem -> 6 CTAs / SM to overlap TMA and compute
@@ -820,12 +821,12 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {           
 // ---------------------------------------------------------------------------------------------
 // Fused pre-smoother + defect + full-weighting restriction: one pass reads
 // u, b and writes the smoothed iterate u'' (tile) and b_c = R(b - S u'') (coarse tile), 26 B per
-// fine point instead of 24 + 18.  Fine tile 58 x 32 at (x0, y0), coarse tile 29 x 16 at
+// fine point instead of 24 + 18.  Fine tile 58 x TY at (x0, y0), coarse tile 29 x TY/2 at
 // (x0/2, y0/2).  Local regions (x, y relative to the tile origin):
-//   t   (sweep 1)  [-2, 60] x [-2, 34]      u'' (sweep 2)  [-1, 59] x [-1, 33]
-//   d   (defect)   [ 0, 58] x [ 0, 32]      u box [-4, 61] x [-3, 35],  b box [-2, 61] x [-2, 34]
-// u'' overwrites the u buffer after sweep 1, d overwrites the t buffer after sweep 2.
-// MODE 0: u from memory; MODE 1: u == 0 (nothing read).
+//   t   (sweep 1)  [-2, 60] x [-2, TY+2]    u'' (sweep 2)  [-1, 59] x [-1, TY+1]
+//   d   (defect)   [ 0, 58] x [ 0, TY]      u box [-4, 61] x [-3, TY+3],  b box [-2, 61] x [-2, TY+2]
+// u'' overwrites the u buffer after sweep 1; the defect and the full weighting stay in registers
+// (fr_defect_fw).  MODE 0: u from memory; MODE 1: u == 0 (nothing read).
 // ---------------------------------------------------------------------------------------------
 // Tile height TY (rows): 32 on the large levels (half the band-start loads per output of 16-row
 // tiles; ~58 KB -> 3 CTAs/SM), 16 on the small ones (more CTAs).  FR_TY16 / FR_TY32 below.
