@@ -132,7 +132,8 @@ struct isdc_ctx {
                                // trigger, slower with an early trigger)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
     bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
-    int res_nmw = 2;           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
+    int res_nmw = 2;
+    bool tail_fuse_dr = true;   // ISDC_TAIL_FUSE=0: 2D tail with a separate defect phase (fused: cfg1 -2 %)           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
     int sr_ty = 32;            // ISDC_SR_TY: their height (24 or 32)
     int sm_ty32_min = 2047;    // ISDC_SM_TY32_MIN: the same for k_smooth2
@@ -1827,6 +1828,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *st = getenv("ISDC_SR_TY32_MIN")) h->sr_ty32_min = atoi(st);
     if (const char *st = getenv("ISDC_SR_TY")) h->sr_ty = atoi(st) == 24 ? 24 : 32;
     if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
+    if (const char *tf = getenv("ISDC_TAIL_FUSE")) h->tail_fuse_dr = tf[0] != '0';
     if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
     if (const char *st = getenv("ISDC_SM_TY")) h->sm_ty = atoi(st) == 24 ? 24 : 32;
     if (const char *st = getenv("ISDC_SMALL_N")) h->small_n = atoi(st);
@@ -1928,6 +1930,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                 T.nu1 = prob->mg.nu1; T.nu2 = prob->mg.nu2;
                 T.Ginv = h->Ginv + (size_t)m * Pc * Pc;
                 T.b_in = nullptr; T.u_in = nullptr; T.u_out = nullptr; T.pitch = 0;
+                T.fuse_dr = h->tail_fuse_dr ? 1 : 0;
             }
             h->tail_smem = (h->d == 2) ? tail_smem_bytes<2>(h->tailp[0]) : tail_smem_bytes<3>(h->tailp[0]);
             if (h->tailp[0].nlev > TAIL_MAX_LEVELS || tail_dispatch(h, h->tailp[0], true) != ISDC_OK) h->tail_l0 = -1;

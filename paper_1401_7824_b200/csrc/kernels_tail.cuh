@@ -24,6 +24,7 @@ struct TailParams {
     const double *u_in;             // pitched initial iterate, or null for zero
     double *u_out;                  // pitched result
     int pitch;                      // pitch of b_in / u_in / u_out (n0 + 1)
+    int fuse_dr;                    // 2D: defect formed inside the restriction phase
 };
 
 template <int D>
@@ -143,6 +144,26 @@ __device__ __noinline__ void tail_ph_restrict(int od, int obc, int n, int nc) {
         return ((8.0 * d[o] + 4.0 * faces) + (2.0 * edges + co)) * 0.015625;
     });
 }
+// b_c = R (b - S u) with the defect formed on the fly at the 9 fine points of each coarse point
+// (2D; the same tail_S / restriction trees as tail_ph_defect + tail_ph_restrict, one barrier less)
+__device__ __noinline__ void tail_ph_defect_restrict2(int ou, int ob, int obc, int n, int nc, SCoef c) {
+    const double *u = tsm + ou, *B = tsm + ob;
+    double *Bc = tsm + obc;
+    const int np = n + 2;
+    tail_map<2>(nc, Bc, [&](int, int I, int J, int) {
+        const int o = 1 + np * (2 * J + 2) + 2 * I + 1;
+        auto d = [&](int q) { return B[q] - tail_S<2>(u, q, np, 0, c); };
+        const double dmm = d(o - np - 1), dmp = d(o - np + 1), dpm = d(o + np - 1), dpp = d(o + np + 1);
+        const double dcm = d(o - 1), dcp = d(o + 1), dmc = d(o - np), dpc = d(o + np), dcc = d(o);
+        const double rm = dmm + dmp;
+        const double rc = dcm + dcp;
+        const double rp = dpm + dpp;
+        const double f = rc + (dmc + dpc);
+        const double e = rm + rp;
+        return ((4.0 * dcc + 2.0 * f) + e) * 0.0625;
+    });
+}
+
 // u += P e                             (sums nest x, then y, then z; one multiply by 0.5^#even)
 template <int D>
 __device__ __noinline__ void tail_ph_prolong(int oe, int ou, int n, int nc) {
@@ -213,9 +234,13 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailParams P) {
     for (int l = 0; l < L - 1; ++l) {
         smooth(l, P.nu1);
         const int w = (cur >> l) & 1;
-        tail_ph_defect<D>(ofs(l, w), ofs(l, 1 - w), ofs(l, 2), P.n[l], P.c[l]);
-        __syncthreads();
-        tail_ph_restrict<D>(ofs(l, 1 - w), ofs(l + 1, 2), P.n[l], P.n[l + 1]);
+        if (D == 2 && P.fuse_dr) {
+            tail_ph_defect_restrict2(ofs(l, w), ofs(l, 2), ofs(l + 1, 2), P.n[l], P.n[l + 1], P.c[l]);
+        } else {
+            tail_ph_defect<D>(ofs(l, w), ofs(l, 1 - w), ofs(l, 2), P.n[l], P.c[l]);
+            __syncthreads();
+            tail_ph_restrict<D>(ofs(l, 1 - w), ofs(l + 1, 2), P.n[l], P.n[l + 1]);
+        }
         __syncthreads();
         // the next level starts from a zero iterate (its buffers are zero except where written;
         // buffer 0 of level l+1 has never been written at this point of the down sweep)
