@@ -132,8 +132,8 @@ struct isdc_ctx {
                                // trigger, slower with an early trigger)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
     bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
-    int res_nmw = 2;
-    bool tail_fuse_dr = true;   // ISDC_TAIL_FUSE=0: 2D tail with a separate defect phase (fused: cfg1 -2 %)           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
+    int res_nmw = 2;           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
+    bool tail_fuse_dr = true;  // ISDC_TAIL_FUSE=0: 2D tail with a separate defect phase (fused: cfg1 -2 %)
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
     int sr_ty = 32;            // ISDC_SR_TY: their height (24 or 32)
     int sm_ty32_min = 2047;    // ISDC_SM_TY32_MIN: the same for k_smooth2
@@ -141,8 +141,8 @@ struct isdc_ctx {
     int small_n = 511;         // ISDC_SMALL_N: levels n <= small_n use the short tiles below (more CTAs)
     int sr_ty_small = 8, sm_ty_small = 8;   // ISDC_SR_TY_SMALL / ISDC_SM_TY_SMALL (8 or 16)            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
-    bool bl16 = true;
-    bool bl_nm4 = false;       // ISDC_BL_NM4=1: 3D residual in one pass (4 nodes, 12 warps x 1 row)          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
+    bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
+    bool bl_nm4 = false;       // ISDC_BL_NM4=1: 3D residual in one pass (4 nodes, 12 warps x 1 row; slower)
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
     bool fuse3d = false;       // ISDC_FUSE3D=1: fused 3D prolongation + smoother (slower so far)
     bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
