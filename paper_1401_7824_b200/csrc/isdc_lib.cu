@@ -137,9 +137,9 @@ struct isdc_ctx {
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
     int sr_ty = 32;            // ISDC_SR_TY: their height (24 or 32)
     int sm_ty32_min = 2047;    // ISDC_SM_TY32_MIN: the same for k_smooth2
-    int sm_ty = 24;
+    int sm_ty = 24;            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
     int small_n = 511;         // ISDC_SMALL_N: levels n <= small_n use the short tiles below (more CTAs)
-    int sr_ty_small = 8, sm_ty_small = 8;   // ISDC_SR_TY_SMALL / ISDC_SM_TY_SMALL (8 or 16)            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
+    int sr_ty_small = 8, sm_ty_small = 8;   // ISDC_SR_TY_SMALL / ISDC_SM_TY_SMALL (8 or 16)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
     bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
     bool bl_nm4 = false;       // ISDC_BL_NM4=1: 3D residual in one pass (4 nodes, 12 warps x 1 row; slower)
