@@ -222,3 +222,37 @@ def test_execution_paths_bitwise(gpu, ora, monkeypatch, env, mode):
         assert np.array_equal(st["node_cycles"], st_ref["node_cycles"])
         assert np.array_equal(st["res_hist"], st_ref["res_hist"])
         assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)
+
+
+# --------------------------------------------------------------------------- edge cases
+EDGE = [  # (dim, n, M, L, nu1, nu2, guess, mode, fe)
+    (2, 3, 2, 2, 2, 2, 0, MODE_ISDC, FE_NONE),         # a single level: the exact coarse solve only
+    (3, 3, 3, 1, 2, 2, 0, MODE_SDC, FE_NONE),
+    (2, 7, 8, 1, 1, 0, 0, MODE_ISDC, FE_CUBIC),        # M = 8 (the maximum), L = 1, V(1,0)
+    (2, 63, 2, 3, 0, 2, 0, MODE_ISDC, FE_FORCING),     # M = 2, V(0,2): no pre-smoothing
+    (2, 127, 5, 2, 3, 1, 0, MODE_ISDC, FE_NONE),       # V(3,1): an extra unfused pre-sweep on the fast levels
+    (3, 31, 3, 2, 1, 3, 0, MODE_ISDC, FE_ADVECTION),   # odd sweep counts in 3D
+    (2, 127, 3, 2, 2, 2, 2, MODE_SDC, FE_NONE),        # initial guess u_m^{k+1} (P:187 ablation)
+    (2, 63, 3, 2, 2, 2, 1, MODE_SDC, FE_NONE),         # zero initial guess
+    (3, 15, 3, 2, 2, 2, 2, MODE_SDC, FE_NONE),
+]
+
+
+@pytest.mark.parametrize("dim,n,M,L,nu1,nu2,guess,mode,fe", EDGE)
+def test_edge_cases_bitwise(gpu, ora, dim, n, M, L, nu1, nu2, guess, mode, fe):
+    cfg = synth.Config(0, dim, n, M, 0.01, 0.7, fe, fe_a=(1.0, -0.5, 0.25), L=L, nu1=nu1, nu2=nu2,
+                       sweep_tol=1e-9, max_sweeps=60)
+    G = synth.forcing_field(n, dim) if fe == FE_FORCING else None
+    u0 = synth.random_field(n, dim, 77)
+    h = make(gpu, cfg, G, mode=mode, guess=guess)
+    h.set_initial(torch.from_numpy(u0).cuda(), 0)
+    prob = ora.Problem(cfg, G, mode=mode, guess=guess)
+    u_ref = u0.copy()
+    for s in range(2):
+        st = h.step()
+        u_ref, st_ref = ora.step(prob, u_ref, float(s) * cfg.dt)
+        assert st["sweeps"] == st_ref["sweeps"] and st["vcycles"] == st_ref["vcycles"]
+        assert st["converged"] == st_ref["converged"]
+        assert np.array_equal(st["node_cycles"], st_ref["node_cycles"])
+        assert np.array_equal(st["res_hist"], st_ref["res_hist"])
+        assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)
