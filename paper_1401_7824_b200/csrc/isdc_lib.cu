@@ -159,7 +159,11 @@ struct isdc_ctx {
     cudaStream_t cap = nullptr;
     cudaStream_t cap2 = nullptr;   // capture stream of conditional-node bodies (device SDC loop)
     struct SdcCtl *ctl = nullptr;  // device SDC loop state (workspace)
+    unsigned long long *hist = nullptr;   // fixed-sweep steps: residual slots of every sweep (workspace)
+    cudaGraphExec_t step_exec = nullptr;  // fixed-sweep step as one graph (ISDC mode)
+    long step_nkernels = 0;
     bool dev_sdc = true;           // ISDC_DEVICE_SDC=0: SDC / capped node solves tested on the host
+    bool step_graph = true;        // ISDC_STEP_GRAPH=0: fixed-sweep steps sweep by sweep
     bool graphs = true;
     struct Graph {
         cudaGraphExec_t exec = nullptr; std::vector<Pending> events; long nkernels = 0;
@@ -185,6 +189,7 @@ struct isdc_ctx {
         for (auto e : evpool) cudaEventDestroy(e);
         if (cap) cudaStreamDestroy(cap);
         if (cap2) cudaStreamDestroy(cap2);
+        if (step_exec) cudaGraphExecDestroy(step_exec);
     }
 };
 
@@ -399,7 +404,10 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     double *ctd = (double *)take(ISDC_MAXM * sizeof(double));
     unsigned long long *al = (unsigned long long *)take(3 * ISDC_MAXM * sizeof(unsigned long long));
     SdcCtl *ctl = (SdcCtl *)take(sizeof(SdcCtl));
-    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; h->ctl = ctl; }
+    unsigned long long *hist = nullptr;
+    if (p->solve.fixed_sweeps > 0 && p->solve.fixed_sweeps <= 256)
+        hist = (unsigned long long *)take((size_t)p->solve.fixed_sweeps * (M - 1) * sizeof(unsigned long long));
+    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; h->ctl = ctl; h->hist = hist; }
     return off;
 }
 
@@ -1677,6 +1685,74 @@ isdc_status graph_sweep(isdc_ctx *h) {
     return ISDC_OK;
 }
 
+// A fixed-sweep step (config 1: K sweeps, no tolerance test) in ISDC mode as ONE graph: the K
+// sweeps alternate the iterate sets exactly as the host loop would, and each residual's M-1 slots
+// are copied into the device history `hist` (read once per step).  The step starts from the
+// spread state in set 0.
+isdc_status graph_fixed_step(isdc_ctx *h, int K, double *res_hist, double *res_last) {
+    const int M = h->M;
+    if (!h->step_exec) {
+        if (!h->cap) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+        const int cur0 = h->cur;
+        const bool spread0 = h->spread, fv0 = h->fold_valid[0], fv1 = h->fold_valid[1];
+        cudaStream_t user = h->s;
+        const long l0 = h->launches;
+        h->s = h->cap;
+        h->capturing = true;
+        cudaError_t e = cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal);
+        isdc_status st = e == cudaSuccess ? ISDC_OK : ISDC_ERR_CUDA;
+        for (int k = 0; k < K && st == ISDC_OK; ++k) {
+            st = enqueue_isdc_sweep(h);
+            if (st == ISDC_OK &&
+                cudaMemcpyAsync(h->hist + (size_t)k * (M - 1), h->red + SLOT_RES0, (M - 1) * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToDevice, h->s) != cudaSuccess)
+                st = ISDC_ERR_CUDA;
+            h->cur = 1 - h->cur;
+            h->spread = false;
+            h->fold_valid[h->cur] = folds_on(h);
+        }
+        cudaGraph_t g = nullptr;
+        cudaError_t e2 = cudaStreamEndCapture(h->cap, &g);
+        h->capturing = false;
+        h->s = user;
+        h->cur = cur0; h->spread = spread0; h->fold_valid[0] = fv0; h->fold_valid[1] = fv1;
+        if (e != cudaSuccess || e2 != cudaSuccess || st != ISDC_OK) {
+            if (g) cudaGraphDestroy(g);
+            if (st == ISDC_OK || st == ISDC_ERR_CUDA)
+                h->err = std::string("step graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
+            return st == ISDC_OK ? ISDC_ERR_CUDA : st;
+        }
+        h->step_nkernels = h->launches - l0;
+        h->launches = l0;
+        CUDA_TRY(h, cudaGraphInstantiate(&h->step_exec, g, 0));
+        cudaGraphDestroy(g);
+    }
+    CUDA_TRY(h, cudaGraphLaunch(h->step_exec, h->s));
+    h->launches += h->step_nkernels;
+    for (int k = 0; k < K; ++k) {
+        h->cur = 1 - h->cur;
+        h->spread = false;
+        h->fold_valid[h->cur] = folds_on(h);
+    }
+    std::vector<unsigned long long> raw((size_t)K * (M - 1));
+    CUDA_TRY(h, cudaMemcpyAsync(raw.data(), h->hist, raw.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->s));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    for (int k = 0; k < K; ++k) {   // read_residual's reduction of each sweep's slots
+        double mx = 0.0;
+        bool bad = false;
+        for (int m = 0; m < M - 1; ++m) {
+            double v;
+            std::memcpy(&v, &raw[(size_t)k * (M - 1) + m], sizeof v);
+            if (!std::isfinite(v)) bad = true;
+            if (v > mx) mx = v;
+        }
+        if (bad) { h->err = "non-finite residual"; return ISDC_ERR_NONFINITE; }
+        if (res_hist) res_hist[k] = mx;
+        *res_last = mx;
+    }
+    return ISDC_OK;
+}
+
 // the device W-solve's counters (W-cycles per residual node; launches of the extra loop passes)
 isdc_status read_wcycles(isdc_ctx *h) {
     SdcCtl ctl;
@@ -1912,6 +1988,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         }
     }
     if (const char *ds = getenv("ISDC_DEVICE_SDC")) h->dev_sdc = ds[0] != '0';
+    if (const char *sg = getenv("ISDC_STEP_GRAPH")) h->step_graph = sg[0] != '0';
     const char *eg = getenv("ISDC_NO_GRAPHS");
     h->graphs = !(eg && eg[0] == '1');
     // single-CTA tail: levels n <= 63 (2D) / 15 (3D) in shared memory
@@ -2079,6 +2156,15 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     int k = 0, caps = 0, conv = 0;
     long vc = 0;
     double res = 0.0;
+    if (o.fixed_sweeps > 0 && o.mode == ISDC_MODE_ISDC_FIXED && h->graphs && h->prof == 0 &&
+        h->P.residual_kind == 0 && h->hist && h->spread && h->cur == 0 && h->step_graph) {
+        // the whole fixed-sweep step as one graph: no host synchronisation between its sweeps
+        TRY(graph_fixed_step(h, o.fixed_sweeps, res_hist, &res));
+        k = o.fixed_sweeps;
+        vc = (long)k * (h->M - 1) * o.L;
+        if (node_cycles)
+            for (int q = 0; q < k * (h->M - 1); ++q) node_cycles[q] = o.L;
+    }
     while (k < kmax) {
         int cyc[ISDC_MAXM], cap = 0;
         TRY(sweep_impl(h, nullptr, &res, cyc, &cap));

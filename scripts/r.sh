@@ -1,2 +1,3 @@
-ISDC_TAIL_FUSE=1 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "not cfg5" 2>&1 | tail -2 > gpurun_out/par.log
-for f in 0 1; do ISDC_TAIL_FUSE=$f python bench.py --config 1 --steps 20 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/b1_f$f.json 2>/dev/null; ISDC_TAIL_FUSE=$f python bench.py --config 2 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b2_f$f.json 2>/dev/null; ISDC_TAIL_FUSE=$f python bench.py --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b3_f$f.json 2>/dev/null; done
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/par.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+for sg in 0 1; do ISDC_STEP_GRAPH=$sg python bench.py --config 1 --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/b1_sg$sg.json 2>/dev/null; done
