@@ -58,6 +58,49 @@ __global__ void k_sdc_test(SdcCtl *ctl, int m, unsigned long long *dslot, int ca
     }
 }
 
+// Whole ISDC steps on the device (tolerance-stopped): the sweep count, the iterate set holding the
+// latest sweep and the residual history, maintained by k_step_test after every sweep's residual.
+constexpr int kStepHist = 1024;
+struct StepCtl {
+    int k;                   // sweeps done
+    int last;                // iterate set written by the last sweep
+    int bad;                 // a residual came out non-finite
+    int cont;                // the last test's verdict (continue sweeping)
+    double hist[kStepHist];  // max_m ||r~_m|| after each sweep (read_residual's reduction)
+};
+__global__ void k_step_init(StepCtl *ctl) {
+    pdl_wait();
+    if (threadIdx.x == 0) { ctl->k = 0; ctl->last = 0; ctl->bad = 0; ctl->cont = 0; }
+}
+// after a sweep that wrote set `set_after`: record its residual; continue while r >= tol and k < kmax.
+// The verdict goes to ctl->cont and, if hset, to the conditional handle hc.
+__global__ void k_step_test(StepCtl *ctl, const unsigned long long *slots, int nm, double tol, int kmax, int set_after,
+                            cudaGraphConditionalHandle hc, int hset) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        bool bad = false;
+        for (int m = 0; m < nm; ++m) {
+            const double v = __longlong_as_double((long long)slots[m]);
+            if (!isfinite(v)) bad = true;
+            if (v > mx) mx = v;
+        }
+        const int k = ctl->k;
+        ctl->hist[k] = mx;
+        ctl->k = k + 1;
+        ctl->last = set_after;
+        if (bad) ctl->bad = 1;
+        const unsigned cont = (!bad && !(mx < tol) && k + 1 < kmax) ? 1u : 0u;
+        ctl->cont = (int)cont;
+        if (hset) cudaGraphSetConditional(hc, cont);
+    }
+}
+// at the end of a loop body: continue the WHILE loop iff the last test said so
+__global__ void k_step_loop(const StepCtl *ctl, cudaGraphConditionalHandle hw) {
+    pdl_wait();
+    if (threadIdx.x == 0) cudaGraphSetConditional(hw, (unsigned)ctl->cont);
+}
+
 // residual_kind 1 (NEXT f2) on the device: the W-solve of unweighted_norms, one node m at a time
 __global__ void k_w_init(SdcCtl *ctl, int m, const unsigned long long *rslot, double w_tol) {
     pdl_wait();
@@ -162,6 +205,10 @@ struct isdc_ctx {
     unsigned long long *hist = nullptr;   // fixed-sweep steps: residual slots of every sweep (workspace)
     cudaGraphExec_t step_exec = nullptr;  // fixed-sweep step as one graph (ISDC mode)
     long step_nkernels = 0;
+    cudaGraphExec_t tstep_exec = nullptr; // tolerance-stopped ISDC step as one graph (conditional loop)
+    long tstep_n[3] = {0, 0, 0};          // kernels of its first sweep / loop sweep A (+ tests) / sweep B
+    struct StepCtl *sctl = nullptr;       // its device state (workspace)
+    cudaStream_t cap3 = nullptr;          // capture stream of the nested IF body
     bool dev_sdc = true;           // ISDC_DEVICE_SDC=0: SDC / capped node solves tested on the host
     bool step_graph = true;        // ISDC_STEP_GRAPH=0: fixed-sweep steps sweep by sweep
     bool graphs = true;
@@ -190,6 +237,8 @@ struct isdc_ctx {
         if (cap) cudaStreamDestroy(cap);
         if (cap2) cudaStreamDestroy(cap2);
         if (step_exec) cudaGraphExecDestroy(step_exec);
+        if (tstep_exec) cudaGraphExecDestroy(tstep_exec);
+        if (cap3) cudaStreamDestroy(cap3);
     }
 };
 
@@ -407,7 +456,8 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     unsigned long long *hist = nullptr;
     if (p->solve.fixed_sweeps > 0 && p->solve.fixed_sweeps <= 256)
         hist = (unsigned long long *)take((size_t)p->solve.fixed_sweeps * (M - 1) * sizeof(unsigned long long));
-    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; h->ctl = ctl; h->hist = hist; }
+    StepCtl *sctl = (StepCtl *)take(sizeof(StepCtl));
+    if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; h->ctl = ctl; h->hist = hist; h->sctl = sctl; }
     return off;
 }
 
@@ -1491,37 +1541,45 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
 // taking the handle) is enqueued first and sets the condition; `body` is captured into the loop
 // body on h->cap2 and must end with the same test.  Used by the device-side node-solve and W-solve
 // loops.
+// pre: a handle already created on the graph being captured (its condition set by earlier work),
+// or nullptr to create one here
 template <typename TestF, typename BodyF>
-isdc_status capture_while(isdc_ctx *h, TestF test, BodyF body) {
-    if (!h->cap2) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap2, cudaStreamNonBlocking));
+isdc_status capture_cond(isdc_ctx *h, cudaGraphConditionalNodeType type, cudaStream_t &bs,
+                         const cudaGraphConditionalHandle *pre, TestF test, BodyF body) {
+    if (!bs) CUDA_TRY(h, cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
     cudaStreamCaptureStatus cs;
     cudaGraph_t cg = nullptr;
     const cudaGraphNode_t *deps = nullptr;
     size_t ndeps = 0;
     CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs, nullptr, &cg, &deps, &ndeps));
     cudaGraphConditionalHandle hnd;
-    CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hnd, cg, 0, 0));
+    if (pre) hnd = *pre;
+    else CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hnd, cg, 0, 0));
     TRY(test(hnd));
     CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs, nullptr, &cg, &deps, &ndeps));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = hnd;
-    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.type = type;
     cp.conditional.size = 1;
     cudaGraphNode_t cn;
     CUDA_TRY(h, cudaGraphAddNode(&cn, cg, deps, ndeps, &cp));
     cudaGraph_t bg = cp.conditional.phGraph_out[0];
     CUDA_TRY(h, cudaStreamUpdateCaptureDependencies(h->s, &cn, 1, cudaStreamSetCaptureDependencies));
     cudaStream_t outer = h->s;
-    CUDA_TRY(h, cudaStreamBeginCaptureToGraph(h->cap2, bg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    h->s = h->cap2;
+    CUDA_TRY(h, cudaStreamBeginCaptureToGraph(bs, bg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    h->s = bs;
     isdc_status st = body(hnd);
     cudaGraph_t bo = nullptr;
-    cudaError_t ee = cudaStreamEndCapture(h->cap2, &bo);
+    cudaError_t ee = cudaStreamEndCapture(bs, &bo);
     h->s = outer;
     if (st != ISDC_OK) return st;
     CUDA_TRY(h, ee);
     return ISDC_OK;
+}
+template <typename TestF, typename BodyF>
+isdc_status capture_while(isdc_ctx *h, TestF test, BodyF body) {
+    return capture_cond(h, cudaGraphCondTypeWhile, h->cap2, nullptr, test, body);
 }
 
 // residual_kind 1 on the device (enqueued after the residual kernels, which wrote r~_m into RT):
@@ -1750,6 +1808,112 @@ isdc_status graph_fixed_step(isdc_ctx *h, int K, double *res_hist, double *res_l
         if (res_hist) res_hist[k] = mx;
         *res_last = mx;
     }
+    return ISDC_OK;
+}
+
+// A tolerance-stopped ISDC step as ONE graph: the first sweep (spread state, set 0 -> 1) and its
+// test, then a conditional WHILE loop whose body is sweep 1 -> 0, its test, a conditional IF around
+// sweep 0 -> 1 and its test, and k_step_loop; k_step_test records each sweep's residual and stops
+// at ||r~|| < tol or at max_sweeps -- the host loop's logic with one synchronisation per step.
+isdc_status graph_tol_step(isdc_ctx *h, int *k_out, double *res_hist, double *res_last) {
+    const int M = h->M;
+    const isdc_solve_opts &o = h->P.solve;
+    if (!h->tstep_exec) {
+        if (!h->cap) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+        const int cur0 = h->cur;
+        const bool spread0 = h->spread, fv0 = h->fold_valid[0], fv1 = h->fold_valid[1];
+        cudaStream_t user = h->s;
+        h->s = h->cap;
+        h->capturing = true;
+        const long lc = h->launches;
+        const unsigned long long *slots = h->red + SLOT_RES0;
+        auto sweep_into = [&](int from, bool spread) -> isdc_status {
+            h->cur = from;
+            h->spread = spread;
+            h->fold_valid[from] = !spread && folds_on(h);
+            return enqueue_isdc_sweep(h);
+        };
+        auto body_all = [&]() -> isdc_status {
+            ++h->launches;
+            kl(h, k_step_init, 1, 32, 0)(h->sctl);
+            LAUNCH_CHECK(h);
+            TRY(sweep_into(0, true));
+            cudaStreamCaptureStatus cs;
+            cudaGraph_t cg = nullptr;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t ndeps = 0;
+            CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs, nullptr, &cg, &deps, &ndeps));
+            cudaGraphConditionalHandle hw;
+            CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hw, cg, 0, 0));
+            ++h->launches;
+            kl(h, k_step_test, 1, 32, 0)(h->sctl, slots, M - 1, o.sweep_tol, o.max_sweeps, 1, hw, 1);
+            LAUNCH_CHECK(h);
+            h->tstep_n[0] = h->launches - lc;
+            auto none = [&](cudaGraphConditionalHandle) -> isdc_status { return ISDC_OK; };
+            return capture_cond(h, cudaGraphCondTypeWhile, h->cap2, &hw, none, [&](cudaGraphConditionalHandle) -> isdc_status {
+                const long la = h->launches;
+                TRY(sweep_into(1, false));
+                cudaStreamCaptureStatus cs2;
+                cudaGraph_t bg = nullptr;
+                const cudaGraphNode_t *d2 = nullptr;
+                size_t nd2 = 0;
+                CUDA_TRY(h, cudaStreamGetCaptureInfo(h->s, &cs2, nullptr, &bg, &d2, &nd2));
+                cudaGraphConditionalHandle hif;
+                CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hif, bg, 0, 0));
+                ++h->launches;
+                kl(h, k_step_test, 1, 32, 0)(h->sctl, slots, M - 1, o.sweep_tol, o.max_sweeps, 0, hif, 1);
+                LAUNCH_CHECK(h);
+                TRY(capture_cond(h, cudaGraphCondTypeIf, h->cap3, &hif, none, [&](cudaGraphConditionalHandle) -> isdc_status {
+                    const long lb = h->launches;
+                    TRY(sweep_into(0, false));
+                    ++h->launches;
+                    kl(h, k_step_test, 1, 32, 0)(h->sctl, slots, M - 1, o.sweep_tol, o.max_sweeps, 1, hif, 0);
+                    LAUNCH_CHECK(h);
+                    h->tstep_n[2] = h->launches - lb;
+                    return ISDC_OK;
+                }));
+                ++h->launches;
+                kl(h, k_step_loop, 1, 32, 0)(h->sctl, hw);
+                LAUNCH_CHECK(h);
+                h->tstep_n[1] = h->launches - la - h->tstep_n[2];
+                return ISDC_OK;
+            });
+        };
+        cudaError_t e = cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal);
+        isdc_status st = e == cudaSuccess ? body_all() : ISDC_ERR_CUDA;
+        cudaGraph_t g = nullptr;
+        cudaError_t e2 = cudaStreamEndCapture(h->cap, &g);
+        h->capturing = false;
+        h->s = user;
+        h->launches = lc;   // capture is not execution
+        h->cur = cur0; h->spread = spread0; h->fold_valid[0] = fv0; h->fold_valid[1] = fv1;
+        if (e != cudaSuccess || e2 != cudaSuccess || st != ISDC_OK) {
+            if (g) cudaGraphDestroy(g);
+            if (st == ISDC_OK)
+                h->err = std::string("step graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
+            return st == ISDC_OK ? ISDC_ERR_CUDA : st;
+        }
+        CUDA_TRY(h, cudaGraphInstantiate(&h->tstep_exec, g, 0));
+        cudaGraphDestroy(g);
+    }
+    CUDA_TRY(h, cudaGraphLaunch(h->tstep_exec, h->s));
+    int hdr[4];
+    CUDA_TRY(h, cudaMemcpyAsync(hdr, h->sctl, sizeof hdr, cudaMemcpyDeviceToHost, h->s));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    const int k = hdr[0];
+    if (k < 1 || k > kStepHist) { h->err = "step graph: bad sweep count"; return ISDC_ERR_CUDA; }
+    std::vector<double> hs(k);
+    CUDA_TRY(h, cudaMemcpy(hs.data(), reinterpret_cast<char *>(h->sctl) + offsetof(StepCtl, hist), k * sizeof(double),
+                           cudaMemcpyDeviceToHost));
+    const int ka = k / 2, kb = (k - 1) / 2;   // loop sweeps A (1 -> 0) and B (0 -> 1) alternate
+    h->launches += h->tstep_n[0] + (long)ka * h->tstep_n[1] + (long)kb * h->tstep_n[2];
+    h->cur = hdr[1];
+    h->spread = false;
+    h->fold_valid[h->cur] = folds_on(h);
+    if (res_hist) for (int q = 0; q < k; ++q) res_hist[q] = hs[q];
+    *res_last = hs[k - 1];
+    *k_out = k;
+    if (hdr[2]) { h->err = "non-finite residual"; return ISDC_ERR_NONFINITE; }
     return ISDC_OK;
 }
 
@@ -2156,16 +2320,27 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     int k = 0, caps = 0, conv = 0;
     long vc = 0;
     double res = 0.0;
+    bool graphed = false;   // the whole step ran as one graph
     if (o.fixed_sweeps > 0 && o.mode == ISDC_MODE_ISDC_FIXED && h->graphs && h->prof == 0 &&
         h->P.residual_kind == 0 && h->hist && h->spread && h->cur == 0 && h->step_graph) {
         // the whole fixed-sweep step as one graph: no host synchronisation between its sweeps
         TRY(graph_fixed_step(h, o.fixed_sweeps, res_hist, &res));
+        graphed = true;
         k = o.fixed_sweeps;
         vc = (long)k * (h->M - 1) * o.L;
         if (node_cycles)
             for (int q = 0; q < k * (h->M - 1); ++q) node_cycles[q] = o.L;
+    } else if (o.fixed_sweeps <= 0 && o.mode == ISDC_MODE_ISDC_FIXED && h->graphs && h->prof == 0 &&
+               h->P.residual_kind == 0 && h->spread && h->cur == 0 && h->step_graph && o.max_sweeps <= kStepHist) {
+        // the whole tolerance-stopped step as one graph (conditional loop over sweep pairs)
+        TRY(graph_tol_step(h, &k, res_hist, &res));
+        graphed = true;
+        vc = (long)k * (h->M - 1) * o.L;
+        if (node_cycles)
+            for (int q = 0; q < k * (h->M - 1); ++q) node_cycles[q] = o.L;
+        if (res < o.sweep_tol) conv = 1;
     }
-    while (k < kmax) {
+    while (!graphed && k < kmax) {
         int cyc[ISDC_MAXM], cap = 0;
         TRY(sweep_impl(h, nullptr, &res, cyc, &cap));
         caps += cap;
