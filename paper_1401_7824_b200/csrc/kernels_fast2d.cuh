@@ -78,25 +78,31 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
         // Column pairs (lx, lx+1), lx = 2k even: the even point takes the coarse pair (k, k+1),
         // the odd one coarse k+1, so one row of e serves both; 16-byte u accesses.  Same trees
         // as the per-point form: sx(r) = e[r][xa] (+ e[r][xa+1]); sz = sx(ya) (+ sx(ya+1)).
+        // two fine rows per thread, (2r, 2r+1): the even row takes coarse rows (r, r+1), the odd one
+        // row r+1, so three of the four coarse values per column pair serve both rows
         constexpr int PW = UW / 2;
-        for (int q = tid; q < PW * UH; q += NT) {
-            const int ly = q / PW, k = q - ly * PW, lx = 2 * k;
+        static_assert(UH % 2 == 0, "row pairs");
+        for (int q = tid; q < PW * (UH / 2); q += NT) {
+            const int lr = q / PW, k = q - lr * PW, lx = 2 * k, ly = 2 * lr;
             const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
-            if (gy < 0 || gy >= n || gx + 1 < 0 || gx >= n) continue;
-            const bool ye = !(ly & 1);
-            const int ya = ye ? ly / 2 : (ly + 1) / 2;
+            if (gx + 1 < 0 || gx >= n) continue;
+            const int ya = ly / 2;                  // even row: coarse rows ya, ya + 1; odd row: ya + 1
             const double ea0 = S.e[ya][k], ea1 = S.e[ya][k + 1];
-            double sze = ea0 + ea1, szo = ea1, we = 0.5, wo = 1.0;
-            if (ye) {
-                const double eb0 = S.e[ya + 1][k], eb1 = S.e[ya + 1][k + 1];
-                sze = sze + (eb0 + eb1);
-                szo = szo + eb1;
-                we = 0.25; wo = 0.5;
+            const double eb0 = S.e[ya + 1][k], eb1 = S.e[ya + 1][k + 1];
+            if (gy >= 0 && gy < n) {                // even row (ye): weights 0.25 / 0.5
+                const double sze = (ea0 + ea1) + (eb0 + eb1), szo = ea1 + eb1;
+                double2 v = *reinterpret_cast<const double2 *>(&S.u[ly][lx]);
+                if (gx >= 0) v.x = v.x + sze * 0.25;
+                if (gx + 1 < n) v.y = v.y + szo * 0.5;
+                *reinterpret_cast<double2 *>(&S.u[ly][lx]) = v;
             }
-            double2 v = *reinterpret_cast<const double2 *>(&S.u[ly][lx]);
-            if (gx >= 0) v.x = v.x + sze * we;
-            if (gx + 1 < n) v.y = v.y + szo * wo;
-            *reinterpret_cast<double2 *>(&S.u[ly][lx]) = v;
+            if (gy + 1 >= 0 && gy + 1 < n) {        // odd row: weights 0.5 / 1
+                const double sze = eb0 + eb1, szo = eb1;
+                double2 v = *reinterpret_cast<const double2 *>(&S.u[ly + 1][lx]);
+                if (gx >= 0) v.x = v.x + sze * 0.5;
+                if (gx + 1 < n) v.y = v.y + szo * 1.0;
+                *reinterpret_cast<double2 *>(&S.u[ly + 1][lx]) = v;
+            }
         }
         __syncthreads();
     }
