@@ -206,10 +206,12 @@ def test_unweighted_residual_steps_bitwise(gpu, ora, cid, n, mode):
 # ------------------------------------------------ alternative execution paths (same bits)
 @pytest.mark.parametrize("env,mode", [({"ISDC_DEVICE_SDC": "0"}, MODE_SDC), ({"ISDC_DEVICE_SDC": "0"}, MODE_ISDC_CAPPED),
                                       ({"ISDC_NO_GRAPHS": "1"}, MODE_ISDC), ({"ISDC_NO_GRAPHS": "1"}, MODE_SDC),
-                                      ({"ISDC_GENERIC_KERNELS": "1"}, MODE_ISDC), ({"ISDC_FOLDS": "0"}, MODE_ISDC)])
+                                      ({"ISDC_GENERIC_KERNELS": "1"}, MODE_ISDC), ({"ISDC_FOLDS": "0"}, MODE_ISDC),
+                                      ({"ISDC_STEP_GRAPH": "0"}, MODE_ISDC), ({"ISDC_TAIL_FUSE": "0"}, MODE_ISDC)])
 def test_execution_paths_bitwise(gpu, ora, monkeypatch, env, mode):
-    """Host-side node-solve tests, un-captured sweeps, the generic kernels and the fold-free RHS
-    produce the oracle's bits too (the environment is read when the handle is created)."""
+    """Host-side node-solve tests, un-captured sweeps, sweep-by-sweep steps, the generic kernels, the
+    fold-free RHS and the unfused tail produce the oracle's bits too (the environment is read when
+    the handle is created)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for cid, n in ((2, 127), (4, 31)):
