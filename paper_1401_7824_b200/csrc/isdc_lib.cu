@@ -178,7 +178,7 @@ struct isdc_ctx {
     int res_nmw = 2;           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
     bool tail_fuse_dr = true;  // ISDC_TAIL_FUSE=0: 2D tail with a separate defect phase (fused: cfg1 -2 %)
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
-    int sr_ty = 32;            // ISDC_SR_TY: their height (24 or 32)
+    int sr_ty = 40;            // ISDC_SR_TY: their height (24, 32, 40 or 48; 40: 53.4 ms, 32: 56.1, 48: 61.7 per cfg-3 step)
     int sm_ty32_min = 2047;    // ISDC_SM_TY32_MIN: the same for k_smooth2
     int sm_ty = 24;            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
     int small_n = 511;         // ISDC_SMALL_N: levels n <= small_n use the short tiles below (more CTAs)
@@ -785,7 +785,15 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
     const int cls = level == 0 ? PROF_RESTRICT : PROF_COARSE;
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::FR_TX - 1) / f2d::FR_TX, (g.n + TY - 1) / TY);
-    if (TY == 32) {
+    if (TY == 48) {
+        size_t sm = sizeof(f2d::SmemSR<48>) + 128;
+        if (in) kl(h, f2d::k_smooth2r<0, 48>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+        else kl(h, f2d::k_smooth2r<1, 48>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    } else if (TY == 40) {
+        size_t sm = sizeof(f2d::SmemSR<40>) + 128;
+        if (in) kl(h, f2d::k_smooth2r<0, 40>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+        else kl(h, f2d::k_smooth2r<1, 40>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    } else if (TY == 32) {
         size_t sm = sizeof(f2d::SmemSR<32>) + 128;
         if (in) kl(h, f2d::k_smooth2r<0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
         else kl(h, f2d::k_smooth2r<1, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
@@ -2066,7 +2074,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
     if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
     if (const char *st = getenv("ISDC_SR_TY32_MIN")) h->sr_ty32_min = atoi(st);
-    if (const char *st = getenv("ISDC_SR_TY")) h->sr_ty = atoi(st) == 24 ? 24 : 32;
+    if (const char *st = getenv("ISDC_SR_TY")) { const int v = atoi(st); h->sr_ty = (v == 24 || v == 40 || v == 48) ? v : 32; }
     if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
     if (const char *tf = getenv("ISDC_TAIL_FUSE")) h->tail_fuse_dr = tf[0] != '0';
     if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
@@ -2104,6 +2112,14 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                              (int)sizeof(f2d::SmemSR<16>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSR<16>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<0, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<48>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<1, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<48>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<0, 40>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<40>) + 128);
+        cudaFuncSetAttribute(f2d::k_smooth2r<1, 40>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(f2d::SmemSR<40>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<0, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(f2d::SmemSR<24>) + 128);
         cudaFuncSetAttribute(f2d::k_smooth2r<1, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
