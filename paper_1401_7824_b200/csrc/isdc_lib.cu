@@ -180,7 +180,7 @@ struct isdc_ctx {
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
     int sr_ty = 40;            // ISDC_SR_TY: their height (24, 32, 40 or 48; 40: 53.4 ms, 32: 56.1, 48: 61.7 per cfg-3 step)
     int sm_ty32_min = 2047;    // ISDC_SM_TY32_MIN: the same for k_smooth2
-    int sm_ty = 24;            // ISDC_SM_TY: their height (24: 46.4 ms, 32: 48.4 ms, 16: 46.9 ms per cfg-3 step)
+    int sm_ty = 24;            // ISDC_SM_TY: their height (24: 45.1 ms, 40: 45.4, 32: 47.5, 16: 46.9 per cfg-3 step)
     int small_n = 511;         // ISDC_SMALL_N: levels n <= small_n use the short tiles below (more CTAs)
     int sr_ty_small = 8, sm_ty_small = 8;   // ISDC_SR_TY_SMALL / ISDC_SM_TY_SMALL (8 or 16)
     bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
@@ -609,7 +609,13 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
     const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + TY - 1) / TY);
-    if (TY == 8) {
+    if (TY == 40) {
+        size_t sm = sizeof(f2d::SmemSmoothT<40>) + 128;
+        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
+        else if (e) kl(h, f2d::k_smooth2<false, 2, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else if (!in) kl(h, f2d::k_smooth2<false, 1, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else kl(h, f2d::k_smooth2<false, 0, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    } else if (TY == 8) {
         size_t sm = sizeof(f2d::SmemSmoothT<8>) + 128;
         if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
         else if (e) kl(h, f2d::k_smooth2<false, 2, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
@@ -2078,7 +2084,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
     if (const char *tf = getenv("ISDC_TAIL_FUSE")) h->tail_fuse_dr = tf[0] != '0';
     if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
-    if (const char *st = getenv("ISDC_SM_TY")) h->sm_ty = atoi(st) == 24 ? 24 : 32;
+    if (const char *st = getenv("ISDC_SM_TY")) { const int v = atoi(st); h->sm_ty = (v == 24 || v == 40) ? v : 32; }
     if (const char *st = getenv("ISDC_SMALL_N")) h->small_n = atoi(st);
     if (const char *st = getenv("ISDC_SR_TY_SMALL")) h->sr_ty_small = atoi(st) == 8 ? 8 : 16;
     if (const char *st = getenv("ISDC_SM_TY_SMALL")) h->sm_ty_small = atoi(st) == 8 ? 8 : 16;
@@ -2104,6 +2110,10 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                           f2d::k_smooth2<false, 2, 32>})
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(f2d::SmemSmoothT<32>) + 128);
+        for (auto kern : {f2d::k_smooth2<true, 0, 40>, f2d::k_smooth2<false, 0, 40>, f2d::k_smooth2<false, 1, 40>,
+                          f2d::k_smooth2<false, 2, 40>})
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(f2d::SmemSmoothT<40>) + 128);
         for (auto kern : {f2d::k_smooth2<true, 0, 24>, f2d::k_smooth2<false, 0, 24>, f2d::k_smooth2<false, 1, 24>,
                           f2d::k_smooth2<false, 2, 24>})
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
