@@ -176,6 +176,7 @@ struct isdc_ctx {
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
     bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
     int res_nmw = 2;           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
+    int stream_yc = 0;         // ISDC_STREAM_YC: rows per CTA of the 2D streaming RHS / residual (0 = by size)
     bool tail_fuse_dr = true;  // ISDC_TAIL_FUSE=0: 2D tail with a separate defect phase (fused: cfg1 -2 %)
     int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
     int sr_ty = 40;            // ISDC_SR_TY: their height (24, 32, 40 or 48; 40: 53.4 ms, 32: 56.1, 48: 61.7 per cfg-3 step)
@@ -1126,6 +1127,7 @@ dim3 stream2d_grid(const isdc_ctx *h, int &yc) {
     const int strips = (n + f2d::SW_OUT - 1) / f2d::SW_OUT;
     const int cx = (strips + f2d::SW_NT / 32 - 1) / (f2d::SW_NT / 32);
     yc = n >= 2047 ? 64 : (n >= 511 ? 32 : 16);
+    if (h->stream_yc > 0) yc = h->stream_yc;   // ISDC_STREAM_YC: rows per CTA chunk
     return dim3(cx, (n + yc - 1) / yc);
 }
 bool stream2d_ok(const isdc_ctx *h) { return fast2d_pointwise_fe(h) && (h->M == 3 || h->M == 5) && h->stream2d; }
@@ -2083,6 +2085,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *st = getenv("ISDC_SR_TY")) { const int v = atoi(st); h->sr_ty = (v == 24 || v == 40 || v == 48) ? v : 32; }
     if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
     if (const char *tf = getenv("ISDC_TAIL_FUSE")) h->tail_fuse_dr = tf[0] != '0';
+    if (const char *yc = getenv("ISDC_STREAM_YC")) h->stream_yc = atoi(yc);
     if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
     if (const char *st = getenv("ISDC_SM_TY")) { const int v = atoi(st); h->sm_ty = (v == 24 || v == 40) ? v : 32; }
     if (const char *st = getenv("ISDC_SMALL_N")) h->small_n = atoi(st);
