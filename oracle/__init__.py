@@ -21,11 +21,24 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC", "-Wall"]
 
 
+def _hash() -> str:
+    import hashlib
+    with open(_SRC, "rb") as f:
+        return hashlib.sha256(f.read() + " ".join(CFLAGS).encode()).hexdigest()
+
+
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lquadmath", "-lm"]
-        subprocess.run(cmd, check=True)
+    """Compile liboracle.so with gcc (no FMA contraction, no fast-math); rebuilt whenever the
+    source or the flags differ from the stamp of the last build."""
+    stamp = _LIB + ".sha256"
+    h = _hash()
+    fresh = os.path.exists(_LIB) and os.path.exists(stamp) and open(stamp).read().strip() == h
+    if force or not fresh:
+        tmp = _LIB + ".tmp"
+        subprocess.run(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lquadmath", "-lm"], check=True)
+        os.replace(tmp, _LIB)
+        with open(stamp, "w") as f:
+            f.write(h + "\n")
     return _LIB
 
 
@@ -79,6 +92,7 @@ def _declare(L):
                            C.POINTER(C.c_long), _dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                            C.POINTER(C.c_int)]
     L.ora_num_threads.restype = C.c_int
+    L.ora_set_num_threads.argtypes = [C.c_int]
     L.ora_last_wcycles.restype = C.c_long
     L.ora_set_bc.argtypes = [C.c_int]
     L.ora_weno5.argtypes = [C.c_double] * 5
@@ -96,6 +110,11 @@ def _c(a) -> np.ndarray:
 
 def num_threads() -> int:
     return lib().ora_num_threads()
+
+
+def set_num_threads(t: int) -> None:
+    """OpenMP threads of the oracle's grid loops (timing only; results are thread-count independent)."""
+    lib().ora_set_num_threads(int(t))
 
 
 # ---------------------------------------------------------------------------------------------

@@ -40,6 +40,15 @@ int ora_num_threads(void) {
     return 1;
 #endif
 }
+/* Thread count of the OpenMP loops (timing only: every loop is over independent grid points or an
+ * exact max, so the results do not depend on it). */
+void ora_set_num_threads(int t) {
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}
 
 /* ------------------------------------------------------------------------------------------ */
 /* Quadrature tables (Eq. 2).  Gauss-Lobatto nodes on [0,1]; Q_{m,j} = int_0^{tau_m}  */

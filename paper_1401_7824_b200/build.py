@@ -5,6 +5,7 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -29,11 +30,31 @@ def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*"))) + [os.path.join(INCLUDE, "isdc.h")]
 
 
+STAMP = LIB + ".sha256"
+
+
+def source_hash() -> str:
+    """SHA-256 over every source file (name + bytes), the compilers' flags and nvcc's version: the
+    library is rebuilt whenever any of them differs from the stamp written by the last build (file
+    modification times are not trusted: a checkout or a copy can make an old library look new)."""
+    h = hashlib.sha256()
+    for s in _sources():
+        h.update(os.path.basename(s).encode())
+        with open(s, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(ARCH + NVFLAGS + CXXFLAGS).encode())
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
+    except OSError:
+        pass
+    return h.hexdigest()
+
+
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(s) > t for s in _sources())
+    with open(STAMP) as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -60,6 +81,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lquadmath"], check=True)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(source_hash() + "\n")
     return LIB
 
 

@@ -155,14 +155,6 @@ __device__ __forceinline__ double fe_at(const FeDesc &fe, const double *u, const
     return -((dx + dy) + dz);
 }
 
-// ---- programmatic dependent launch (sm_90+): kernels are launched with programmatic stream
-// serialization, so a kernel may start while its predecessor drains.  Every kernel calls
-// pdl_launch() at entry (lets its own successor launch early) and pdl_wait() before its first
-// global-memory access (waits for the predecessor's completion and memory flush); only shared
-// memory / parameter work may precede pdl_wait().
-__device__ __forceinline__ void pdl_launch() {}   // implicit trigger at CTA exit (an early trigger measured slower: waiting successor CTAs hold SM resources)
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 // ---- max-norm reduction: non-negative doubles ordered as uint64; NaN bits exceed +Inf ---------
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll

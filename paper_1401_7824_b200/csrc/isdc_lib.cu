@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <utility>
@@ -33,7 +35,6 @@ struct SdcCtl {
     int wcn[ISDC_MAXM];      // W-cycles per residual node
 };
 __global__ void k_sdc_init(SdcCtl *ctl, int m, const unsigned long long *bslot, double inner_tol) {
-    pdl_wait();
     if (threadIdx.x == 0) {
         const double bn = __longlong_as_double((long long)*bslot);
         ctl->thr[m] = inner_tol * fmax(1.0, bn);   // the host expression of node_solve
@@ -45,7 +46,6 @@ __global__ void k_sdc_init(SdcCtl *ctl, int m, const unsigned long long *bslot, 
 // one test before every cycle (node_solve): stop when dn <= thr, or at the cap; clears the slot
 __global__ void k_sdc_test(SdcCtl *ctl, int m, unsigned long long *dslot, int capc, int sdc,
                            cudaGraphConditionalHandle hnd) {
-    pdl_wait();
     if (threadIdx.x == 0) {
         const double dn = __longlong_as_double((long long)*dslot);
         unsigned go = 0;
@@ -69,14 +69,12 @@ struct StepCtl {
     double hist[kStepHist];  // max_m ||r~_m|| after each sweep (read_residual's reduction)
 };
 __global__ void k_step_init(StepCtl *ctl) {
-    pdl_wait();
     if (threadIdx.x == 0) { ctl->k = 0; ctl->last = 0; ctl->bad = 0; ctl->cont = 0; }
 }
 // after a sweep that wrote set `set_after`: record its residual; continue while r >= tol and k < kmax.
 // The verdict goes to ctl->cont and, if hset, to the conditional handle hc.
 __global__ void k_step_test(StepCtl *ctl, const unsigned long long *slots, int nm, double tol, int kmax, int set_after,
                             cudaGraphConditionalHandle hc, int hset) {
-    pdl_wait();
     if (threadIdx.x == 0) {
         double mx = 0.0;
         bool bad = false;
@@ -97,13 +95,11 @@ __global__ void k_step_test(StepCtl *ctl, const unsigned long long *slots, int n
 }
 // at the end of a loop body: continue the WHILE loop iff the last test said so
 __global__ void k_step_loop(const StepCtl *ctl, cudaGraphConditionalHandle hw) {
-    pdl_wait();
     if (threadIdx.x == 0) cudaGraphSetConditional(hw, (unsigned)ctl->cont);
 }
 
 // residual_kind 1 (NEXT f2) on the device: the W-solve of unweighted_norms, one node m at a time
 __global__ void k_w_init(SdcCtl *ctl, int m, const unsigned long long *rslot, double w_tol) {
-    pdl_wait();
     if (threadIdx.x == 0) {
         ctl->wthr[m] = w_tol * __longlong_as_double((long long)*rslot);   // the host expression
         ctl->wcn[m] = 0;
@@ -111,7 +107,6 @@ __global__ void k_w_init(SdcCtl *ctl, int m, const unsigned long long *rslot, do
     }
 }
 __global__ void k_w_test(SdcCtl *ctl, int m, unsigned long long *dslot, int wcap, cudaGraphConditionalHandle hnd) {
-    pdl_wait();
     if (threadIdx.x == 0) {
         const double dn = __longlong_as_double((long long)*dslot);
         unsigned go = 0;
@@ -169,29 +164,13 @@ struct isdc_ctx {
     unsigned long long *alpha = nullptr;   // Burgers: max|u| slots, [0,M) uold_j, [8,8+M) unew_m, [16,16+M) residual u_j
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
-    int tail3d = 15;           // ISDC_TAIL3D: largest 3D level handled by the tail (fast kernels above)
-    int tail2d = 31;           // ISDC_TAIL2D: largest 2D level handled by the single-CTA tail (31 measured best)
-    bool pdl = false;          // ISDC_PDL=1: programmatic dependent launch (measured neutral with the implicit
-                               // trigger, slower with an early trigger)
+    int tail3d = 15;           // largest 3D level handled by the single-CTA tail (fast kernels above)
+    int tail2d = 31;           // largest 2D level handled by the single-CTA tail (31 measured best)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
-    bool sr_stream = false;    // ISDC_SR_STREAM=1: warp-shuffle streaming k_sr_s (bitwise equal, 2x slower)
-    int res_nmw = 2;           // ISDC_RES_NMW: 2D residual nodes per warp for M = 5 (2 or 1)
-    int stream_yc = 0;         // ISDC_STREAM_YC: rows per CTA of the 2D streaming RHS / residual (0 = by size)
     bool tail_fuse_dr = true;  // ISDC_TAIL_FUSE=0: 2D tail with a separate defect phase (fused: cfg1 -2 %)
-    int sr_ty32_min = 2047;    // ISDC_SR_TY32_MIN: smallest level n using the tall k_smooth2r tiles
-    int sr_ty = 40;            // ISDC_SR_TY: their height (24, 32, 40 or 48; 40: 53.4 ms, 32: 56.1, 48: 61.7 per cfg-3 step)
-    int sm_ty32_min = 2047;    // ISDC_SM_TY32_MIN: the same for k_smooth2
-    int sm_ty = 24;            // ISDC_SM_TY: their height (24: 45.1 ms, 40: 45.4, 32: 47.5, 16: 46.9 per cfg-3 step)
-    int small_n = 511;         // ISDC_SMALL_N: levels n <= small_n use the short tiles below (more CTAs)
-    int sr_ty_small = 8, sm_ty_small = 8;   // ISDC_SR_TY_SMALL / ISDC_SM_TY_SMALL (8 or 16)
-    bool rhs16 = true;         // ISDC_RHS16=0: 3D RHS with 8 warps x 4 rows instead of 16 x 2
-    bool bl16 = true;          // ISDC_BL16=0: 3D residual passes with 8 warps x 2 rows instead of 16 x 1
-    bool bl_nm4 = false;       // ISDC_BL_NM4=1: 3D residual in one pass (4 nodes, 12 warps x 1 row; slower)
     bool folds = true;         // ISDC_FOLDS=0: RHS without stored folds (3D CD4)
-    bool fuse3d = false;       // ISDC_FUSE3D=1: fused 3D prolongation + smoother (slower so far)
     bool fuse2d = true;        // ISDC_FUSE2D=0: separate prolongation / zero-fill launches in 2D
     bool stream2d = true;      // ISDC_STREAM2D=0: the tile-based 2D RHS / residual kernels instead
-    int smooth3d_rows = 0;     // ISDC_SMOOTH3D_ROWS: rows per thread of the 3D fused smoother (2, 3, 4; 0 = auto)
     int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
     TailParams tailp[ISDC_MAXM];
@@ -265,10 +244,8 @@ struct isdc_ctx {
 
 namespace {
 
-// Kernel launch with programmatic dependent launch (PDL): the kernel may start while its stream
-// predecessor drains; every kernel waits (griddepcontrol.wait, common.cuh) before touching global
-// memory, so only its launch latency and shared-memory prologue overlap.  Captured into the
-// CUDA graphs as programmatic dependency edges.  Usage: kl(h, kernel, grid, block, smem)(args...).
+// Kernel launch on the handle's stream with the first launch error kept for LAUNCH_CHECK.
+// Usage: kl(h, kernel, grid, block, smem)(args...).
 template <typename... KA>
 struct KLaunch {
     isdc_ctx *h;
@@ -282,11 +259,8 @@ struct KLaunch {
         cfg.blockDim = b;
         cfg.dynamicSmemBytes = sm;
         cfg.stream = h->s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.attrs = nullptr;
+        cfg.numAttrs = 0;
         cudaError_t e = cudaLaunchKernelEx(&cfg, k, std::forward<A>(a)...);
         if (e != cudaSuccess && h->kl_err == cudaSuccess) h->kl_err = e;
     }
@@ -554,44 +528,32 @@ int pick_chunk(const isdc_ctx *h, int tiles, int planes, int halo) {
     return best;
 }
 
-// e != nullptr: u + P e first (fused trilinear prolongation + correction); in == nullptr:
-// zero iterate.  Shape (rows per thread SR x warps): 4 x 8 (32-row region, default), 2 x 16, 3 x 12.
+// two fused Jacobi sweeps, z-streaming; in == nullptr: zero iterate.  Shape (rows
+// per thread SR x warps NWW): 3 x 12 up to 255^3 (measured 1.5 % faster on config 4), 4 x 8 above.
 template <int SR, int NWW>
 isdc_status launch_smooth2_3d_t(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
-                                const SCoef &c, int level, const double *e, const GridDesc *gc) {
+                                const SCoef &c, int level) {
     using Z = f3d::SS<SR * NWW>;
     const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, Z::BH, 1);
     const CUtensorMap *mu = in ? tmap(h, in, g, f3d::S_UW, Z::UH, 1) : mb;
-    const CUtensorMap *me = e ? tmap(h, e, *gc, f3d::S_EW, f3d::S_EH, 1) : mb;
-    if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
-    const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
+    const int cls = level == 0 ? PROF_SMOOTH : PROF_COARSE;
     int pe = prof_begin(h, cls);
     int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + Z::TY - 1) / Z::TY;
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(f3d::k_smooth2<SR, 0, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<SR, 1, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM);
-        cudaFuncSetAttribute(f3d::k_smooth2<SR, 2, NWW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM_PRO);
-        attr = true;
-    }
-    if (e) kl(h, f3d::k_smooth2<SR, 2, NWW>, grd, 32 * NWW, Z::SMEM_PRO)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
-    else if (!in) kl(h, f3d::k_smooth2<SR, 1, NWW>, grd, 32 * NWW, Z::SMEM)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
-    else kl(h, f3d::k_smooth2<SR, 0, NWW>, grd, 32 * NWW, Z::SMEM)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc, *me);
-    // algorithmic bytes: read u (unless zero), b (+ e / 8); write u''
-    prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 1.0 : 0.0)) * npts_of(h, g));
+    if (!in) kl(h, f3d::k_smooth2<SR, 1, NWW>, grd, 32 * NWW, Z::SMEM)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
+    else kl(h, f3d::k_smooth2<SR, 0, NWW>, grd, 32 * NWW, Z::SMEM)(*mu, *mb, out, g.n, g.pitch, g.plane, c, zc);
+    // algorithmic bytes: read u (unless zero), b; write u''
+    prof_end(h, pe, cls, (in ? 24.0 : 16.0) * npts_of(h, g));
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
 isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
-                              const SCoef &c, int level, const double *e = nullptr, const GridDesc *gc = nullptr) {
-    // auto: 3 x 12 warps up to 255^3 (measured 1.5 % faster on config 4), 4 x 8 above (config 5)
-    const int rows = h->smooth3d_rows ? h->smooth3d_rows : (g.n <= 255 ? 3 : 4);
-    if (rows == 2) return launch_smooth2_3d_t<2, 16>(h, out, in, b, g, c, level, e, gc);
-    if (rows == 3) return launch_smooth2_3d_t<3, 12>(h, out, in, b, g, c, level, e, gc);
-    return launch_smooth2_3d_t<4, 8>(h, out, in, b, g, c, level, e, gc);
+                              const SCoef &c, int level) {
+    if (g.n <= 255) return launch_smooth2_3d_t<3, 12>(h, out, in, b, g, c, level);
+    return launch_smooth2_3d_t<4, 8>(h, out, in, b, g, c, level);
 }
 
 // two fused Jacobi sweeps on the fine 2D level
@@ -599,9 +561,8 @@ isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const 
 isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                            const SCoef &c, unsigned long long *norm_slot, int level, const double *e = nullptr,
                            const GridDesc *gc = nullptr) {
-    // 32-row tiles on the large levels (ISDC_SM_TY32_MIN), 16-row tiles below
-    const bool t32 = g.n >= h->sm_ty32_min;
-    const int TY = t32 ? h->sm_ty : (g.n <= h->small_n ? h->sm_ty_small : 16);
+    // 24-row tiles on the large levels, 16 rows in between, 8 on n <= 511 (more CTAs on the latency-bound levels)
+    const int TY = g.n >= 2047 ? 24 : (g.n <= 511 ? 8 : 16);
     const CUtensorMap *mb = tmap(h, b, g, f2d::BW, TY + 2);
     const CUtensorMap *mu = in ? tmap(h, in, g, f2d::UW, TY + 4) : mb;
     const CUtensorMap *me = e ? tmap(h, e, *gc, f2d::EW, TY / 2 + 3) : mb;
@@ -610,37 +571,17 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
     const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::TX - 1) / f2d::TX, (g.n + TY - 1) / TY);
-    if (TY == 40) {
-        size_t sm = sizeof(f2d::SmemSmoothT<40>) + 128;
-        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
-        else if (e) kl(h, f2d::k_smooth2<false, 2, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else if (!in) kl(h, f2d::k_smooth2<false, 1, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else kl(h, f2d::k_smooth2<false, 0, 40>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    } else if (TY == 8) {
-        size_t sm = sizeof(f2d::SmemSmoothT<8>) + 128;
-        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
-        else if (e) kl(h, f2d::k_smooth2<false, 2, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else if (!in) kl(h, f2d::k_smooth2<false, 1, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else kl(h, f2d::k_smooth2<false, 0, 8>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    } else if (TY == 24) {
-        size_t sm = sizeof(f2d::SmemSmoothT<24>) + 128;
-        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 24>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
-        else if (e) kl(h, f2d::k_smooth2<false, 2, 24>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else if (!in) kl(h, f2d::k_smooth2<false, 1, 24>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else kl(h, f2d::k_smooth2<false, 0, 24>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    } else if (t32) {
-        size_t sm = sizeof(f2d::SmemSmoothT<32>) + 128;
-        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
-        else if (e) kl(h, f2d::k_smooth2<false, 2, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else if (!in) kl(h, f2d::k_smooth2<false, 1, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else kl(h, f2d::k_smooth2<false, 0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    } else {
-        size_t sm = sizeof(f2d::SmemSmooth) + 128;
-        if (norm_slot) kl(h, f2d::k_smooth2<true, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
-        else if (e) kl(h, f2d::k_smooth2<false, 2>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else if (!in) kl(h, f2d::k_smooth2<false, 1>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-        else kl(h, f2d::k_smooth2<false, 0>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
-    }
+    auto go = [&](auto tyc) {
+        constexpr int T = decltype(tyc)::value;
+        const size_t sm = sizeof(f2d::SmemSmoothT<T>) + 128;
+        if (norm_slot) kl(h, f2d::k_smooth2<true, 0, T>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, norm_slot, *me);
+        else if (e) kl(h, f2d::k_smooth2<false, 2, T>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else if (!in) kl(h, f2d::k_smooth2<false, 1, T>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+        else kl(h, f2d::k_smooth2<false, 0, T>, grd, f2d::NT, sm)(*mu, *mb, out, g.n, g.pitch, c, nullptr, *me);
+    };
+    if (TY == 24) go(std::integral_constant<int, 24>{});
+    else if (TY == 8) go(std::integral_constant<int, 8>{});
+    else go(std::integral_constant<int, 16>{});
     // algorithmic bytes: read u (unless zero), b (+ e / 4); write u''
     prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 2.0 : 0.0)) * npts_of(h, g));
     LAUNCH_CHECK(h);
@@ -699,32 +640,27 @@ isdc_status launch_fe(isdc_ctx *h, double *F, const double *u) {
 constexpr int kMaxDynSmem = 232448 - 1024;   // 227 KB opt-in per CTA on sm_100, less static shared memory
 
 // B a +- L c streaming kernel (3D RHS / residual), DESIGN.md §6.10.  fields[k] are pitched level-0
-// fields; nm outputs per pass.  Picks the region height (RR) and pipeline depth that fit shared
-// memory and registers: RHS (nm = 1) prefers RR = 4; residual passes with nm = 2 use RR = 2.
+// fields; nm (1 or 2) outputs per pass.  Shapes (rings cost 14 * RR * NM doubles per thread):
+// nm = 1: 16 warps x 2 rows (32-row region) while >= 3 pipeline stages fit, else 8 warps x 2 rows;
+// nm = 2: 16 warps x 1 row (16-row region).
 template <int MODE>
 isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f3d::BLArgs A, int prof_cls,
                       double bytes) {
     const GridDesc &g = h->lev[0].g;
-    // rings cost 14 * RR * NM doubles per thread: NM = 1 -> RR = 4, NM = 2 -> RR = 2 (or RR = 1 with
-    // 16 warps: the same 16-row region, twice the warps), NM = 4 -> RR = 1
-    const bool w16 = (nm == 2) && h->bl16;
-    const bool w12 = (nm == 4) && h->bl_nm4;   // 12 warps x 1 row: 170 registers for the 4 nodes' rings
-    const bool r16 = (nm == 1) && h->rhs16;   // RHS: 16 warps x 2 rows (same 32-row region as 8 x 4)
-    int rr = (nm == 1) ? (r16 ? 2 : 4) : (nm == 2 && !w16 ? 2 : 1), ns = (nm == 4) ? 6 : 4;
-    auto smem_of = [&](int r_, int ns_) {
-        return w12 ? f3d::BLShape<1, 12>::smem(K, ns_, nm) : w16 ? f3d::BLShape<1, 16>::smem(K, ns_, nm) : r16 ? f3d::BLShape<2, 16>::smem(K, ns_, nm)
-                   : (r_ == 4 ? f3d::BLShape<4>::smem(K, ns_, nm)
-                              : (r_ == 2 ? f3d::BLShape<2>::smem(K, ns_, nm) : f3d::BLShape<1>::smem(K, ns_, nm)));
+    enum { S32, S16, R16 } shape = (nm == 1) ? S32 : R16;
+    auto smem_of = [&](int ns_) -> size_t {
+        return shape == S32 ? f3d::BLShape<2, 16>::smem(K, ns_, nm)
+                            : (shape == S16 ? f3d::BLShape<2>::smem(K, ns_, nm) : f3d::BLShape<1, 16>::smem(K, ns_, nm));
     };
-    while (ns >= 2 && smem_of(rr, ns) > (size_t)kMaxDynSmem) --ns;
-    bool r16b = r16;
-    if ((rr == 4 || r16) && ns < 3) {   // too many fields for a 32-row region: 8 warps x 2 rows
-        r16b = false; rr = 2; ns = 4;
-        auto sm8 = [&](int ns_) { return f3d::BLShape<2>::smem(K, ns_, nm); };
-        while (ns >= 2 && sm8(ns) > (size_t)kMaxDynSmem) --ns;
+    int ns = 4;
+    while (ns >= 2 && smem_of(ns) > (size_t)kMaxDynSmem) --ns;
+    if (shape == S32 && ns < 3) {   // too many fields for a 32-row region
+        shape = S16;
+        ns = 4;
+        while (ns >= 2 && smem_of(ns) > (size_t)kMaxDynSmem) --ns;
     }
-    if (ns < 2) { h->err = "too many fields for the 3D stream kernel"; return ISDC_ERR_UNSUPPORTED; }
-    int rh = w12 ? 12 : (w16 ? 16 : (r16b ? 32 : f3d::NW * rr));
+    if (ns < 2 || nm < 1 || nm > 2) { h->err = "too many fields for the 3D stream kernel"; return ISDC_ERR_UNSUPPORTED; }
+    const int rh = shape == S32 ? 32 : 16;
     f3d::BLMaps maps;
     for (int k = 0; k < K; ++k) {
         const CUtensorMap *mk = tmap(h, fields[k], g, f3d::RW + 2, rh, 1);
@@ -735,32 +671,20 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     int tx = (g.n + f3d::RW - 3) / (f3d::RW - 2), ty = (g.n + rh - 3) / (rh - 2);
     A.zc = pick_chunk(h, tx * ty, g.n, 2);
     dim3 grd(tx, ty, (g.n + A.zc - 1) / A.zc);
-    size_t sm = r16b ? f3d::BLShape<2, 16>::smem(K, ns, nm) : (r16 ? f3d::BLShape<2>::smem(K, ns, nm) : smem_of(rr, ns));
+    const size_t sm = smem_of(ns);
     ++h->launches;
     int pe = prof_begin(h, prof_cls);
-    int fe = h->fe.kind;
-#define ISDC_BL(FE_, RR_, NM_) kl(h, f3d::k_bl<FE_, MODE, RR_, NM_>, grd, f3d::NT, sm)(maps, A, ns)
-#define ISDC_BL16(FE_) kl(h, f3d::k_bl<FE_, MODE, 1, 2, 16>, grd, 512, sm)(maps, A, ns)
-#define ISDC_BL12(FE_) kl(h, f3d::k_bl<FE_, MODE, 1, 4, 12>, grd, 384, sm)(maps, A, ns)
-#define ISDC_RHS16(FE_) kl(h, f3d::k_bl<FE_, MODE, 2, 1, 16>, grd, 512, sm)(maps, A, ns)
-#define ISDC_BL_FE(RR_, NM_)                                                   \
-    do {                                                                       \
-        if (fe == 0) ISDC_BL(0, RR_, NM_);                                     \
-        else if (fe == 1) ISDC_BL(1, RR_, NM_);                                \
-        else if (fe == 2) ISDC_BL(2, RR_, NM_);                                \
-        else ISDC_BL(3, RR_, NM_);                                             \
-    } while (0)
-    if (nm == 1 && r16b) { if (fe == 0) ISDC_RHS16(0); else if (fe == 1) ISDC_RHS16(1); else if (fe == 2) ISDC_RHS16(2); else ISDC_RHS16(3); }
-    else if (nm == 1) { if (rr == 4) ISDC_BL_FE(4, 1); else ISDC_BL_FE(2, 1); }
-    else if (w16) { if (fe == 0) ISDC_BL16(0); else if (fe == 1) ISDC_BL16(1); else if (fe == 2) ISDC_BL16(2); else ISDC_BL16(3); }
-    else if (nm == 2) ISDC_BL_FE(2, 2);
-    else if (w12) { if (fe == 0) ISDC_BL12(0); else if (fe == 1) ISDC_BL12(1); else if (fe == 2) ISDC_BL12(2); else ISDC_BL12(3); }
-    else ISDC_BL_FE(1, 4);
-#undef ISDC_BL_FE
-#undef ISDC_BL16
-#undef ISDC_BL12
-#undef ISDC_RHS16
-#undef ISDC_BL
+    auto go = [&](auto fec) {
+        constexpr int FE = decltype(fec)::value;
+        if (shape == S32) kl(h, f3d::k_bl<FE, MODE, 2, 1, 16>, grd, 512, sm)(maps, A, ns);
+        else if (shape == S16) kl(h, f3d::k_bl<FE, MODE, 2, 1>, grd, f3d::NT, sm)(maps, A, ns);
+        else kl(h, f3d::k_bl<FE, MODE, 1, 2, 16>, grd, 512, sm)(maps, A, ns);
+    };
+    const int fe = h->fe.kind;
+    if (fe == 0) go(std::integral_constant<int, 0>{});
+    else if (fe == 1) go(std::integral_constant<int, 1>{});
+    else if (fe == 2) go(std::integral_constant<int, 2>{});
+    else go(std::integral_constant<int, 3>{});
     prof_end(h, pe, prof_cls, bytes);
     LAUNCH_CHECK(h);
     return ISDC_OK;
@@ -769,22 +693,8 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
 // fused pre-smoother (2 sweeps) + defect + full weighting, 2D; in == nullptr: zero iterate
 isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                             double *bc, const GridDesc &gc, const SCoef &c, int level) {
-    if (h->sr_stream) {   // warp-strip streaming variant (no shared memory)
-        ++h->launches;
-        const int cls = level == 0 ? PROF_RESTRICT : PROF_COARSE;
-        int pe = prof_begin(h, cls);
-        const int strips = (g.n + f2d::SR_OUT - 1) / f2d::SR_OUT;
-        const int yc = g.n >= 1023 ? 64 : 32;
-        dim3 grd((strips + f2d::SW_NT / 32 - 1) / (f2d::SW_NT / 32), (g.n + yc - 1) / yc);
-        if (in) kl(h, f2d::k_sr_s<0>, grd, f2d::SW_NT, 0)(in, b, out, bc, g.n, g.pitch, gc.n, gc.pitch, c, yc);
-        else kl(h, f2d::k_sr_s<1>, grd, f2d::SW_NT, 0)(in, b, out, bc, g.n, g.pitch, gc.n, gc.pitch, c, yc);
-        prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + 2.0) * npts_of(h, g));
-        LAUNCH_CHECK(h);
-        return ISDC_OK;
-    }
-    // 32-row tiles on the large levels, 16-row tiles where more CTAs matter (ISDC_SR_TY32_MIN)
-    const bool t32 = g.n >= h->sr_ty32_min;
-    const int TY = t32 ? h->sr_ty : (g.n <= h->small_n ? h->sr_ty_small : 16);
+    // 40-row tiles on the large levels, 16 rows in between, 8 on n <= 511
+    const int TY = g.n >= 2047 ? 40 : (g.n <= 511 ? 8 : 16);
     const CUtensorMap *mb = tmap(h, b, g, f2d::FR_BW, TY + 5);
     const CUtensorMap *mu = in ? tmap(h, in, g, f2d::FR_UW, TY + 7) : mb;
     if (!mu || !mb) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
@@ -792,31 +702,15 @@ isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const do
     const int cls = level == 0 ? PROF_RESTRICT : PROF_COARSE;
     int pe = prof_begin(h, cls);
     dim3 grd((g.n + f2d::FR_TX - 1) / f2d::FR_TX, (g.n + TY - 1) / TY);
-    if (TY == 48) {
-        size_t sm = sizeof(f2d::SmemSR<48>) + 128;
-        if (in) kl(h, f2d::k_smooth2r<0, 48>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-        else kl(h, f2d::k_smooth2r<1, 48>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    } else if (TY == 40) {
-        size_t sm = sizeof(f2d::SmemSR<40>) + 128;
-        if (in) kl(h, f2d::k_smooth2r<0, 40>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-        else kl(h, f2d::k_smooth2r<1, 40>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    } else if (TY == 32) {
-        size_t sm = sizeof(f2d::SmemSR<32>) + 128;
-        if (in) kl(h, f2d::k_smooth2r<0, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-        else kl(h, f2d::k_smooth2r<1, 32>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    } else if (TY == 8) {
-        size_t sm = sizeof(f2d::SmemSR<8>) + 128;
-        if (in) kl(h, f2d::k_smooth2r<0, 8>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-        else kl(h, f2d::k_smooth2r<1, 8>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    } else if (TY == 24) {
-        size_t sm = sizeof(f2d::SmemSR<24>) + 128;
-        if (in) kl(h, f2d::k_smooth2r<0, 24>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-        else kl(h, f2d::k_smooth2r<1, 24>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    } else {
-        size_t sm = sizeof(f2d::SmemSR<16>) + 128;
-        if (in) kl(h, f2d::k_smooth2r<0, 16>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-        else kl(h, f2d::k_smooth2r<1, 16>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
-    }
+    auto go = [&](auto tyc) {
+        constexpr int T = decltype(tyc)::value;
+        const size_t sm = sizeof(f2d::SmemSR<T>) + 128;
+        if (in) kl(h, f2d::k_smooth2r<0, T>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+        else kl(h, f2d::k_smooth2r<1, T>, grd, f2d::NT, sm)(*mu, *mb, out, bc, g.n, g.pitch, gc.n, gc.pitch, c);
+    };
+    if (TY == 40) go(std::integral_constant<int, 40>{});
+    else if (TY == 8) go(std::integral_constant<int, 8>{});
+    else go(std::integral_constant<int, 16>{});
     // algorithmic bytes: read u (unless zero), b; write u'', b_c
     prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + 2.0) * npts_of(h, g));
     LAUNCH_CHECK(h);
@@ -982,13 +876,7 @@ isdc_status smooth(isdc_ctx *h, int l, double *X, double *T, const double *b, co
 // X holds the iterate on exit; src (nullable) is the initial iterate when it lives elsewhere
 // (first cycle of a node solve reads u_{m+1}^k in place, never writing it).
 // ---------------------------------------------------------------------------------------------
-isdc_status tail_dispatch(isdc_ctx *h, const TailParams &P, bool attr_only = false) {
-    if (attr_only) {
-        cudaError_t e = (h->d == 2)
-            ? cudaFuncSetAttribute(k_tail<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem)
-            : cudaFuncSetAttribute(k_tail<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tail_smem);
-        return e == cudaSuccess ? ISDC_OK : ISDC_ERR_CUDA;
-    }
+isdc_status tail_dispatch(isdc_ctx *h, const TailParams &P) {
     if (h->d == 2) kl(h, k_tail<2>, 1, TAIL_THREADS, h->tail_smem)(P);
     else kl(h, k_tail<3>, 1, TAIL_THREADS, h->tail_smem)(P);
     return ISDC_OK;
@@ -1070,12 +958,6 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
         TRY(launch_smooth2(h, dst, curw, b, g, c, nullptr, l, C.e, &C.g));
         cu = dst;
         TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2 - 2));
-    } else if (use_fast3d(h, l) && h->fuse3d && h->P.mg.nu2 >= 2) {
-        // fused trilinear prolongation + correction + two sweeps (one z-stream)
-        double *dst = (curw == T) ? X : T;
-        TRY(launch_smooth2_3d(h, dst, curw, b, g, c, l, C.e, &C.g));
-        cu = dst;
-        TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2 - 2));
     } else {
         TRY(launch_prolong(h, curw, g, C.e, C.g, l));
         TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2));
@@ -1127,7 +1009,6 @@ dim3 stream2d_grid(const isdc_ctx *h, int &yc) {
     const int strips = (n + f2d::SW_OUT - 1) / f2d::SW_OUT;
     const int cx = (strips + f2d::SW_NT / 32 - 1) / (f2d::SW_NT / 32);
     yc = n >= 2047 ? 64 : (n >= 511 ? 32 : 16);
-    if (h->stream_yc > 0) yc = h->stream_yc;   // ISDC_STREAM_YC: rows per CTA chunk
     return dim3(cx, (n + yc - 1) / yc);
 }
 bool stream2d_ok(const isdc_ctx *h) { return fast2d_pointwise_fe(h) && (h->M == 3 || h->M == 5) && h->stream2d; }
@@ -1293,10 +1174,10 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         double dt = h->P.dt, nudt = h->P.nu * dt;
         // two nodes per pass (RR = 2); the single-pass NM = 4 / RR = 1 variant measured slower
         // (cfg 5: 8.7 ms vs 2 x 3.4 ms per residual: 208 registers, 8-row regions)
-        const int per = h->bl_nm4 ? 4 : 2;   // ISDC_BL_NM4=1: all four nodes in one pass (12 warps x 1 row)
+        const int per = 2;
         const int passes = (M - 1 + per - 1) / per;
         for (int m0 = 1; m0 < M; m0 += per) {
-            const int nm = std::min(per, M - m0) == 3 ? 2 : std::min(per, M - m0);
+            const int nm = std::min(per, M - m0);
             for (int k = 0; k < f3d::BL_MAXNM; ++k) A.slot[k] = nullptr;
             for (int k = 0; k < nm; ++k) {
                 const int m = m0 + k;
@@ -1351,9 +1232,9 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             }
         }
         dim3 grd = stream2d_grid(h, A.yc);
-        if (M == 5) {   // ISDC_RES_NMW nodes per warp (2: 4 strips per CTA; 1: 2 strips per CTA)
+        if (M == 5) {   // two nodes per warp: 4 strips per CTA
             const int strips = (h->n + f2d::SW_OUT - 1) / f2d::SW_OUT;
-            grd.x = h->res_nmw == 1 ? (strips + 1) / 2 : (strips + 3) / 4;
+            grd.x = (strips + 3) / 4;
         }
         ++h->launches;
         int pe = prof_begin(h, PROF_RESID);
@@ -1372,8 +1253,7 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             } else if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
             else { if (fe == 0) ISDC_RS(0, 5); else if (fe == 1) ISDC_RS(1, 5); else ISDC_RS(2, 5); }
         };
-        if (h->res_nmw == 1) dispatch(std::integral_constant<int, 1>{});
-        else dispatch(std::integral_constant<int, 2>{});
+        dispatch(std::integral_constant<int, 2>{});
 #undef ISDC_RS
 #undef ISDC_RSW
         // algorithmic bytes: the node fields (+G) read; the folds are implementation traffic
@@ -1913,14 +1793,14 @@ isdc_status graph_tol_step(isdc_ctx *h, int *k_out, double *res_hist, double *re
         cudaGraphDestroy(g);
     }
     CUDA_TRY(h, cudaGraphLaunch(h->tstep_exec, h->s));
-    int hdr[4];
-    CUDA_TRY(h, cudaMemcpyAsync(hdr, h->sctl, sizeof hdr, cudaMemcpyDeviceToHost, h->s));
+    // the whole control block (counters + residual history) in one stream-ordered copy
+    std::vector<StepCtl> sc(1);
+    CUDA_TRY(h, cudaMemcpyAsync(sc.data(), h->sctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, h->s));
     CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    const int hdr[4] = {sc[0].k, sc[0].last, sc[0].bad, sc[0].cont};
     const int k = hdr[0];
     if (k < 1 || k > kStepHist) { h->err = "step graph: bad sweep count"; return ISDC_ERR_CUDA; }
-    std::vector<double> hs(k);
-    CUDA_TRY(h, cudaMemcpy(hs.data(), reinterpret_cast<char *>(h->sctl) + offsetof(StepCtl, hist), k * sizeof(double),
-                           cudaMemcpyDeviceToHost));
+    std::vector<double> hs(sc[0].hist, sc[0].hist + k);
     const int ka = k / 2, kb = (k - 1) / 2;   // loop sweeps A (1 -> 0) and B (0 -> 1) alternate
     h->launches += h->tstep_n[0] + (long)ka * h->tstep_n[1] + (long)kb * h->tstep_n[2];
     h->cur = hdr[1];
@@ -2018,6 +1898,63 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
     return run_residual(h, h->U[h->cur], res_per_node, res_max, h->Fs[h->cur], folds_on(h));
 }
 
+// Opt every kernel that takes dynamic shared memory into the full 227 KB per CTA, once per device
+// (the limit is an upper bound, so one value serves every handle; occupancy follows the launch's
+// actual size).  Guarded by a mutex: handles may be created from several threads.
+bool kernel_attrs(isdc_ctx *h) {
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { h->err = "cudaGetDevice failed"; return false; }
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(dev)) return true;
+    const int lim = kMaxDynSmem;
+    cudaError_t first = cudaSuccess;
+    auto set = [&](const void *k) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        if (e != cudaSuccess && first == cudaSuccess) first = e;
+    };
+    auto set2 = [&](auto T) {
+        constexpr int t = decltype(T)::value;
+        set((const void *)f2d::k_smooth2<true, 0, t>);
+        set((const void *)f2d::k_smooth2<false, 0, t>);
+        set((const void *)f2d::k_smooth2<false, 1, t>);
+        set((const void *)f2d::k_smooth2<false, 2, t>);
+    };
+    set2(std::integral_constant<int, 8>{}); set2(std::integral_constant<int, 16>{}); set2(std::integral_constant<int, 24>{});
+    auto setr = [&](auto T) {
+        constexpr int t = decltype(T)::value;
+        set((const void *)f2d::k_smooth2r<0, t>);
+        set((const void *)f2d::k_smooth2r<1, t>);
+    };
+    setr(std::integral_constant<int, 8>{}); setr(std::integral_constant<int, 16>{}); setr(std::integral_constant<int, 40>{});
+    set((const void *)f2d::k_restrict);
+    set((const void *)f2d::k_resid<0>); set((const void *)f2d::k_resid<1>); set((const void *)f2d::k_resid<2>);
+    set((const void *)f3d::k_smooth2<3, 0, 12>); set((const void *)f3d::k_smooth2<3, 1, 12>);
+    set((const void *)f3d::k_smooth2<4, 0, 8>); set((const void *)f3d::k_smooth2<4, 1, 8>);
+    set((const void *)f3d::k_restrict);
+    set((const void *)f3d::k_fe_cd4);
+    auto setbl = [&](auto F) {
+        constexpr int fe = decltype(F)::value;
+        for (const void *k : {(const void *)f3d::k_bl<fe, 0, 2, 1, 16>, (const void *)f3d::k_bl<fe, 0, 2, 1>,
+                              (const void *)f3d::k_bl<fe, 0, 1, 2, 16>, (const void *)f3d::k_bl<fe, 1, 2, 1, 16>,
+                              (const void *)f3d::k_bl<fe, 1, 2, 1>, (const void *)f3d::k_bl<fe, 1, 1, 2, 16>,
+                              (const void *)f3d::k_bl<fe, 2, 2, 1, 16>, (const void *)f3d::k_bl<fe, 2, 2, 1>,
+                              (const void *)f3d::k_bl<fe, 2, 1, 2, 16>})
+            set(k);
+    };
+    setbl(std::integral_constant<int, 0>{}); setbl(std::integral_constant<int, 1>{});
+    setbl(std::integral_constant<int, 2>{}); setbl(std::integral_constant<int, 3>{});
+    set((const void *)k_tail<2>); set((const void *)k_tail<3>);
+    set((const void *)k_ptail<2>); set((const void *)k_ptail<3>);
+    if (first != cudaSuccess) {
+        h->err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(first);
+        return false;
+    }
+    done.insert(dev);
+    return true;
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -2073,99 +2010,15 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
-    if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';
-    if (const char *b16 = getenv("ISDC_BL16")) h->bl16 = b16[0] != '0';
-    if (const char *b4 = getenv("ISDC_BL_NM4")) h->bl_nm4 = b4[0] != '0';
-    if (const char *r16 = getenv("ISDC_RHS16")) h->rhs16 = r16[0] != '0';
-    if (const char *t2 = getenv("ISDC_TAIL2D")) h->tail2d = atoi(t2);
-    if (const char *pd = getenv("ISDC_PDL")) h->pdl = pd[0] != '0';
-    if (const char *ss = getenv("ISDC_SR_STREAM")) h->sr_stream = ss[0] != '0';
-    if (const char *st = getenv("ISDC_SR_TY32_MIN")) h->sr_ty32_min = atoi(st);
-    if (const char *st = getenv("ISDC_SR_TY")) { const int v = atoi(st); h->sr_ty = (v == 24 || v == 40 || v == 48) ? v : 32; }
-    if (const char *rn = getenv("ISDC_RES_NMW")) h->res_nmw = atoi(rn) == 1 ? 1 : 2;
     if (const char *tf = getenv("ISDC_TAIL_FUSE")) h->tail_fuse_dr = tf[0] != '0';
-    if (const char *yc = getenv("ISDC_STREAM_YC")) h->stream_yc = atoi(yc);
-    if (const char *st = getenv("ISDC_SM_TY32_MIN")) h->sm_ty32_min = atoi(st);
-    if (const char *st = getenv("ISDC_SM_TY")) { const int v = atoi(st); h->sm_ty = (v == 24 || v == 40) ? v : 32; }
-    if (const char *st = getenv("ISDC_SMALL_N")) h->small_n = atoi(st);
-    if (const char *st = getenv("ISDC_SR_TY_SMALL")) h->sr_ty_small = atoi(st) == 8 ? 8 : 16;
-    if (const char *st = getenv("ISDC_SM_TY_SMALL")) h->sm_ty_small = atoi(st) == 8 ? 8 : 16;
-    if (const char *t3 = getenv("ISDC_TAIL3D")) h->tail3d = atoi(t3);
-    if (const char *sr = getenv("ISDC_SMOOTH3D_ROWS")) { int v = atoi(sr); h->smooth3d_rows = (v == 2 || v == 3 || v == 4) ? v : 0; }
     {
         int dev = 0, nsm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
             h->nsm = nsm;
     }
-    static bool attrs = false;
-    if (!attrs) {
-        cudaFuncSetAttribute(f2d::k_smooth2<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSmooth) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSmooth) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSmooth) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSmooth) + 128);
-        for (auto kern : {f2d::k_smooth2<true, 0, 32>, f2d::k_smooth2<false, 0, 32>, f2d::k_smooth2<false, 1, 32>,
-                          f2d::k_smooth2<false, 2, 32>})
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(f2d::SmemSmoothT<32>) + 128);
-        for (auto kern : {f2d::k_smooth2<true, 0, 40>, f2d::k_smooth2<false, 0, 40>, f2d::k_smooth2<false, 1, 40>,
-                          f2d::k_smooth2<false, 2, 40>})
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(f2d::SmemSmoothT<40>) + 128);
-        for (auto kern : {f2d::k_smooth2<true, 0, 24>, f2d::k_smooth2<false, 0, 24>, f2d::k_smooth2<false, 1, 24>,
-                          f2d::k_smooth2<false, 2, 24>})
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(f2d::SmemSmoothT<24>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<16>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<16>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<0, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<48>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<1, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<48>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<0, 40>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<40>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<1, 40>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<40>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<0, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<24>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<1, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<24>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<0, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<32>) + 128);
-        cudaFuncSetAttribute(f2d::k_smooth2r<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemSR<32>) + 128);
-        cudaFuncSetAttribute(f2d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(f2d::SmemRestrict) + 128);
-        cudaFuncSetAttribute(f3d::k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::R_SMEM);
-        cudaFuncSetAttribute(f3d::k_fe_cd4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3d::FE_SMEM);
-#define ISDC_BL_ATTR(FE_, MODE_, RR_, NM_) \
-        cudaFuncSetAttribute(f3d::k_bl<FE_, MODE_, RR_, NM_>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-#define ISDC_BL_ATTR4(MODE_, RR_, NM_) \
-        ISDC_BL_ATTR(0, MODE_, RR_, NM_) ISDC_BL_ATTR(1, MODE_, RR_, NM_) ISDC_BL_ATTR(2, MODE_, RR_, NM_) ISDC_BL_ATTR(3, MODE_, RR_, NM_)
-        ISDC_BL_ATTR4(0, 4, 1) ISDC_BL_ATTR4(0, 2, 1) ISDC_BL_ATTR4(1, 4, 1) ISDC_BL_ATTR4(1, 2, 1) ISDC_BL_ATTR4(1, 2, 2)
-        ISDC_BL_ATTR4(0, 2, 2) ISDC_BL_ATTR4(1, 1, 4) ISDC_BL_ATTR4(2, 4, 1) ISDC_BL_ATTR4(2, 2, 1)
-        for (auto kern : {f3d::k_bl<0, 1, 1, 4, 12>, f3d::k_bl<1, 1, 1, 4, 12>, f3d::k_bl<2, 1, 1, 4, 12>,
-                          f3d::k_bl<3, 1, 1, 4, 12>,
-                          f3d::k_bl<0, 1, 1, 2, 16>, f3d::k_bl<1, 1, 1, 2, 16>, f3d::k_bl<2, 1, 1, 2, 16>,
-                          f3d::k_bl<3, 1, 1, 2, 16>, f3d::k_bl<0, 0, 2, 1, 16>, f3d::k_bl<1, 0, 2, 1, 16>,
-                          f3d::k_bl<2, 0, 2, 1, 16>, f3d::k_bl<3, 0, 2, 1, 16>, f3d::k_bl<0, 2, 2, 1, 16>,
-                          f3d::k_bl<1, 2, 2, 1, 16>, f3d::k_bl<2, 2, 2, 1, 16>, f3d::k_bl<3, 2, 2, 1, 16>})
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-#undef ISDC_BL_ATTR4
-#undef ISDC_BL_ATTR
-        int rs = 2 * (ISDC_MAXM - 1) * f2d::ZH * f2d::ZW * (int)sizeof(double);
-        cudaFuncSetAttribute(f2d::k_resid<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
-        cudaFuncSetAttribute(f2d::k_resid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
-        cudaFuncSetAttribute(f2d::k_resid<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs);
-        attrs = true;
-    }
+    if (!kernel_attrs(h)) { delete h; return ISDC_ERR_CUDA; }
     const int cn = coarsest(h->per), Pc = (h->d == 3) ? cn * cn * cn : cn * cn;
     std::vector<double> Gi((size_t)h->M * Pc * Pc);
     h->wslot = h->M - 1;
@@ -2203,7 +2056,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                 T.fuse_dr = h->tail_fuse_dr ? 1 : 0;
             }
             h->tail_smem = (h->d == 2) ? tail_smem_bytes<2>(h->tailp[0]) : tail_smem_bytes<3>(h->tailp[0]);
-            if (h->tailp[0].nlev > TAIL_MAX_LEVELS || tail_dispatch(h, h->tailp[0], true) != ISDC_OK) h->tail_l0 = -1;
+            if (h->tailp[0].nlev > TAIL_MAX_LEVELS || h->tail_smem > (size_t)kMaxDynSmem) h->tail_l0 = -1;
         }
     }
     // periodic grids: levels n <= 64 (2D) / 16 (3D) in one single-CTA launch (kernels_ptail.cuh)
@@ -2225,10 +2078,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                 T.b_in = nullptr; T.u_in = nullptr; T.u_out = nullptr;
             }
             h->ptail_smem = (h->d == 2) ? ptail_smem_bytes<2>(h->ptailp[0]) : ptail_smem_bytes<3>(h->ptailp[0]);
-            cudaError_t ea = (h->d == 2)
-                ? cudaFuncSetAttribute(k_ptail<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ptail_smem)
-                : cudaFuncSetAttribute(k_ptail<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ptail_smem);
-            if (ea != cudaSuccess || h->ptail_smem > kMaxDynSmem) { cudaGetLastError(); h->ptail_l0 = -1; }
+            if (h->ptail_smem > (size_t)kMaxDynSmem) h->ptail_l0 = -1;
         } else {
             h->ptail_l0 = -1;   // a single level: the coarse solve alone
         }

@@ -45,7 +45,6 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
                                                 const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
                                                 int n, int pitch, SCoef c, unsigned long long *slot,
                                                 const __grid_constant__ CUtensorMap te) {
-    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // the tile-height dependent sizes (shadow the 16-row namespace constants)
     constexpr int TY = TY_, SB1 = (TY + 2 + 3) / 4, SB2 = TY / 4, UH = TY + 4, BH = TY + 2, TH = TY + 2;
@@ -60,7 +59,6 @@ __global__ void __launch_bounds__(NT) k_smooth2(const __grid_constant__ CUtensor
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     if (tid == 0) {
         mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : UW * UH) + BW * BH + (MODE == 2 ? EW * EH : 0)) * 8);
         if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 - 2, y0 - 2, &S.bar);
@@ -224,7 +222,6 @@ struct __align__(128) SmemRestrict {
 __global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtensorMap tu,
                                                   const __grid_constant__ CUtensorMap tb, double *__restrict__ bc,
                                                   int nf, int nc, int pitch_c, SCoef c) {
-    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemRestrict &S = *reinterpret_cast<SmemRestrict *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     const int tid = threadIdx.x;
@@ -237,7 +234,6 @@ __global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtens
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     if (tid == 0) {
         mbar_expect_tx(&S.bar, (RUW * RUH + RBW * RBH) * 8);
         tma_load_2d(&S.u[0][0], &tu, fx0 - 2, fy0 - 1, &S.bar);
@@ -295,8 +291,6 @@ __global__ void __launch_bounds__(RNT) k_restrict(const __grid_constant__ CUtens
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf, int pitch_f,
                                                  const double *__restrict__ e, int nc, int pitch_c) {
-    pdl_launch();
-    pdl_wait();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;   // column pair
     const int y = blockIdx.y;
     const int x = 2 * t;
@@ -357,8 +351,6 @@ struct RhsArgs {
 
 template <int FE>
 __global__ void __launch_bounds__(QNT) k_rhs(RhsArgs A, double *__restrict__ bout, unsigned long long *slot) {
-    pdl_launch();
-    pdl_wait();
     __shared__ double vs[QH][QW];
     __shared__ double ws[QH][QW];
     const int tid = threadIdx.x;
@@ -457,8 +449,6 @@ struct ResArgs {
 
 template <int FE>
 __global__ void __launch_bounds__(ZNT) k_resid(ResArgs A, unsigned long long *slots) {
-    pdl_launch();
-    pdl_wait();
     extern __shared__ __align__(16) double zsm[];
     const int M = A.M;
     double *ps = zsm;                                  // [M-1][ZH][ZW]
@@ -657,8 +647,6 @@ __device__ __forceinline__ void rhs_row(const StreamArgs &A, const double (&L)[M
 
 template <int FE, int MM, bool FOLD = false>
 __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
-    pdl_launch();
-    pdl_wait();
     const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5);
     const int n = A.n;
     const int x = strip * SW_OUT - 1 + lane;
@@ -715,8 +703,6 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
 // register rings and doubles the resident warps.
 template <int FE, int MM, int NMW, bool WRT = false, bool WF = false>   // WRT: also store the r~_m fields (unweighted
 __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {              // residual); WF: the next sweep's RHS folds
-    pdl_launch();
-    pdl_wait();
     constexpr int G = (MM - 1) / NMW;
     const int wid = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32 / G) + wid / G;
@@ -954,7 +940,6 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
                                                  const __grid_constant__ CUtensorMap tb, double *__restrict__ out,
                                                  double *__restrict__ bc, int n, int pitch, int nc, int pitch_c,
                                                  SCoef c) {
-    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using SR = SRT<FR_TY>;
     SmemSR<FR_TY> &S = *reinterpret_cast<SmemSR<FR_TY> *>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
@@ -967,7 +952,6 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     if (tid == 0) {
         mbar_expect_tx(&S.bar, ((MODE == 1 ? 0 : FR_UW * SR::UH) + FR_BW * SR::BH) * 8);
         if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 + FR_UOX, y0 + FR_UOY, &S.bar);
@@ -992,103 +976,6 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
     // takes the x-pair sums d(x-1) + d(x+1) by shuffles and emits the coarse points of fine rows
     // 4*band + 1 and 4*band + 3 at its odd columns (chunk 0: 1..29, chunk 1: 31..57).
     fr_defect_fw(S, x0, y0, nc, pitch_c, c, bc);
-}
-
-// ---------------------------------------------------------------------------------------------
-// Warp-strip y-streaming version of the fused pre-smoother + defect + full weighting (DESIGN.md
-// §6.2c): no shared memory.  A warp owns 24 output columns (lane l <-> fine column xs - 3 + l) and
-// walks down a chunk of rows; x-neighbour sums come from warp shuffles, y-neighbours from register
-// rings, so every stage (t = sweep 1, u'' = sweep 2, d = defect, full weighting) runs one row behind
-// the previous one.  Valid lanes shrink by one per stage (t 1..30, u'' 2..29, d 3..27); u'' is
-// stored on lanes 3..26 (the strip's 24 columns) and b_c at the 12 odd fine columns xs+1..xs+23.
-// Same canonical trees as k_smooth2r (bit-identical).
-// ---------------------------------------------------------------------------------------------
-constexpr int SR_OUT = 24;      // fine output columns per warp strip
-
-template <int MODE>
-__global__ void __launch_bounds__(SW_NT) k_sr_s(const double *__restrict__ u, const double *__restrict__ b,
-                                                double *__restrict__ out, double *__restrict__ bc, int n,
-                                                int pitch, int nc, int pitch_c, SCoef c, int yc) {
-    pdl_launch();
-    pdl_wait();
-    const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5);
-    const int xs = strip * SR_OUT;
-    if (xs >= n) return;                                  // whole warp leaves together
-    const int x = xs - 3 + lane;
-    const bool xin = x >= 0 && x < n;
-    const int y0 = blockIdx.y * yc, y1 = min(y0 + yc, n);    // yc even: coarse rows J with 2J+1 in [y0, y1)
-    const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
-    const bool store_u = lane >= 3 && lane < 3 + SR_OUT && x < n;
-    const bool store_c = lane >= 4 && lane <= 26 && (x & 1);   // odd fine x in xs+1 .. xs+23
-    const int I = (x - 1) / 2;
-    double uL[3];
-    double qu[3], ru[3], qt[3], rt[3], q2[3], r2[3], qd[3], rd[3];
-    const int nit = y1 - y0 + 7;                          // ingest rows y0-3 .. y1+3
-    auto ldu = [&](int r) -> double {
-        if (MODE == 1 || !xin || r < 0 || r >= n) return 0.0;
-        return __ldcs(u + (long long)r * pitch + x);
-    };
-    auto ldb = [&](int r) -> double {
-        if (!xin || r < 0 || r >= n) return 0.0;
-        return __ldg(b + (long long)r * pitch + x);
-    };
-    uL[0] = ldu(y0 - 3);
-    uL[1] = ldu(y0 - 2);
-    auto step = [&](auto Kc, int it) {
-        constexpr int k = decltype(Kc)::value, k1 = (k + 2) % 3, k2 = (k + 1) % 3;   // it, it-1, it-2 mod 3
-        const int r = y0 - 3 + it;
-        uL[k1] = ldu(r + 2);                              // row r+2 = it+2 (mod 3) = slot of row r-1
-        // ingest u(r)
-        const double q = uL[k];
-        qu[k] = q;
-        ru[k] = shfl_up1(q) + shfl_dn1(q);
-        // stage A: t at row r-1
-        if (it >= 2) {
-            const int ry = r - 1;
-            const double f = ru[k1] + (qu[k2] + qu[k]);
-            const double e = ru[k2] + ru[k];
-            const double su = (c0 * qu[k1] + c1 * f) + c2 * e;
-            const double tv = (xin && ry >= 0 && ry < n) ? qu[k1] + wd * (ldb(ry) - su) : 0.0;
-            qt[k1] = tv;
-            rt[k1] = shfl_up1(tv) + shfl_dn1(tv);
-        }
-        // stage B: u'' at row r-2 (t rows r-3, r-2, r-1 at slots k, k2, k1)
-        if (it >= 4) {
-            const int ry = r - 2;
-            const double f = rt[k2] + (qt[k] + qt[k1]);
-            const double e = rt[k] + rt[k1];
-            const double su = (c0 * qt[k2] + c1 * f) + c2 * e;
-            const bool in = xin && ry >= 0 && ry < n;
-            const double v = in ? qt[k2] + wd * (ldb(ry) - su) : 0.0;
-            q2[k2] = v;
-            r2[k2] = shfl_up1(v) + shfl_dn1(v);
-            if (store_u && ry >= y0 && ry < y1 && ry < n) out[(long long)ry * pitch + x] = v;
-        }
-        // stage C: d at row r-3 (u'' rows r-4, r-3, r-2 at slots k1, k, k2)
-        if (it >= 6) {
-            const int ry = r - 3;
-            const double f = r2[k] + (q2[k1] + q2[k2]);
-            const double e = r2[k1] + r2[k2];
-            const double su = (c0 * q2[k] + c1 * f) + c2 * e;
-            const double dv = ldb(ry) - su;
-            qd[k] = dv;
-            rd[k] = shfl_up1(dv) + shfl_dn1(dv);
-            // full weighting when d row r-3 = 2J+2 (rows 2J, 2J+1, 2J+2 at slots k2, k1, k)
-            if (((ry - y0) & 1) == 0 && ry >= y0 + 2) {
-                const int J = ry / 2 - 1;
-                if (store_c && I < nc && J < nc) {
-                    const double fd = rd[k1] + (qd[k2] + qd[k]);
-                    const double ed = rd[k2] + rd[k];
-                    bc[(long long)J * pitch_c + I] = ((4.0 * qd[k1] + 2.0 * fd) + ed) * 0.0625;
-                }
-            }
-        }
-    };
-    for (int base = 0; base < nit; base += 3) {
-        step(std::integral_constant<int, 0>{}, base);
-        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
-        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
-    }
 }
 
 }  // namespace f2d

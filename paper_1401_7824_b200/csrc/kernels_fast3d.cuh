@@ -65,12 +65,6 @@ constexpr int S_TW = RW + 2, S_TH = RH + 2;
 constexpr int S_NS = 6;          // TMA pipeline depth (planes in flight)
 constexpr int S_UPL = a128(S_UW * S_UH * 8), S_BPL = a128(S_BW * S_BH * 8), S_TPL = a128(S_TW * S_TH * 8);
 constexpr size_t S_SMEM = (size_t)S_NS * (S_UPL + S_BPL) + 2 * S_TPL + 8 * S_NS + 128;
-// fused trilinear prolongation (PRO): per stage the two coarse planes (Za, Zb) of the fine plane p,
-// boxes of 20 x 18 at (ex0, ey0) with ex0 = (x0/2 - 2) rounded down to even (TMA rule)
-constexpr int S_EW = 20, S_EH = 18;
-constexpr int S_EPL = a128(S_EW * S_EH * 8);
-constexpr int S_EOFF = S_NS * (S_UPL + S_BPL) + 2 * S_TPL + 128;   // after the mbarriers
-constexpr size_t S_SMEM_PRO = (size_t)S_EOFF + (size_t)S_NS * 2 * S_EPL + 128;
 
 // region-height-dependent sizes of the fused smoother (region RHR = SR x warps rows; the constants
 // above are the 32-row case)
@@ -79,8 +73,6 @@ struct SS {
     static constexpr int TY = RHR - 2, UH = RHR + 2, BH = RHR, TH = RHR + 2;
     static constexpr int UPL = a128(S_UW * UH * 8), BPL = a128(S_BW * BH * 8), TPL = a128(S_TW * TH * 8);
     static constexpr size_t SMEM = (size_t)S_NS * (UPL + BPL) + 2 * TPL + 8 * S_NS + 128;
-    static constexpr int EOFF = S_NS * (UPL + BPL) + 2 * TPL + 128;
-    static constexpr size_t SMEM_PRO = (size_t)EOFF + (size_t)S_NS * 2 * S_EPL + 128;
 };
 
 // Register state of one thread (SR owned points).  Rings are indexed by the iteration that
@@ -97,8 +89,6 @@ template <int SR>
 struct SmoothCtx {
     const double *Us, *Bs;
     double *Ts;
-    const double *Es;              // PRO: coarse planes, 2 per stage
-    int x0, y0, ex0, ey0;          // PRO: tile and coarse-box origins
     uint64_t *bar;
     double *optr;                  // output address of the owned column at plane z0 - 4, row ly0
     long long plane;
@@ -107,47 +97,7 @@ struct SmoothCtx {
     double c0, c1, c2, wd;
 };
 
-// PRO: u(p) += P e on the whole u box of plane p (in place, in-domain points only), canonical
-// nesting x, then y, then z; one multiply by 0.5^(#even axes).  Warp = box row
-// (rows w, w + nwarps, ...), lane = box column (plus lanes 0-1 for columns 32-33); the column
-// quantities are per-lane constants, the row quantities per-row constants.
-__device__ __noinline__ void prolong_plane(double *U, const double *Ea, const double *Eb, int p, int n, int x0, int y0,
-                                           int ex0, int ey0, int uh) {
-    // out of line: the z loop is unrolled by 6, an inlined copy per step overflows the i-cache
-    if ((unsigned)p >= (unsigned)n) return;
-    const bool ze = !(p & 1);
-    const double *E1 = ze ? Eb : Ea;
-    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-        const int lx = lane + 32 * cc;
-        if (lx >= S_UW) break;
-        const int gx = x0 - 2 + lx;
-        if ((unsigned)gx >= (unsigned)n) continue;
-        const bool xe = !(gx & 1);
-        const int xa = (xe ? gx / 2 - 1 : (gx - 1) / 2) - ex0;
-        const double wx = xe ? 0.5 : 1.0;
-        for (int ly = threadIdx.x >> 5; ly < uh; ly += nw) {
-            const int gy = y0 - 2 + ly;
-            if ((unsigned)gy >= (unsigned)n) continue;
-            const bool ye = !(gy & 1);
-            const int ya = (ye ? gy / 2 - 1 : (gy - 1) / 2) - ey0;
-            auto sx = [&](const double *E, int r) {
-                const double *row = E + r * S_EW + xa;
-                return xe ? row[0] + row[1] : row[0];
-            };
-            auto sy = [&](const double *E) { return ye ? sx(E, ya) + sx(E, ya + 1) : sx(E, ya); };
-            const double sz = ze ? sy(Ea) + sy(E1) : sy(Ea);
-            double w = wx;
-            if (ye) w *= 0.5;
-            if (ze) w *= 0.5;
-            double &uu = U[ly * S_UW + lx];
-            uu = uu + sz * w;
-        }
-    }
-}
-
-template <int SR, int K, bool PRO, int RHR>   // K = it % 6 = it % S_NS (the z loop is unrolled by 6 from it = 0)
+template <int SR, int K, int RHR>   // K = it % 6 = it % S_NS (the z loop is unrolled by 6 from it = 0)
 __device__ __forceinline__ void smooth_step(const SmoothCtx<SR> &C, SmoothRegs<SR> &G, int it, uint32_t phase) {
     using Z = SS<RHR>;
     static_assert(S_NS == 6, "stage index = K");
@@ -155,11 +105,6 @@ __device__ __forceinline__ void smooth_step(const SmoothCtx<SR> &C, SmoothRegs<S
     constexpr int i2 = K % 2, m2 = (K + 1) % 2;                       // it, it-1 (mod 2)
     constexpr int s = K;
     mbar_wait(&C.bar[s], phase);
-    if (PRO) {
-        prolong_plane(const_cast<double *>(C.Us + s * (Z::UPL / 8)), C.Es + (2 * s) * (S_EPL / 8),
-                      C.Es + (2 * s + 1) * (S_EPL / 8), C.z0 - 2 + it, C.n, C.x0, C.y0, C.ex0, C.ey0, Z::UH);
-        __syncthreads();
-    }
     plane_partials<true, SR>(C.Us + s * (Z::UPL / 8), S_UW, C.row0, C.lane, G.q[i3], G.f[i3], G.e[i2]);
     double *T = C.Ts + i2 * (Z::TPL / 8);
     if (it >= 2) {   // sweep 1 at plane gz = p-1 on the 32 x 32 region
@@ -203,18 +148,14 @@ __device__ __forceinline__ void smooth_step2(const SmoothCtx<SR> &C, SmoothRegs<
 }
 
 // u box 34 x 34 at (x0-2, y0-2); b box 34 x 32 at (x0-2, y0-1); t plane 34 x 34 (pad ring).
-// SR rows per thread, 32 / SR warps (the region is always 32 x 32).  MODE 0: u from memory;
-// MODE 1: u == 0 (first smoothing of a coarse correction: u is neither stored nor read, the
-// u stages stay zero); MODE 2: u + P e first (fused trilinear prolongation + correction, te =
-// coarse correction map with 20 x 18 x 1 boxes).
+// SR rows per thread, NWW warps (region SR * NWW rows).  MODE 0: u from memory; MODE 1: u == 0
+// (first smoothing of a coarse correction: u is neither stored nor read, the u stages stay zero).
 template <int SR, int MODE, int NWW = 32 / SR>
 __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__ CUtensorMap tu,
                                                                 const __grid_constant__ CUtensorMap tb,
                                                                 double *__restrict__ out, int n, int pitch,
-                                                                long long plane, SCoef c, int zc,
-                                                                const __grid_constant__ CUtensorMap te) {
-    pdl_launch();
-    constexpr bool PRO = MODE == 2, ZERO = MODE == 1;
+                                                                long long plane, SCoef c, int zc) {
+    constexpr bool ZERO = MODE == 1;
     constexpr int RHR = SR * NWW;   // region rows
     using Z = SS<RHR>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -224,9 +165,7 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__
     C.Bs = reinterpret_cast<const double *>(sm + S_NS * Z::UPL);
     C.Ts = reinterpret_cast<double *>(sm + S_NS * (Z::UPL + Z::BPL));
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S_NS * (Z::UPL + Z::BPL) + 2 * Z::TPL);
-    double *Esw = reinterpret_cast<double *>(sm + Z::EOFF);
     C.bar = bar;
-    C.Es = Esw;
     const int tid = threadIdx.x;
     C.lane = tid & 31;
     C.row0 = SR * (tid >> 5);
@@ -234,18 +173,12 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__
     const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, n);
     const int nit = z1 - z0 + 4;
     C.z0 = z0; C.n = n; C.pitch = pitch; C.plane = plane;
-    C.x0 = x0; C.y0 = y0; C.ex0 = (x0 / 2 - 2) & ~1; C.ey0 = y0 / 2 - 2;
     double *Usw = reinterpret_cast<double *>(sm), *Bsw = reinterpret_cast<double *>(sm + S_NS * Z::UPL);
     auto issue = [&](int it) {
         const int s = it % S_NS, p = z0 - 2 + it;
-        mbar_expect_tx(&bar[s], ((ZERO ? 0 : S_UW * Z::UH) + S_BW * Z::BH + (PRO ? 2 * S_EW * S_EH : 0)) * 8);
+        mbar_expect_tx(&bar[s], ((ZERO ? 0 : S_UW * Z::UH) + S_BW * Z::BH) * 8);
         if (!ZERO) tma_load_3d(Usw + s * (Z::UPL / 8), &tu, x0 - 2, y0 - 2, p, &bar[s]);
         tma_load_3d(Bsw + s * (Z::BPL / 8), &tb, x0 - 2, y0 - 1, p - 1, &bar[s]);
-        if (PRO) {   // coarse planes Za, Zb of fine plane p (Za = Zb for odd p)
-            const int za = (p & 1) ? (p - 1) / 2 : p / 2 - 1, zb = (p & 1) ? za : p / 2;
-            tma_load_3d(Esw + (2 * s) * (S_EPL / 8), &te, C.ex0, C.ey0, za, &bar[s]);
-            tma_load_3d(Esw + (2 * s + 1) * (S_EPL / 8), &te, C.ex0, C.ey0, zb, &bar[s]);
-        }
     };
     if (tid == 0) {
         tma_prefetch_desc(&tu);
@@ -257,7 +190,6 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__
         for (int s = 0; s < S_NS; ++s)
             for (int q = tid; q < S_UW * Z::UH; q += blockDim.x) Usw[s * (Z::UPL / 8) + q] = 0.0;
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < S_NS && it < nit; ++it) issue(it);
 
@@ -283,7 +215,7 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__
     {                                                                  \
         const int it = base + (K);                                     \
         if (it < nit) {                                                \
-            smooth_step<SR, K, (MODE == 2), RHR>(C, G, it, phase);    \
+            smooth_step<SR, K, RHR>(C, G, it, phase);    \
             __syncthreads();                                           \
             if (tid == 0 && it + S_NS < nit) issue(it + S_NS);         \
             smooth_step2<SR, K, RHR>(C, G, it);                       \
@@ -316,7 +248,6 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
                                                     const __grid_constant__ CUtensorMap tb,
                                                     double *__restrict__ bc, int nf, int nc, int pitch_c,
                                                     long long plane_c, SCoef c, int kc) {
-    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);   // stays a shared pointer
     double *Us = reinterpret_cast<double *>(sm);
@@ -341,7 +272,6 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < R_NS && it < nit; ++it) issue(it);
 
@@ -419,8 +349,6 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
 __global__ void __launch_bounds__(256) k_prolong(double *__restrict__ u, int nf, int pitch_f, long long plane_f,
                                                  const double *__restrict__ e, int nc, int pitch_c,
                                                  long long plane_c) {
-    pdl_launch();
-    pdl_wait();
     // two fine rows (y0, y0 + 1) per thread: both 16-byte u loads are issued before either update
     // (memory-level parallelism); the per-point expressions are unchanged
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -670,7 +598,6 @@ __device__ __forceinline__ void bl_resid_point(const BLArgs &A, const double *F,
 // NWW warps (region rows NWW * RR).
 template <int FE, int MODE, int RR, int NM, int NWW = NW>
 __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
-    pdl_launch();
     using SH = BLShape<RR, NWW>;
     constexpr bool RHS = MODE != 1;   // MODE 0: RHS, 1: residual, 2: RHS from stored folds
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -695,7 +622,6 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < ns && it < nit; ++it) issue(it);
 
@@ -819,7 +745,6 @@ constexpr size_t FE_SMEM = (size_t)FE_NS * FE_PL + 8 * FE_NS + 128;
 __global__ void __launch_bounds__(NT, 1) k_fe_cd4(const __grid_constant__ CUtensorMap tu, double *__restrict__ Fout,
                                                   int n, int pitch, long long plane, double kx, double ky,
                                                   double kz, int zc) {
-    pdl_launch();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     double *Us = reinterpret_cast<double *>(sm);
@@ -838,7 +763,6 @@ __global__ void __launch_bounds__(NT, 1) k_fe_cd4(const __grid_constant__ CUtens
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     if (tid == 0)
         for (int it = 0; it < FE_NS && it < nit; ++it) issue(it);
     const int gx = x0 + lane;

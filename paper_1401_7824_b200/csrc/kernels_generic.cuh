@@ -41,8 +41,6 @@ struct PZParams {                 // residual of node m
 template <int D>
 __global__ void k_jacobi(double *__restrict__ out, const double *__restrict__ u, const double *__restrict__ b,
                          GridDesc g, SCoef c) {
-    pdl_launch();
-    pdl_wait();
     POINT_INDEX_OR_RETURN(g)
     if (!inside) return;
     long long p = gidx(g, i, j, k);
@@ -53,8 +51,6 @@ __global__ void k_jacobi(double *__restrict__ out, const double *__restrict__ u,
 template <int D>
 __global__ void k_defect_norm(const double *__restrict__ u, const double *__restrict__ b, GridDesc g, SCoef c,
                               unsigned long long *slot) {
-    pdl_launch();
-    pdl_wait();
     POINT_INDEX_OR_RETURN(g)
     double v = 0.0;
     if (inside) v = fabs(b[gidx(g, i, j, k)] - apply_S<D>(c, u, g, i, j, k));
@@ -64,8 +60,6 @@ __global__ void k_defect_norm(const double *__restrict__ u, const double *__rest
 // ||q||_inf into *slot
 template <int D>
 __global__ void k_norm(const double *__restrict__ q, GridDesc g, unsigned long long *slot) {
-    pdl_launch();
-    pdl_wait();
     POINT_INDEX_OR_RETURN(g)
     double v = 0.0;
     if (inside) v = fabs(q[gidx(g, i, j, k)]);
@@ -123,8 +117,6 @@ __device__ __forceinline__ double fw_defect(const SCoef &c, const double *u, con
 template <int D>
 __global__ void k_restrict_defect(double *__restrict__ bc, GridDesc gc, const double *__restrict__ u,
                                   const double *__restrict__ b, GridDesc gf, SCoef c) {
-    pdl_launch();
-    pdl_wait();
     int I = blockIdx.x * blockDim.x + threadIdx.x;
     int J = blockIdx.y * blockDim.y + threadIdx.y;
     int K = (D == 3) ? (int)blockIdx.z : 0;
@@ -171,8 +163,6 @@ __device__ __forceinline__ double prolong_val(const double *e, const GridDesc &g
 }
 template <int D>
 __global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double *__restrict__ e, GridDesc gc) {
-    pdl_launch();
-    pdl_wait();
     POINT_INDEX_OR_RETURN(gf)
     if (!inside) return;
     long long p = gidx(gf, i, j, k);
@@ -183,8 +173,6 @@ __global__ void k_prolong_add(double *__restrict__ u, GridDesc gf, const double 
 template <int D>
 __global__ void k_coarse_solve(double *__restrict__ u, const double *__restrict__ b, GridDesc g,
                                const double *__restrict__ Ginv) {
-    pdl_launch();
-    pdl_wait();
     const int n = g.n, P = (D == 3) ? n * n * n : n * n;
     __shared__ double bs[64];
     int t = threadIdx.x;
@@ -200,8 +188,6 @@ __global__ void k_coarse_solve(double *__restrict__ u, const double *__restrict_
 // RHS pass 1: v and w of Eq. (5), pointwise (CD4 reads radius 2)
 template <int D>
 __global__ void k_vw(double *__restrict__ V, double *__restrict__ W, VWParams P) {
-    pdl_launch();
-    pdl_wait();
     const GridDesc &g = P.g;
     POINT_INDEX_OR_RETURN(g)
     if (!inside) return;
@@ -228,8 +214,6 @@ __global__ void k_vw(double *__restrict__ V, double *__restrict__ W, VWParams P)
 template <int D>
 __global__ void k_bvw(double *__restrict__ Bout, const double *__restrict__ V, const double *__restrict__ W,
                       GridDesc g, BLConst c, unsigned long long *slot) {
-    pdl_launch();
-    pdl_wait();
     POINT_INDEX_OR_RETURN(g)
     double val = 0.0;
     if (inside) {
@@ -242,8 +226,6 @@ __global__ void k_bvw(double *__restrict__ Bout, const double *__restrict__ V, c
 // residual pass 1 for node m: p = (u_m - u_0) - sum qa_j fE(u_j),  z = sum qb_j u_j
 template <int D>
 __global__ void k_pz(double *__restrict__ Pf, double *__restrict__ Zf, PZParams P) {
-    pdl_launch();
-    pdl_wait();
     const GridDesc &g = P.g;
     POINT_INDEX_OR_RETURN(g)
     if (!inside) return;
@@ -268,8 +250,6 @@ __global__ void k_pz(double *__restrict__ Pf, double *__restrict__ Zf, PZParams 
 template <int D>
 __global__ void k_resid(const double *__restrict__ Pf, const double *__restrict__ Zf, GridDesc g, BLConst c,
                         unsigned long long *slot, double *__restrict__ out) {
-    pdl_launch();
-    pdl_wait();
     POINT_INDEX_OR_RETURN(g)
     double val = 0.0;
     if (inside) {
@@ -283,8 +263,6 @@ __global__ void k_resid(const double *__restrict__ Pf, const double *__restrict_
 template <int D>
 __global__ void k_fe(double *__restrict__ F, const double *__restrict__ u, GridDesc g, FeDesc fe,
                      const unsigned long long *aux) {
-    pdl_launch();
-    pdl_wait();
     POINT_INDEX_OR_RETURN(g)
     if (!inside) return;
     const double a = __longlong_as_double((long long)*aux);

@@ -135,7 +135,6 @@ __device__ __noinline__ void ptail_prolong2(int n, double *u, const double *e) {
 
 template <int D>
 __global__ void __launch_bounds__(PTAIL_THREADS, 1) k_ptail(PTailParams P) {
-    pdl_launch();
     extern __shared__ double sm[];
     double *U[PTAIL_MAX_LEVELS], *B[PTAIL_MAX_LEVELS], *T[PTAIL_MAX_LEVELS];
     {
@@ -147,7 +146,6 @@ __global__ void __launch_bounds__(PTAIL_THREADS, 1) k_ptail(PTailParams P) {
             T[l] = sm + off; off += pts;
         }
     }
-    pdl_wait();
     const int L = P.nlev - 1;
     ptail_points<D>(P.n[0], [&](int p, int, int, int) {
         B[0][p] = P.b_in[p];

@@ -191,7 +191,6 @@ __device__ __noinline__ void tail_ph_prolong(int oe, int ou, int n, int nc) {
 
 template <int D>
 __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailParams P) {
-    pdl_launch();
     const int L = P.nlev;
     const int lane = threadIdx.x & 31;
     __shared__ int offs[TAIL_MAX_LEVELS], szs[TAIL_MAX_LEVELS];
@@ -206,7 +205,6 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailParams P) {
         for (int q = threadIdx.x; q < tot; q += TAIL_THREADS) tsm[q] = 0.0;
     }
     __syncthreads();
-    pdl_wait();   // only shared-memory setup above
     // buffer w in {0,1} = iterate ping-pong, 2 = right-hand side
     auto ofs = [&](int l, int w) { return offs[l] + w * szs[l]; };
     {

@@ -171,10 +171,20 @@ class ISDC:
                 msg = self.L.isdc_last_error(self.h).decode()
             raise IsdcError(st, msg)
 
-    def _field(self, x) -> torch.Tensor:
-        t = torch.as_tensor(x, dtype=torch.float64).to(self.device).contiguous()
+    def _check_shape(self, t):
         if tuple(t.shape) != (self.n,) * self.dim:
             raise ValueError(f"field shape {tuple(t.shape)} != {(self.n,) * self.dim}")
+
+    def _field(self, x) -> torch.Tensor:
+        """A dense device field for the library.  A copy made here lives on torch's current stream:
+        the handle's stream waits for it and the tensor is recorded on that stream, so neither the
+        copy nor the caching allocator can race the library's stream-ordered reads."""
+        t = torch.as_tensor(x, dtype=torch.float64).to(self.device).contiguous()
+        self._check_shape(t)
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != self.stream.cuda_stream:
+            self.stream.wait_stream(cur)
+            t.record_stream(self.stream)
         return t
 
     def empty_field(self) -> torch.Tensor:
@@ -193,6 +203,7 @@ class ISDC:
         """u0: device tensor, or a host numpy array / CPU tensor (copied H2D by the library)."""
         if isinstance(u0, np.ndarray) or (isinstance(u0, torch.Tensor) and not u0.is_cuda):
             a = np.ascontiguousarray(u0 if isinstance(u0, np.ndarray) else u0.numpy(), dtype=np.float64)
+            self._check_shape(a)
             self._host_u0 = a
             self._check(self.L.isdc_set_initial_host(self.h, _np_ptr(a), step_index))
         else:
@@ -230,7 +241,9 @@ class ISDC:
     def vcycle(self, m: int, b, u: torch.Tensor):
         """One V-cycle in place on the device tensor u; returns (defect_before, defect_after)."""
         bt = self._field(b)
-        assert u.is_cuda and u.dtype == torch.float64 and u.is_contiguous()
+        if not (u.is_cuda and u.dtype == torch.float64 and u.is_contiguous()):
+            raise ValueError("u must be a contiguous float64 CUDA tensor (updated in place)")
+        self._check_shape(u)   # mg_vcycle writes n^d doubles into u
         d0, d1 = C.c_double(0), C.c_double(0)
         self._check(self.L.mg_vcycle(self.h, m, bt.data_ptr(), u.data_ptr(), C.byref(d0), C.byref(d1)))
         return d0.value, d1.value
@@ -244,12 +257,18 @@ class ISDC:
     def solution(self, node: int = -1, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         node = node % self.M
         out = self.empty_field() if out is None else out
+        if not (out.is_cuda and out.dtype == torch.float64 and out.is_contiguous()):
+            raise ValueError("out must be a contiguous float64 CUDA tensor")
+        self._check_shape(out)
         self._check(self.L.isdc_get_solution(self.h, node, out.data_ptr()))
         return out
 
     def solution_host(self, node: int = -1, out: Optional[np.ndarray] = None) -> np.ndarray:
         node = node % self.M
         out = np.empty((self.n,) * self.dim) if out is None else out
+        if out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 array")
+        self._check_shape(out)
         self._check(self.L.isdc_get_solution_host(self.h, node, _np_ptr(out)))
         return out
 

@@ -1,6 +1,9 @@
 """Summarise a per-kernel ncu metric CSV (scripts/ncu_classes.sh) into a committed table.
 
-    python scripts/ncu_class_summary.py gpurun_out/<tag>/ncu_cfg5.csv profiles/<name>.txt "<title>"
+    python scripts/ncu_class_summary.py gpurun_out/<tag>/ncu_cfg5.csv profiles/<name>.txt "<title>" [WORKLOAD]
+
+With WORKLOAD (e.g. cfg5_advdiff3d_511_M5) it also records, in profiles/ncu_traffic.json, the DRAM
+bytes per launch of each kernel class's fine-level launch (bench.py's roofline "traffic").
 
 Groups launches by (kernel, grid) -- the grid tells the multigrid level apart -- and reports per
 group: launches, mean duration, DRAM bytes read / written per launch, DRAM throughput %, warps
@@ -8,7 +11,20 @@ active %, issue active %, L1/LSU %, shared-memory wavefronts, L2 hit %, fp64 pip
 """
 import collections
 import csv
+import json
+import os
+import re
 import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# bench.py kernel classes -> kernel-name patterns (the fine level is the launch with the largest grid)
+CLASS_PATTERNS = {
+    "fine_smoother": [r"f3d::k_smooth2<\d+, 0,"],
+    "fine_defect_restrict": [r"f3d::k_restrict", r"f2d::k_smooth2r<0,"],
+    "fine_prolong_correct": [r"f3d::k_prolong", r"f2d::k_smooth2<false, 2,", r"f2d::k_smooth2<0, 2,"],
+    "residual": [r"k_resid", r"f3d::k_bl<\d+, 1,"],
+    "rhs": [r"k_rhs", r"f3d::k_bl<\d+, [02],"],
+}
 
 SHORT = {
     "gpu__time_duration.sum": "us",
@@ -34,7 +50,14 @@ def short_name(k):
     return k.replace("void ", "")
 
 
-def main(path, out, title):
+def grid_size(g):
+    v = 1
+    for x in re.findall(r"\d+", g):
+        v *= int(x)
+    return v
+
+
+def main(path, out, title, workload=None):
     rows = [r for r in csv.reader(l for l in open(path) if not l.startswith("=="))]
     hdr, rows = rows[0], rows[1:]
     ix = {h: i for i, h in enumerate(hdr)}
@@ -66,7 +89,25 @@ def main(path, out, title):
         lines.append("%-34s %-14s %5d %6.3f " % (name[:34], grid, len(ms), share) + " ".join(vals))
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
+    if workload:
+        tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        db = json.load(open(tj)) if os.path.exists(tj) else {}
+        ent = {}
+        for cls, pats in CLASS_PATTERNS.items():
+            # the fine-level launch of a class is its longest one (grid sizes mix tiles and z chunks)
+            cand = [(sum(m.get("gpu__time_duration.sum", 0) for m in ms) / len(ms), name, grid, ms)
+                    for (name, grid, blk), ms in groups.items() if any(re.search(p, name) for p in pats)]
+            if not cand:
+                continue
+            gsz, name, grid, ms = max(cand)
+            rd = sum(m.get("dram__bytes_read.sum", 0) for m in ms) / len(ms)
+            wr = sum(m.get("dram__bytes_write.sum", 0) for m in ms) / len(ms)
+            ent[cls] = {"kernel": name, "grid": grid, "dram_bytes_per_launch": rd + wr, "dram_read": rd,
+                        "dram_write": wr, "source": f"{os.path.relpath(out, ROOT)} (longest launch of the class = fine level)"}
+        db[workload] = ent
+        json.dump(db, open(tj, "w"), indent=1)
+        print("traffic ->", tj, list(ent))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "")
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "", sys.argv[4] if len(sys.argv) > 4 else None)

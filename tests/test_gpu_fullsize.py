@@ -37,6 +37,9 @@ def test_fullsize_against_oracle_golden(path):
         r_gpu = np.array([float.fromhex(x) for x in got])
         r_ref = np.array([float.fromhex(x) for x in ref["res_hist"]])
         assert np.all(np.abs(r_gpu - r_ref) <= 1e-9 * np.abs(r_ref))   # the north-star bar (implied)
+        if "sha256" in ref:   # the end value u_M of every step of the trajectory
+            u_s = h.solution(0).cpu().numpy()
+            assert hashlib.sha256(np.ascontiguousarray(u_s, dtype="<f8").tobytes()).hexdigest() == ref["sha256"], s
     u = h.solution(0).cpu().numpy()
     for p, hx in rec["samples"]:
         assert float(u[tuple(reversed(p))]).hex() == hx, p

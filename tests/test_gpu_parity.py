@@ -207,11 +207,15 @@ def test_unweighted_residual_steps_bitwise(gpu, ora, cid, n, mode):
 @pytest.mark.parametrize("env,mode", [({"ISDC_DEVICE_SDC": "0"}, MODE_SDC), ({"ISDC_DEVICE_SDC": "0"}, MODE_ISDC_CAPPED),
                                       ({"ISDC_NO_GRAPHS": "1"}, MODE_ISDC), ({"ISDC_NO_GRAPHS": "1"}, MODE_SDC),
                                       ({"ISDC_GENERIC_KERNELS": "1"}, MODE_ISDC), ({"ISDC_FOLDS": "0"}, MODE_ISDC),
-                                      ({"ISDC_STEP_GRAPH": "0"}, MODE_ISDC), ({"ISDC_TAIL_FUSE": "0"}, MODE_ISDC)])
+                                      ({"ISDC_STEP_GRAPH": "0"}, MODE_ISDC), ({"ISDC_TAIL_FUSE": "0"}, MODE_ISDC),
+                                      ({"ISDC_STREAM2D": "0"}, MODE_ISDC), ({"ISDC_FUSE2D": "0"}, MODE_ISDC),
+                                      ({"ISDC_FAST3D_MASK": "0x1"}, MODE_ISDC), ({"ISDC_FAST3D_MASK": "0x6"}, MODE_ISDC),
+                                      ({"ISDC_FAST3D_MASK": "0x18"}, MODE_ISDC)])
 def test_execution_paths_bitwise(gpu, ora, monkeypatch, env, mode):
     """Host-side node-solve tests, un-captured sweeps, sweep-by-sweep steps, the generic kernels, the
-    fold-free RHS and the unfused tail produce the oracle's bits too (the environment is read when
-    the handle is created)."""
+    fold-free RHS, the unfused tail, the tile-based 2D RHS / residual, the unfused 2D transfers and
+    every subset of the fast 3D kernels (mask bits: 1 smoother, 2 restriction, 4 prolongation, 8 RHS,
+    16 residual) produce the oracle's bits too (the environment is read when the handle is created)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for cid, n in ((2, 127), (4, 31)):
@@ -258,3 +262,66 @@ def test_edge_cases_bitwise(gpu, ora, dim, n, M, L, nu1, nu2, guess, mode, fe):
         assert np.array_equal(st["node_cycles"], st_ref["node_cycles"])
         assert np.array_equal(st["res_hist"], st_ref["res_hist"])
         assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)
+
+
+# ------------------------------------------------------------- non-finite detection (errors)
+@pytest.mark.parametrize("cid,n,mode,bad", [(1, 63, MODE_ISDC, np.nan), (2, 127, MODE_ISDC, np.inf),
+                                            (3, 127, MODE_SDC, np.nan), (4, 31, MODE_ISDC, -np.inf),
+                                            (5, 31, MODE_ISDC, np.nan), (2, 127, MODE_ISDC_CAPPED, np.nan)])
+def test_nonfinite_input_raises(gpu, cid, n, mode, bad):
+    """A NaN / Inf in u0 propagates into the residual (or the SDC defect test) and the step returns
+    ISDC_ERR_NONFINITE (include/isdc.h) instead of a silent result, on every execution path: the
+    fixed-sweep step graph (cfg 1), the tolerance-stopped step graph (cfgs 2, 4, 5), the device SDC /
+    capped node-solve loop (cfg 3 SDC, cfg 2 capped)."""
+    cfg, u0, G = synth.problem_inputs(cid, 0, n)
+    u0 = u0.copy()
+    u0[(n // 3,) * cfg.dim] = bad
+    h = make(gpu, cfg, G, mode=mode)
+    h.set_initial(torch.from_numpy(u0).cuda(), 0)
+    with pytest.raises(gpu.IsdcError) as ei:
+        h.step()
+    assert ei.value.status == 4, str(ei.value)
+    # residual_norm on the spread state of a poisoned u0 reports it too
+    h.set_initial(torch.from_numpy(u0).cuda(), 0)
+    with pytest.raises(gpu.IsdcError) as ei:
+        h.residual()
+    assert ei.value.status == 4
+
+
+def test_binding_rejects_bad_shapes(gpu):
+    cfg = synth.Config(0, 2, 63, 3, 0.01, 1.0, FE_NONE)
+    h = make(gpu, cfg)
+    b = synth.random_field(63, 2, 1)
+    with pytest.raises(ValueError):
+        h.vcycle(0, b, torch.zeros(31, 31, dtype=torch.float64, device="cuda"))   # would be an OOB write
+    with pytest.raises(ValueError):
+        h.set_initial(torch.zeros(62, 63, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        h.solution(0, out=torch.zeros(63, 64, dtype=torch.float64, device="cuda"))
+
+
+def test_handle_on_side_stream_matches_default(gpu, ora):
+    """A handle bound to a non-default stream (temporaries recorded on it) gives the same bits."""
+    cfg, u0, G = synth.problem_inputs(2, 0, 127)
+    side = torch.cuda.Stream()
+    h = gpu.ISDC.from_config(cfg, None, mode=MODE_ISDC, stream=side)
+    h.set_initial(torch.from_numpy(u0).cuda(), 0)
+    st = h.step()
+    u_ref, st_ref = ora.step(ora.Problem(cfg, G), u0, 0.0)
+    assert st["sweeps"] == st_ref["sweeps"]
+    assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)
+
+
+def test_handles_with_different_tail_sizes_coexist(gpu, ora):
+    """creating a small 3D handle must not break a larger one created earlier (the
+    kernels' shared-memory limits are set once per device to the maximum)."""
+    cfg_big, u_big, _ = synth.problem_inputs(4, 0, 63)
+    big = make(gpu, cfg_big)
+    small = make(gpu, synth.Config(0, 3, 7, 3, 0.01, 1.0, FE_NONE))
+    small.set_initial(torch.from_numpy(synth.random_field(7, 3, 3)).cuda(), 0)
+    small.step()
+    big.set_initial(torch.from_numpy(u_big).cuda(), 0)
+    st = big.step()
+    u_ref, st_ref = ora.step(ora.Problem(cfg_big), u_big, 0.0)
+    assert st["sweeps"] == st_ref["sweeps"]
+    assert np.array_equal(big.solution(0).cpu().numpy(), u_ref)
