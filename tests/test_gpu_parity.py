@@ -124,7 +124,7 @@ STEP_CASES = [
     (2, 0, 127, MODE_ISDC), (2, 1, 127, MODE_ISDC), (2, 2, 127, MODE_ISDC),
     (3, 0, 255, MODE_ISDC), (3, 0, 255, MODE_SDC),
     (4, 0, 31, MODE_ISDC), (4, 1, 31, MODE_ISDC), (4, 2, 31, MODE_ISDC),
-    (5, 0, 31, MODE_ISDC),
+    (5, 0, 31, MODE_ISDC), (5, 0, 63, MODE_ISDC),
     (2, 0, 127, MODE_ISDC_CAPPED), (4, 0, 31, MODE_ISDC_CAPPED),
 ]
 
