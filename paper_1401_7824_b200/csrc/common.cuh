@@ -155,6 +155,12 @@ __device__ __forceinline__ double fe_at(const FeDesc &fe, const double *u, const
     return -((dx + dy) + dz);
 }
 
+// ---- named barrier over `count` threads (warp-specialised kernels: the roles reach it from
+// different code locations; count is a multiple of 32)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ---- max-norm reduction: non-negative doubles ordered as uint64; NaN bits exceed +Inf ---------
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll

@@ -163,7 +163,8 @@ struct isdc_ctx {
     bool per = false;          // periodic grid (NEXT f3): generic kernels on every level
     unsigned long long *alpha = nullptr;   // Burgers: max|u| slots, [0,M) uold_j, [8,8+M) unew_m, [16,16+M) residual u_j
     double cthost[ISDC_MAXM];
-    int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual
+    int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual,
+                               // 32 the single-pass four-node residual (M = 5; else two nodes per pass)
     int tail3d = 15;           // largest 3D level handled by the single-CTA tail (fast kernels above)
     int tail2d = 31;           // largest 2D level handled by the single-CTA tail (31 measured best)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
@@ -690,6 +691,33 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     return ISDC_OK;
 }
 
+// the four-node residual pass of M = 5 (f^E none or stored CD4), DESIGN.md §6.14
+isdc_status launch_resid4(isdc_ctx *h, const double *const *fields, int K, f3d::BLArgs A, double bytes) {
+    using SH = f3d::R4Shape;
+    const GridDesc &g = h->lev[0].g;
+    int ns = 4;
+    while (ns >= 2 && SH::smem(K, ns) > (size_t)kMaxDynSmem) --ns;
+    if (ns < 2) { h->err = "too many fields for the 3D residual kernel"; return ISDC_ERR_UNSUPPORTED; }
+    f3d::BLMaps maps;
+    for (int k = 0; k < K; ++k) {
+        const CUtensorMap *mk = tmap(h, fields[k], g, SH::FW, SH::FH, 1);
+        if (!mk) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+        maps.m[k] = *mk;
+    }
+    A.K = K; A.n = g.n; A.pitch = g.pitch; A.plane = g.plane; A.bl = h->bl; A.ct = h->ctdev;
+    const int tx = (g.n + SH::TX - 1) / SH::TX, ty = (g.n + SH::TY - 1) / SH::TY;
+    A.zc = pick_chunk(h, tx * ty, g.n, 2);
+    dim3 grd(tx, ty, (g.n + A.zc - 1) / A.zc);
+    const size_t sm = SH::smem(K, ns);
+    ++h->launches;
+    int pe = prof_begin(h, PROF_RESID);
+    if (h->fe.kind == 3) kl(h, f3d::k_resid4<3>, grd, f3d::R4_NT, sm)(maps, A, ns);
+    else kl(h, f3d::k_resid4<0>, grd, f3d::R4_NT, sm)(maps, A, ns);
+    prof_end(h, pe, PROF_RESID, bytes);
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
 // fused pre-smoother (2 sweeps) + defect + full weighting, 2D; in == nullptr: zero iterate
 isdc_status launch_smooth2r(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                             double *bc, const GridDesc &gc, const SCoef &c, int level) {
@@ -1172,8 +1200,28 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         int qnext = 0;   // next RHS node whose folds are still to be written
         A.M = M; A.dtm = A.gm = 0.0; A.out = nullptr;
         double dt = h->P.dt, nudt = h->P.nu * dt;
-        // two nodes per pass (RR = 2); the single-pass NM = 4 / RR = 1 variant measured slower
-        // (cfg 5: 8.7 ms vs 2 x 3.4 ms per residual: 208 registers, 8-row regions)
+        if (M == 5 && (fe == 0 || fe == 3) && use_fast3d(h, 0, 32)) {
+            // all four nodes (and the folds) in one pass: warp-specialised k_resid4
+            for (int k = 0; k < 4; ++k) {
+                const int m = k + 1;
+                A.mnode[k] = m;
+                for (int j = 0; j < M; ++j) { A.a[k][j] = dt * h->Q[m * M + j]; A.beta[k][j] = nudt * h->Q[m * M + j]; }
+                A.slot[k] = h->red + SLOT_RES0 + m - 1;
+                A.qnode[k] = k;
+            }
+            A.nfold = 0;
+            if (write_folds && fe == 3) {
+                for (int q = 0; q < 4; ++q) {
+                    for (int j = 0; j < M; ++j) { A.sa[q][j] = dts * h->S[q * M + j]; A.sb[q][j] = nudts * h->S[q * M + j]; }
+                    A.fgm[q] = h->P.nu * (h->P.dt * h->dtau[q]);   // the RHS's gamma_q = nu * dtm
+                    A.fa_out[q] = h->FA[q];
+                    A.wb_out[q] = h->WB[q];
+                }
+                A.nfold = 4;
+            }
+            return launch_resid4(h, fields, K, A, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
+        }
+        // two nodes per pass (16 warps x 1 row, 16-row regions)
         const int per = 2;
         const int passes = (M - 1 + per - 1) / per;
         for (int m0 = 1; m0 < M; m0 += per) {
@@ -1945,6 +1993,7 @@ bool kernel_attrs(isdc_ctx *h) {
     };
     setbl(std::integral_constant<int, 0>{}); setbl(std::integral_constant<int, 1>{});
     setbl(std::integral_constant<int, 2>{}); setbl(std::integral_constant<int, 3>{});
+    set((const void *)f3d::k_resid4<0>); set((const void *)f3d::k_resid4<3>);
     set((const void *)k_tail<2>); set((const void *)k_tail<3>);
     set((const void *)k_ptail<2>); set((const void *)k_ptail<3>);
     if (first != cudaSuccess) {

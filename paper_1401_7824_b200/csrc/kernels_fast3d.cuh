@@ -733,6 +733,145 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
 }
 
 // ---------------------------------------------------------------------------------------------
+// Weighted SDC residual of all four nodes of M = 5 (r~_m = B p_m - L z_m, m = 1..4)
+// and, for stored-f^E CD4, the next sweep's RHS folds (FA_q, WB_q, q = 0..3, §6.12) in ONE z-stream
+// pass: every node field u_j (and F_j) is read from HBM once per sweep instead of
+// once per two-node pass.  Warp-specialised: R4_PW producer warps form the pointwise (p_m, z_m) of
+// all four nodes and the folds from the TMA-staged planes (bl_resid_point: one shared load per input
+// field and point), store them to double-buffered shared planes and the folds to global memory;
+// 4 x R4_WG consumer warps -- one group per node -- take in-plane partials into register rings and
+// emit |r~_m| at plane p-1 (the trees of k_bl MODE 1).  Producers run one plane ahead of the
+// consumers; one block barrier per plane.  Region 32 x R4_RH (tile 30 x (R4_RH - 2) + halo 1).
+// ---------------------------------------------------------------------------------------------
+constexpr int R4_WG = 3, R4_RR = 4, R4_RH = R4_WG * R4_RR;   // consumer warps per node, rows per thread
+constexpr int R4_PW = 2;                                     // producer warps
+constexpr int R4_NT = 32 * (4 * R4_WG + R4_PW);
+struct R4Shape {
+    static constexpr int RH = R4_RH, TX = RW - 2, TY = R4_RH - 2;
+    static constexpr int FW = RW + 2, FH = R4_RH;              // input box 34 x RH at (x0-2, y0-1)
+    static constexpr int PW = RW + 2, PH = R4_RH + 2;          // p / z planes with a pad ring
+    static constexpr int FPL = a128(FW * FH * 8), PPL = a128(PW * PH * 8);
+    static size_t smem(int K, int ns) { return (size_t)ns * K * FPL + 2 * 8 * (size_t)PPL + 8 * 8 + 128; }
+};
+
+template <int FE>
+__global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
+    using SH = R4Shape;
+    constexpr int NM = 4, RR = R4_RR;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    const int K = A.K;
+    double *Fs = reinterpret_cast<double *>(sm);                                   // ns stages x K boxes
+    double *Ps = reinterpret_cast<double *>(sm + (size_t)ns * K * SH::FPL);        // [buf][node][p|z]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + (size_t)ns * K * SH::FPL + 16 * SH::PPL);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int n = A.n;
+    const int x0 = blockIdx.x * SH::TX, y0 = blockIdx.y * SH::TY;
+    const int z0 = blockIdx.z * A.zc, z1 = min(z0 + A.zc, n);
+    const int nit = z1 - z0 + 2;              // ingest planes z0-1 .. z1
+    constexpr int PROD0 = 4 * R4_WG;          // first producer warp
+    const bool producer = w >= PROD0;
+    auto issue = [&](int it) {
+        const int s = it % ns, p = z0 - 1 + it;
+        mbar_expect_tx(&bar[s], K * SH::FW * SH::FH * 8);
+        for (int k = 0; k < K; ++k)
+            tma_load_3d(Fs + ((size_t)s * K + k) * (SH::FPL / 8), &maps.m[k], x0 - 2, y0 - 1, p, &bar[s]);
+    };
+    const int ptid = tid - 32 * PROD0;        // producer thread index
+    if (ptid == 0) {
+        for (int s = 0; s < ns; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        for (int s = 0; s < ns && s < nit; ++s) issue(s);
+    }
+    __syncthreads();
+    const bool folds = FE == 3 && A.nfold > 0;
+    // the two roles run separate loops (so the consumers' rings are not live in the producers' code)
+    // that meet at one named barrier per plane
+    if (producer) {
+        for (int it = 0; it < nit; ++it) {
+            const int p = z0 - 1 + it, s = it % ns;
+            mbar_wait(&bar[s], (it / ns) & 1);
+            const double *F = Fs + (size_t)s * K * (SH::FPL / 8);
+            double *Pb = Ps + (it & 1) * 8 * (SH::PPL / 8);
+            const bool zin = (unsigned)p < (unsigned)n, zout = p >= z0 && p < z1;
+            for (int q = ptid; q < RW * SH::RH; q += 32 * R4_PW) {
+                const int col = q & 31, row = q >> 5;        // region column / row
+                const int px = x0 - 1 + col, py = y0 - 1 + row;
+                double av[NM], cv[NM], fo[NM], wo[NM];
+                if (zin && (unsigned)px < (unsigned)n && (unsigned)py < (unsigned)n) {
+                    bl_resid_point<FE, NM>(A, F, SH::FPL / 8, row * SH::FW + col + 1, folds, av, cv, fo, wo);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NM; ++k) { av[k] = 0.0; cv[k] = 0.0; }
+                }
+                const int po = (row + 1) * SH::PW + col + 1;
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    Pb[(2 * k) * (SH::PPL / 8) + po] = av[k];
+                    Pb[(2 * k + 1) * (SH::PPL / 8) + po] = cv[k];
+                }
+                if (folds && zout && col >= 1 && col - 1 < SH::TX && px < n && row >= 1 && row - 1 < SH::TY && py < n) {
+                    const long long gofs = (long long)p * A.plane + (long long)py * A.pitch + px;
+#pragma unroll
+                    for (int k = 0; k < NM; ++k) {
+                        A.fa_out[k][gofs] = fo[k];
+                        A.wb_out[k][gofs] = wo[k];
+                    }
+                }
+            }
+            named_bar_sync(1, R4_NT);
+            if (ptid == 0 && it + ns < nit) issue(it + ns);   // the producers have consumed stage it % ns
+        }
+        return;
+    }
+    // consumer role: node kc = w / R4_WG, rows RR*wi .. RR*wi+RR-1 of the region
+    const int kc = w / R4_WG, wi = w % R4_WG;
+    const int gx = x0 + lane - 1;
+    const bool xout = lane >= 1 && lane - 1 < SH::TX && gx < n;
+    unsigned oks = 0u;
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+        const int ly = RR * wi + r - 1, gy = y0 + ly;
+        if (xout && ly >= 0 && ly < SH::TY && gy < n) oks |= 1u << r;
+    }
+    const BLConst c = A.bl;
+    double vmax = 0.0;
+    double aq[3][RR], af[2][RR], cq[3][RR], cf[3][RR], ce[2][RR];
+    auto step = [&](auto Kc, int it) {
+        constexpr int Kk = decltype(Kc)::value;
+        constexpr int i3 = Kk % 3, m3 = (Kk + 2) % 3, mm3 = (Kk + 1) % 3;
+        constexpr int i2 = Kk % 2, m2 = (Kk + 1) % 2;
+        named_bar_sync(1, R4_NT);
+        const double *Pa = Ps + (i2 * 8 + 2 * kc) * (SH::PPL / 8), *Pc = Pa + SH::PPL / 8;
+        double dummy[RR];
+        plane_partials<false, RR>(Pa, SH::PW, RR * wi, lane, aq[i3], af[i2], dummy);
+        plane_partials<true, RR>(Pc, SH::PW, RR * wi, lane, cq[i3], cf[i3], ce[i2]);
+        if (it >= 2) {   // output plane p-1
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                const double fa_ = af[m2][r] + (aq[mm3][r] + aq[i3][r]);
+                const double fc_ = cf[m3][r] + (cq[mm3][r] + cq[i3][r]);
+                const double ec_ = ce[m2][r] + (cf[mm3][r] + cf[i3][r]);
+                const double Ba = c.kB0 * aq[m3][r] + c.kB1 * fa_;
+                const double Lc = (c.kL0 * cq[m3][r] + c.kL1 * fc_) + c.kL2 * ec_;
+                if ((oks >> r) & 1u) vmax = amax(vmax, fabs(Ba - Lc));
+            }
+        }
+    };
+    for (int base = 0; base < nit; base += 6) {
+        if (base + 0 < nit) step(std::integral_constant<int, 0>{}, base + 0);
+        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
+        if (base + 3 < nit) step(std::integral_constant<int, 3>{}, base + 3);
+        if (base + 4 < nit) step(std::integral_constant<int, 4>{}, base + 4);
+        if (base + 5 < nit) step(std::integral_constant<int, 5>{}, base + 5);
+    }
+    // one atomic per consumer warp into its node's slot
+    const unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(vmax));
+    if (lane == 0 && v) atomicMax(A.slot[kc], v);
+}
+
+// ---------------------------------------------------------------------------------------------
 // f^E = -a . grad u with CD4 differences and zero ghosts, stored once per new
 // node field so that the RHS / residual kernels read it pointwise.  32 x 32 tile, z-streaming
 // with a 5-plane ring of 36 x 36 boxes at (x0-2, y0-2).  DESIGN.md §6.11.
