@@ -95,6 +95,12 @@ def _declare(L):
     L.ora_set_num_threads.argtypes = [C.c_int]
     L.ora_last_wcycles.restype = C.c_long
     L.ora_set_bc.argtypes = [C.c_int]
+    L.ora_inject.argtypes = [C.c_int, C.c_int, _dp, _dp]
+    L.ora_prolong4_add.argtypes = [C.c_int, C.c_int, _dp, _dp]
+    L.ora_mlsdc_correction.argtypes = [C.POINTER(OraProblem), C.c_int, C.c_double, PP, C.c_void_p, C.c_int]
+    L.ora_mlsdc_correction.restype = C.c_long
+    L.ora_mlsdc_step.argtypes = [C.POINTER(OraProblem), C.c_int, _dp, C.c_double, C.POINTER(C.c_int),
+                                 C.POINTER(C.c_long), C.POINTER(C.c_long), _dp, C.POINTER(C.c_int)]
     L.ora_weno5.argtypes = [C.c_double] * 5
     L.ora_weno5.restype = C.c_double
 
@@ -288,3 +294,43 @@ def run(prob: Problem, u0, steps=None):
         u, st = step(prob, u, float(s) * cfg.dt)
         stats.append(st)
     return u, stats
+
+
+# ---------------------------------------------------------------------------------------------
+# MLSDC with ISDC sweeps (NEXT f4; isdc_oracle.c ora_mlsdc_step, reading R32)
+# ---------------------------------------------------------------------------------------------
+def inject(uf):
+    """Injection coarse I <- fine 2I+1 (Dirichlet)."""
+    uf = _c(uf); nc = (uf.shape[0] - 1) // 2
+    out = np.zeros((nc,) * uf.ndim)
+    _bc(False).ora_inject(uf.ndim, uf.shape[0], _p(uf), _p(out)); return out
+
+
+def prolong4_add(ec, uf):
+    """u += P4 e: 4th-order (cubic Lagrange) interpolation of a coarse correction (Dirichlet)."""
+    ec = _c(ec); uf = _c(uf).copy()
+    _bc(False).ora_prolong4_add(ec.ndim, ec.shape[0], _p(ec), _p(uf)); return uf
+
+
+def mlsdc_correction(prob: Problem, t_n, u, coarse_sweeps=1, fas=True):
+    """Steps 2-5 of an MLSDC iteration on node fields u[M]; returns (corrected u, coarse V-cycles)."""
+    u = [_c(x).copy() for x in u]
+    cv = lib().ora_mlsdc_correction(C.byref(prob.s), int(coarse_sweeps), t_n, _ptrs(u), None, 0 if fas else 1)
+    return u, cv
+
+
+def mlsdc_step(prob: Problem, u0, t_n, coarse_sweeps=1):
+    """One two-level MLSDC time step with ISDC sweeps; returns (u_M, stats dict)."""
+    cfg = prob.cfg
+    u = _c(u0).copy()
+    kmax = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
+    hist = np.zeros(kmax)
+    sw, vc, cvc, conv = C.c_int(0), C.c_long(0), C.c_long(0), C.c_int(0)
+    t0 = time.perf_counter()
+    rc = lib().ora_mlsdc_step(C.byref(prob.s), int(coarse_sweeps), _p(u), t_n, C.byref(sw), C.byref(vc),
+                              C.byref(cvc), _p(hist), C.byref(conv))
+    if rc:
+        raise ValueError(f"ora_mlsdc_step: unsupported problem ({rc})")
+    k = sw.value
+    return u, dict(sweeps=k, vcycles=vc.value, coarse_vcycles=cvc.value, res_hist=hist[:k].copy(),
+                   converged=bool(conv.value), seconds=time.perf_counter() - t0)

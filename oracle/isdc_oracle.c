@@ -596,7 +596,7 @@ static long g_wcycles;   /* W-cycles of the last ora_step (not V-cycles: P:165) 
  * The f^E(unew_m)-f^E(uold_m) and sum a_j fE terms are absent when fE = NONE.                  */
 static void rhs_m(const ora_problem *P, const double *tau, const double *S, const double *dtau,
                   double t_n, int m, double *const *uold, double *const *unew, double *b,
-                  double *v, double *w, double *ftmp, double *ftmp2) {
+                  double *v, double *w, double *ftmp, double *ftmp2, double *const *fas) {
     int d = P->dim, n = P->n, M = P->M;
     size_t NP = npts(d, n);
     double dtm = P->dt * dtau[m];
@@ -630,14 +630,25 @@ static void rhs_m(const ora_problem *P, const double *tau, const double *S, cons
         size_t p = IDX(d, n);
         b[p] = B_at(&c, v, d, n, ii, jj, kk) + L_at(&c, w, d, n, ii, jj, kk);
     }
+    /* MLSDC coarse level (NEXT f4, R32): the node-to-node difference of the FAS
+     * correction, b <- b + (fas_{m+1} - fas_m), fas_0 = 0 (node 1 = u_0 carries no correction) */
+    if (fas)
+        for (size_t p = 0; p < NP; ++p) b[p] = b[p] + (fas[m + 1][p] - (m == 0 ? 0.0 : fas[m][p]));
 }
 
 /* Weighted SDC residual (R15-R16): for nodes m = 1..M-1 (0-based),
  *   p_m = (u_m - u_0) - sum_j qa_j fE(u_j),  qa_j = dt*Q_{m,j}   (fE = NONE: p_m = u_m - u_0)
  *   z_m = sum_j qb_j u_j,                    qb_j = (nu*dt)*Q_{m,j}
  *   r~_m = B p_m - L z_m ;  reported: max_m ||r~_m||_inf (and per node)                        */
+static double residual_fields(const ora_problem *P, const double *tau, const double *Q, double t_n,
+                              double *const *u, double *per_node, double *const *rout);
 double ora_residual_state(const ora_problem *P, const double *tau, const double *Q, double t_n,
                           double *const *u, double *per_node) {
+    return residual_fields(P, tau, Q, t_n, u, per_node, NULL);
+}
+/* rout (nullable): rout[m] (m = 1..M-1) receives the field r~_m (MLSDC, NEXT f4) */
+static double residual_fields(const ora_problem *P, const double *tau, const double *Q, double t_n,
+                              double *const *u, double *per_node, double *const *rout) {
     int d = P->dim, n = P->n, M = P->M;
     size_t NP = npts(d, n);
     bl_consts c = make_bl(d, n);
@@ -667,6 +678,7 @@ double ora_residual_state(const ora_problem *P, const double *tau, const double 
             r[p] = B_at(&c, pm, d, n, ii, jj, kk) - L_at(&c, zm, d, n, ii, jj, kk);
         }
         double nm = maxabs(r, NP);
+        if (rout) memcpy(rout[m], r, NP * sizeof(double));
         if (P->res_kind == 1) {
             /* unweighted residual: x = W^{-1} r~ by V(nu1,nu2)-cycles on
              * S = B_h (gamma = 0, the same multigrid components) from x = 0, until
@@ -718,8 +730,15 @@ static int node_solve(const ora_problem *P, double gamma, const double *b, doubl
 /* One SDC/ISDC sweep k -> k+1 (Eq. 4 in the weighted form Eq. 5; node order
  * m = 0..M-2 is sequential since u_{m+1}^{k+1} needs u_m^{k+1}).  uold/unew: M fields each;
  * unew[0] must already hold u_0.  cycles[m] = V-cycles of node solve m. Returns cap hits. */
+static int sweep_fas(const ora_problem *P, const double *tau, const double *S, const double *dtau,
+                     double t_n, double *const *uold, double *const *unew, int *cycles, double *const *fas);
 int ora_sweep(const ora_problem *P, const double *tau, const double *S, const double *dtau,
               double t_n, double *const *uold, double *const *unew, int *cycles) {
+    return sweep_fas(P, tau, S, dtau, t_n, uold, unew, cycles, NULL);
+}
+/* fas (nullable): the MLSDC coarse-level FAS correction fas[1..M-1] (rhs_m) */
+static int sweep_fas(const ora_problem *P, const double *tau, const double *S, const double *dtau,
+                     double t_n, double *const *uold, double *const *unew, int *cycles, double *const *fas) {
     int d = P->dim, n = P->n, M = P->M;
     size_t NP = npts(d, n);
     double *b = malloc(NP * sizeof(double)), *v = malloc(NP * sizeof(double));
@@ -727,7 +746,7 @@ int ora_sweep(const ora_problem *P, const double *tau, const double *S, const do
     double *f2 = malloc(NP * sizeof(double));
     int caps = 0;
     for (int m = 0; m + 1 < M; ++m) {
-        rhs_m(P, tau, S, dtau, t_n, m, uold, unew, b, v, w, f1, f2);
+        rhs_m(P, tau, S, dtau, t_n, m, uold, unew, b, v, w, f1, f2, fas);
         if (P->guess == 0) memcpy(unew[m + 1], uold[m + 1], NP * sizeof(double));
         else if (P->guess == 1) memset(unew[m + 1], 0, NP * sizeof(double));
         else memcpy(unew[m + 1], unew[m], NP * sizeof(double));
@@ -791,7 +810,7 @@ void ora_rhs(const ora_problem *P, double t_n, int m, double *const *uold, doubl
     ora_tables(M, tau, Q, S, dtau);
     double *v = malloc(NP * sizeof(double)), *w = malloc(NP * sizeof(double));
     double *f1 = malloc(NP * sizeof(double)), *f2 = malloc(NP * sizeof(double));
-    rhs_m(P, tau, S, dtau, t_n, m, uold, unew, b, v, w, f1, f2);
+    rhs_m(P, tau, S, dtau, t_n, m, uold, unew, b, v, w, f1, f2, NULL);
     free(v); free(w); free(f1); free(f2);
 }
 double ora_residual(const ora_problem *P, double t_n, double *const *u, double *per_node) {
@@ -805,4 +824,184 @@ int ora_sweep_state(const ora_problem *P, double t_n, double *const *uold, doubl
     double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
     ora_tables(P->M, tau, Q, S, dtau);
     return ora_sweep(P, tau, S, dtau, t_n, uold, unew, cycles);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* MLSDC with ISDC sweeps (NEXT f4; "SDC sweeps in a multigrid-like way on multiple    */
+/* levels ... connected through an FAS correction term"; reading R32).  Two levels,     */
+/* the same M Lobatto nodes, spatial coarsening to the next grid of the V-cycle hierarchy        */
+/* n_c = (n-1)/2 (Dirichlet).  One iteration:                                                    */
+/*   1. fine sweep (Eq. 5, L V-cycles per node solve) and the fine weighted residual r~_h;        */
+/*      stop when max_m ||r~_h,m|| < sweep_tol (or at fixed_sweeps / max_sweeps)                  */
+/*   2. restrict the iterate by injection, U_j = Ubar_j = R_i u_j (coarse I <-> fine 2I+1)        */
+/*   3. FAS correction fas_m = r~_H(Ubar)_m - R_fw r~_h,m (m = 1..M-1; r~_H the coarse weighted   */
+/*      residual of the restricted iterate, R_fw full weighting) -- with it the restricted fine   */
+/*      collocation solution solves the coarse collocation problem                               */
+/*        B_H(U_m - U_0) - dt sum_j Q_mj (B_H f^E(U_j) + nu L_H U_j) = fas_m                        */
+/*   4. coarse_sweeps coarse sweeps of that problem: Eq. (5) with b + (fas_{m+1} - fas_m)          */
+/*   5. interpolate the coarse correction with 4th-order (cubic Lagrange) interpolation, the order */
+/*      of the compact discretisation: u_j <- u_j + P4(U_j - Ubar_j), j = 1..M-1 (ora_prolong4_add; */
+/*      bilinear interpolation measured to stall the iteration, R32)                    */
+/* The step ends with a fine sweep (no correction after the last one).  Forcing: the coarse G is  */
+/* the injection of the fine G (the same samples).  ISDC mode only (the paper's proposal).        */
+/* ------------------------------------------------------------------------------------------ */
+/* 4th-order interpolation of a coarse correction onto the fine grid, added: u += P4 e (Dirichlet).
+ * Separable passes x, then y, then z.  Per axis a fine odd index 2I+1 takes the coarse value I; a
+ * fine even index x lies between coarse a = x/2-1 and b = x/2 and takes the cubic Lagrange midpoint
+ *   (9*(c(a) + c(b)) - (c(a-1) + c(b+1))) * 0.0625
+ * with c(-1) = c(nc) = 0 (the boundary) and the odd reflections c(-2) = -c(0), c(nc+1) = -c(nc-1).
+ * The last pass adds into u: u = u + v.                                                          */
+static double c4(const double *row, long stride, int nc, int i) {
+    if (i >= 0 && i < nc) return row[(long)i * stride];
+    if (i == -1 || i == nc) return 0.0;
+    if (i == -2) return -row[0];
+    return -row[(long)(nc - 1) * stride];   /* i == nc + 1 */
+}
+static double interp4(const double *row, long stride, int nc, int x) {
+    if (x & 1) return row[(long)((x - 1) / 2) * stride];
+    int a = x / 2 - 1, b = x / 2;
+    return (9.0 * (c4(row, stride, nc, a) + c4(row, stride, nc, b)) -
+            (c4(row, stride, nc, a - 1) + c4(row, stride, nc, b + 1))) * 0.0625;
+}
+void ora_prolong4_add(int d, int nc, const double *ec, double *uf) {
+    int nf = 2 * nc + 1;
+    if (d == 2) {
+        double *t1 = malloc((size_t)nf * nc * sizeof(double));          /* [J][x] */
+        for (int J = 0; J < nc; ++J)
+            for (int x = 0; x < nf; ++x) t1[(size_t)J * nf + x] = interp4(ec + (size_t)J * nc, 1, nc, x);
+        for (int y = 0; y < nf; ++y)
+            for (int x = 0; x < nf; ++x) {
+                double v = interp4(t1 + x, nf, nc, y);
+                uf[(size_t)y * nf + x] = uf[(size_t)y * nf + x] + v;
+            }
+        free(t1);
+    } else {
+        double *t1 = malloc((size_t)nf * nc * nc * sizeof(double));     /* [K][J][x] */
+        double *t2 = malloc((size_t)nf * nf * nc * sizeof(double));     /* [K][y][x] */
+        for (int K = 0; K < nc; ++K)
+            for (int J = 0; J < nc; ++J)
+                for (int x = 0; x < nf; ++x)
+                    t1[((size_t)K * nc + J) * nf + x] = interp4(ec + ((size_t)K * nc + J) * nc, 1, nc, x);
+        for (int K = 0; K < nc; ++K)
+            for (int y = 0; y < nf; ++y)
+                for (int x = 0; x < nf; ++x)
+                    t2[((size_t)K * nf + y) * nf + x] = interp4(t1 + (size_t)K * nc * nf + x, nf, nc, y);
+        for (int z = 0; z < nf; ++z)
+            for (int y = 0; y < nf; ++y)
+                for (int x = 0; x < nf; ++x) {
+                    double v = interp4(t2 + (size_t)y * nf + x, (long)nf * nf, nc, z);
+                    size_t p = ((size_t)z * nf + y) * nf + x;
+                    uf[p] = uf[p] + v;
+                }
+        free(t1); free(t2);
+    }
+}
+
+void ora_inject(int d, int nf, const double *uf, double *uc) {
+    int nc = coarser(nf);
+    FOR_POINTS(d, nc) {
+        int x = 2 * ii + 1, y = 2 * jj + 1, z = (d == 3) ? 2 * kk + 1 : 0;
+        uc[IDX(d, nc)] = at(uf, d, nf, x, y, z);
+    }
+}
+
+/* Steps 2-5 on the fine node fields u[0..M-1] (u[1..M-1] updated in place).  rh: the fine
+ * residual fields r~_h,m (m = 1..M-1) of u, or NULL to compute them here.  flags bit 0: omit the
+ * FAS correction (negative control for the tests only).  Returns the coarse V-cycles. */
+long ora_mlsdc_correction(const ora_problem *P, int coarse_sweeps, double t_n, double *const *u,
+                          double *const *rh_in, int flags) {
+    ora_set_bc(0);
+    int d = P->dim, n = P->n, M = P->M, nc = (n - 1) / 2;
+    size_t NP = npts(d, n), NPc = npts(d, nc);
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    if (ora_tables(M, tau, Q, S, dtau)) return -1;
+    ora_problem Pc = *P;
+    Pc.n = nc;
+    double *Gc = NULL;
+    if (P->fe == FE_FORCING) {
+        Gc = malloc(NPc * sizeof(double));
+        ora_inject(d, n, P->G, Gc);
+        Pc.G = Gc;
+    }
+    double *U[32], *V[32], *Ub[32], *fas[32], *rH[32], *rh[32];
+    for (int j = 0; j < M; ++j) {
+        U[j] = malloc(NPc * sizeof(double));
+        V[j] = malloc(NPc * sizeof(double));
+        Ub[j] = malloc(NPc * sizeof(double));
+        fas[j] = malloc(NPc * sizeof(double));
+        rH[j] = malloc(NPc * sizeof(double));
+        rh[j] = rh_in ? rh_in[j] : malloc(NP * sizeof(double));
+    }
+    if (!rh_in) residual_fields(P, tau, Q, t_n, u, NULL, rh);
+    double *tc = malloc(NPc * sizeof(double)), *ec = malloc(NPc * sizeof(double));
+    for (int j = 0; j < M; ++j) {                                                   /* 2. */
+        ora_inject(d, n, u[j], Ub[j]);
+        memcpy(U[j], Ub[j], NPc * sizeof(double));
+    }
+    residual_fields(&Pc, tau, Q, t_n, Ub, NULL, rH);                                /* 3. */
+    for (int m = 1; m < M; ++m) {
+        ora_restrict(d, n, rh[m], tc);
+        for (size_t p = 0; p < NPc; ++p) fas[m][p] = rH[m][p] - tc[p];
+    }
+    double **cu = U, **cn = V;                                                       /* 4. */
+    long cvc = 0;
+    memcpy(cn[0], cu[0], NPc * sizeof(double));
+    for (int sw = 0; sw < coarse_sweeps; ++sw) {
+        int cyc[32];
+        sweep_fas(&Pc, tau, S, dtau, t_n, cu, cn, cyc, (flags & 1) ? NULL : fas);
+        for (int m = 0; m + 1 < M; ++m) cvc += cyc[m];
+        double **tt = cu; cu = cn; cn = tt;
+        memcpy(cn[0], cu[0], NPc * sizeof(double));
+    }
+    for (int j = 1; j < M; ++j) {                                                   /* 5. */
+        for (size_t p = 0; p < NPc; ++p) ec[p] = cu[j][p] - Ub[j][p];
+        ora_prolong4_add(d, nc, ec, u[j]);
+    }
+    for (int j = 0; j < M; ++j) {
+        free(U[j]); free(V[j]); free(Ub[j]); free(fas[j]); free(rH[j]);
+        if (!rh_in) free(rh[j]);
+    }
+    free(tc); free(ec); free(Gc);
+    return cvc;
+}
+
+int ora_mlsdc_step(const ora_problem *P, int coarse_sweeps, double *u0, double t_n, int *sweeps,
+                   long *vcycles, long *cvcycles, double *res_hist, int *converged) {
+    ora_set_bc(0);
+    if (P->bc != 0 || P->n < 7 || P->mode != 0 || P->res_kind != 0) return -2;
+    int M = P->M;
+    size_t NP = npts(P->dim, P->n);
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    if (ora_tables(M, tau, Q, S, dtau)) return -1;
+    double *A[32], *Bf[32], *rh[32];
+    for (int j = 0; j < M; ++j) {
+        A[j] = (j == 0) ? u0 : malloc(NP * sizeof(double));
+        Bf[j] = (j == 0) ? u0 : malloc(NP * sizeof(double));
+        if (j) memcpy(A[j], u0, NP * sizeof(double));
+        rh[j] = malloc(NP * sizeof(double));
+    }
+    double **uold = A, **unew = Bf;
+    int k = 0, conv = 0;
+    long vc = 0, cvc = 0;
+    int kmax = P->fixed_sweeps > 0 ? P->fixed_sweeps : P->max_sweeps;
+    while (k < kmax) {
+        int cyc[32];
+        sweep_fas(P, tau, S, dtau, t_n, uold, unew, cyc, NULL);                      /* 1. */
+        for (int m = 0; m + 1 < M; ++m) vc += cyc[m];
+        double res = residual_fields(P, tau, Q, t_n, unew, NULL, rh);
+        if (res_hist) res_hist[k] = res;
+        ++k;
+        double **t = uold; uold = unew; unew = t;
+        if (P->fixed_sweeps <= 0 && res < P->sweep_tol) { conv = 1; break; }
+        if (k >= kmax) break;
+        cvc += ora_mlsdc_correction(P, coarse_sweeps, t_n, uold, rh, 0);             /* 2.-5. */
+    }
+    if (P->fixed_sweeps > 0) conv = 1;
+    memcpy(u0, uold[M - 1], NP * sizeof(double));
+    for (int j = 0; j < M; ++j) {
+        if (j) { free(A[j]); free(Bf[j]); }
+        free(rh[j]);
+    }
+    *sweeps = k; *vcycles = vc; *cvcycles = cvc; *converged = conv;
+    return 0;
 }
