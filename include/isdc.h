@@ -122,6 +122,16 @@ typedef struct {
     int residual_kind;
     double w_tol;                /* 1e-6 */
     int w_cap;                   /* 50   */
+    /* Two-level MLSDC with ISDC sweeps (NEXT f4; "SDC sweeps in a multigrid-like way on
+     * multiple levels ... connected through an FAS correction term"; reading R32).
+     * mlsdc_levels 0 or 1: single-level ISDC; 2: every iteration is a fine ISDC sweep (stop test on
+     * the fine residual), then -- unless the step stops -- injection of the iterate to the next
+     * coarser grid n_c = (n-1)/2, the FAS correction fas_m = r~_H(R u)_m - R_fw r~_h,m, coarse_sweeps
+     * ISDC sweeps of the FAS-corrected coarse collocation problem, and the 4th-order interpolation of
+     * the coarse correction back onto every fine node.  Dirichlet grids with n >= 7, mode
+     * ISDC_MODE_ISDC_FIXED, residual_kind 0 (else ISDC_ERR_UNSUPPORTED). */
+    int mlsdc_levels;
+    int coarse_sweeps;           /* coarse ISDC sweeps per MLSDC iteration (1) */
 } isdc_problem;
 
 /* Per-step statistics (Table 1 accounting; SPEC RunStats S:249-252). */
@@ -132,6 +142,7 @@ typedef struct {
     int converged;       /* residual < sweep_tol reached (always 1 with fixed_sweeps)           */
     double final_residual;
     long wcycles;        /* W-cycles of the unweighted residual (residual_kind 1)         */
+    long coarse_vcycles; /* MLSDC: V-cycles of the coarse-level sweeps (counted apart)          */
 } isdc_step_stats;
 
 /* Bytes of device workspace a problem needs (fields, MG hierarchy, reductions, tables). */

@@ -22,6 +22,7 @@
 #include "kernels_fast3d.cuh"
 #include "kernels_tail.cuh"
 #include "kernels_ptail.cuh"
+#include "kernels_mlsdc.cuh"
 #include "tables.h"
 
 // Device-side node-solve loop of the SDC / capped-ISDC modes (one CUDA graph per sweep): the
@@ -204,6 +205,20 @@ struct isdc_ctx {
     long last_wbody[ISDC_MAXM] = {};
     std::map<std::tuple<int, int, int, int>, Graph> sweep_graphs;
     bool capturing = false;
+    // two-level MLSDC (NEXT f4, R32): the fine handle owns a coarse handle on n_c
+    struct isdc_ctx *coarse = nullptr;
+    double *RF[ISDC_MAXM] = {};    // fine residual fields r~_h,m (m = 1..M-1 at RF[m])
+    double *UB[ISDC_MAXM] = {};    // coarse: restricted iterate Ubar_j
+    double *RC[ISDC_MAXM] = {};    // coarse: residual fields r~_H(Ubar)_m
+    double *FAS[ISDC_MAXM] = {};   // coarse: FAS correction fas_m (FAS[0] unused = 0)
+    double *EC = nullptr;          // coarse: correction U_j - Ubar_j
+    double *P4a = nullptr, *P4b = nullptr;   // scratch of the 4th-order interpolation passes
+    double *GC = nullptr;          // dense coarse forcing profile (injection of G), copied by the coarse create
+    char *cws = nullptr;           // the coarse handle's workspace
+    size_t cws_bytes = 0;
+    const double *const *fas_in = nullptr;   // coarse handle: add (fas_{m+1} - fas_m) to every RHS
+    bool skip_residual = false;    // coarse handle: its sweeps compute no residual (the fine one decides)
+    long cvcyc = 0;                // coarse V-cycles since the step start
     // live kernel timing (isdc_profile_*)
     int prof = 0;               // 0 off, 1 fine smoother only, 2 every class
     std::vector<cudaEvent_t> evpool;
@@ -212,6 +227,7 @@ struct isdc_ctx {
     double prof_ms[8] = {0}, prof_bytes[8] = {0};
     long prof_cnt[8] = {0};
     ~isdc_ctx() {
+        delete coarse;
         for (auto &g : sweep_graphs)
             if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
         for (auto e : evpool) cudaEventDestroy(e);
@@ -352,6 +368,10 @@ isdc_status validate(const isdc_problem *p) {
     if (p->residual_kind < 0 || p->residual_kind > 1) return ISDC_ERR_INVALID_ARG;
     if (p->residual_kind == 1 && (p->grid.dim != 2 || p->M > ISDC_MAXM - 1)) return ISDC_ERR_UNSUPPORTED;
     if (p->residual_kind == 1 && (!(p->w_tol >= 0) || p->w_cap < 0)) return ISDC_ERR_INVALID_ARG;
+    if (p->mlsdc_levels < 0 || p->mlsdc_levels > 2 || p->coarse_sweeps < 0) return ISDC_ERR_INVALID_ARG;
+    if (p->mlsdc_levels == 2 && (per || p->grid.n < 7 || p->solve.mode != ISDC_MODE_ISDC_FIXED ||
+                                 p->residual_kind != 0 || p->fe == ISDC_FE_BURGERS_WENO5))
+        return ISDC_ERR_UNSUPPORTED;
     return ISDC_OK;
 }
 
@@ -433,6 +453,30 @@ size_t layout(isdc_ctx *h, const isdc_problem *p, char *base) {
     if (p->solve.fixed_sweeps > 0 && p->solve.fixed_sweeps <= 256)
         hist = (unsigned long long *)take((size_t)p->solve.fixed_sweeps * (M - 1) * sizeof(unsigned long long));
     StepCtl *sctl = (StepCtl *)take(sizeof(StepCtl));
+    if (p->mlsdc_levels == 2) {
+        // MLSDC (R32): fine residual fields, coarse restricted iterate / residual / FAS / correction
+        // fields, the interpolation scratch, the dense coarse forcing and the coarse handle's workspace
+        const int nc = (n - 1) / 2;
+        const size_t fc = field_elems(d, nc, false) * sizeof(double);
+        for (int m = 1; m < M; ++m) { double *f = (double *)take(fe); if (h) h->RF[m] = f; }
+        for (int j = 0; j < M; ++j) { double *f = (double *)take(fc); if (h) h->UB[j] = f; }
+        for (int m = 1; m < M; ++m) {
+            double *a = (double *)take(fc), *b = (double *)take(fc);
+            if (h) { h->RC[m] = a; h->FAS[m] = b; }
+        }
+        double *ec = (double *)take(fc);
+        const size_t nf = (size_t)n, ncs = (size_t)nc;
+        double *pa = (double *)take((d == 3 ? nf * ncs * ncs : nf * ncs) * sizeof(double));
+        double *pb = (d == 3) ? (double *)take(nf * nf * ncs * sizeof(double)) : nullptr;
+        double *gc = (p->fe == ISDC_FE_FORCING) ? (double *)take((d == 3 ? ncs * ncs * ncs : ncs * ncs) * sizeof(double)) : nullptr;
+        isdc_problem pc = *p;
+        pc.grid.n = nc;
+        pc.mlsdc_levels = 0;
+        pc.fe_field_dev = gc;
+        const size_t cb = layout(nullptr, &pc, nullptr);
+        char *cw = take(cb);
+        if (h) { h->EC = ec; h->P4a = pa; h->P4b = pb; h->GC = gc; h->cws = cw; h->cws_bytes = cb; }
+    }
     if (h) { h->Ginv = Gi; h->red = red; h->nlev = nl; h->ctdev = ctd; h->alpha = al; h->ctl = ctl; h->hist = hist; h->sctl = sctl; }
     return off;
 }
@@ -1469,6 +1513,13 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
     const bool fold_ok = !h->spread && h->fold_valid[h->cur];
     for (int m = 0; m + 1 < M; ++m) {
         TRY(run_rhs(h, m, uold, unew[m], h->Bf, false, Fold, Fnew[m], fold_ok));
+        if (h->fas_in) {   // MLSDC coarse level: b + (fas_{m+1} - fas_m), fas_0 = 0 (R32)
+            const GridDesc &g = h->lev[0].g;
+            ++h->launches;
+            if (h->d == 2) kl(h, k_add_fas<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->Bf, g, h->fas_in[m + 1], m == 0 ? nullptr : h->fas_in[m]);
+            else kl(h, k_add_fas<3>, point_grid<3>(g, kBlk), kBlk, 0)(h->Bf, g, h->fas_in[m + 1], m == 0 ? nullptr : h->fas_in[m]);
+            LAUNCH_CHECK(h);
+        }
         const double *src;
         if (h->P.solve.guess == 1) { TRY(zero_field(h, unew[m + 1], h->lev[0].g)); src = nullptr; }
         else if (h->P.solve.guess == 2) src = unew[m];
@@ -1476,8 +1527,102 @@ isdc_status enqueue_isdc_sweep(isdc_ctx *h) {
         for (int l = 0; l < h->P.solve.L; ++l) TRY(vcycle(h, 0, m, unew[m + 1], h->T, h->Bf, l == 0 ? src : nullptr));
         TRY(launch_fe(h, Fnew[m + 1], unew[m + 1]));
     }
+    if (h->skip_residual) return ISDC_OK;
     TRY(enqueue_residual(h, unew, Fnew, folds_on(h)));
     if (h->capturing && dev_wsolve(h)) TRY(enqueue_wsolve(h));
+    return ISDC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Two-level MLSDC (NEXT f4, R32): steps 2-5 of an iteration after a fine sweep, on the
+// latest fine iterate: injection to the coarse handle, the FAS correction from the fine and coarse
+// residual FIELDS, coarse_sweeps coarse ISDC sweeps with b + (fas_{m+1} - fas_m), and the
+// 4th-order interpolation of the coarse correction onto the fine nodes 1..M-1.
+// ---------------------------------------------------------------------------------------------
+// residual fields r~_m (m = 1..M-1) of the node fields u (generic kernels, the trees of §4.5)
+isdc_status residual_fields(isdc_ctx *h, double *const *u, double *const *F, double *const *out) {
+    const GridDesc &g = h->lev[0].g;
+    const int M = h->M;
+    const double dt = h->P.dt, nudt = h->P.nu * dt;
+    TRY(clear_slots(h, SLOT_SCRATCH, 1));
+    for (int m = 1; m < M; ++m) {
+        PZParams P;
+        P.M = M; P.m = m;
+        for (int j = 0; j < M; ++j) { P.u[j] = u[j]; P.qa[j] = dt * h->Q[m * M + j]; P.qb[j] = nudt * h->Q[m * M + j]; }
+        P.ct = h->ctdev;
+        for (int j = 0; j < ISDC_MAXM; ++j) P.F[j] = (F && need_F(h) && j < M) ? F[j] : nullptr;
+        P.fe = h->fe;
+        P.g = g;
+        h->launches += 2;
+        if (h->d == 2) {
+            kl(h, k_pz<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->V, h->W, P);
+            kl(h, k_resid<2>, point_grid<2>(g, kBlk), kBlk, 0)(h->V, h->W, g, h->bl, h->red + SLOT_SCRATCH, out[m]);
+        } else {
+            kl(h, k_pz<3>, point_grid<3>(g, kBlk), kBlk, 0)(h->V, h->W, P);
+            kl(h, k_resid<3>, point_grid<3>(g, kBlk), kBlk, 0)(h->V, h->W, g, h->bl, h->red + SLOT_SCRATCH, out[m]);
+        }
+        LAUNCH_CHECK(h);
+    }
+    return ISDC_OK;
+}
+
+isdc_status mlsdc_correct(isdc_ctx *h) {
+    isdc_ctx *c = h->coarse;
+    const int M = h->M, D = h->d;
+    const GridDesc &gf = h->lev[0].g, &gc = c->lev[0].g;
+    double *u[ISDC_MAXM], *F[ISDC_MAXM];
+    for (int j = 0; j < M; ++j) {
+        u[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
+        F[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
+    }
+    TRY(residual_fields(h, u, F, h->RF));                                   // r~_h,m
+    const dim3 cg = (D == 2) ? point_grid<2>(gc, kBlk) : point_grid<3>(gc, kBlk);
+    for (int j = 0; j < M; ++j) {                                            // Ubar_j = R_i u_j
+        h->launches += 2;
+        if (D == 2) {
+            kl(h, k_inject<2>, cg, kBlk, 0)(h->UB[j], gc, u[j], gf);
+            kl(h, k_inject<2>, cg, kBlk, 0)(c->U[0][j], gc, u[j], gf);
+        } else {
+            kl(h, k_inject<3>, cg, kBlk, 0)(h->UB[j], gc, u[j], gf);
+            kl(h, k_inject<3>, cg, kBlk, 0)(c->U[0][j], gc, u[j], gf);
+        }
+        LAUNCH_CHECK(h);
+        TRY(launch_fe(c, c->Fs[0][j], c->U[0][j]));
+    }
+    c->cur = 0; c->spread = false; c->fold_valid[0] = c->fold_valid[1] = false;
+    TRY(residual_fields(c, h->UB, c->Fs[0], h->RC));                        // r~_H(Ubar)_m
+    for (int m = 1; m < M; ++m) {                                            // fas_m
+        ++h->launches;
+        if (D == 2) kl(h, k_fas<2>, cg, kBlk, 0)(h->FAS[m], gc, h->RC[m], h->RF[m], gf);
+        else kl(h, k_fas<3>, cg, kBlk, 0)(h->FAS[m], gc, h->RC[m], h->RF[m], gf);
+        LAUNCH_CHECK(h);
+    }
+    c->fas_in = h->FAS;                                                      // coarse sweeps
+    c->skip_residual = true;
+    for (int s = 0; s < h->P.coarse_sweeps; ++s) {
+        const long l0 = c->launches;
+        TRY(enqueue_isdc_sweep(c));
+        h->launches += c->launches - l0;
+        c->cur = 1 - c->cur;
+        h->cvcyc += (long)(M - 1) * c->P.solve.L;
+    }
+    for (int j = 1; j < M; ++j) {                                            // u_j += P4 (U_j - Ubar_j)
+        const dim3 bx(32, 8, 1);
+        h->launches += (D == 2) ? 3 : 4;
+        if (D == 2) {
+            kl(h, k_sub<2>, cg, kBlk, 0)(h->EC, gc, c->U[c->cur][j], h->UB[j]);
+            kl(h, k_p4x<2>, dim3((gf.n + 31) / 32, (gc.n + 7) / 8, 1), bx, 0)(h->P4a, h->EC, gc, gf.n);
+            kl(h, k_p4y<2>, dim3((gf.n + 31) / 32, (gf.n + 7) / 8, 1), bx, 0)(u[j], h->P4a, gc.n, gf);
+        } else {
+            kl(h, k_sub<3>, cg, kBlk, 0)(h->EC, gc, c->U[c->cur][j], h->UB[j]);
+            kl(h, k_p4x<3>, dim3((gf.n + 31) / 32, (gc.n + 7) / 8, gc.n), bx, 0)(h->P4a, h->EC, gc, gf.n);
+            kl(h, k_p4y<3>, dim3((gf.n + 31) / 32, (gf.n + 7) / 8, gc.n), bx, 0)(h->P4b, h->P4a, gc.n, gf);
+            kl(h, k_p4z, dim3((gf.n + 31) / 32, (gf.n + 7) / 8, gf.n), bx, 0)(u[j], h->P4b, gc.n, gf);
+        }
+        LAUNCH_CHECK(h);
+        TRY(launch_fe(h, F[j], u[j]));                                       // stored f^E of the new u_j
+    }
+    h->fold_valid[h->cur] = false;
     return ISDC_OK;
 }
 
@@ -2142,6 +2287,29 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
                               g.n * sizeof(double), rows, cudaMemcpyDeviceToDevice, h->s);
     }
     if (e == cudaSuccess && upload_ct(h) != ISDC_OK) e = cudaErrorUnknown;
+    if (e == cudaSuccess && prob->mlsdc_levels == 2) {
+        // the coarse MLSDC level (R32): its own handle on n_c inside this workspace; its forcing
+        // profile is the injection of G (the same samples)
+        const int nc = (h->n - 1) / 2;
+        isdc_problem pc = *prob;
+        pc.grid.n = nc;
+        pc.mlsdc_levels = 0;
+        pc.fe_field_dev = nullptr;
+        if (h->GC) {
+            GridDesc gd;
+            gd.n = nc; gd.pitch = nc; gd.plane = (h->d == 3) ? (long long)nc * nc : 0; gd.per = 0;
+            const GridDesc &gf = h->lev[0].g;
+            if (h->d == 2) kl(h, k_inject<2>, point_grid<2>(gd, kBlk), kBlk, 0)(h->GC, gd, h->Gp, gf);
+            else kl(h, k_inject<3>, point_grid<3>(gd, kBlk), kBlk, 0)(h->GC, gd, h->Gp, gf);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = h->kl_err;
+            pc.fe_field_dev = h->GC;
+        }
+        if (e == cudaSuccess) {
+            isdc_status cs = isdc_create(&pc, h->cws, h->cws_bytes, stream, &h->coarse);
+            if (cs != ISDC_OK) { delete h; return cs; }
+        }
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->s);
     if (e != cudaSuccess) { delete h; return ISDC_ERR_CUDA; }
     *out = h;
@@ -2249,7 +2417,24 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     long vc = 0;
     double res = 0.0;
     bool graphed = false;   // the whole step ran as one graph
-    if (o.fixed_sweeps > 0 && o.mode == ISDC_MODE_ISDC_FIXED && h->graphs && h->prof == 0 &&
+    h->cvcyc = 0;
+    if (h->P.mlsdc_levels == 2) {
+        // two-level MLSDC (R32): fine sweep + stop test, then the coarse correction unless the step stops
+        while (k < kmax) {
+            int cyc[ISDC_MAXM], cap = 0;
+            TRY(sweep_impl(h, nullptr, &res, cyc, &cap));
+            for (int m = 0; m + 1 < h->M; ++m) {
+                vc += cyc[m];
+                if (node_cycles) node_cycles[k * (h->M - 1) + m] = cyc[m];
+            }
+            if (res_hist) res_hist[k] = res;
+            ++k;
+            if (o.fixed_sweeps <= 0 && res < o.sweep_tol) { conv = 1; break; }
+            if (k >= kmax) break;
+            TRY(mlsdc_correct(h));
+        }
+        graphed = true;
+    } else if (o.fixed_sweeps > 0 && o.mode == ISDC_MODE_ISDC_FIXED && h->graphs && h->prof == 0 &&
         h->P.residual_kind == 0 && h->hist && h->spread && h->cur == 0 && h->step_graph) {
         // the whole fixed-sweep step as one graph: no host synchronisation between its sweeps
         TRY(graph_fixed_step(h, o.fixed_sweeps, res_hist, &res));
@@ -2293,6 +2478,7 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
         stats->sweeps = k; stats->vcycles = vc; stats->cap_hits = caps; stats->converged = conv;
         stats->final_residual = res;
         stats->wcycles = h->wcyc;
+        stats->coarse_vcycles = h->cvcyc;
     }
     return ISDC_OK;
 }

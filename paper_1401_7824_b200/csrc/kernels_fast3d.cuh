@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
 // consumers; one block barrier per plane.  Region 32 x R4_RH (tile 30 x (R4_RH - 2) + halo 1).
 // ---------------------------------------------------------------------------------------------
 constexpr int R4_WG = 3, R4_RR = 4, R4_RH = R4_WG * R4_RR;   // consumer warps per node, rows per thread
-constexpr int R4_PW = 2;                                     // producer warps
+constexpr int R4_PW = 4;                                     // producer warps (one per SM sub-partition)
 constexpr int R4_NT = 32 * (4 * R4_WG + R4_PW);
 struct R4Shape {
     static constexpr int RH = R4_RH, TX = RW - 2, TY = R4_RH - 2;
@@ -753,6 +753,43 @@ struct R4Shape {
     static constexpr int FPL = a128(FW * FH * 8), PPL = a128(PW * PH * 8);
     static size_t smem(int K, int ns) { return (size_t)ns * K * FPL + 2 * 8 * (size_t)PPL + 8 * 8 + 128; }
 };
+
+// Pointwise part of the residual pass for M = 5 at one point, with every node index fixed at compile
+// time (the trees of bl_resid_point: each accumulator is c_0 x_0, then acc + c_j x_j, j ascending).
+// Node k = 0..3 is residual node m = k + 1; its fold is RHS node q = k (u_{q+1} = u_{k+1}).
+template <int FE>
+__device__ __forceinline__ void r4_point(const BLArgs &A, const double *F, int fpl, int o, bool folds, double (&av)[4],
+                                         double (&cv)[4], double (&fo)[4], double (&wo)[4]) {
+    double u[5], f[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) u[j] = F[(A.iu0 + j) * fpl + o];
+    if (FE == 3) {
+#pragma unroll
+        for (int j = 0; j < 5; ++j) f[j] = F[(A.iF0 + j) * fpl + o];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double c = A.beta[k][0] * u[0];
+#pragma unroll
+        for (int j = 1; j < 5; ++j) c = c + A.beta[k][j] * u[j];
+        cv[k] = c;
+        double diff = u[k + 1] - u[0];
+        if (FE == 3) {
+            double fa = A.a[k][0] * f[0];
+#pragma unroll
+            for (int j = 1; j < 5; ++j) fa = fa + A.a[k][j] * f[j];
+            diff = diff - fa;
+            if (folds) {
+                double x = A.sa[k][0] * f[0], y = A.sb[k][0] * u[0];
+#pragma unroll
+                for (int j = 1; j < 5; ++j) { x = x + A.sa[k][j] * f[j]; y = y + A.sb[k][j] * u[j]; }
+                fo[k] = x;
+                wo[k] = y - A.fgm[k] * u[k + 1];
+            }
+        }
+        av[k] = diff;
+    }
+}
 
 template <int FE>
 __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLMaps maps, const BLArgs A, int ns) {
@@ -788,6 +825,9 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
     // the two roles run separate loops (so the consumers' rings are not live in the producers' code)
     // that meet at one named barrier per plane
     if (producer) {
+        // warp-specialised register split (sm_90+): the producer warpgroup gives registers to the
+        // three consumer warpgroups, whose stencil rings need ~132 (4 x 104 + 12 x 136 warps x 32 = 64 K)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
         for (int it = 0; it < nit; ++it) {
             const int p = z0 - 1 + it, s = it % ns;
             mbar_wait(&bar[s], (it / ns) & 1);
@@ -799,7 +839,7 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
                 const int px = x0 - 1 + col, py = y0 - 1 + row;
                 double av[NM], cv[NM], fo[NM], wo[NM];
                 if (zin && (unsigned)px < (unsigned)n && (unsigned)py < (unsigned)n) {
-                    bl_resid_point<FE, NM>(A, F, SH::FPL / 8, row * SH::FW + col + 1, folds, av, cv, fo, wo);
+                    r4_point<FE>(A, F, SH::FPL / 8, row * SH::FW + col + 1, folds, av, cv, fo, wo);
                 } else {
 #pragma unroll
                     for (int k = 0; k < NM; ++k) { av[k] = 0.0; cv[k] = 0.0; }
@@ -825,6 +865,7 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
         return;
     }
     // consumer role: node kc = w / R4_WG, rows RR*wi .. RR*wi+RR-1 of the region
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 136;\n" ::: "memory");
     const int kc = w / R4_WG, wi = w % R4_WG;
     const int gx = x0 + lane - 1;
     const bool xout = lane >= 1 && lane - 1 < SH::TX && gx < n;

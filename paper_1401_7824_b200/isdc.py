@@ -47,12 +47,12 @@ class _Problem(C.Structure):
     _fields_ = [("grid", _Grid), ("M", C.c_int), ("nodes", C.c_int), ("dt", C.c_double), ("nu", C.c_double),
                 ("fe", C.c_int), ("fe_params", C.c_double * 3), ("fe_field_dev", C.c_void_p),
                 ("mg", _Mg), ("solve", _Solve), ("residual_kind", C.c_int), ("w_tol", C.c_double),
-                ("w_cap", C.c_int)]
+                ("w_cap", C.c_int), ("mlsdc_levels", C.c_int), ("coarse_sweeps", C.c_int)]
 
 
 class _Stats(C.Structure):
     _fields_ = [("sweeps", C.c_int), ("vcycles", C.c_long), ("cap_hits", C.c_int), ("converged", C.c_int),
-                ("final_residual", C.c_double), ("wcycles", C.c_long)]
+                ("final_residual", C.c_double), ("wcycles", C.c_long), ("coarse_vcycles", C.c_long)]
 
 
 _lib = None
@@ -122,6 +122,7 @@ class ISDC:
                  inner_tol: float = 1e-12, inner_cap: int = 50, sweep_tol: float = 1e-10, max_sweeps: int = 200,
                  fixed_sweeps: int = 0, nu1: int = 2, nu2: int = 2, omega: float = 0.8, guess: int = 0,
                  residual_kind: int = 0, w_tol: float = 1e-6, w_cap: int = 50, bc: int = BC_DIRICHLET,
+                 mlsdc_levels: int = 0, coarse_sweeps: int = 1,
                  device: Optional[torch.device] = None, stream: Optional[torch.cuda.Stream] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ISDC needs a CUDA device (no CPU fallback)")
@@ -144,6 +145,7 @@ class ISDC:
         s.mode, s.L, s.inner_tol, s.inner_cap = mode, L, inner_tol, inner_cap
         s.sweep_tol, s.max_sweeps, s.fixed_sweeps, s.guess = sweep_tol, max_sweeps, fixed_sweeps, guess
         p.residual_kind, p.w_tol, p.w_cap = residual_kind, w_tol, w_cap
+        p.mlsdc_levels, p.coarse_sweeps = mlsdc_levels, coarse_sweeps
         self.p = p
         self.dim, self.n, self.M = dim, n, M
         self.kmax = fixed_sweeps if fixed_sweeps > 0 else max_sweeps
@@ -230,6 +232,7 @@ class ISDC:
         k = st.sweeps
         return dict(sweeps=k, vcycles=st.vcycles, cap_hits=st.cap_hits, converged=bool(st.converged),
                     final_residual=st.final_residual, res_hist=hist[:k].copy(), wcycles=st.wcycles,
+                    coarse_vcycles=st.coarse_vcycles,
                     node_cycles=np.array(ncyc[: k * (self.M - 1)]).reshape(k, self.M - 1))
 
     def run(self, nsteps: int):

@@ -71,6 +71,27 @@ def test_workspace_and_validation_without_gpu(L):
         assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == code, (n, cn)
     q.grid.bc = 2
     assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == 1
+    # two-level MLSDC (NEXT f4): Dirichlet, n >= 7, ISDC mode, weighted residual; the coarse handle's
+    # workspace and the transfer fields are part of the caller's workspace
+    one = C.c_size_t(0)
+    assert L.isdc_workspace_bytes(C.byref(p), C.byref(one)) == 0
+    q = _Problem.from_buffer_copy(p)
+    q.mlsdc_levels, q.coarse_sweeps = 2, 1
+    assert L.isdc_workspace_bytes(C.byref(q), C.byref(nb)) == 0
+    assert nb.value > one.value + (3 - 1) * 63 * 64 * 8
+    for field, bad, code in [("coarse_sweeps", -1, 1), ("mlsdc_levels", 3, 1)]:
+        r = _Problem.from_buffer_copy(q)
+        setattr(r, field, bad)
+        assert L.isdc_workspace_bytes(C.byref(r), C.byref(nb)) == code, field
+    r = _Problem.from_buffer_copy(q)
+    r.solve.mode = 1
+    assert L.isdc_workspace_bytes(C.byref(r), C.byref(nb)) == 2
+    r = _Problem.from_buffer_copy(q)
+    r.grid.n = 3
+    assert L.isdc_workspace_bytes(C.byref(r), C.byref(nb)) == 2
+    r = _Problem.from_buffer_copy(q)
+    r.residual_kind = 1
+    assert L.isdc_workspace_bytes(C.byref(r), C.byref(nb)) == 2
     # create refuses a missing / too-small workspace before touching the device
     h = C.c_void_p()
     assert L.isdc_create(C.byref(p), None, 0, None, C.byref(h)) == 5
