@@ -914,6 +914,10 @@ isdc_status upload_ct(isdc_ctx *h) {
     double tn = (double)h->step_index * h->P.dt;
     for (int j = 0; j < h->M; ++j) h->cthost[j] = std::cos(tn + h->P.dt * h->tau[j]);
     CUDA_TRY(h, cudaMemcpyAsync(h->ctdev, h->cthost, h->M * sizeof(double), cudaMemcpyHostToDevice, h->s));
+    if (h->coarse) {   // MLSDC: the coarse level runs on the same time interval
+        h->coarse->step_index = h->step_index;
+        return upload_ct(h->coarse);
+    }
     return ISDC_OK;
 }
 

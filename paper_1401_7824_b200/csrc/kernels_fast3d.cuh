@@ -743,8 +743,9 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
 // emit |r~_m| at plane p-1 (the trees of k_bl MODE 1).  Producers run one plane ahead of the
 // consumers; one block barrier per plane.  Region 32 x R4_RH (tile 30 x (R4_RH - 2) + halo 1).
 // ---------------------------------------------------------------------------------------------
-constexpr int R4_WG = 3, R4_RR = 4, R4_RH = R4_WG * R4_RR;   // consumer warps per node, rows per thread
-constexpr int R4_PW = 4;                                     // producer warps (one per SM sub-partition)
+constexpr int R4_WG = 2, R4_RR = 4, R4_RH = R4_WG * R4_RR;   // consumer warps per node, rows per thread
+constexpr int R4_PW = 8;                                     // producer warps (two per SM sub-partition)
+constexpr int R4_PREG = 104, R4_CREG = 152;                  // setmaxnreg split (8 x 32 x (104 + 152) = 64 K)
 constexpr int R4_NT = 32 * (4 * R4_WG + R4_PW);
 struct R4Shape {
     static constexpr int RH = R4_RH, TX = RW - 2, TY = R4_RH - 2;
@@ -825,9 +826,9 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
     // the two roles run separate loops (so the consumers' rings are not live in the producers' code)
     // that meet at one named barrier per plane
     if (producer) {
-        // warp-specialised register split (sm_90+): the producer warpgroup gives registers to the
-        // three consumer warpgroups, whose stencil rings need ~132 (4 x 104 + 12 x 136 warps x 32 = 64 K)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
+        // warp-specialised register split (sm_90+): the producer warpgroups give registers to the
+        // consumer warpgroups, whose stencil rings (13 x R4_RR doubles per thread) need ~140
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(R4_PREG) : "memory");
         for (int it = 0; it < nit; ++it) {
             const int p = z0 - 1 + it, s = it % ns;
             mbar_wait(&bar[s], (it / ns) & 1);
@@ -838,8 +839,11 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
                 const int col = q & 31, row = q >> 5;        // region column / row
                 const int px = x0 - 1 + col, py = y0 - 1 + row;
                 double av[NM], cv[NM], fo[NM], wo[NM];
+                // the folds only at the tile's own points (they are stored, not stencilled)
+                const bool fpt = folds && zout && col >= 1 && col - 1 < SH::TX && px < n && row >= 1 &&
+                                 row - 1 < SH::TY && py < n;
                 if (zin && (unsigned)px < (unsigned)n && (unsigned)py < (unsigned)n) {
-                    r4_point<FE>(A, F, SH::FPL / 8, row * SH::FW + col + 1, folds, av, cv, fo, wo);
+                    r4_point<FE>(A, F, SH::FPL / 8, row * SH::FW + col + 1, fpt, av, cv, fo, wo);
                 } else {
 #pragma unroll
                     for (int k = 0; k < NM; ++k) { av[k] = 0.0; cv[k] = 0.0; }
@@ -850,7 +854,7 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
                     Pb[(2 * k) * (SH::PPL / 8) + po] = av[k];
                     Pb[(2 * k + 1) * (SH::PPL / 8) + po] = cv[k];
                 }
-                if (folds && zout && col >= 1 && col - 1 < SH::TX && px < n && row >= 1 && row - 1 < SH::TY && py < n) {
+                if (fpt) {
                     const long long gofs = (long long)p * A.plane + (long long)py * A.pitch + px;
 #pragma unroll
                     for (int k = 0; k < NM; ++k) {
@@ -865,7 +869,7 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
         return;
     }
     // consumer role: node kc = w / R4_WG, rows RR*wi .. RR*wi+RR-1 of the region
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 136;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R4_CREG) : "memory");
     const int kc = w / R4_WG, wi = w % R4_WG;
     const int gx = x0 + lane - 1;
     const bool xout = lane >= 1 && lane - 1 < SH::TX && gx < n;
