@@ -166,6 +166,13 @@ struct isdc_ctx {
     double cthost[ISDC_MAXM];
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual,
                                // 32 the single-pass four-node residual (M = 5; else two nodes per pass)
+    bool resid2d_tma = true;   // ISDC_RESID2D_TMA: 2D residual through the TMA ring
+    int rs_ns = 3;             // ISDC_RS_NS: its ring depth (3 or 5)
+    int rs_chunk_mul = 16;     // ISDC_RS_CHUNK: row chunks ~ this x SMs / column tiles
+    bool ws3d = true;          // ISDC_WS3D: warp-specialised 3D smoother on levels n >= ws3d_min
+    int ws3d_min = 63;         // ISDC_WS3D_MIN
+    bool fuse3d = false;       // ISDC_FUSE3D: 3D prolongation fused into the post-smoother (needs ws3d;
+                               // bitwise equal, measured slower: 1.34 ms vs 0.42 + 0.77 ms at 511^3)
     int tail3d = 15;           // largest 3D level handled by the single-CTA tail (fast kernels above)
     int tail2d = 31;           // largest 2D level handled by the single-CTA tail (31 measured best)
     cudaError_t kl_err = cudaSuccess;   // first failed launch since the last LAUNCH_CHECK
@@ -595,8 +602,31 @@ isdc_status launch_smooth2_3d_t(isdc_ctx *h, double *out, const double *in, cons
     LAUNCH_CHECK(h);
     return ISDC_OK;
 }
+// warp-specialised two-sweep smoother; e != nullptr: u + P e first (fused
+// trilinear prolongation + correction, MODE 2), in == nullptr: zero iterate (MODE 1)
+isdc_status launch_smooth2_3d_ws(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
+                                 const SCoef &c, int level, const double *e = nullptr, const GridDesc *gc = nullptr) {
+    const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, f3d::S_BH, 1);
+    const CUtensorMap *mu = in ? tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1) : mb;
+    const CUtensorMap *me = e ? tmap(h, e, *gc, f3d::WS_EW, f3d::WS_EH, 1) : mb;
+    if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+    ++h->launches;
+    const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
+    int pe = prof_begin(h, cls);
+    int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + f3d::S_TY - 1) / f3d::S_TY;
+    int zc = pick_chunk(h, tx * ty, g.n, 4);
+    dim3 grd(tx, ty, (g.n + zc - 1) / zc);
+    if (e) kl(h, f3d::k_smooth2ws<2>, grd, f3d::WSCfg<2>::NT, f3d::WSCfg<2>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    else if (!in) kl(h, f3d::k_smooth2ws<1>, grd, f3d::WSCfg<1>::NT, f3d::WSCfg<1>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    else kl(h, f3d::k_smooth2ws<0>, grd, f3d::WSCfg<0>::NT, f3d::WSCfg<0>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    // algorithmic bytes: read u (unless zero), b (+ e / 8); write u''
+    prof_end(h, pe, cls, ((in ? 24.0 : 16.0) + (e ? 1.0 : 0.0)) * npts_of(h, g));
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
 isdc_status launch_smooth2_3d(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                               const SCoef &c, int level) {
+    if (h->ws3d && g.n >= h->ws3d_min) return launch_smooth2_3d_ws(h, out, in, b, g, c, level);
     if (g.n <= 255) return launch_smooth2_3d_t<3, 12>(h, out, in, b, g, c, level);
     return launch_smooth2_3d_t<4, 8>(h, out, in, b, g, c, level);
 }
@@ -1034,6 +1064,13 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
         TRY(launch_smooth2(h, dst, curw, b, g, c, nullptr, l, C.e, &C.g));
         cu = dst;
         TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2 - 2));
+    } else if (use_fast3d(h, l) && use_fast3d(h, l, 4) && h->ws3d && h->fuse3d && g.n >= h->ws3d_min &&
+               h->P.mg.nu2 >= 2) {
+        // 3D: fused trilinear prolongation + correction + two sweeps (one pass)
+        double *dst = (curw == T) ? X : T;
+        TRY(launch_smooth2_3d_ws(h, dst, curw, b, g, c, l, C.e, &C.g));
+        cu = dst;
+        TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2 - 2));
     } else {
         TRY(launch_prolong(h, curw, g, C.e, C.g, l));
         TRY(smooth(h, l, X, T, b, c, cu, h->P.mg.nu2));
@@ -1326,6 +1363,53 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
                 A.fgm[q] = nu * dtm;
                 A.wf[q] = h->WB[q];
             }
+        }
+        if (h->resid2d_tma) {
+            // TMA-ring residual: one consumer warp per (strip, node), RS_SPC strips per CTA
+            f2d::TMaps2 maps;
+            const int K = M + (h->fe.kind == 2 ? 1 : 0);
+            for (int k = 0; k < K; ++k) {
+                const CUtensorMap *mk = tmap(h, k < M ? u[k] : h->Gp, g, f2d::RS_BW, f2d::RS_RB);
+                if (!mk) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
+                maps.m[k] = *mk;
+            }
+            const int strips = (h->n + f2d::SW_OUT - 1) / f2d::SW_OUT;
+            const int tx = (strips + f2d::RS_SPC - 1) / f2d::RS_SPC;
+            const int chunks = std::max(1, (h->rs_chunk_mul * h->nsm + tx - 1) / tx);
+            A.yc = std::max(f2d::RS_RB, (h->n + chunks - 1) / chunks);
+            dim3 grd(tx, (h->n + A.yc - 1) / A.yc);
+            ++h->launches;
+            int pe = prof_begin(h, PROF_RESID);
+            const int fe = h->fe.kind;
+            const bool wrt = h->P.residual_kind == 1;
+            auto go = [&](auto FEc, auto Mc, auto WRTc, auto WFc) {
+                constexpr int FE_ = decltype(FEc)::value, M_ = decltype(Mc)::value;
+                constexpr bool WRT_ = decltype(WRTc)::value, WF_ = decltype(WFc)::value;
+                if (h->rs_ns == 5) {
+                    using Z = f2d::RST<M_, FE_, 5>;
+                    kl(h, f2d::k_resid_t<FE_, M_, WRT_, WF_, 5>, grd, Z::NT, Z::SMEM)(maps, A);
+                } else {
+                    using Z = f2d::RST<M_, FE_, 3>;
+                    kl(h, f2d::k_resid_t<FE_, M_, WRT_, WF_, 3>, grd, Z::NT, Z::SMEM)(maps, A);
+                }
+            };
+            using F_ = std::false_type;
+            using T_ = std::true_type;
+            auto byfe = [&](auto Mc, auto WRTc, auto WFc) {
+                if (fe == 0) go(std::integral_constant<int, 0>{}, Mc, WRTc, WFc);
+                else if (fe == 1) go(std::integral_constant<int, 1>{}, Mc, WRTc, WFc);
+                else go(std::integral_constant<int, 2>{}, Mc, WRTc, WFc);
+            };
+            auto bym = [&](auto WRTc, auto WFc) {
+                if (M == 3) byfe(std::integral_constant<int, 3>{}, WRTc, WFc);
+                else byfe(std::integral_constant<int, 5>{}, WRTc, WFc);
+            };
+            if (wfo) bym(F_{}, T_{});
+            else if (wrt) bym(T_{}, F_{});
+            else bym(F_{}, F_{});
+            prof_end(h, pe, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
+            LAUNCH_CHECK(h);
+            return ISDC_OK;
         }
         dim3 grd = stream2d_grid(h, A.yc);
         if (M == 5) {   // two nodes per warp: 4 strips per CTA
@@ -2129,6 +2213,7 @@ bool kernel_attrs(isdc_ctx *h) {
     set((const void *)f2d::k_resid<0>); set((const void *)f2d::k_resid<1>); set((const void *)f2d::k_resid<2>);
     set((const void *)f3d::k_smooth2<3, 0, 12>); set((const void *)f3d::k_smooth2<3, 1, 12>);
     set((const void *)f3d::k_smooth2<4, 0, 8>); set((const void *)f3d::k_smooth2<4, 1, 8>);
+    set((const void *)f3d::k_smooth2ws<0>); set((const void *)f3d::k_smooth2ws<1>); set((const void *)f3d::k_smooth2ws<2>);
     set((const void *)f3d::k_restrict);
     set((const void *)f3d::k_fe_cd4);
     auto setbl = [&](auto F) {
@@ -2143,6 +2228,16 @@ bool kernel_attrs(isdc_ctx *h) {
     setbl(std::integral_constant<int, 0>{}); setbl(std::integral_constant<int, 1>{});
     setbl(std::integral_constant<int, 2>{}); setbl(std::integral_constant<int, 3>{});
     set((const void *)f3d::k_resid4<0>); set((const void *)f3d::k_resid4<3>);
+    auto setrt = [&](auto FEc) {
+        constexpr int F_ = decltype(FEc)::value;
+        set((const void *)f2d::k_resid_t<F_, 3, false, false, 3>); set((const void *)f2d::k_resid_t<F_, 5, false, false, 3>);
+        set((const void *)f2d::k_resid_t<F_, 3, true, false, 3>); set((const void *)f2d::k_resid_t<F_, 5, true, false, 3>);
+        set((const void *)f2d::k_resid_t<F_, 3, false, true, 3>); set((const void *)f2d::k_resid_t<F_, 5, false, true, 3>);
+        set((const void *)f2d::k_resid_t<F_, 3, false, false, 5>); set((const void *)f2d::k_resid_t<F_, 5, false, false, 5>);
+        set((const void *)f2d::k_resid_t<F_, 3, true, false, 5>); set((const void *)f2d::k_resid_t<F_, 5, true, false, 5>);
+        set((const void *)f2d::k_resid_t<F_, 3, false, true, 5>); set((const void *)f2d::k_resid_t<F_, 5, false, true, 5>);
+    };
+    setrt(std::integral_constant<int, 0>{}); setrt(std::integral_constant<int, 1>{}); setrt(std::integral_constant<int, 2>{});
     set((const void *)k_tail<2>); set((const void *)k_tail<3>);
     set((const void *)k_ptail<2>); set((const void *)k_ptail<3>);
     if (first != cudaSuccess) {
@@ -2206,6 +2301,12 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     h->fast = !(env && env[0] == '1') && !h->per;   // the tuned kernels assume Dirichlet zeros
     if (h->fast && !tma_encoder()) h->fast = false;
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
+    if (const char *w3 = getenv("ISDC_WS3D")) h->ws3d = w3[0] != '0';
+    if (const char *r2 = getenv("ISDC_RESID2D_TMA")) h->resid2d_tma = r2[0] != '0';
+    if (const char *rn = getenv("ISDC_RS_NS")) h->rs_ns = atoi(rn);
+    if (const char *rc = getenv("ISDC_RS_CHUNK")) h->rs_chunk_mul = atoi(rc);
+    if (const char *w3m = getenv("ISDC_WS3D_MIN")) h->ws3d_min = atoi(w3m);
+    if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
     if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';

@@ -811,6 +811,161 @@ __global__ void __launch_bounds__(SW_NT, 2) k_resid_s(StreamArgs A) {           
 }
 
 // ---------------------------------------------------------------------------------------------
+// Residual of nodes m = 1..M-1 (and the next sweep's RHS folds, WF; the r~_m fields, WRT) with the
+// node-field rows fed through a TMA / mbarrier ring: a CTA owns RS_SPC strips of
+// 30 output columns and a chunk of rows; a producer warp streams boxes of RS_RB rows x (30 SPC + 4)
+// columns of every input field (u_0..u_{M-1} [, G]) into RS_NS stages; one consumer warp per
+// (strip, node m) -- which also forms fold q = m - 1 -- reads its column of every field from shared
+// memory, so each field is read from HBM once per sweep and the loads in flight are set by the
+// ring depth, not by per-warp register prefetch.  Every value is formed by the trees of k_resid_s.
+// ---------------------------------------------------------------------------------------------
+struct TMaps2 {
+    CUtensorMap m[ISDC_MAXM + 1];
+};
+constexpr int RS_SPC = 2, RS_RB = 6;                // strips per CTA, rows per stage
+constexpr int RS_BW = SW_OUT * RS_SPC + 4;           // box width (even start: x0 - 2)
+template <int MM, int FE, int RS_NS = 3>           // RS_NS stages (55 KB: 4 CTAs per SM)
+struct RST {
+    static constexpr int K = MM + (FE == 2 ? 1 : 0);         // fields per stage
+    static constexpr int NCW = RS_SPC * (MM - 1);            // consumer warps
+    static constexpr int NT = 32 * (NCW + 1);                // + the producer warp
+    static constexpr int FPL = RS_BW * RS_RB;                // doubles per field box
+    static constexpr size_t SMEM = (size_t)RS_NS * K * FPL * 8 + 16 * RS_NS + 128;
+};
+
+template <int FE, int MM, bool WRT, bool WF, int RS_NS = 3>
+__global__ void __launch_bounds__(RST<MM, FE, RS_NS>::NT) k_resid_t(const __grid_constant__ TMaps2 maps, StreamArgs A) {
+    using Z = RST<MM, FE, RS_NS>;
+    constexpr int K = Z::K, FPL = Z::FPL;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    double *Fs = reinterpret_cast<double *>(sm);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)RS_NS * K * FPL * 8);
+    uint64_t *empty = full + RS_NS;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = A.n;
+    const int y0 = blockIdx.y * A.yc, y1 = min(y0 + A.yc, n);
+    const int nit = y1 - y0 + 2;                              // rows y0-1 .. y1
+    const int nst = (nit + RS_RB - 1) / RS_RB;
+    const int X0 = blockIdx.x * (SW_OUT * RS_SPC) - 2;        // box origin (even)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < RS_NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], Z::NCW); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (wid == Z::NCW) {   // producer
+        if (lane == 0) {
+            for (int k = 0; k < K; ++k) tma_prefetch_desc(&maps.m[k]);
+            for (int t = 0; t < nst; ++t) {
+                const int s = t % RS_NS;
+                if (t >= RS_NS) mbar_wait(&empty[s], ((t / RS_NS) - 1) & 1);
+                mbar_expect_tx(&full[s], K * FPL * 8);
+                for (int k = 0; k < K; ++k)
+                    tma_load_2d(Fs + ((size_t)s * K + k) * FPL, &maps.m[k], X0, y0 - 1 + t * RS_RB, &full[s]);
+            }
+        }
+        return;
+    }
+    const int strip_l = wid / (MM - 1), role = wid % (MM - 1);
+    const int strip = blockIdx.x * RS_SPC + strip_l;
+    const int x = strip * SW_OUT - 1 + lane;
+    const int col = SW_OUT * strip_l + 1 + lane;             // box column of x
+    const bool xin = x >= 0 && x < n, xout = lane >= 1 && lane <= SW_OUT && x < n;
+    const BLConst c = A.bl;
+    auto rowoff = [&](int y) { return (long long)y * A.pitch + x; };
+    // node m = role + 1, fold q = role: run-time indices (one code path for every warp keeps the
+    // kernel inside the instruction cache); the node selections are select chains, not indexing
+    const int m = role + 1, q = role;
+    // the warp's coefficient rows in registers (loaded once; no constant-bank or cos(t) loads per row)
+    double ca[MM], cb[MM], cf[MM], ctr[MM];
+#pragma unroll
+    for (int j = 0; j < MM; ++j) {
+        ca[j] = A.a[m][j];
+        cb[j] = A.beta[m][j];
+        cf[j] = WF ? A.fb[q][j] : 0.0;
+        ctr[j] = FE == 2 ? A.ct[j] : 0.0;
+    }
+    const double cgm = WF ? A.fgm[q] : 0.0;
+    double *const wfq = WF ? A.wf[q] : nullptr;
+    double *const rtm = WRT ? A.rt[m - 1] : nullptr;
+    double pq[3], pr[3], zq[3], zr[3];
+    double rmax = 0.0;
+    auto row = [&](auto Kc, const double *F, int it) {
+        constexpr int k = decltype(Kc)::value;               // it % 3
+        constexpr int km1 = (k + 2) % 3, km2 = (k + 1) % 3;
+        const int y = y0 - 1 + it;
+        const bool in = xin && y >= 0 && y < n;
+        double uj[MM], fj[MM];
+#pragma unroll
+        for (int j = 0; j < MM; ++j) uj[j] = F[j * FPL];
+        if (FE == 1) {
+#pragma unroll
+            for (int j = 0; j < MM; ++j) fj[j] = fe_of<1>(uj[j]);
+        } else if (FE == 2) {
+            const double g = F[MM * FPL];
+#pragma unroll
+            for (int j = 0; j < MM; ++j) fj[j] = g * ctr[j];
+        }
+        double um = uj[0];                                   // u_m (= u_{q+1} of the fold)
+#pragma unroll
+        for (int j = 1; j < MM; ++j)
+            if (j == m) um = uj[j];
+        if (WF && in && xout && y >= y0 && y < y1) {
+            double acc = cf[0] * uj[0];
+#pragma unroll
+            for (int j = 1; j < MM; ++j) acc = acc + cf[j] * uj[j];
+            __stcs(wfq + rowoff(y), acc - cgm * um);         // read again only by the next sweep
+        }
+        double diff = um - uj[0];
+        if (FE != 0) {
+            double fa = ca[0] * fj[0];
+#pragma unroll
+            for (int j = 1; j < MM; ++j) fa = fa + ca[j] * fj[j];
+            diff = diff - fa;
+        }
+        double acc = cb[0] * uj[0];
+#pragma unroll
+        for (int j = 1; j < MM; ++j) acc = acc + cb[j] * uj[j];
+        const double pv = in ? diff : 0.0, zv = in ? acc : 0.0;
+        pq[k] = pv; zq[k] = zv;
+        pr[k] = shfl_up1(pv) + shfl_dn1(pv);
+        zr[k] = shfl_up1(zv) + shfl_dn1(zv);
+        if (it >= 2 && xout) {
+            const double fp = pr[km1] + (pq[km2] + pq[k]);
+            const double fz = zr[km1] + (zq[km2] + zq[k]);
+            const double ez = zr[km2] + zr[k];
+            const double Bp = c.kB0 * pq[km1] + c.kB1 * fp;
+            const double Lz = (c.kL0 * zq[km1] + c.kL1 * fz) + c.kL2 * ez;
+            const double rv = Bp - Lz;
+            rmax = amax(rmax, fabs(rv));
+            if (WRT) rtm[rowoff(y - 1)] = rv;
+        }
+    };
+    static_assert(RS_RB % 3 == 0, "ring index = row % 3");
+    for (int t = 0; t < nst; ++t) {
+        const int s = t % RS_NS;
+        mbar_wait(&full[s], (t / RS_NS) & 1);
+        const double *F = Fs + (size_t)s * K * FPL + col;
+        const int it0 = t * RS_RB;
+#pragma unroll 1
+        for (int r = 0; r < RS_RB; r += 3) {
+            if (it0 + r + 2 < nit) {   // three rows (the common case): no per-row guards
+                row(std::integral_constant<int, 0>{}, F + r * RS_BW, it0 + r);
+                row(std::integral_constant<int, 1>{}, F + (r + 1) * RS_BW, it0 + r + 1);
+                row(std::integral_constant<int, 2>{}, F + (r + 2) * RS_BW, it0 + r + 2);
+            } else {
+                if (it0 + r < nit) row(std::integral_constant<int, 0>{}, F + r * RS_BW, it0 + r);
+                if (it0 + r + 1 < nit) row(std::integral_constant<int, 1>{}, F + (r + 1) * RS_BW, it0 + r + 1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(rmax));
+    if (lane == 0 && v) atomicMax(A.slot + m - 1, v);
+}
+
+// ---------------------------------------------------------------------------------------------
 // Fused pre-smoother + defect + full-weighting restriction: one pass reads
 // u, b and writes the smoothed iterate u'' (tile) and b_c = R(b - S u'') (coarse tile), 26 B per
 // fine point instead of 24 + 18.  Fine tile 58 x TY at (x0, y0), coarse tile 29 x TY/2 at

@@ -230,6 +230,215 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------------------------
+// Warp-specialised fused two-sweep Jacobi: the tiles, trees and TMA boxes of
+// k_smooth2<4, MODE, 8>, with sweep 1 and sweep 2 in separate groups of 8 warps (register rings of
+// one sweep each, 16 warps per SM instead of 8) that run one plane apart and meet at one block
+// barrier per plane.  MODE 0: u from memory; 1: u == 0 (nothing read); 2: u + P e first -- the
+// trilinear prolongation + correction fused in (the sweep-1 group adds P e to each u plane in
+// shared memory, in place, one plane ahead of its own partials; the two coarse planes of each fine
+// plane arrive by TMA with its stage), so the fine post-smoothing moves 25 B/pt instead of 17 + 24.
+// Stage j (plane p = z0 - 2 + j): u box 34 x 34 at (x0-2, y0-2, p), b box 34 x 32 at
+// (x0-2, y0-1, p-1), MODE 2: coarse boxes 20 x 18 at (ex0, ey0) of planes za, za + 1.
+// At iteration it sweep 1 handles stage it (t(p-1) -> T[it % 2]; MODE 2: first P e into stage
+// it + 1), sweep 2 the t plane of stage it - 1 (output at p - 3 with b from stage it - 2).
+// ---------------------------------------------------------------------------------------------
+constexpr int WS_SR = 4, WS_GW = 8;                 // rows per thread, warps per sweep group
+constexpr int WS_EW = 20, WS_EH = 18;               // coarse boxes (MODE 2)
+constexpr int WS_EPL = a128(WS_EW * WS_EH * 8);
+template <int MODE>
+struct WSCfg {
+    static constexpr int NS = MODE == 2 ? 7 : 6;    // stages in use: it - 2 .. it (+ 1 in MODE 2)
+    static constexpr int NT = 32 * 2 * WS_GW;
+    static constexpr int UPL = S_UPL, BPL = S_BPL, EPL = MODE == 2 ? 2 * WS_EPL : 0;
+    static constexpr int SPL = UPL + BPL + EPL;     // one stage: u | b | e(za) | e(za+1)
+    static constexpr size_t SMEM = (size_t)NS * SPL + 2 * S_TPL + 8 * NS + 128;
+};
+
+// MODE 2: u(p) += P e on the u box of one stage (in-domain points only), 2 x 2 fine blocks per
+// thread (one double2 per box row), canonical nesting x, then y, then z, one multiply by
+// 0.5^(#even axes) (the trees of k_prolong).
+__device__ __forceinline__ void ws_prolong_plane(double *U, const double *Ea, const double *Eb, int p, int n, int x0,
+                                                 int y0, int dlt, int ptid) {
+    if ((unsigned)p >= (unsigned)n) return;
+    const bool ze = !(p & 1);
+    const double zw = ze ? 0.5 : 1.0;
+    for (int q = ptid; q < 17 * 17; q += 32 * WS_GW) {
+        const int a = q % 17, b = q / 17;           // fine box cols 2a, 2a+1; rows 2b, 2b+1
+        const int gxe = x0 - 2 + 2 * a, gye = y0 - 2 + 2 * b;
+        const bool ine = (unsigned)gxe < (unsigned)n, ino = (unsigned)(gxe + 1) < (unsigned)n;
+        if (!ine && !ino) continue;
+        const double *ra = Ea + b * WS_EW + a + dlt;
+        double see = (ra[0] + ra[1]) + (ra[WS_EW] + ra[WS_EW + 1]);
+        double soe = ra[1] + ra[WS_EW + 1];
+        double seo = ra[WS_EW] + ra[WS_EW + 1];
+        double soo = ra[WS_EW + 1];
+        if (ze) {
+            const double *rb = Eb + b * WS_EW + a + dlt;
+            see = see + ((rb[0] + rb[1]) + (rb[WS_EW] + rb[WS_EW + 1]));
+            soe = soe + (rb[1] + rb[WS_EW + 1]);
+            seo = seo + (rb[WS_EW] + rb[WS_EW + 1]);
+            soo = soo + rb[WS_EW + 1];
+        }
+        // weights (ye ? 0.5 : 1) * (ze ? 0.5 : 1), the even column * 0.5 (exact powers of two)
+        const double w_e = 0.5 * zw, w_o = zw;      // even row, odd row
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int gy = gye + rr;
+            if ((unsigned)gy >= (unsigned)n) continue;
+            double2 *up = reinterpret_cast<double2 *>(U + (2 * b + rr) * S_UW + 2 * a);
+            double2 v = *up;
+            const double w = rr ? w_o : w_e;
+            if (ine) v.x = v.x + (rr ? seo : see) * (w * 0.5);
+            if (ino) v.y = v.y + (rr ? soo : soe) * w;
+            *up = v;
+        }
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(WSCfg<MODE>::NT, 1) k_smooth2ws(const __grid_constant__ CUtensorMap tu,
+                                                                 const __grid_constant__ CUtensorMap tb,
+                                                                 const __grid_constant__ CUtensorMap te,
+                                                                 double *__restrict__ out, int n, int pitch,
+                                                                 long long plane, SCoef c, int zc) {
+    using W = WSCfg<MODE>;
+    constexpr int NS = W::NS, SR = WS_SR;
+    constexpr bool ZERO = MODE == 1, PRO = MODE == 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    double *St = reinterpret_cast<double *>(sm);
+    double *Ts = reinterpret_cast<double *>(sm + NS * W::SPL);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + NS * W::SPL + 2 * S_TPL);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int x0 = blockIdx.x * S_TX, y0 = blockIdx.y * S_TY;
+    const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, n);
+    const int nit = z1 - z0 + 4;                    // stages: planes z0-2 .. z1+1
+    const int niter = nit + 1;                      // sweep 2 trails the stages by one
+    const int ex0 = ((x0 >> 1) - 2) & ~1, ey0 = (y0 >> 1) - 2;   // coarse box origin (even x: TMA rule)
+    auto stage = [&](int j) { return St + (size_t)(j % NS) * (W::SPL / 8); };
+    auto issue = [&](int j) {
+        const int p = z0 - 2 + j;
+        double *S = stage(j);
+        uint64_t *bb = &bar[j % NS];
+        mbar_expect_tx(bb, ((ZERO ? 0 : S_UW * S_UH) + S_BW * S_BH + (PRO ? 2 * WS_EW * WS_EH : 0)) * 8);
+        if (!ZERO) tma_load_3d(S, &tu, x0 - 2, y0 - 2, p, bb);
+        tma_load_3d(S + W::UPL / 8, &tb, x0 - 2, y0 - 1, p - 1, bb);
+        if (PRO) {
+            const int za = (p & 1) ? (p - 1) / 2 : p / 2 - 1;   // odd p: (p-1)/2; even p: p/2 - 1 and p/2
+            tma_load_3d(S + (W::UPL + W::BPL) / 8, &te, ex0, ey0, za, bb);
+            tma_load_3d(S + (W::UPL + W::BPL + WS_EPL) / 8, &te, ex0, ey0, za + 1, bb);
+        }
+    };
+    if (tid == 0) {
+        tma_prefetch_desc(&tu);
+        tma_prefetch_desc(&tb);
+        if (PRO) tma_prefetch_desc(&te);
+        for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    if (ZERO)
+        for (int s = 0; s < NS; ++s)
+            for (int q = tid; q < S_UW * S_UH; q += blockDim.x) St[s * (W::SPL / 8) + q] = 0.0;
+    __syncthreads();
+    if (tid == 0)
+        for (int j = 0; j < NS && j < nit; ++j) issue(j);
+
+    const int role = w < WS_GW ? 0 : 1;             // sweep 1 | sweep 2
+    const int row0 = SR * (w % WS_GW);
+    const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
+    const int lx = lane - 1, ly0 = row0 - 1;
+    const int gx = x0 + lx;
+    const bool xin = gx >= 0 && gx < n;
+    const bool xout = lx >= 0 && lx < S_TX && gx < n;
+    unsigned inxy = 0u, oks = 0u;
+#pragma unroll
+    for (int r = 0; r < SR; ++r) {
+        const int ly = ly0 + r, gy = y0 + ly;
+        if (xin && gy >= 0 && gy < n) inxy |= 1u << r;
+        if (xout && ly >= 0 && ly < S_TY && gy < n) oks |= 1u << r;
+    }
+    double *optr = out + (long long)(z0 - 4) * plane + (long long)(y0 + ly0) * pitch + gx;
+    // rings of one sweep (role 0: u partials; role 1: t partials), indexed by stage mod 3 / mod 2
+    double q[3][SR], f[3][SR], e[2][SR];
+    const int dlt = ((x0 >> 1) - 2) - ex0;
+    auto prolong = [&](int j) {   // MODE 2, sweep-1 group: stage j's u plane += P e
+        mbar_wait(&bar[j % NS], (j / NS) & 1);
+        double *S = stage(j);
+        ws_prolong_plane(S, S + (W::UPL + W::BPL) / 8, S + (W::UPL + W::BPL + WS_EPL) / 8, z0 - 2 + j, n, x0, y0,
+                         dlt, tid);
+    };
+    if (PRO) {
+        if (role == 0) prolong(0);
+        __syncthreads();
+    }
+
+    auto step = [&](auto Kc, int it) {
+        constexpr int K = decltype(Kc)::value;      // it % 6
+        if (role == 0) {
+            constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3, i2 = K % 2, m2 = (K + 1) % 2;
+            const int j = it;
+            if (j < nit) {
+                if (PRO) {
+                    if (j + 1 < nit) prolong(j + 1);   // visible to the group after this plane's barrier
+                } else {
+                    mbar_wait(&bar[j % NS], (j / NS) & 1);
+                }
+                const double *S = stage(j);
+                plane_partials<true, SR>(S, S_UW, row0, lane, q[i3], f[i3], e[i2]);
+                if (j >= 2) {   // sweep 1 at plane z0 - 3 + j on the 32 x 32 region
+                    const int gz = z0 - 3 + j;
+                    const unsigned in = ((unsigned)gz < (unsigned)n) ? inxy : 0u;
+                    const double *Bp = S + W::UPL / 8 + row0 * S_BW + lane + 1;
+                    double *Tp = Ts + i2 * (S_TPL / 8) + (row0 + 1) * S_TW + lane + 1;
+#pragma unroll
+                    for (int r = 0; r < SR; ++r) {
+                        const double faces = f[m3][r] + (q[mm3][r] + q[i3][r]);
+                        const double edges = e[m2][r] + (f[mm3][r] + f[i3][r]);
+                        const double su = (c0 * q[m3][r] + c1 * faces) + c2 * edges;
+                        const double t = q[m3][r] + wd * (Bp[r * S_BW] - su);
+                        Tp[r * S_TW] = ((in >> r) & 1u) ? t : 0.0;
+                    }
+                }
+            }
+        } else if (role == 1) {
+            constexpr int KJ = (K + 5) % 6;         // j2 % 6
+            constexpr int i3 = KJ % 3, m3 = (KJ + 2) % 3, mm3 = (KJ + 1) % 3, i2 = KJ % 2, m2 = (KJ + 1) % 2;
+            const int j2 = it - 1;
+            if (j2 >= 2 && j2 < nit) {
+                plane_partials<true, SR>(Ts + i2 * (S_TPL / 8), S_TW, row0, lane, q[i3], f[i3], e[i2]);
+                if (j2 >= 4) {   // sweep 2 at plane z0 - 4 + j2 on the 30 x 30 tile, b from stage j2 - 1
+                    const double *Bp = stage(j2 - 1) + W::UPL / 8 + row0 * S_BW + lane + 1;
+                    double *op = optr + (long long)j2 * plane;
+#pragma unroll
+                    for (int r = 0; r < SR; ++r) {
+                        const double faces = f[m3][r] + (q[mm3][r] + q[i3][r]);
+                        const double edges = e[m2][r] + (f[mm3][r] + f[i3][r]);
+                        const double su = (c0 * q[m3][r] + c1 * faces) + c2 * edges;
+                        const double o = q[m3][r] + wd * (Bp[r * S_BW] - su);
+                        if ((oks >> r) & 1u) *op = o;
+                        op += pitch;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // stage it - 2 is free (sweep 2 read its b): refill it with stage it - 2 + NS
+        if (tid == 0) {
+            const int jr = it - 2;
+            if (jr >= 0 && jr + NS < nit) issue(jr + NS);
+        }
+    };
+    for (int base = 0; base < niter; base += 6) {
+        if (base + 0 < niter) step(std::integral_constant<int, 0>{}, base + 0);
+        if (base + 1 < niter) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < niter) step(std::integral_constant<int, 2>{}, base + 2);
+        if (base + 3 < niter) step(std::integral_constant<int, 3>{}, base + 3);
+        if (base + 4 < niter) step(std::integral_constant<int, 4>{}, base + 4);
+        if (base + 5 < niter) step(std::integral_constant<int, 5>{}, base + 5);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Defect + full-weighting restriction, one HBM pass (read u, b; write b_c), DESIGN.md §6.8.
 // Coarse tile 15 x 15 x a coarse z chunk [K0, K1).  Fine defect region 31 x 31 at
 // (2 I0, 2 J0), streamed over fine planes 2 K0 .. 2 K1; d(z) goes to a shared plane, coarse
