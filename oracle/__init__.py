@@ -101,6 +101,17 @@ def _declare(L):
     L.ora_mlsdc_correction.restype = C.c_long
     L.ora_mlsdc_step.argtypes = [C.POINTER(OraProblem), C.c_int, _dp, C.c_double, C.POINTER(C.c_int),
                                  C.POINTER(C.c_long), C.POINTER(C.c_long), _dp, C.POINTER(C.c_int)]
+    L.ora_pf_fine.argtypes = [C.POINTER(OraProblem), C.c_double, PP, PP, PP, C.POINTER(C.c_long)]
+    L.ora_pf_fine.restype = C.c_double
+    L.ora_pf_restrict.argtypes = [C.POINTER(OraProblem), C.c_double, PP, PP, PP, PP, PP]
+    L.ora_pf_coarse.argtypes = [C.POINTER(OraProblem), C.c_int, C.c_double, C.c_void_p, PP, PP]
+    L.ora_pf_coarse.restype = C.c_long
+    L.ora_pf_interpolate.argtypes = [C.POINTER(OraProblem), PP, PP, PP]
+    L.ora_pf_residual.argtypes = [C.POINTER(OraProblem), C.c_double, PP, PP]
+    L.ora_pf_residual.restype = C.c_double
+    L.ora_pfasst_block.argtypes = [C.POINTER(OraProblem), C.c_int, C.c_int, C.c_int, _dp, C.c_int,
+                                   C.POINTER(C.c_int), C.POINTER(C.c_long), C.POINTER(C.c_long), _dp,
+                                   C.POINTER(C.c_int), _dp]
     L.ora_weno5.argtypes = [C.c_double] * 5
     L.ora_weno5.restype = C.c_double
 
@@ -334,3 +345,84 @@ def mlsdc_step(prob: Problem, u0, t_n, coarse_sweeps=1):
     k = sw.value
     return u, dict(sweeps=k, vcycles=vc.value, coarse_vcycles=cvc.value, res_hist=hist[:k].copy(),
                    converged=bool(conv.value), seconds=time.perf_counter() - t0)
+
+
+# ---------------------------------------------------------------------------------------------
+# PFASST with ISDC sweeps (NEXT f4b; isdc_oracle.c ora_pfasst_block, reading R33)
+# ---------------------------------------------------------------------------------------------
+def pfasst_block(prob: Problem, u0, nslices, step0=0, coarse_sweeps=1, predictor=True):
+    """One PFASST block of `nslices` time slices (steps step0 .. step0+nslices-1) from u0, serial
+    emulation in the order of R33.  Returns (fine end value of every slice [nslices, ...], stats)."""
+    cfg = prob.cfg
+    u = _c(u0).copy()
+    kmax = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
+    hist = np.zeros(kmax * nslices)
+    uend = np.zeros((nslices,) + u.shape)
+    it, vc, cvc, conv = C.c_int(0), C.c_long(0), C.c_long(0), C.c_int(0)
+    t0 = time.perf_counter()
+    rc = lib().ora_pfasst_block(C.byref(prob.s), int(nslices), int(coarse_sweeps), 1 if predictor else 0, _p(u),
+                                int(step0), C.byref(it), C.byref(vc), C.byref(cvc), _p(hist), C.byref(conv),
+                                _p(uend))
+    if rc:
+        raise ValueError(f"ora_pfasst_block: unsupported problem ({rc})")
+    k = it.value
+    return uend, dict(iterations=k, vcycles=vc.value, coarse_vcycles=cvc.value,
+                      res_hist=hist[: k * nslices].reshape(k, nslices).copy(), converged=bool(conv.value),
+                      seconds=time.perf_counter() - t0)
+
+
+class PfasstSlice:
+    """One PFASST time slice on the oracle (phases A-D of isdc_oracle.c, R33): the same per-slice
+    operations the CUDA slice handle performs; used by the multi-process tests of the product's
+    PFASST driver (tests/test_pfasst_driver.py)."""
+
+    def __init__(self, prob: Problem, u0, step_index, coarse_sweeps=1):
+        self.prob, self.cfg = prob, prob.cfg
+        self.coarse_sweeps = coarse_sweeps
+        M, n, d = self.cfg.M, self.cfg.n, self.cfg.dim
+        nc = (n - 1) // 2
+        self.t_n = float(step_index) * self.cfg.dt
+        u0 = _c(u0)
+        self.u0 = u0.copy()
+        self.uold = [self.u0] + [u0.copy() for _ in range(M - 1)]
+        self.unew = [self.u0] + [np.zeros_like(u0) for _ in range(M - 1)]
+        self.rh = [np.zeros_like(u0) for _ in range(M)]
+        self.Ub = [np.zeros((nc,) * d) for _ in range(M)]
+        self.U = [np.zeros((nc,) * d) for _ in range(M)]
+        self.fas = [np.zeros((nc,) * d) for _ in range(M)]
+        self.vcycles = 0
+        self.coarse_vcycles = 0
+
+    def set_u0(self, u0):
+        self.u0[...] = u0
+
+    def predict_restrict(self):
+        """Predictor: the fine residual fields of the current (spread) state, then phase B."""
+        lib().ora_pf_residual(C.byref(self.prob.s), self.t_n, _ptrs(self.uold), _ptrs(self.rh))
+        self.restrict()
+
+    def fine(self):
+        vc = C.c_long(0)
+        r = lib().ora_pf_fine(C.byref(self.prob.s), self.t_n, _ptrs(self.uold), _ptrs(self.unew), _ptrs(self.rh),
+                              C.byref(vc))
+        self.vcycles += vc.value
+        self.uold, self.unew = self.unew, self.uold
+        return float(r)
+
+    def restrict(self):
+        lib().ora_pf_restrict(C.byref(self.prob.s), self.t_n, _ptrs(self.uold), _ptrs(self.rh), _ptrs(self.Ub),
+                              _ptrs(self.U), _ptrs(self.fas))
+
+    def coarse(self, U0=None):
+        U0c = None if U0 is None else _c(U0)
+        self.coarse_vcycles += lib().ora_pf_coarse(C.byref(self.prob.s), int(self.coarse_sweeps), self.t_n,
+                                                   None if U0c is None else U0c.ctypes.data, _ptrs(self.U),
+                                                   _ptrs(self.fas))
+        return self.U[-1].copy()
+
+    def interpolate(self):
+        lib().ora_pf_interpolate(C.byref(self.prob.s), _ptrs(self.U), _ptrs(self.Ub), _ptrs(self.uold))
+        return self.uold[-1].copy()
+
+    def end(self):
+        return self.uold[-1].copy()

@@ -1005,3 +1005,205 @@ int ora_mlsdc_step(const ora_problem *P, int coarse_sweeps, double *u0, double t
     *sweeps = k; *vcycles = vc; *cvcycles = cvc; *converged = conv;
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* PFASST with ISDC sweeps (NEXT f4b; "SDC sweeps on multiple levels combined with a  */
+/* forward transfer of updated initial values in a manner similar to Parareal ... on each time   */
+/* level, only a single SDC sweep is performed"; reading R33).  A block of P time      */
+/* slices (slice p = time step step0 + p, t_n = (double)(step0 + p)*dt, R28), each a two-level   */
+/* MLSDC iterate (R32).  The block's initial value u0 is spread over every slice and node, then: */
+/*   predictor (optional): on every slice, the fine residual fields of the spread state,         */
+/*     injection + FAS (phase B); stages s = 0..P-1: slice p >= s first takes (s >= 1) the coarse */
+/*     end value of slice p-1 from stage s-1 as its coarse node 0, then coarse_sweeps coarse      */
+/*     sweeps (phase C); so slice p performs p+1 stages; then interpolation (phase D) everywhere. */
+/*   iteration k = 1, 2, ...:                                                                    */
+/*     1. slice p >= 1 replaces its fine node 0 by the fine end value of slice p-1 as it stood   */
+/*        at the end of iteration k-1 (the forward transfer of updated initial values)           */
+/*     2. fine ISDC sweep + fine weighted residual on every slice (phase A)                      */
+/*     3. stop when max over slices of the residual < sweep_tol (or after fixed_sweeps           */
+/*        iterations); the block ends after a fine sweep                                         */
+/*     4. injection + FAS on every slice (phase B)                                               */
+/*     5. for p = 0..P-1 in order: slice p >= 1 takes the coarse end value of slice p-1 from     */
+/*        THIS iteration as its coarse node 0, then coarse_sweeps coarse sweeps (phase C)        */
+/*     6. interpolation of the coarse correction on every slice (phase D)                        */
+/* Replacing node 0 replaces it in both iterate sets (node 0 is one buffer, as in ora_step).     */
+/* Slices, iterations and phases run here one after another; a time-parallel run (one slice per  */
+/* GPU) computes the same values because each phase reads only what the dependencies above give. */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Phase A: fine sweep uold -> unew (unew[0] must alias uold[0]) and the residual fields rh of
+ * unew; returns max_m ||r~_m||; *vc += the V-cycles of the sweep. */
+double ora_pf_fine(const ora_problem *P, double t_n, double *const *uold, double *const *unew,
+                   double *const *rh, long *vc) {
+    ora_set_bc(0);
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    if (ora_tables(P->M, tau, Q, S, dtau)) return -1.0;
+    int cyc[32];
+    sweep_fas(P, tau, S, dtau, t_n, uold, unew, cyc, NULL);
+    for (int m = 0; m + 1 < P->M; ++m) *vc += cyc[m];
+    return residual_fields(P, tau, Q, t_n, unew, NULL, rh);
+}
+
+/* The fine residual fields rh of the current iterate u without a sweep (the predictor works on the
+ * spread state); returns max_m ||r~_m||. */
+double ora_pf_residual(const ora_problem *P, double t_n, double *const *u, double *const *rh) {
+    ora_set_bc(0);
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    if (ora_tables(P->M, tau, Q, S, dtau)) return -1.0;
+    return residual_fields(P, tau, Q, t_n, u, NULL, rh);
+}
+
+static ora_problem coarse_problem(const ora_problem *P, double **Gc) {
+    ora_problem Pc = *P;
+    Pc.n = (P->n - 1) / 2;
+    *Gc = NULL;
+    if (P->fe == FE_FORCING) {
+        *Gc = malloc(npts(P->dim, Pc.n) * sizeof(double));
+        ora_inject(P->dim, P->n, P->G, *Gc);
+        Pc.G = *Gc;
+    }
+    return Pc;
+}
+
+/* Phase B: Ub_j = U_j = R_i u_j (j = 0..M-1); fas_m = r~_H(Ub)_m - R_fw rh_m (m = 1..M-1). */
+void ora_pf_restrict(const ora_problem *P, double t_n, double *const *u, double *const *rh,
+                     double *const *Ub, double *const *U, double *const *fas) {
+    ora_set_bc(0);
+    int d = P->dim, M = P->M;
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    ora_tables(M, tau, Q, S, dtau);
+    double *Gc;
+    ora_problem Pc = coarse_problem(P, &Gc);
+    size_t NPc = npts(d, Pc.n);
+    double *rH[32] = {0}, *tc = malloc(NPc * sizeof(double));
+    for (int j = 0; j < M; ++j) {
+        ora_inject(d, P->n, u[j], Ub[j]);
+        memcpy(U[j], Ub[j], NPc * sizeof(double));
+        rH[j] = malloc(NPc * sizeof(double));
+    }
+    residual_fields(&Pc, tau, Q, t_n, Ub, NULL, rH);
+    for (int m = 1; m < M; ++m) {
+        ora_restrict(d, P->n, rh[m], tc);
+        for (size_t p = 0; p < NPc; ++p) fas[m][p] = rH[m][p] - tc[p];
+    }
+    for (int j = 0; j < M; ++j) free(rH[j]);
+    free(tc); free(Gc);
+}
+
+/* Phase C: U_0 <- U0 (when U0 is not NULL), then coarse_sweeps coarse ISDC sweeps of the
+ * FAS-corrected coarse problem, in place in U.  Returns the coarse V-cycles. */
+long ora_pf_coarse(const ora_problem *P, int coarse_sweeps, double t_n, const double *U0,
+                   double *const *U, double *const *fas) {
+    ora_set_bc(0);
+    int M = P->M;
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    ora_tables(M, tau, Q, S, dtau);
+    double *Gc;
+    ora_problem Pc = coarse_problem(P, &Gc);
+    size_t NPc = npts(P->dim, Pc.n);
+    if (U0) memcpy(U[0], U0, NPc * sizeof(double));
+    double *V[32], *cu[32], *cn[32];
+    for (int j = 0; j < M; ++j) { V[j] = (j == 0) ? U[0] : malloc(NPc * sizeof(double)); cu[j] = U[j]; cn[j] = V[j]; }
+    long cvc = 0;
+    for (int sw = 0; sw < coarse_sweeps; ++sw) {
+        int cyc[32];
+        sweep_fas(&Pc, tau, S, dtau, t_n, cu, cn, cyc, fas);
+        for (int m = 0; m + 1 < M; ++m) cvc += cyc[m];
+        for (int j = 1; j < M; ++j) { double *t = cu[j]; cu[j] = cn[j]; cn[j] = t; }
+    }
+    for (int j = 1; j < M; ++j)
+        if (cu[j] != U[j]) memcpy(U[j], cu[j], NPc * sizeof(double));
+    for (int j = 1; j < M; ++j) free(V[j]);
+    free(Gc);
+    return cvc;
+}
+
+/* Phase D: u_j <- u_j + P4(U_j - Ub_j), j = 1..M-1. */
+void ora_pf_interpolate(const ora_problem *P, double *const *U, double *const *Ub, double *const *u) {
+    ora_set_bc(0);
+    int d = P->dim, nc = (P->n - 1) / 2;
+    size_t NPc = npts(d, nc);
+    double *ec = malloc(NPc * sizeof(double));
+    for (int j = 1; j < P->M; ++j) {
+        for (size_t p = 0; p < NPc; ++p) ec[p] = U[j][p] - Ub[j][p];
+        ora_prolong4_add(d, nc, ec, u[j]);
+    }
+    free(ec);
+}
+
+/* One PFASST block.  u0 (in/out): the block's initial value; on return the fine end value of the
+ * last slice.  res_hist[k*nslices + p] = slice p's residual after the fine sweep of iteration
+ * k+1 (capacity kmax*nslices); uend (nullable, nslices*n^d): every slice's fine end value.
+ * Returns 0, -2 for an unsupported problem. */
+int ora_pfasst_block(const ora_problem *P, int nslices, int coarse_sweeps, int predictor, double *u0,
+                     int step0, int *iters, long *vcycles, long *cvcycles, double *res_hist,
+                     int *converged, double *uend) {
+    ora_set_bc(0);
+    if (P->bc != 0 || P->n < 7 || P->mode != 0 || P->res_kind != 0 || nslices < 1 || nslices > 64) return -2;
+    int d = P->dim, M = P->M, NS = nslices, nc = (P->n - 1) / 2;
+    size_t NP = npts(d, P->n), NPc = npts(d, nc);
+    double **A = malloc((size_t)NS * M * sizeof(double *)), **Bf = malloc((size_t)NS * M * sizeof(double *));
+    double **RH = malloc((size_t)NS * M * sizeof(double *)), **UB = malloc((size_t)NS * M * sizeof(double *));
+    double **UC = malloc((size_t)NS * M * sizeof(double *)), **FS = malloc((size_t)NS * M * sizeof(double *));
+    double *E = malloc((size_t)NS * NP * sizeof(double));
+    for (int p = 0; p < NS; ++p)
+        for (int j = 0; j < M; ++j) {
+            int q = p * M + j;
+            A[q] = malloc(NP * sizeof(double));
+            memcpy(A[q], u0, NP * sizeof(double));
+            Bf[q] = (j == 0) ? A[q] : malloc(NP * sizeof(double));
+            RH[q] = malloc(NP * sizeof(double));
+            UB[q] = malloc(NPc * sizeof(double));
+            UC[q] = malloc(NPc * sizeof(double));
+            FS[q] = calloc(NPc, sizeof(double));
+        }
+    double **uold = A, **unew = Bf;   /* per slice: uold + p*M, unew + p*M (swapped together) */
+    long vc = 0, cvc = 0;
+    double tau[32], Q[32 * 32], S[32 * 32], dtau[32];
+    ora_tables(M, tau, Q, S, dtau);
+#define TN(p) ((double)(step0 + (p)) * P->dt)
+    if (predictor) {
+        for (int p = 0; p < NS; ++p) {
+            residual_fields(P, tau, Q, TN(p), uold + p * M, NULL, RH + p * M);
+            ora_pf_restrict(P, TN(p), uold + p * M, RH + p * M, UB + p * M, UC + p * M, FS + p * M);
+        }
+        for (int s = 0; s < NS; ++s)
+            for (int p = NS - 1; p >= s; --p)   /* descending: slice p-1 still holds its stage s-1 value */
+                cvc += ora_pf_coarse(P, coarse_sweeps, TN(p), s >= 1 ? UC[(p - 1) * M + M - 1] : NULL,
+                                     UC + p * M, FS + p * M);
+        for (int p = 0; p < NS; ++p) ora_pf_interpolate(P, UC + p * M, UB + p * M, uold + p * M);
+    }
+    int kmax = P->fixed_sweeps > 0 ? P->fixed_sweeps : P->max_sweeps;
+    int k = 0, conv = 0;
+    while (k < kmax) {
+        for (int p = 0; p < NS; ++p) memcpy(E + p * NP, uold[p * M + M - 1], NP * sizeof(double));  /* 1. */
+        for (int p = 1; p < NS; ++p) memcpy(uold[p * M], E + (p - 1) * NP, NP * sizeof(double));
+        double res = 0.0;
+        for (int p = 0; p < NS; ++p) {                                                                /* 2. */
+            double r = ora_pf_fine(P, TN(p), uold + p * M, unew + p * M, RH + p * M, &vc);
+            if (res_hist) res_hist[k * NS + p] = r;
+            if (r > res || isinf(r) || isnan(r)) res = r;
+        }
+        ++k;
+        double **t = uold; uold = unew; unew = t;
+        if (P->fixed_sweeps <= 0 && res < P->sweep_tol) { conv = 1; break; }                        /* 3. */
+        if (k >= kmax) break;
+        for (int p = 0; p < NS; ++p)                                                                  /* 4. */
+            ora_pf_restrict(P, TN(p), uold + p * M, RH + p * M, UB + p * M, UC + p * M, FS + p * M);
+        for (int p = 0; p < NS; ++p)                                                                  /* 5. */
+            cvc += ora_pf_coarse(P, coarse_sweeps, TN(p), p >= 1 ? UC[(p - 1) * M + M - 1] : NULL, UC + p * M, FS + p * M);
+        for (int p = 0; p < NS; ++p) ora_pf_interpolate(P, UC + p * M, UB + p * M, uold + p * M);  /* 6. */
+    }
+#undef TN
+    if (P->fixed_sweeps > 0) conv = 1;
+    memcpy(u0, uold[(NS - 1) * M + M - 1], NP * sizeof(double));
+    if (uend)
+        for (int p = 0; p < NS; ++p) memcpy(uend + p * NP, uold[p * M + M - 1], NP * sizeof(double));
+    for (int q = 0; q < NS * M; ++q) {
+        if (q % M) free(Bf[q]);
+        free(A[q]); free(RH[q]); free(UB[q]); free(UC[q]); free(FS[q]);
+    }
+    free(A); free(Bf); free(RH); free(UB); free(UC); free(FS); free(E);
+    *iters = k; *vcycles = vc; *cvcycles = cvc; *converged = conv;
+    return 0;
+}

@@ -19,7 +19,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # bench.py kernel classes -> kernel-name patterns (the fine level is the launch with the largest grid)
 CLASS_PATTERNS = {
-    "fine_smoother": [r"f3d::k_smooth2<\d+, 0,"],
+    "fine_smoother": [r"f3d::k_smooth2<\d+, 0,", r"f3d::k_smooth2ws<0>"],
     "fine_defect_restrict": [r"f3d::k_restrict", r"f2d::k_smooth2r<0,"],
     "fine_prolong_correct": [r"f3d::k_prolong", r"f2d::k_smooth2<false, 2,", r"f2d::k_smooth2<0, 2,"],
     "residual": [r"k_resid", r"f3d::k_bl<\d+, 1,"],
