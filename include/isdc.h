@@ -187,6 +187,28 @@ isdc_status residual_norm(isdc_handle h, double *per_node, double *max_norm);
 isdc_status isdc_get_solution(isdc_handle h, int node, double *out_dev);
 isdc_status isdc_get_solution_host(isdc_handle h, int node, double *out_host);
 
+/* ---- PFASST slice operations (NEXT f4b; "SDC sweeps on multiple levels combined with
+ * a forward transfer of updated initial values in a manner similar to Parareal ... only a single
+ * SDC sweep is performed" per level and iteration; reading R33) ------------------------
+ * A PFASST time slice is a handle with mlsdc_levels = 2 (ISDC_ERR_INVALID_ARG otherwise).  A block
+ * starts with isdc_set_initial (the block's u0 spread, the slice's step index); then, per R33:
+ *   isdc_pfasst_restrict     phase B: fine residual fields of the current iterate (predictor: the
+ *                            spread state), injection Ubar_j = U_j = R_i u_j, FAS correction
+ *   isdc_pfasst_coarse       phase C: coarse node 0 <- U0 (dense n_c^d device field; NULL keeps it),
+ *                            coarse_sweeps coarse ISDC sweeps, the coarse end value U_M -> Uend
+ *                            (dense device, nullable), the coarse V-cycles -> *coarse_vcycles
+ *   isdc_pfasst_interpolate  phase D: u_j += P4(U_j - Ubar_j), j = 1..M-1; the fine end value
+ *                            u_M -> uend (dense n^d device, nullable)
+ *   isdc_pfasst_set_u0       step 1: node 0 of the fine iterate <- u0 (dense device), in both iterate
+ *                            sets (the forward transfer)
+ *   isdc_sweep               phase A: one fine ISDC sweep + the fine weighted residual
+ * Calls with device outputs synchronise the handle's stream before returning.  The caller moves the
+ * dense end values between slices (on one GPU, or between ranks: paper_1401_7824_b200/pfasst.py). */
+isdc_status isdc_pfasst_set_u0(isdc_handle h, const double *u0_dev);
+isdc_status isdc_pfasst_restrict(isdc_handle h);
+isdc_status isdc_pfasst_coarse(isdc_handle h, const double *U0_dev, double *Uend_dev, long *coarse_vcycles);
+isdc_status isdc_pfasst_interpolate(isdc_handle h, double *uend_dev);
+
 /* Load a full node state u[0..M-1] (dense device fields; used by parity tests). */
 isdc_status isdc_set_state(isdc_handle h, const double *const *u_dev, int step_index);
 

@@ -392,6 +392,7 @@ class PfasstSlice:
         self.fas = [np.zeros((nc,) * d) for _ in range(M)]
         self.vcycles = 0
         self.coarse_vcycles = 0
+        self.fine_shape, self.coarse_shape, self.wants_torch = (n,) * d, (nc,) * d, False
 
     def set_u0(self, u0):
         self.u0[...] = u0

@@ -1654,15 +1654,34 @@ isdc_status residual_fields(isdc_ctx *h, double *const *u, double *const *F, dou
     return ISDC_OK;
 }
 
-isdc_status mlsdc_correct(isdc_ctx *h) {
+// The current iterate as node-field pointers (spread: every node reads u_0).
+static void node_fields(isdc_ctx *h, double **u, double **F) {
+    for (int j = 0; j < h->M; ++j) {
+        u[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
+        F[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
+    }
+}
+
+// Spread state -> explicit node fields u_j = u_0 (PFASST's predictor corrects the nodes in place).
+static isdc_status materialize(isdc_ctx *h) {
+    if (!h->spread) return ISDC_OK;
+    for (int j = 1; j < h->M; ++j) {
+        TRY(copy_field(h, h->U[h->cur][j], h->U[h->cur][0], h->lev[0].g));
+        if (need_F(h)) TRY(copy_field(h, h->Fs[h->cur][j], h->Fs[h->cur][0], h->lev[0].g));
+    }
+    h->spread = false;
+    h->fold_valid[0] = h->fold_valid[1] = false;
+    return ISDC_OK;
+}
+
+// MLSDC / PFASST phase B (R32 steps 2-3, R33): r~_h of the current fine iterate, injection
+// Ubar_j = U_j = R_i u_j into the coarse handle, r~_H(Ubar) and fas_m = r~_H(Ubar)_m - R_fw r~_h,m.
+isdc_status mlsdc_restrict(isdc_ctx *h) {
     isdc_ctx *c = h->coarse;
     const int M = h->M, D = h->d;
     const GridDesc &gf = h->lev[0].g, &gc = c->lev[0].g;
     double *u[ISDC_MAXM], *F[ISDC_MAXM];
-    for (int j = 0; j < M; ++j) {
-        u[j] = h->spread ? h->U[h->cur][0] : h->U[h->cur][j];
-        F[j] = h->spread ? h->Fs[h->cur][0] : h->Fs[h->cur][j];
-    }
+    node_fields(h, u, F);
     TRY(residual_fields(h, u, F, h->RF));                                   // r~_h,m
     const dim3 cg = (D == 2) ? point_grid<2>(gc, kBlk) : point_grid<3>(gc, kBlk);
     for (int j = 0; j < M; ++j) {                                            // Ubar_j = R_i u_j
@@ -1685,16 +1704,34 @@ isdc_status mlsdc_correct(isdc_ctx *h) {
         else kl(h, k_fas<3>, cg, kBlk, 0)(h->FAS[m], gc, h->RC[m], h->RF[m], gf);
         LAUNCH_CHECK(h);
     }
-    c->fas_in = h->FAS;                                                      // coarse sweeps
+    return ISDC_OK;
+}
+
+// Phase C (R32 step 4, R33): coarse_sweeps coarse ISDC sweeps with b + (fas_{m+1} - fas_m).
+isdc_status mlsdc_coarse_sweeps(isdc_ctx *h) {
+    isdc_ctx *c = h->coarse;
+    c->fas_in = h->FAS;
     c->skip_residual = true;
     for (int s = 0; s < h->P.coarse_sweeps; ++s) {
         const long l0 = c->launches;
         TRY(enqueue_isdc_sweep(c));
         h->launches += c->launches - l0;
         c->cur = 1 - c->cur;
-        h->cvcyc += (long)(M - 1) * c->P.solve.L;
+        h->cvcyc += (long)(h->M - 1) * c->P.solve.L;
     }
-    for (int j = 1; j < M; ++j) {                                            // u_j += P4 (U_j - Ubar_j)
+    return ISDC_OK;
+}
+
+// Phase D (R32 step 5, R33): u_j += P4 (U_j - Ubar_j), j = 1..M-1 (4th-order interpolation).
+isdc_status mlsdc_interpolate(isdc_ctx *h) {
+    isdc_ctx *c = h->coarse;
+    const int M = h->M, D = h->d;
+    const GridDesc &gf = h->lev[0].g, &gc = c->lev[0].g;
+    TRY(materialize(h));
+    double *u[ISDC_MAXM], *F[ISDC_MAXM];
+    node_fields(h, u, F);
+    const dim3 cg = (D == 2) ? point_grid<2>(gc, kBlk) : point_grid<3>(gc, kBlk);
+    for (int j = 1; j < M; ++j) {
         const dim3 bx(32, 8, 1);
         h->launches += (D == 2) ? 3 : 4;
         if (D == 2) {
@@ -1712,6 +1749,12 @@ isdc_status mlsdc_correct(isdc_ctx *h) {
     }
     h->fold_valid[h->cur] = false;
     return ISDC_OK;
+}
+
+isdc_status mlsdc_correct(isdc_ctx *h) {
+    TRY(mlsdc_restrict(h));
+    TRY(mlsdc_coarse_sweeps(h));
+    return mlsdc_interpolate(h);
 }
 
 // Insert a conditional WHILE node into the graph being captured on h->s: `test` (a kernel launch
@@ -2469,6 +2512,46 @@ isdc_status isdc_set_initial_host(isdc_handle h, const double *u0, int step_inde
     h->cur = 0; h->spread = true; h->step_index = step_index;
     h->fold_valid[0] = h->fold_valid[1] = false;
     return upload_ct(h);
+}
+
+// ---- PFASST slice operations (NEXT f4b; reading R33) --------------------
+static bool pfasst_ok(isdc_ctx *h) { return h && h->coarse && h->P.mlsdc_levels == 2; }
+
+isdc_status isdc_pfasst_set_u0(isdc_handle h, const double *u0) {
+    if (!pfasst_ok(h) || !u0) return ISDC_ERR_INVALID_ARG;
+    TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyDeviceToDevice));   // node 0 is one buffer
+    TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
+    h->fold_valid[0] = h->fold_valid[1] = false;
+    return ISDC_OK;
+}
+
+isdc_status isdc_pfasst_restrict(isdc_handle h) {
+    if (!pfasst_ok(h)) return ISDC_ERR_INVALID_ARG;
+    return mlsdc_restrict(h);
+}
+
+isdc_status isdc_pfasst_coarse(isdc_handle h, const double *U0, double *Uend, long *coarse_vcycles) {
+    if (!pfasst_ok(h)) return ISDC_ERR_INVALID_ARG;
+    isdc_ctx *c = h->coarse;
+    if (U0) {
+        TRY(dense_to_pitched(c, c->U[0][0], U0, cudaMemcpyDeviceToDevice));
+        TRY(launch_fe(c, c->Fs[0][0], c->U[0][0]));
+        c->fold_valid[0] = c->fold_valid[1] = false;
+    }
+    const long v0 = h->cvcyc;
+    TRY(mlsdc_coarse_sweeps(h));
+    if (coarse_vcycles) *coarse_vcycles = h->cvcyc - v0;
+    if (Uend) TRY(pitched_to_dense(c, Uend, c->U[c->cur][h->M - 1], cudaMemcpyDeviceToDevice));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    return ISDC_OK;
+}
+
+isdc_status isdc_pfasst_interpolate(isdc_handle h, double *uend) {
+    if (!pfasst_ok(h)) return ISDC_ERR_INVALID_ARG;
+    TRY(mlsdc_interpolate(h));
+    if (uend) TRY(pitched_to_dense(h, uend, h->U[h->cur][h->M - 1], cudaMemcpyDeviceToDevice));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s));
+    return ISDC_OK;
 }
 
 isdc_status isdc_set_state(isdc_handle h, const double *const *u, int step_index) {

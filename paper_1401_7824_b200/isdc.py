@@ -87,6 +87,10 @@ def lib():
         L.isdc_kernel_launches.argtypes = [_vp]
         L.isdc_kernel_launches.restype = C.c_long
         L.isdc_destroy.argtypes = [_vp]
+        L.isdc_pfasst_set_u0.argtypes = [_vp, _vp]
+        L.isdc_pfasst_restrict.argtypes = [_vp]
+        L.isdc_pfasst_coarse.argtypes = [_vp, _vp, _vp, C.POINTER(C.c_long)]
+        L.isdc_pfasst_interpolate.argtypes = [_vp, _vp]
         L.isdc_last_error.argtypes = [_vp]
         L.isdc_last_error.restype = C.c_char_p
         L.isdc_profile_enable.argtypes = [_vp, C.c_int]
@@ -289,6 +293,45 @@ class ISDC:
         arr = (_vp * self.M)(*[t.data_ptr() for t in ts])
         self.set_initial(un, step_index)
         self._check(self.L.isdc_rhs(self.h, m, arr, un.data_ptr(), out.data_ptr()))
+        return out
+
+    # ------------------------------------------------------------------ PFASST slice (R33)
+    def coarse_n(self) -> int:
+        return (self.n - 1) // 2
+
+    def pfasst_set_u0(self, u0):
+        """Forward transfer (R33 step 1): node 0 of the fine iterate <- u0 (dense device field)."""
+        t = self._field(u0)
+        self._check(self.L.isdc_pfasst_set_u0(self.h, t.data_ptr()))
+
+    def pfasst_restrict(self):
+        """Phase B: injection + FAS from the current fine iterate (the spread state in the predictor)."""
+        self._check(self.L.isdc_pfasst_restrict(self.h))
+
+    def pfasst_coarse(self, U0=None, out: Optional[torch.Tensor] = None):
+        """Phase C: coarse node 0 <- U0 (dense n_c^d, None keeps it), coarse sweeps; returns (coarse
+        end value, coarse V-cycles)."""
+        nc = self.coarse_n()
+        ptr = None
+        if U0 is not None:
+            t = torch.as_tensor(U0, dtype=torch.float64).to(self.device).contiguous()
+            if tuple(t.shape) != (nc,) * self.dim:
+                raise ValueError(f"coarse field shape {tuple(t.shape)} != {(nc,) * self.dim}")
+            cur = torch.cuda.current_stream(self.device)
+            if cur.cuda_stream != self.stream.cuda_stream:
+                self.stream.wait_stream(cur)
+                t.record_stream(self.stream)
+            ptr, self._U0_keep = t.data_ptr(), t
+        out = torch.empty((nc,) * self.dim, dtype=torch.float64, device=self.device) if out is None else out
+        cv = C.c_long(0)
+        self._check(self.L.isdc_pfasst_coarse(self.h, ptr, out.data_ptr(), C.byref(cv)))
+        return out, cv.value
+
+    def pfasst_interpolate(self, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Phase D: u_j += P4(U_j - Ubar_j); returns the fine end value u_M (dense device field)."""
+        out = self.empty_field() if out is None else out
+        self._check_shape(out)
+        self._check(self.L.isdc_pfasst_interpolate(self.h, out.data_ptr()))
         return out
 
     def profile(self, level: int = 1):
