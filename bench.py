@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--mode", choices=["isdc", "sdc"], default="isdc")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--extra", type=str, default="3", help="comma-separated extra configs measured in the same run")
+    ap.add_argument("--pfasst", type=int, default=4, help="slices of the one-GPU PFASST block in 'extra' (0: off)")
+    ap.add_argument("--pfasst-config", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
@@ -414,6 +416,65 @@ def measure(pk, torch, a, cid, rank, world, local, barrier, reduce_max, with_e2e
     return line
 
 
+def measure_pfasst(pk, torch, cid, P, seed=0):
+    """PFASST (NEXT f4b, R33) on ONE GPU: a block of P time slices of config cid, every slice an
+    MLSDC handle on the same stream, scheduled by the product driver's one-GPU transport (the
+    slices run one after another).  Reported: the block's device time (CUDA events around the
+    block, after an identical warm-up block), its iterations and sweeps, and the same P steps as
+    serial single-level ISDC steps for comparison.  `model_p_gpu_ms` is a MODEL, not a measurement:
+    the block's critical path on P GPUs = predictor (P coarse stages) + iterations x (one fine sweep
+    + P chained coarse sweeps), from the measured per-phase times (transfers not included)."""
+    from paper_1401_7824_b200 import pfasst
+    cfg, u0, G = synth.problem_inputs(cid, seed)
+    Gt = None if G is None else torch.from_numpy(G)
+    stream = torch.cuda.current_stream()
+    hs = [pk.ISDC.from_config(cfg, Gt, mode=synth.MODE_ISDC, mlsdc_levels=2, coarse_sweeps=1) for _ in range(P)]
+    u0d = torch.from_numpy(u0).cuda()
+    kw = dict(max_iters=cfg.max_sweeps, fixed_iters=cfg.fixed_sweeps, tol=cfg.sweep_tol, predictor=True)
+
+    def block():
+        sl = [pfasst.CudaSlice(hs[p], u0d, p) for p in range(P)]
+        return sl, pfasst.run_block_local(sl, **kw)
+
+    block()                                   # warm-up (graph capture)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sl, out = block()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    blk_ms = e0.elapsed_time(e1)
+    it = out[0].iterations
+    # per-phase device times on slice P-1 (fine sweep; coarse sweep) for the critical-path model
+    h = hs[-1]
+    f0, f1, c1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    f0.record(stream); h.sweep(); f1.record(stream)
+    h.pfasst_restrict(); h.pfasst_coarse(None); c1.record(stream)
+    torch.cuda.synchronize()
+    t_fine, t_coarse = f0.elapsed_time(f1), f1.elapsed_time(c1)
+    # the same P steps as serial single-level ISDC steps
+    hi = pk.ISDC.from_config(cfg, Gt, mode=synth.MODE_ISDC)
+    hi.set_initial(u0d, 0); hi.step(); torch.cuda.synchronize()
+    hi.set_initial(u0d, 0)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    ser = [hi.step() for _ in range(P)]
+    s1.record(stream)
+    torch.cuda.synchronize()
+    ser_ms = s0.elapsed_time(s1)
+    res = {"workload": WORKLOAD[cid], "slices": P, "block_ms_1gpu": blk_ms, "iterations": it,
+           "converged": out[0].converged, "fine_sweeps": P * it, "vcycles": sum(o.vcycles for o in out),
+           "coarse_vcycles": sum(o.coarse_vcycles for o in out),
+           "serial_isdc_ms": ser_ms, "serial_isdc_sweeps": sum(s["sweeps"] for s in ser),
+           "fine_sweep_ms": t_fine, "restrict_coarse_ms": t_coarse,
+           "model_p_gpu_ms": P * t_coarse + it * (t_fine + P * t_coarse),
+           "note": "1 GPU runs the P slices one after another; model_p_gpu_ms is a critical-path MODEL "
+                   "(P GPUs, transfers excluded), not a measurement"}
+    del sl, hs, hi
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -453,6 +514,8 @@ def main():
                                                  "vcycles_per_step", "point_updates_per_s", "step_alg_GBps",
                                                  "step_alg_frac_of_peak", "roofline", "kernels", "clocks",
                                                  "gpu_launches", "config")}
+    if a.pfasst > 1 and world == 1:
+        extra["pfasst"] = measure_pfasst(pk, torch, a.pfasst_config, a.pfasst)
     if rank == 0:
         line = {"metric": METRIC, "value": main_line["value"], "unit": "steps/s", "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": main_line["ms_per_step"], "higher_is_better": True,

@@ -24,6 +24,13 @@
 #include "kernels_ptail.cuh"
 #include "kernels_mlsdc.cuh"
 #include "tables.h"
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX ranges around the public calls (visible in Nsight timelines; no cost without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Device-side node-solve loop of the SDC / capped-ISDC modes (one CUDA graph per sweep): the
 // defect test of node_solve runs in k_sdc_test, which drives a conditional WHILE node.
@@ -171,6 +178,7 @@ struct isdc_ctx {
     int rs_chunk_mul = 16;     // ISDC_RS_CHUNK: row chunks ~ this x SMs / column tiles
     bool ws3d = true;          // ISDC_WS3D: warp-specialised 3D smoother on levels n >= ws3d_min
     int ws3d_min = 63;         // ISDC_WS3D_MIN
+    int ws_ns = 6;             // ISDC_WS_NS: TMA stages of the ws smoother (experiment)
     bool fuse3d = false;       // ISDC_FUSE3D: 3D prolongation fused into the post-smoother (needs ws3d;
                                // bitwise equal, measured slower: 1.34 ms vs 0.42 + 0.77 ms at 511^3)
     int tail3d = 15;           // largest 3D level handled by the single-CTA tail (fast kernels above)
@@ -617,6 +625,13 @@ isdc_status launch_smooth2_3d_ws(isdc_ctx *h, double *out, const double *in, con
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
     if (e) kl(h, f3d::k_smooth2ws<2>, grd, f3d::WSCfg<2>::NT, f3d::WSCfg<2>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    else if (h->ws_ns == 8) {
+        if (!in) kl(h, f3d::k_smooth2ws<1, 8>, grd, f3d::WSCfg<1, 8>::NT, f3d::WSCfg<1, 8>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+        else kl(h, f3d::k_smooth2ws<0, 8>, grd, f3d::WSCfg<0, 8>::NT, f3d::WSCfg<0, 8>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    } else if (h->ws_ns == 10) {
+        if (!in) kl(h, f3d::k_smooth2ws<1, 10>, grd, f3d::WSCfg<1, 10>::NT, f3d::WSCfg<1, 10>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+        else kl(h, f3d::k_smooth2ws<0, 10>, grd, f3d::WSCfg<0, 10>::NT, f3d::WSCfg<0, 10>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    }
     else if (!in) kl(h, f3d::k_smooth2ws<1>, grd, f3d::WSCfg<1>::NT, f3d::WSCfg<1>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     else kl(h, f3d::k_smooth2ws<0>, grd, f3d::WSCfg<0>::NT, f3d::WSCfg<0>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     // algorithmic bytes: read u (unless zero), b (+ e / 8); write u''
@@ -2257,6 +2272,8 @@ bool kernel_attrs(isdc_ctx *h) {
     set((const void *)f3d::k_smooth2<3, 0, 12>); set((const void *)f3d::k_smooth2<3, 1, 12>);
     set((const void *)f3d::k_smooth2<4, 0, 8>); set((const void *)f3d::k_smooth2<4, 1, 8>);
     set((const void *)f3d::k_smooth2ws<0>); set((const void *)f3d::k_smooth2ws<1>); set((const void *)f3d::k_smooth2ws<2>);
+    set((const void *)f3d::k_smooth2ws<0, 8>); set((const void *)f3d::k_smooth2ws<1, 8>);
+    set((const void *)f3d::k_smooth2ws<0, 10>); set((const void *)f3d::k_smooth2ws<1, 10>);
     set((const void *)f3d::k_restrict);
     set((const void *)f3d::k_fe_cd4);
     auto setbl = [&](auto F) {
@@ -2349,6 +2366,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *rn = getenv("ISDC_RS_NS")) h->rs_ns = atoi(rn);
     if (const char *rc = getenv("ISDC_RS_CHUNK")) h->rs_chunk_mul = atoi(rc);
     if (const char *w3m = getenv("ISDC_WS3D_MIN")) h->ws3d_min = atoi(w3m);
+    if (const char *wn = getenv("ISDC_WS_NS")) h->ws_ns = atoi(wn);
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
@@ -2526,11 +2544,13 @@ isdc_status isdc_pfasst_set_u0(isdc_handle h, const double *u0) {
 }
 
 isdc_status isdc_pfasst_restrict(isdc_handle h) {
+    NvtxRange nvtx_("isdc_pfasst_restrict");
     if (!pfasst_ok(h)) return ISDC_ERR_INVALID_ARG;
     return mlsdc_restrict(h);
 }
 
 isdc_status isdc_pfasst_coarse(isdc_handle h, const double *U0, double *Uend, long *coarse_vcycles) {
+    NvtxRange nvtx_("isdc_pfasst_coarse");
     if (!pfasst_ok(h)) return ISDC_ERR_INVALID_ARG;
     isdc_ctx *c = h->coarse;
     if (U0) {
@@ -2547,6 +2567,7 @@ isdc_status isdc_pfasst_coarse(isdc_handle h, const double *U0, double *Uend, lo
 }
 
 isdc_status isdc_pfasst_interpolate(isdc_handle h, double *uend) {
+    NvtxRange nvtx_("isdc_pfasst_interpolate");
     if (!pfasst_ok(h)) return ISDC_ERR_INVALID_ARG;
     TRY(mlsdc_interpolate(h));
     if (uend) TRY(pitched_to_dense(h, uend, h->U[h->cur][h->M - 1], cudaMemcpyDeviceToDevice));
@@ -2592,11 +2613,13 @@ isdc_status isdc_get_tables(isdc_handle h, double *tau, double *Q, double *S, do
 }
 
 isdc_status isdc_sweep(isdc_handle h, double *res_per_node, double *res_max, int *cycles) {
+    NvtxRange nvtx_("isdc_sweep");
     if (!h) return ISDC_ERR_INVALID_ARG;
     return sweep_impl(h, res_per_node, res_max, cycles, nullptr);
 }
 
 isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, int *node_cycles) {
+    NvtxRange nvtx_("isdc_step");
     if (!h) return ISDC_ERR_INVALID_ARG;
     const isdc_solve_opts &o = h->P.solve;
     int kmax = o.fixed_sweeps > 0 ? o.fixed_sweeps : o.max_sweeps;
@@ -2672,12 +2695,14 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
 }
 
 isdc_status isdc_run(isdc_handle h, int nsteps, isdc_step_stats *stats) {
+    NvtxRange nvtx_("isdc_run");
     if (!h || nsteps < 0) return ISDC_ERR_INVALID_ARG;
     for (int s = 0; s < nsteps; ++s) TRY(isdc_step(h, stats ? stats + s : nullptr, nullptr, nullptr));
     return ISDC_OK;
 }
 
 isdc_status mg_vcycle(isdc_handle h, int node_m, const double *b, double *u, double *dbefore, double *dafter) {
+    NvtxRange nvtx_("mg_vcycle");
     if (!h || !b || !u || node_m < 0 || node_m >= h->M - 1) return ISDC_ERR_INVALID_ARG;
     const GridDesc &g = h->lev[0].g;
     // stage into pitched scratch: Bf <- b, V <- u
@@ -2701,6 +2726,7 @@ isdc_status mg_vcycle(isdc_handle h, int node_m, const double *b, double *u, dou
 }
 
 isdc_status residual_norm(isdc_handle h, double *per_node, double *max_norm) {
+    NvtxRange nvtx_("residual_norm");
     if (!h) return ISDC_ERR_INVALID_ARG;
     double *u[ISDC_MAXM], *F[ISDC_MAXM];
     for (int j = 0; j < h->M; ++j) {

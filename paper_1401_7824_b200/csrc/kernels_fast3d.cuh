@@ -245,9 +245,9 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__
 constexpr int WS_SR = 4, WS_GW = 8;                 // rows per thread, warps per sweep group
 constexpr int WS_EW = 20, WS_EH = 18;               // coarse boxes (MODE 2)
 constexpr int WS_EPL = a128(WS_EW * WS_EH * 8);
-template <int MODE>
+template <int MODE, int NSX = 0>
 struct WSCfg {
-    static constexpr int NS = MODE == 2 ? 7 : 6;    // stages in use: it - 2 .. it (+ 1 in MODE 2)
+    static constexpr int NS = NSX ? NSX : (MODE == 2 ? 7 : 6);   // TMA stages (>= 3 in use: it - 2 .. it)
     static constexpr int NT = 32 * 2 * WS_GW;
     static constexpr int UPL = S_UPL, BPL = S_BPL, EPL = MODE == 2 ? 2 * WS_EPL : 0;
     static constexpr int SPL = UPL + BPL + EPL;     // one stage: u | b | e(za) | e(za+1)
@@ -295,13 +295,13 @@ __device__ __forceinline__ void ws_prolong_plane(double *U, const double *Ea, co
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(WSCfg<MODE>::NT, 1) k_smooth2ws(const __grid_constant__ CUtensorMap tu,
+template <int MODE, int NSX = 0>
+__global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __grid_constant__ CUtensorMap tu,
                                                                  const __grid_constant__ CUtensorMap tb,
                                                                  const __grid_constant__ CUtensorMap te,
                                                                  double *__restrict__ out, int n, int pitch,
                                                                  long long plane, SCoef c, int zc) {
-    using W = WSCfg<MODE>;
+    using W = WSCfg<MODE, NSX>;
     constexpr int NS = W::NS, SR = WS_SR;
     constexpr bool ZERO = MODE == 1, PRO = MODE == 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
