@@ -157,6 +157,9 @@ __device__ __forceinline__ double fe_at(const FeDesc &fe, const double *u, const
 
 // ---- named barrier over `count` threads (warp-specialised kernels: the roles reach it from
 // different code locations; count is a multiple of 32)
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }

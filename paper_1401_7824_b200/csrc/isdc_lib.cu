@@ -178,7 +178,6 @@ struct isdc_ctx {
     int rs_chunk_mul = 16;     // ISDC_RS_CHUNK: row chunks ~ this x SMs / column tiles
     bool ws3d = true;          // ISDC_WS3D: warp-specialised 3D smoother on levels n >= ws3d_min
     int ws3d_min = 63;         // ISDC_WS3D_MIN
-    int ws_ns = 6;             // ISDC_WS_NS: TMA stages of the ws smoother (experiment)
     bool fuse3d = false;       // ISDC_FUSE3D: 3D prolongation fused into the post-smoother (needs ws3d;
                                // bitwise equal, measured slower: 1.34 ms vs 0.42 + 0.77 ms at 511^3)
     int tail3d = 15;           // largest 3D level handled by the single-CTA tail (fast kernels above)
@@ -223,6 +222,7 @@ struct isdc_ctx {
     // two-level MLSDC (NEXT f4, R32): the fine handle owns a coarse handle on n_c
     struct isdc_ctx *coarse = nullptr;
     double *RF[ISDC_MAXM] = {};    // fine residual fields r~_h,m (m = 1..M-1 at RF[m])
+    bool rf_valid = false;         // RF holds the residual fields of the current iterate (2D fast path)
     double *UB[ISDC_MAXM] = {};    // coarse: restricted iterate Ubar_j
     double *RC[ISDC_MAXM] = {};    // coarse: residual fields r~_H(Ubar)_m
     double *FAS[ISDC_MAXM] = {};   // coarse: FAS correction fas_m (FAS[0] unused = 0)
@@ -625,13 +625,6 @@ isdc_status launch_smooth2_3d_ws(isdc_ctx *h, double *out, const double *in, con
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
     if (e) kl(h, f3d::k_smooth2ws<2>, grd, f3d::WSCfg<2>::NT, f3d::WSCfg<2>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
-    else if (h->ws_ns == 8) {
-        if (!in) kl(h, f3d::k_smooth2ws<1, 8>, grd, f3d::WSCfg<1, 8>::NT, f3d::WSCfg<1, 8>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
-        else kl(h, f3d::k_smooth2ws<0, 8>, grd, f3d::WSCfg<0, 8>::NT, f3d::WSCfg<0, 8>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
-    } else if (h->ws_ns == 10) {
-        if (!in) kl(h, f3d::k_smooth2ws<1, 10>, grd, f3d::WSCfg<1, 10>::NT, f3d::WSCfg<1, 10>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
-        else kl(h, f3d::k_smooth2ws<0, 10>, grd, f3d::WSCfg<0, 10>::NT, f3d::WSCfg<0, 10>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
-    }
     else if (!in) kl(h, f3d::k_smooth2ws<1>, grd, f3d::WSCfg<1>::NT, f3d::WSCfg<1>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     else kl(h, f3d::k_smooth2ws<0>, grd, f3d::WSCfg<0>::NT, f3d::WSCfg<0>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     // algorithmic bytes: read u (unless zero), b (+ e / 8); write u''
@@ -679,6 +672,14 @@ isdc_status launch_smooth2(isdc_ctx *h, double *out, const double *in, const dou
 }
 
 // f^E(u) (CD4 advection) into a stored field (3D fast path), DESIGN.md §6.11
+// MLSDC fine handle in 2D on the TMA-ring residual: the sweep's residual pass also stores the r~_m
+// fields (h->RF), so the FAS restriction does not recompute them
+bool stream2d_ok(const isdc_ctx *h);
+bool mlsdc_rf_fast(const isdc_ctx *h) {
+    return h->P.mlsdc_levels == 2 && h->coarse && h->d == 2 && h->resid2d_tma && h->P.residual_kind == 0 &&
+           !h->skip_residual && stream2d_ok(h);
+}
+
 bool need_F(const isdc_ctx *h) {
     // stored f^E(u_j) fields: 3D CD4 fast kernels; Burgers always (each WENO5 f^E is evaluated
     // once per new node field instead of (M+2)(M-1) + M(M-1) times per sweep)
@@ -1367,6 +1368,8 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
         for (int j = 0; j < ISDC_MAXM; ++j) A.rt[j] = nullptr;
         if (h->P.residual_kind == 1)
             for (int m = 1; m < M; ++m) A.rt[m - 1] = h->RT[m - 1];
+        else if (mlsdc_rf_fast(h))   // MLSDC / PFASST: the fine r~_m fields for the FAS restriction
+            for (int m = 1; m < M; ++m) A.rt[m - 1] = h->RF[m];
         const bool wfo = write_folds && folds2d_on(h);
         A.wfold = nullptr;
         for (int q = 0; q < ISDC_MAXM; ++q) A.wf[q] = nullptr;
@@ -1396,7 +1399,7 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             ++h->launches;
             int pe = prof_begin(h, PROF_RESID);
             const int fe = h->fe.kind;
-            const bool wrt = h->P.residual_kind == 1;
+            const bool wrt = h->P.residual_kind == 1 || mlsdc_rf_fast(h);
             auto go = [&](auto FEc, auto Mc, auto WRTc, auto WFc) {
                 constexpr int FE_ = decltype(FEc)::value, M_ = decltype(Mc)::value;
                 constexpr bool WRT_ = decltype(WRTc)::value, WF_ = decltype(WFc)::value;
@@ -1419,7 +1422,8 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
                 if (M == 3) byfe(std::integral_constant<int, 3>{}, WRTc, WFc);
                 else byfe(std::integral_constant<int, 5>{}, WRTc, WFc);
             };
-            if (wfo) bym(F_{}, T_{});
+            if (wfo && wrt) bym(T_{}, T_{});
+            else if (wfo) bym(F_{}, T_{});
             else if (wrt) bym(T_{}, F_{});
             else bym(F_{}, F_{});
             prof_end(h, pe, PROF_RESID, (M + (fe == 2 ? 1 : 0)) * 8.0 * npts_of(h, g));
@@ -1697,7 +1701,7 @@ isdc_status mlsdc_restrict(isdc_ctx *h) {
     const GridDesc &gf = h->lev[0].g, &gc = c->lev[0].g;
     double *u[ISDC_MAXM], *F[ISDC_MAXM];
     node_fields(h, u, F);
-    TRY(residual_fields(h, u, F, h->RF));                                   // r~_h,m
+    if (!(h->rf_valid && !h->spread)) TRY(residual_fields(h, u, F, h->RF));  // r~_h,m
     const dim3 cg = (D == 2) ? point_grid<2>(gc, kBlk) : point_grid<3>(gc, kBlk);
     for (int j = 0; j < M; ++j) {                                            // Ubar_j = R_i u_j
         h->launches += 2;
@@ -1763,6 +1767,7 @@ isdc_status mlsdc_interpolate(isdc_ctx *h) {
         TRY(launch_fe(h, F[j], u[j]));                                       // stored f^E of the new u_j
     }
     h->fold_valid[h->cur] = false;
+    h->rf_valid = false;
     return ISDC_OK;
 }
 
@@ -2175,6 +2180,7 @@ isdc_status sweep_impl(isdc_ctx *h, double *res_per_node, double *res_max, int *
         h->cur = 1 - h->cur;
         h->spread = false;
         h->fold_valid[h->cur] = folds_on(h);   // the residual stored the folds of the new iterate
+        h->rf_valid = mlsdc_rf_fast(h);        // ... and, for MLSDC in 2D, its r~_m fields
         if (h->graphs && dev_wsolve(h)) {
             TRY(read_wcycles(h));
             return read_residual(h, res_per_node, res_max, true);
@@ -2272,8 +2278,6 @@ bool kernel_attrs(isdc_ctx *h) {
     set((const void *)f3d::k_smooth2<3, 0, 12>); set((const void *)f3d::k_smooth2<3, 1, 12>);
     set((const void *)f3d::k_smooth2<4, 0, 8>); set((const void *)f3d::k_smooth2<4, 1, 8>);
     set((const void *)f3d::k_smooth2ws<0>); set((const void *)f3d::k_smooth2ws<1>); set((const void *)f3d::k_smooth2ws<2>);
-    set((const void *)f3d::k_smooth2ws<0, 8>); set((const void *)f3d::k_smooth2ws<1, 8>);
-    set((const void *)f3d::k_smooth2ws<0, 10>); set((const void *)f3d::k_smooth2ws<1, 10>);
     set((const void *)f3d::k_restrict);
     set((const void *)f3d::k_fe_cd4);
     auto setbl = [&](auto F) {
@@ -2296,6 +2300,8 @@ bool kernel_attrs(isdc_ctx *h) {
         set((const void *)f2d::k_resid_t<F_, 3, false, false, 5>); set((const void *)f2d::k_resid_t<F_, 5, false, false, 5>);
         set((const void *)f2d::k_resid_t<F_, 3, true, false, 5>); set((const void *)f2d::k_resid_t<F_, 5, true, false, 5>);
         set((const void *)f2d::k_resid_t<F_, 3, false, true, 5>); set((const void *)f2d::k_resid_t<F_, 5, false, true, 5>);
+        set((const void *)f2d::k_resid_t<F_, 3, true, true, 3>); set((const void *)f2d::k_resid_t<F_, 5, true, true, 3>);
+        set((const void *)f2d::k_resid_t<F_, 3, true, true, 5>); set((const void *)f2d::k_resid_t<F_, 5, true, true, 5>);
     };
     setrt(std::integral_constant<int, 0>{}); setrt(std::integral_constant<int, 1>{}); setrt(std::integral_constant<int, 2>{});
     set((const void *)k_tail<2>); set((const void *)k_tail<3>);
@@ -2366,7 +2372,6 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *rn = getenv("ISDC_RS_NS")) h->rs_ns = atoi(rn);
     if (const char *rc = getenv("ISDC_RS_CHUNK")) h->rs_chunk_mul = atoi(rc);
     if (const char *w3m = getenv("ISDC_WS3D_MIN")) h->ws3d_min = atoi(w3m);
-    if (const char *wn = getenv("ISDC_WS_NS")) h->ws_ns = atoi(wn);
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
@@ -2519,6 +2524,7 @@ isdc_status isdc_set_initial(isdc_handle h, const double *u0, int step_index) {
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyDeviceToDevice));
     TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
     h->cur = 0; h->spread = true; h->step_index = step_index;
+    h->rf_valid = false;
     h->fold_valid[0] = h->fold_valid[1] = false;
     return upload_ct(h);
 }
@@ -2528,6 +2534,7 @@ isdc_status isdc_set_initial_host(isdc_handle h, const double *u0, int step_inde
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyHostToDevice));
     TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
     h->cur = 0; h->spread = true; h->step_index = step_index;
+    h->rf_valid = false;
     h->fold_valid[0] = h->fold_valid[1] = false;
     return upload_ct(h);
 }
@@ -2540,6 +2547,7 @@ isdc_status isdc_pfasst_set_u0(isdc_handle h, const double *u0) {
     TRY(dense_to_pitched(h, h->U[0][0], u0, cudaMemcpyDeviceToDevice));   // node 0 is one buffer
     TRY(launch_fe(h, h->Fs[0][0], h->U[0][0]));
     h->fold_valid[0] = h->fold_valid[1] = false;
+    h->rf_valid = false;
     return ISDC_OK;
 }
 
@@ -2582,6 +2590,7 @@ isdc_status isdc_set_state(isdc_handle h, const double *const *u, int step_index
         TRY(launch_fe(h, h->Fs[0][j], h->U[0][j]));
     }
     h->cur = 0; h->spread = false; h->step_index = step_index;
+    h->rf_valid = false;
     h->fold_valid[0] = h->fold_valid[1] = false;
     return upload_ct(h);
 }
@@ -2684,6 +2693,7 @@ isdc_status isdc_step(isdc_handle h, isdc_step_stats *stats, double *res_hist, i
     h->cur = 0;
     h->spread = true;
     h->step_index += 1;
+    h->rf_valid = false;
     TRY(upload_ct(h));
     if (stats) {
         stats->sweeps = k; stats->vcycles = vc; stats->cap_hits = caps; stats->converged = conv;
@@ -2757,6 +2767,7 @@ isdc_status isdc_rhs(isdc_handle h, int node_m, const double *const *uold, const
     CUDA_TRY(h, cudaStreamSynchronize(h->s));
     h->spread = true;  // the staged data overwrote the iterate sets
     h->fold_valid[0] = h->fold_valid[1] = false;
+    h->rf_valid = false;
     return ISDC_OK;
 }
 

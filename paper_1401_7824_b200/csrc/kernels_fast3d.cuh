@@ -247,7 +247,9 @@ constexpr int WS_EW = 20, WS_EH = 18;               // coarse boxes (MODE 2)
 constexpr int WS_EPL = a128(WS_EW * WS_EH * 8);
 template <int MODE, int NSX = 0>
 struct WSCfg {
-    static constexpr int NS = NSX ? NSX : (MODE == 2 ? 7 : 6);   // TMA stages (>= 3 in use: it - 2 .. it)
+    // TMA stages (3 in use: it - 2 .. it; + 1 in MODE 2).  8 and 10 stages measured slower at 511^3
+    // (0.83 vs 0.79 ms per fine launch): the kernel is not waiting on the TMA depth
+    static constexpr int NS = NSX ? NSX : (MODE == 2 ? 7 : 6);
     static constexpr int NT = 32 * 2 * WS_GW;
     static constexpr int UPL = S_UPL, BPL = S_BPL, EPL = MODE == 2 ? 2 * WS_EPL : 0;
     static constexpr int SPL = UPL + BPL + EPL;     // one stage: u | b | e(za) | e(za+1)
@@ -370,6 +372,88 @@ __global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __g
     if (PRO) {
         if (role == 0) prolong(0);
         __syncthreads();
+    }
+
+    if constexpr (!PRO) {
+        // Decoupled groups (MODE 0 / 1): no block barrier per plane.  The t plane is double-buffered
+        // between the groups with named barriers -- FULL[b] (sweep 1 arrives after writing T[b],
+        // sweep 2 syncs before reading it) and EMPTY[b] (sweep 2 arrives after reading T[b], sweep 1
+        // syncs before overwriting it) -- so the groups drift by up to two planes.  The sweep-2 group
+        // refills the TMA stage it has finished (its b of stage j2 - 1), after a group-local barrier.
+        constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_SW2 = 5;
+        if (role == 0) {
+            auto step1 = [&](auto Kc, int j) {
+                constexpr int K = decltype(Kc)::value;      // j % 6
+                constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3, i2 = K % 2, m2 = (K + 1) % 2;
+                mbar_wait(&bar[j % NS], (j / NS) & 1);
+                const double *S = stage(j);
+                plane_partials<true, SR>(S, S_UW, row0, lane, q[i3], f[i3], e[i2]);
+                if (j >= 2) {   // sweep 1 at plane z0 - 3 + j on the 32 x 32 region -> T[j % 2]
+                    const int gz = z0 - 3 + j;
+                    const unsigned in = ((unsigned)gz < (unsigned)n) ? inxy : 0u;
+                    const double *Bp = S + W::UPL / 8 + row0 * S_BW + lane + 1;
+                    double *Tp = Ts + i2 * (S_TPL / 8) + (row0 + 1) * S_TW + lane + 1;
+                    double tv[SR];
+#pragma unroll
+                    for (int r = 0; r < SR; ++r) {
+                        const double faces = f[m3][r] + (q[mm3][r] + q[i3][r]);
+                        const double edges = e[m2][r] + (f[mm3][r] + f[i3][r]);
+                        const double su = (c0 * q[m3][r] + c1 * faces) + c2 * edges;
+                        const double t = q[m3][r] + wd * (Bp[r * S_BW] - su);
+                        tv[r] = ((in >> r) & 1u) ? t : 0.0;
+                    }
+                    if (j >= 4) named_bar_sync(BAR_EMPTY + i2, W::NT);   // sweep 2 has read T[i2] of step j - 2
+#pragma unroll
+                    for (int r = 0; r < SR; ++r) Tp[r * S_TW] = tv[r];
+                    named_bar_arrive(BAR_FULL + i2, W::NT);
+                }
+            };
+            for (int base = 0; base < nit; base += 6) {
+                if (base + 0 < nit) step1(std::integral_constant<int, 0>{}, base + 0);
+                if (base + 1 < nit) step1(std::integral_constant<int, 1>{}, base + 1);
+                if (base + 2 < nit) step1(std::integral_constant<int, 2>{}, base + 2);
+                if (base + 3 < nit) step1(std::integral_constant<int, 3>{}, base + 3);
+                if (base + 4 < nit) step1(std::integral_constant<int, 4>{}, base + 4);
+                if (base + 5 < nit) step1(std::integral_constant<int, 5>{}, base + 5);
+            }
+        } else {
+            auto step2 = [&](auto Kc, int j2) {
+                constexpr int K = decltype(Kc)::value;      // j2 % 6
+                constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3, i2 = K % 2, m2 = (K + 1) % 2;
+                if (j2 < 2) return;
+                named_bar_sync(BAR_FULL + i2, W::NT);
+                plane_partials<true, SR>(Ts + i2 * (S_TPL / 8), S_TW, row0, lane, q[i3], f[i3], e[i2]);
+                if (j2 + 2 < nit) named_bar_arrive(BAR_EMPTY + i2, W::NT);   // T[i2] read (sweep 1 reuses it at j2 + 2)
+                if (j2 >= 4) {   // sweep 2 at plane z0 - 4 + j2 on the 30 x 30 tile, b from stage j2 - 1
+                    const double *Bp = stage(j2 - 1) + W::UPL / 8 + row0 * S_BW + lane + 1;
+                    double *op = optr + (long long)j2 * plane;
+#pragma unroll
+                    for (int r = 0; r < SR; ++r) {
+                        const double faces = f[m3][r] + (q[mm3][r] + q[i3][r]);
+                        const double edges = e[m2][r] + (f[mm3][r] + f[i3][r]);
+                        const double su = (c0 * q[m3][r] + c1 * faces) + c2 * edges;
+                        const double o = q[m3][r] + wd * (Bp[r * S_BW] - su);
+                        if ((oks >> r) & 1u) *op = o;
+                        op += pitch;
+                    }
+                }
+                // stages <= j2 - 1 are finished by both groups (sweep 1 passed step j2): refill them
+                named_bar_sync(BAR_SW2, 32 * WS_GW);
+                if (w == WS_GW && lane == 0) {
+                    for (int jr = (j2 == 2 ? 0 : j2 - 1); jr <= j2 - 1; ++jr)
+                        if (jr + NS < nit) issue(jr + NS);
+                }
+            };
+            for (int base = 0; base < nit; base += 6) {
+                if (base + 0 < nit) step2(std::integral_constant<int, 0>{}, base + 0);
+                if (base + 1 < nit) step2(std::integral_constant<int, 1>{}, base + 1);
+                if (base + 2 < nit) step2(std::integral_constant<int, 2>{}, base + 2);
+                if (base + 3 < nit) step2(std::integral_constant<int, 3>{}, base + 3);
+                if (base + 4 < nit) step2(std::integral_constant<int, 4>{}, base + 4);
+                if (base + 5 < nit) step2(std::integral_constant<int, 5>{}, base + 5);
+            }
+        }
+        return;
     }
 
     auto step = [&](auto Kc, int it) {

@@ -75,6 +75,10 @@ def run(cid, seed, mode, steps):
         os.replace(ck_json + ".tmp", ck_json)
         print(f"cfg {cid} seed {seed} mode {mode} step {s}: {st['sweeps']} sweeps, {st['vcycles']} cycles, "
               f"res {st['res_hist'][-1]:.3e}, {st['seconds']:.1f}s", flush=True)
+        write(name, rec, cfg, u)      # after every step: a long job's finished steps are usable at once
+
+
+def write(name, rec, cfg, u):
     pts = sample_points(cfg.n, cfg.dim)
     rec["samples"] = [[p, float(u[tuple(reversed(p))]).hex()] for p in pts]   # p = (x, y[, z])
     rec["sha256"] = sha(u)
