@@ -174,8 +174,7 @@ struct isdc_ctx {
     int fast3d_mask = 0xff;    // ISDC_FAST3D_MASK: 1 smoother, 2 restriction, 4 prolongation, 8 rhs, 16 residual,
                                // 32 the single-pass four-node residual (M = 5; else two nodes per pass)
     bool resid2d_tma = true;   // ISDC_RESID2D_TMA: 2D residual through the TMA ring
-    int rs_ns = 3;             // ISDC_RS_NS: its ring depth (3 or 5)
-    int rs_chunk_mul = 16;     // ISDC_RS_CHUNK: row chunks ~ this x SMs / column tiles
+    int rs_chunk_mul = 16;     // its row chunks ~ this x SMs / column tiles (3-stage ring; 5 stages measured no faster)
     bool ws3d = true;          // ISDC_WS3D: warp-specialised 3D smoother on levels n >= ws3d_min
     int ws3d_min = 63;         // ISDC_WS3D_MIN
     bool fuse3d = false;       // ISDC_FUSE3D: 3D prolongation fused into the post-smoother (needs ws3d;
@@ -1403,13 +1402,8 @@ isdc_status enqueue_residual(isdc_ctx *h, double *const *u, double *const *F = n
             auto go = [&](auto FEc, auto Mc, auto WRTc, auto WFc) {
                 constexpr int FE_ = decltype(FEc)::value, M_ = decltype(Mc)::value;
                 constexpr bool WRT_ = decltype(WRTc)::value, WF_ = decltype(WFc)::value;
-                if (h->rs_ns == 5) {
-                    using Z = f2d::RST<M_, FE_, 5>;
-                    kl(h, f2d::k_resid_t<FE_, M_, WRT_, WF_, 5>, grd, Z::NT, Z::SMEM)(maps, A);
-                } else {
-                    using Z = f2d::RST<M_, FE_, 3>;
-                    kl(h, f2d::k_resid_t<FE_, M_, WRT_, WF_, 3>, grd, Z::NT, Z::SMEM)(maps, A);
-                }
+                using Z = f2d::RST<M_, FE_, 3>;
+                kl(h, f2d::k_resid_t<FE_, M_, WRT_, WF_, 3>, grd, Z::NT, Z::SMEM)(maps, A);
             };
             using F_ = std::false_type;
             using T_ = std::true_type;
@@ -2297,11 +2291,7 @@ bool kernel_attrs(isdc_ctx *h) {
         set((const void *)f2d::k_resid_t<F_, 3, false, false, 3>); set((const void *)f2d::k_resid_t<F_, 5, false, false, 3>);
         set((const void *)f2d::k_resid_t<F_, 3, true, false, 3>); set((const void *)f2d::k_resid_t<F_, 5, true, false, 3>);
         set((const void *)f2d::k_resid_t<F_, 3, false, true, 3>); set((const void *)f2d::k_resid_t<F_, 5, false, true, 3>);
-        set((const void *)f2d::k_resid_t<F_, 3, false, false, 5>); set((const void *)f2d::k_resid_t<F_, 5, false, false, 5>);
-        set((const void *)f2d::k_resid_t<F_, 3, true, false, 5>); set((const void *)f2d::k_resid_t<F_, 5, true, false, 5>);
-        set((const void *)f2d::k_resid_t<F_, 3, false, true, 5>); set((const void *)f2d::k_resid_t<F_, 5, false, true, 5>);
         set((const void *)f2d::k_resid_t<F_, 3, true, true, 3>); set((const void *)f2d::k_resid_t<F_, 5, true, true, 3>);
-        set((const void *)f2d::k_resid_t<F_, 3, true, true, 5>); set((const void *)f2d::k_resid_t<F_, 5, true, true, 5>);
     };
     setrt(std::integral_constant<int, 0>{}); setrt(std::integral_constant<int, 1>{}); setrt(std::integral_constant<int, 2>{});
     set((const void *)k_tail<2>); set((const void *)k_tail<3>);
@@ -2369,8 +2359,6 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *fm = getenv("ISDC_FAST3D_MASK")) h->fast3d_mask = (int)strtol(fm, nullptr, 0);
     if (const char *w3 = getenv("ISDC_WS3D")) h->ws3d = w3[0] != '0';
     if (const char *r2 = getenv("ISDC_RESID2D_TMA")) h->resid2d_tma = r2[0] != '0';
-    if (const char *rn = getenv("ISDC_RS_NS")) h->rs_ns = atoi(rn);
-    if (const char *rc = getenv("ISDC_RS_CHUNK")) h->rs_chunk_mul = atoi(rc);
     if (const char *w3m = getenv("ISDC_WS3D_MIN")) h->ws3d_min = atoi(w3m);
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
@@ -2425,8 +2413,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
         }
     }
     // periodic grids: levels n <= 64 (2D) / 16 (3D) in one single-CTA launch (kernels_ptail.cuh)
-    const char *ept = getenv("ISDC_PTAIL");
-    if (h->per && !(ept && ept[0] == '0')) {
+    if (h->per) {
         const int lim = (h->d == 2) ? 64 : 16;
         for (int l = 0; l < h->nlev; ++l)
             if (h->lev[l].g.n <= lim) { h->ptail_l0 = l; break; }
