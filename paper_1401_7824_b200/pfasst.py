@@ -206,7 +206,8 @@ def run_block_local(slices, **kw) -> List[SliceResult]:
 def run_block_dist(sl, *, group=None, device=None, **kw) -> SliceResult:
     """This rank's slice of a block, one slice per rank of the torch.distributed group (slice p =
     rank p, P = world size): isend/irecv of the dense end values to the neighbours and an
-    all_reduce(MAX) for the stop test (NCCL between GPUs; gloo with CPU tensors)."""
+    all_reduce(MAX) for the stop test.  ``device``: where the transport's tensors live -- the rank's
+    GPU for NCCL (NVLink), None = host memory for gloo (CUDA slices then stage through the host)."""
     import torch
     import torch.distributed as dist
 
@@ -228,7 +229,9 @@ def run_block_dist(sl, *, group=None, device=None, **kw) -> SliceResult:
             return e.value
         first, reply = False, None
         if req[0] == "send":
-            t = as_tensor(req[2]).contiguous().clone()    # the slice may overwrite its buffer
+            # the transport's device (CPU for gloo, the rank's GPU for NCCL); a copy, since the
+            # slice may overwrite its buffer while the send is in flight
+            t = as_tensor(req[2]).to(device if device is not None else torch.device("cpu")).contiguous().clone()
             sends.append((dist.isend(t, req[1], group=group), t))
         elif req[0] == "recv":
             reply = _recv(req[1], req[2], sl, device, group)

@@ -66,3 +66,49 @@ def test_pfasst_needs_mlsdc_handle(gpu):
     with pytest.raises(gpu.IsdcError) as ei:
         h.pfasst_restrict()
     assert ei.value.status == 1
+
+
+def _dist_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1401_7824_b200 as pk
+    from paper_1401_7824_b200 import pfasst
+    cfg, G, u0 = _dist_case()
+    h = pk.ISDC.from_config(cfg, torch.from_numpy(G), mode=MODE_ISDC, mlsdc_levels=2, coarse_sweeps=1)
+    sl = pfasst.CudaSlice(h, torch.from_numpy(u0).cuda(), 1 + rank)
+    res = pfasst.run_block_dist(sl, max_iters=cfg.max_sweeps, fixed_iters=0, tol=cfg.sweep_tol, predictor=True)
+    q.put((rank, res.iterations, list(res.res_hist), sl.end().cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _dist_case():
+    n = 63
+    cfg = Config(0, 2, n, 3, 0.01, 0.1, FE_FORCING, sweep_tol=1e-10, max_sweeps=100)
+    return cfg, synth.forcing_field(n, 2), synth.initial_condition(3, 0, n)
+
+
+def test_pfasst_dist_transport_with_cuda_slices(gpu, ora):
+    """The multi-rank transport (run_block_dist: isend/recv of end values, all_reduce MAX) driving
+    CUDA slices, one per process: two processes on this GPU exchange through host memory over gloo
+    (no kernel waits on another process), bit for bit the oracle block."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=600) for _ in range(2)), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg, G, u0 = _dist_case()
+    ue, st = ora.pfasst_block(ora.Problem(cfg, G), u0, 2, step0=1, coarse_sweeps=1, predictor=True)
+    for rank, it, hist, end in out:
+        assert it == st["iterations"]
+        assert np.array_equal(np.array(hist), st["res_hist"][:, rank])
+        assert np.array_equal(end, ue[rank])
