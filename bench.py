@@ -462,10 +462,20 @@ def measure_pfasst(pk, torch, cid, P, seed=0):
     s1.record(stream)
     torch.cuda.synchronize()
     ser_ms = s0.elapsed_time(s1)
+    # ... and as serial two-level MLSDC steps (the slice handle's own isdc_step)
+    hm = hs[0]
+    hm.set_initial(u0d, 0)
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m0.record(stream)
+    serm = [hm.step() for _ in range(P)]
+    m1.record(stream)
+    torch.cuda.synchronize()
     res = {"workload": WORKLOAD[cid], "slices": P, "block_ms_1gpu": blk_ms, "iterations": it,
            "converged": out[0].converged, "fine_sweeps": P * it, "vcycles": sum(o.vcycles for o in out),
            "coarse_vcycles": sum(o.coarse_vcycles for o in out),
            "serial_isdc_ms": ser_ms, "serial_isdc_sweeps": sum(s["sweeps"] for s in ser),
+           "serial_mlsdc_ms": m0.elapsed_time(m1), "serial_mlsdc_fine_sweeps": sum(s["sweeps"] for s in serm),
+           "serial_mlsdc_coarse_vcycles": sum(s["coarse_vcycles"] for s in serm),
            "fine_sweep_ms": t_fine, "restrict_coarse_ms": t_coarse,
            "model_p_gpu_ms": P * t_coarse + it * (t_fine + P * t_coarse),
            "note": "1 GPU runs the P slices one after another; model_p_gpu_ms is a critical-path MODEL "
