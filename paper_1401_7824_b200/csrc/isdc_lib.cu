@@ -23,6 +23,7 @@
 #include "kernels_tail.cuh"
 #include "kernels_ptail.cuh"
 #include "kernels_mlsdc.cuh"
+#include "kernels_ctail.cuh"
 #include "tables.h"
 #include <nvtx3/nvToolsExt.h>
 
@@ -188,6 +189,10 @@ struct isdc_ctx {
     bool stream2d = true;      // ISDC_STREAM2D=0: the tile-based 2D RHS / residual kernels instead
     int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
+    int ctail_l0 = -1;         // first level handled by the cluster tail (-1: none)
+    int ctail_mode = 1;        // ISDC_CTAIL: 0 off, 1 = 3D (default), 2 = 2D and 3D (2D measured slower, §6.17)
+    CTailParams ctailp[ISDC_MAXM];
+    size_t ctail_smem = 0;
     TailParams tailp[ISDC_MAXM];
     size_t tail_smem = 0;
     int ptail_l0 = -1;         // periodic grids: first level of the single-CTA periodic tail (ISDC_PTAIL=0: none)
@@ -1015,6 +1020,30 @@ isdc_status launch_tail(isdc_ctx *h, int l, int m, const double *b, const double
     return ISDC_OK;
 }
 
+// the cluster tail: one launch of a CT_CS-CTA cluster for every level from ctail_l0 down
+isdc_status launch_ctail(isdc_ctx *h, int l, int m, const double *b, const double *u_in, double *u_out) {
+    CTailParams P = h->ctailp[m];
+    P.b_in = b; P.u_in = u_in; P.u_out = u_out;
+    P.pitch = h->lev[l].g.pitch;
+    ++h->launches;
+    int pe = prof_begin(h, l == 0 ? PROF_SMOOTH : PROF_COARSE);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CT_CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CT_CS, 1, 1);
+    cfg.blockDim = dim3(CT_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = h->ctail_smem;
+    cfg.stream = h->s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = (h->d == 2) ? cudaLaunchKernelEx(&cfg, k_ctail<2>, P) : cudaLaunchKernelEx(&cfg, k_ctail<3>, P);
+    if (e != cudaSuccess && h->kl_err == cudaSuccess) h->kl_err = e;
+    prof_end(h, pe, l == 0 ? PROF_SMOOTH : PROF_COARSE, 16.0 * npts_of(h, h->lev[l].g));
+    LAUNCH_CHECK(h);
+    return ISDC_OK;
+}
+
 isdc_status launch_ptail(isdc_ctx *h, int l, int m, const double *b, const double *u_in, double *u_out) {
     PTailParams P = h->ptailp[m];
     P.b_in = b; P.u_in = u_in; P.u_out = u_out;
@@ -1033,6 +1062,7 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
     Level &L = h->lev[l];
     const GridDesc &g = L.g;
     if (l == h->ptail_l0) return launch_ptail(h, l, m, b, zero_init ? nullptr : (src ? src : X), X);
+    if (l == h->ctail_l0) return launch_ctail(h, l, m, b, zero_init ? nullptr : (src ? src : X), X);
     if (l == h->tail_l0) return launch_tail(h, l, m, b, zero_init ? nullptr : (src ? src : X), X);
     if (l == h->nlev - 1) return launch_coarse(h, X, b, g, m);   // n = 3 (periodic: 4)
     const SCoef &c = L.coef[m];
@@ -1067,7 +1097,9 @@ isdc_status vcycle(isdc_ctx *h, int l, int m, double *X, double *T, const double
         }
         TRY(launch_restrict(h, C.b, C.g, curw, b, g, c, l));
     }
-    if (l + 1 == h->tail_l0) {
+    if (l + 1 == h->ctail_l0) {
+        TRY(launch_ctail(h, l + 1, m, C.b, nullptr, C.e));
+    } else if (l + 1 == h->tail_l0) {
         TRY(launch_tail(h, l + 1, m, C.b, nullptr, C.e));
     } else {
         TRY(vcycle(h, l + 1, m, C.e, C.t, C.b, nullptr, true));
@@ -2295,6 +2327,11 @@ bool kernel_attrs(isdc_ctx *h) {
     };
     setrt(std::integral_constant<int, 0>{}); setrt(std::integral_constant<int, 1>{}); setrt(std::integral_constant<int, 2>{});
     set((const void *)k_tail<2>); set((const void *)k_tail<3>);
+    set((const void *)k_ctail<2>); set((const void *)k_ctail<3>);
+    for (const void *k : {(const void *)k_ctail<2>, (const void *)k_ctail<3>}) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess && first == cudaSuccess) first = e;
+    }
     set((const void *)k_ptail<2>); set((const void *)k_ptail<3>);
     if (first != cudaSuccess) {
         h->err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(first);
@@ -2410,6 +2447,50 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
             }
             h->tail_smem = (h->d == 2) ? tail_smem_bytes<2>(h->tailp[0]) : tail_smem_bytes<3>(h->tailp[0]);
             if (h->tailp[0].nlev > TAIL_MAX_LEVELS || h->tail_smem > (size_t)kMaxDynSmem) h->tail_l0 = -1;
+        }
+    }
+    // cluster tail: every level n <= 255 (2D) / 31 (3D) in one launch of a 16-CTA
+    // cluster, the levels n >= 15 distributed over its shared memories
+    if (const char *ct = getenv("ISDC_CTAIL")) h->ctail_mode = atoi(ct);
+    if (h->fast && (h->d == 3 ? h->ctail_mode >= 1 : h->ctail_mode >= 2)) {
+        const int lim = (h->d == 2) ? 255 : 31;
+        int l0 = -1;
+        for (int l = 0; l < h->nlev; ++l)
+            if (h->lev[l].g.n <= lim) { l0 = l; break; }
+        if (l0 >= 0 && h->lev[l0].g.n >= 15 && h->nlev - l0 <= CT_MAX_LEVELS) {
+            for (int m = 0; m < nslots; ++m) {
+                CTailParams &T = h->ctailp[m];
+                T.nlev = h->nlev - l0;
+                T.ndist = 0;
+                for (int i = 0; i < T.nlev; ++i) {
+                    T.n[i] = h->lev[l0 + i].g.n;
+                    T.c[i] = h->lev[l0 + i].coef[m];
+                    if (T.n[i] >= 15) T.ndist = i + 1;
+                }
+                T.nu1 = prob->mg.nu1; T.nu2 = prob->mg.nu2;
+                T.Ginv = h->Ginv + (size_t)m * Pc * Pc;
+                T.b_in = nullptr; T.u_in = nullptr; T.u_out = nullptr; T.pitch = 0;
+            }
+            h->ctail_smem = ((h->d == 2) ? ct_smem_doubles<2>(h->ctailp[0], nullptr)
+                                         : ct_smem_doubles<3>(h->ctailp[0], nullptr)) * sizeof(double);
+            int ncl = 0;
+            if (h->ctail_smem <= (size_t)kMaxDynSmem) {
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = CT_CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                cfg.gridDim = dim3(CT_CS, 1, 1);
+                cfg.blockDim = dim3(CT_THREADS, 1, 1);
+                cfg.dynamicSmemBytes = h->ctail_smem;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                if (cudaOccupancyMaxActiveClusters(&ncl, (h->d == 2) ? (const void *)k_ctail<2> : (const void *)k_ctail<3>,
+                                                   &cfg) != cudaSuccess) {
+                    ncl = 0;
+                    cudaGetLastError();
+                }
+            }
+            if (ncl > 0) h->ctail_l0 = l0;
         }
     }
     // periodic grids: levels n <= 64 (2D) / 16 (3D) in one single-CTA launch (kernels_ptail.cuh)
