@@ -190,6 +190,7 @@ struct isdc_ctx {
     int nsm = 148;             // SM count (grid sizing of the z-streaming 3D kernels)
     int tail_l0 = -1;          // first level handled by the single-CTA tail kernel (-1: none)
     int ctail_l0 = -1;         // first level handled by the cluster tail (-1: none)
+    bool rhs128 = false;       // ISDC_RHS128=1: the fold RHS with 128-bit loads (k_rhs_f2; measured slower, §6.18)
     int ctail_mode = 1;        // ISDC_CTAIL: 0 off, 1 = 3D (default), 2 = 2D and 3D (2D measured slower, §6.17)
     CTailParams ctailp[ISDC_MAXM];
     size_t ctail_smem = 0;
@@ -1199,7 +1200,13 @@ isdc_status run_rhs(isdc_ctx *h, int m, double *const *uold, const double *unew_
         A.wfold = fold ? h->WB[m] : nullptr;
 #define ISDC_RS(FE_, M_) kl(h, f2d::k_rhs_s<FE_, M_>, grd, f2d::SW_NT, 0)(A)
 #define ISDC_RSF(FE_, M_) kl(h, f2d::k_rhs_s<FE_, M_, true>, grd, f2d::SW_NT, 0)(A)
-        if (fold) {
+        if (fold && h->rhs128) {
+            // 128-bit loads, 62 outputs per warp strip (k_rhs_f2)
+            const int strips = (h->n + 1 + f2d::SP_OUT - 1) / f2d::SP_OUT;
+            dim3 g2((strips + f2d::SW_NT / 32 - 1) / (f2d::SW_NT / 32), grd.y);
+            if (M == 3) { if (fe == 0) kl(h, f2d::k_rhs_f2<0, 3>, g2, f2d::SW_NT, 0)(A); else kl(h, f2d::k_rhs_f2<2, 3>, g2, f2d::SW_NT, 0)(A); }
+            else { if (fe == 0) kl(h, f2d::k_rhs_f2<0, 5>, g2, f2d::SW_NT, 0)(A); else kl(h, f2d::k_rhs_f2<2, 5>, g2, f2d::SW_NT, 0)(A); }
+        } else if (fold) {
             if (M == 3) { if (fe == 0) ISDC_RSF(0, 3); else ISDC_RSF(2, 3); }
             else { if (fe == 0) ISDC_RSF(0, 5); else ISDC_RSF(2, 5); }
         } else if (M == 3) { if (fe == 0) ISDC_RS(0, 3); else if (fe == 1) ISDC_RS(1, 3); else ISDC_RS(2, 3); }
@@ -2452,6 +2459,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     // cluster tail: every level n <= 255 (2D) / 31 (3D) in one launch of a 16-CTA
     // cluster, the levels n >= 15 distributed over its shared memories
     if (const char *ct = getenv("ISDC_CTAIL")) h->ctail_mode = atoi(ct);
+    if (const char *r1 = getenv("ISDC_RHS128")) h->rhs128 = r1[0] == '1';
     if (h->fast && (h->d == 3 ? h->ctail_mode >= 1 : h->ctail_mode >= 2)) {
         const int lim = (h->d == 2) ? 255 : 31;
         int l0 = -1;

@@ -697,6 +697,98 @@ __global__ void __launch_bounds__(SW_NT) k_rhs_s(StreamArgs A) {
     }
 }
 
+// RHS of substep m from the stored fold w_m with 128-bit loads (the north star's "SDC-sweep kernel
+// ... with 128-bit vectorised fp64 loads"): a warp strip covers 64 columns [62 s - 2, 62 s + 62),
+// lane l the column pair (62 s - 2 + 2 l, + 1) as one double2 per field and row (16-byte aligned:
+// even column, pitch 2^p), and emits the 62 outputs [62 s - 1, 62 s + 61).  The x-pair sums take the
+// outer neighbour from the adjacent lane: r(c0) = v(c0 - 1) + v(c0 + 1) = up(v1) + v1,
+// r(c1) = v0 + down(v0) -- the trees of k_rhs_s, so the same bits.
+constexpr int SP_OUT = 62;
+template <int FE, int MM>
+__global__ void __launch_bounds__(SW_NT) k_rhs_f2(StreamArgs A) {
+    const int lane = threadIdx.x & 31, strip = blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5);
+    const int n = A.n;
+    const int c0 = strip * SP_OUT - 2 + 2 * lane;    // even: 16-byte aligned pair (c0, c0 + 1)
+    if (strip * SP_OUT - 1 >= n) return;             // whole warp leaves together
+    const int y0 = blockIdx.y * A.yc, y1 = min(y0 + A.yc, n);
+    const bool in0 = c0 >= 0 && c0 < n, in1 = c0 + 1 >= 0 && c0 + 1 < n;
+    const bool ld = c0 >= 0 && c0 < n;               // c0 + 1 <= n: the pad column (pitch n + 1) is readable
+    const bool out0 = lane >= 1 && in0, out1 = lane <= 30 && in1;
+    const BLConst c = A.bl;
+    const double ctm = A.ct[A.m];
+    double fa_c[MM];
+#pragma unroll
+    for (int j = 0; j < MM; ++j) fa_c[j] = A.ct[j];
+    double2 Lw[3], Lu[3], Lg[3];
+    double vq0[3], wq0[3], vr0[3], wr0[3], vq1[3], wq1[3], vr1[3], wr1[3];
+    double bmax = 0.0;
+    const int nit = y1 - y0 + 2;                     // rows y0-1 .. y1
+    auto rowoff = [&](int y) { return (long long)y * A.pitch + c0; };
+    auto load = [&](int it, int slot) {
+        const int y = y0 - 1 + it;
+        const bool ok = ld && y >= 0 && y < n && it < nit;
+        const double2 z = make_double2(0.0, 0.0);
+        Lw[slot] = ok ? __ldcs(reinterpret_cast<const double2 *>(A.wfold + rowoff(y))) : z;
+        Lu[slot] = ok ? __ldcs(reinterpret_cast<const double2 *>(A.unew + rowoff(y))) : z;
+        if (FE == 2) Lg[slot] = ok ? __ldg(reinterpret_cast<const double2 *>(A.G + rowoff(y))) : z;
+    };
+    // v of one point from (w, unew, G) -- rhs_row_fold's tree
+    auto vpt = [&](double un, double g) {
+        if (FE == 0) return un;
+        double fa = A.a[0][0] * (g * fa_c[0]);
+#pragma unroll
+        for (int j = 1; j < MM; ++j) fa = fa + A.a[0][j] * (g * fa_c[j]);
+        const double fn = g * ctm, fo = g * ctm;
+        return (un + A.dtm * (fn - fo)) + fa;
+    };
+    load(0, 0);
+    load(1, 1);
+    auto step = [&](auto Kc, int it) {
+        constexpr int k = decltype(Kc)::value;       // it % 3
+        constexpr int km1 = (k + 2) % 3, km2 = (k + 1) % 3;
+        load(it + 2, km1);                           // slot of row it-1 is free
+        const int y = y0 - 1 + it;
+        const bool yin = y >= 0 && y < n;
+        double v0 = vpt(Lu[k].x, FE == 2 ? Lg[k].x : 0.0), v1 = vpt(Lu[k].y, FE == 2 ? Lg[k].y : 0.0);
+        double w0 = Lw[k].x, w1 = Lw[k].y;
+        if (!(yin && in0)) { v0 = 0.0; w0 = 0.0; }
+        if (!(yin && in1)) { v1 = 0.0; w1 = 0.0; }
+        vq0[k] = v0; wq0[k] = w0; vq1[k] = v1; wq1[k] = w1;
+        vr0[k] = shfl_up1(v1) + v1;
+        vr1[k] = v0 + shfl_dn1(v0);
+        wr0[k] = shfl_up1(w1) + w1;
+        wr1[k] = w0 + shfl_dn1(w0);
+        if (it >= 2) {                               // output row y-1
+            double *op = A.out + rowoff(y - 1);
+            if (out0) {
+                const double fv = vr0[km1] + (vq0[km2] + vq0[k]);
+                const double fw = wr0[km1] + (wq0[km2] + wq0[k]);
+                const double ew = wr0[km2] + wr0[k];
+                const double b = (c.kB0 * vq0[km1] + c.kB1 * fv) + ((c.kL0 * wq0[km1] + c.kL1 * fw) + c.kL2 * ew);
+                op[0] = b;
+                bmax = amax(bmax, fabs(b));
+            }
+            if (out1) {
+                const double fv = vr1[km1] + (vq1[km2] + vq1[k]);
+                const double fw = wr1[km1] + (wq1[km2] + wq1[k]);
+                const double ew = wr1[km2] + wr1[k];
+                const double b = (c.kB0 * vq1[km1] + c.kB1 * fv) + ((c.kL0 * wq1[km1] + c.kL1 * fw) + c.kL2 * ew);
+                op[1] = b;
+                bmax = amax(bmax, fabs(b));
+            }
+        }
+    };
+    for (int base = 0; base < nit; base += 3) {
+        step(std::integral_constant<int, 0>{}, base);
+        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
+    }
+    if (A.slot) {
+        unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(bmax));
+        if (lane == 0 && v) atomicMax(A.slot, v);
+    }
+}
+
 // residual of nodes m = 1..M-1 in one pass: p_m = (u_m - u_0) [- sum qa_mj fE(u_j)], z_m = sum qb_mj u_j,
 // r~_m = B p_m - L z_m, per-node max into slot[m-1].  The M-1 nodes are split over G = (M-1)/NMW
 // warps per strip (NMW nodes each; the extra loads of the same rows hit L1/L2), which halves the

@@ -214,14 +214,16 @@ def test_unweighted_residual_steps_bitwise(gpu, ora, cid, n, mode):
                                       ({"ISDC_FUSE3D": "1"}, MODE_ISDC), ({"ISDC_WS3D_MIN": "31"}, MODE_ISDC),
                                       ({"ISDC_RESID2D_TMA": "0"}, MODE_ISDC), ({"ISDC_CTAIL": "0"}, MODE_ISDC),
                                       ({"ISDC_CTAIL": "0"}, MODE_SDC), ({"ISDC_CTAIL": "2"}, MODE_ISDC),
-                                      ({"ISDC_CTAIL": "2"}, MODE_SDC)])
+                                      ({"ISDC_CTAIL": "2"}, MODE_SDC),
+                                      ({"ISDC_RHS128": "1"}, MODE_ISDC)])
 def test_execution_paths_bitwise(gpu, ora, monkeypatch, env, mode):
     """Host-side node-solve tests, un-captured sweeps, sweep-by-sweep steps, the generic kernels, the
     fold-free RHS, the unfused tail, the tile-based 2D RHS / residual, the unfused 2D transfers and
     every subset of the fast 3D kernels (mask bits: 1 smoother, 2 restriction, 4 prolongation, 8 RHS,
     16 residual, 32 four-node residual), the 4 x 8 single-group 3D smoother, the 3D prolongation fused
     into the warp-specialised post-smoother and the warp-specialised smoother on 31^3, and the coarse
-    levels without the cluster tail (ISDC_CTAIL=0) or with it in 2D too (ISDC_CTAIL=2) produce the
+    levels without the cluster tail (ISDC_CTAIL=0) or with it in 2D too (ISDC_CTAIL=2), and the fold
+    RHS with 128-bit loads (ISDC_RHS128=1) produce the
     oracle's bits too (the environment is read when the handle is created)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
