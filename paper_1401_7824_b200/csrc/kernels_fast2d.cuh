@@ -1088,7 +1088,7 @@ struct __align__(128) SmemSR {
 // one stencil phase over the region [xs, xs+w) x [ys, ys+h): 2 column chunks of 32 lanes x 4 row
 // bands, one (chunk, band) per warp, rolling a 3-row register window down each column.
 // src/dst are arrays with origins (sox, soy) / (dox, doy) and row lengths sw / dw.
-template <int KIND, int SW_, int DW_, int FR_TY>
+template <int KIND, int SW_, int DW_, int FR_TY, bool ZERO = false>
 __device__ __forceinline__ void fr_phase(const double *__restrict__ src, int sox, int soy, double *__restrict__ dst,
                                          int dox, int doy, const double *__restrict__ B, int xs, int w, int ys,
                                          int h, int x0, int y0, int n, const SCoef &c, double *__restrict__ gout,
@@ -1100,6 +1100,18 @@ __device__ __forceinline__ void fr_phase(const double *__restrict__ src, int sox
     const int r0 = ys + band * bh, r1 = min(r0 + bh, ys + h);
     if (x >= xs + w || r0 >= r1) return;
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
+    if constexpr (ZERO) {
+        // sweep 1 from the zero iterate: S 0 = (c0 0 + c1 0) + c2 0 = +0 for any signs of c1, c2, and
+        // b - (+0) = b, so u' = 0 + wd (b - S 0) = 0.0 + wd b -- the same bits without reading u
+        static_assert(KIND == 0, "zero-iterate shortcut: sweep 1 only");
+        const double *bp = B + (r0 - FR_BOY) * FR_BW + (x - FR_BOX);
+        double *dp = dst + (r0 - doy) * DW_ + (x - dox);
+        const int gx = x0 + x;
+        const bool xin = gx >= 0 && gx < n;
+        for (int y = r0, gy = y0 + r0; y < r1; ++y, ++gy, bp += FR_BW, dp += DW_)
+            *dp = (xin && (unsigned)gy < (unsigned)n) ? 0.0 + wd * *bp : 0.0;
+        return;
+    }
     // row pointers advanced by one row per step (no per-access index arithmetic)
     const double *sp = src + (r0 - 1 - soy) * SW_ + (x - sox);          // row y-1, column x
     const double *bp = B + (r0 - FR_BOY) * FR_BW + (x - FR_BOX);
@@ -1204,15 +1216,12 @@ __global__ void __launch_bounds__(NT) k_smooth2r(const __grid_constant__ CUtenso
         if (MODE != 1) tma_load_2d(&S.u[0][0], &tu, x0 + FR_UOX, y0 + FR_UOY, &S.bar);
         tma_load_2d(&S.b[0][0], &tb, x0 + FR_BOX, y0 + FR_BOY, &S.bar);
     }
-    if (MODE == 1) {
-        for (int q = tid; q < FR_UW * SR::UH; q += NT) (&S.u[0][0])[q] = 0.0;
-        __syncthreads();
-    }
     mbar_wait(&S.bar, 0);
     const double *Bp = &S.b[0][0];
-    // sweep 1: u -> t on [-2, 60] x [-2, 34]
-    fr_phase<0, FR_UW, FR_TW, FR_TY>(&S.u[0][0], FR_UOX, FR_UOY, &S.t[0][0], FR_TOX, FR_TOY, Bp, -2, 63, -2, FR_TY + 5, x0, y0, n,
-                              c, nullptr, pitch);
+    // sweep 1: u -> t on [-2, 60] x [-2, 34] (MODE 1: from the zero iterate, u never read; sweep 2
+    // writes every u'' point the defect reads, so the u buffer needs no zeros)
+    fr_phase<0, FR_UW, FR_TW, FR_TY, MODE == 1>(&S.u[0][0], FR_UOX, FR_UOY, &S.t[0][0], FR_TOX, FR_TOY, Bp, -2, 63, -2,
+                                                FR_TY + 5, x0, y0, n, c, nullptr, pitch);
     __syncthreads();
     // sweep 2: t -> u'' (into the u buffer) on [-1, 59] x [-1, 33]; the tile goes to global
     fr_phase<1, FR_TW, FR_UW, FR_TY>(&S.t[0][0], FR_TOX, FR_TOY, &S.u[0][0], FR_UOX, FR_UOY, Bp, -1, 61, -1, FR_TY + 3, x0, y0, n,
