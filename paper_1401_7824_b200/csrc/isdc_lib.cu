@@ -178,6 +178,7 @@ struct isdc_ctx {
     int rs_chunk_mul = 16;     // its row chunks ~ this x SMs / column tiles (3-stage ring; 5 stages measured no faster)
     bool ws3d = true;          // ISDC_WS3D: warp-specialised 3D smoother on levels n >= ws3d_min
     int ws3d_min = 63;         // ISDC_WS3D_MIN
+    bool shift3d = true;       // ISDC_SHIFT3D: shifted 30-point tiling of the 3D streaming kernels (17 tiles per axis at 511)
     bool fuse3d = false;       // ISDC_FUSE3D: 3D prolongation fused into the post-smoother (needs ws3d;
                                // bitwise equal, measured slower: 1.34 ms vs 0.42 + 0.77 ms at 511^3)
     int tail3d = 15;           // largest 3D level handled by the single-CTA tail (fast kernels above)
@@ -619,17 +620,22 @@ isdc_status launch_smooth2_3d_t(isdc_ctx *h, double *out, const double *in, cons
 // trilinear prolongation + correction, MODE 2), in == nullptr: zero iterate (MODE 1)
 isdc_status launch_smooth2_3d_ws(isdc_ctx *h, double *out, const double *in, const double *b, const GridDesc &g,
                                  const SCoef &c, int level, const double *e = nullptr, const GridDesc *gc = nullptr) {
-    const CUtensorMap *mb = tmap(h, b, g, f3d::S_BW, f3d::S_BH, 1);
-    const CUtensorMap *mu = in ? tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1) : mb;
+    // shifted tiling (MODE 0 / 1, ISDC_SHIFT3D, on): ceil((n - 2) / 30) tiles per axis, boxes u 36 x 34, b 32 x 32
+    const bool sh = h->shift3d && !e;
+    const CUtensorMap *mb = sh ? tmap(h, b, g, f3d::WS_BWS, f3d::S_BH, 1) : tmap(h, b, g, f3d::S_BW, f3d::S_BH, 1);
+    const CUtensorMap *mu = !in ? mb : sh ? tmap(h, in, g, f3d::WS_UWS, f3d::S_UH, 1) : tmap(h, in, g, f3d::S_UW, f3d::S_UH, 1);
     const CUtensorMap *me = e ? tmap(h, e, *gc, f3d::WS_EW, f3d::WS_EH, 1) : mb;
     if (!mu || !mb || !me) { h->err = "tensor map encoding failed"; return ISDC_ERR_CUDA; }
     ++h->launches;
     const int cls = level == 0 ? (e ? PROF_PROLONG : PROF_SMOOTH) : PROF_COARSE;
     int pe = prof_begin(h, cls);
     int tx = (g.n + f3d::S_TX - 1) / f3d::S_TX, ty = (g.n + f3d::S_TY - 1) / f3d::S_TY;
+    if (sh) tx = ty = f3d::sh_tiles(g.n, f3d::S_TX);
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
     if (e) kl(h, f3d::k_smooth2ws<2>, grd, f3d::WSCfg<2>::NT, f3d::WSCfg<2>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    else if (sh && !in) kl(h, f3d::k_smooth2ws<1, 0, true>, grd, f3d::WSCfg<1, 0, true>::NT, f3d::WSCfg<1, 0, true>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    else if (sh) kl(h, f3d::k_smooth2ws<0, 0, true>, grd, f3d::WSCfg<0, 0, true>::NT, f3d::WSCfg<0, 0, true>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     else if (!in) kl(h, f3d::k_smooth2ws<1>, grd, f3d::WSCfg<1>::NT, f3d::WSCfg<1>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     else kl(h, f3d::k_smooth2ws<0>, grd, f3d::WSCfg<0>::NT, f3d::WSCfg<0>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     // algorithmic bytes: read u (unless zero), b (+ e / 8); write u''
@@ -765,6 +771,8 @@ isdc_status launch_bl(isdc_ctx *h, const double *const *fields, int K, int nm, f
     }
     A.K = K; A.n = g.n; A.pitch = g.pitch; A.plane = g.plane; A.bl = h->bl; A.ct = h->ctdev;
     int tx = (g.n + f3d::RW - 3) / (f3d::RW - 2), ty = (g.n + rh - 3) / (rh - 2);
+    A.sh = h->shift3d ? 1 : 0;
+    if (A.sh) { tx = f3d::sh_tiles(g.n, f3d::RW - 2); ty = f3d::sh_tiles(g.n, rh - 2); }
     A.zc = pick_chunk(h, tx * ty, g.n, 2);
     dim3 grd(tx, ty, (g.n + A.zc - 1) / A.zc);
     const size_t sm = smem_of(ns);
@@ -800,7 +808,9 @@ isdc_status launch_resid4(isdc_ctx *h, const double *const *fields, int K, f3d::
         maps.m[k] = *mk;
     }
     A.K = K; A.n = g.n; A.pitch = g.pitch; A.plane = g.plane; A.bl = h->bl; A.ct = h->ctdev;
-    const int tx = (g.n + SH::TX - 1) / SH::TX, ty = (g.n + SH::TY - 1) / SH::TY;
+    int tx = (g.n + SH::TX - 1) / SH::TX, ty = (g.n + SH::TY - 1) / SH::TY;
+    A.sh = h->shift3d ? 1 : 0;
+    if (A.sh) { tx = f3d::sh_tiles(g.n, SH::TX); ty = f3d::sh_tiles(g.n, SH::TY); }
     A.zc = pick_chunk(h, tx * ty, g.n, 2);
     dim3 grd(tx, ty, (g.n + A.zc - 1) / A.zc);
     const size_t sm = SH::smem(K, ns);
@@ -2311,6 +2321,7 @@ bool kernel_attrs(isdc_ctx *h) {
     set((const void *)f3d::k_smooth2<3, 0, 12>); set((const void *)f3d::k_smooth2<3, 1, 12>);
     set((const void *)f3d::k_smooth2<4, 0, 8>); set((const void *)f3d::k_smooth2<4, 1, 8>);
     set((const void *)f3d::k_smooth2ws<0>); set((const void *)f3d::k_smooth2ws<1>); set((const void *)f3d::k_smooth2ws<2>);
+    set((const void *)f3d::k_smooth2ws<0, 0, true>); set((const void *)f3d::k_smooth2ws<1, 0, true>);
     set((const void *)f3d::k_restrict);
     set((const void *)f3d::k_fe_cd4);
     auto setbl = [&](auto F) {
@@ -2405,6 +2416,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *r2 = getenv("ISDC_RESID2D_TMA")) h->resid2d_tma = r2[0] != '0';
     if (const char *w3m = getenv("ISDC_WS3D_MIN")) h->ws3d_min = atoi(w3m);
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
+    if (const char *s3 = getenv("ISDC_SHIFT3D")) h->shift3d = s3[0] != '0';
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
     if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';

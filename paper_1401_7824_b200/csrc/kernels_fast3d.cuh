@@ -25,6 +25,9 @@ constexpr int RW = 32;           // region width (one lane per column)
 constexpr int RH = NW * R;       // region height
 
 __host__ __device__ constexpr int a128(int b) { return (b + 127) / 128 * 128; }
+// tiles per axis of the shifted tiling (tile t, region t + 2): the first tile emits t + 1 points
+// (0 .. t), tile k >= 1 the points kt + 1 .. kt + t, and the region's last point where it is n - 1
+__host__ __device__ constexpr int sh_tiles(int n, int t) { return n <= t + 2 ? 1 : (n - 2 + t - 1) / t; }
 
 // In-plane partial sums of the R owned rows from a plane in shared memory (row stride `ld`):
 // window rows row0 .. row0+R+1 (centre rows row0+1 .. row0+R), columns col0 .. col0+2 (centre
@@ -245,13 +248,22 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_smooth2(const __grid_constant__
 constexpr int WS_SR = 4, WS_GW = 8;                 // rows per thread, warps per sweep group
 constexpr int WS_EW = 20, WS_EH = 18;               // coarse boxes (MODE 2)
 constexpr int WS_EPL = a128(WS_EW * WS_EH * 8);
-template <int MODE, int NSX = 0>
+// SH (MODE 0 / 1): shifted tiling -- the region starts AT the tile origin (x0, y0) = 30 (bx, by)
+// instead of one point before it, and the region's first / last point is an output where it is the
+// domain's first / last point (its outer t neighbour is the Dirichlet zero of the t plane's pad
+// ring, which needs no computing).  ceil((n - 2) / 30) tiles per axis instead of ceil(n / 30): 17
+// instead of 18 at n = 511 (the 18th tile held one column).  Boxes (even x start): u 36 x 34 at
+// (x0 - 2, y0 - 1), b 32 x 32 at (x0, y0).
+constexpr int WS_UWS = RW + 4, WS_BWS = RW;
+constexpr int WS_UPLS = a128(WS_UWS * S_UH * 8), WS_BPLS = a128(WS_BWS * S_BH * 8);
+template <int MODE, int NSX = 0, bool SH = false>
 struct WSCfg {
     // TMA stages (3 in use: it - 2 .. it; + 1 in MODE 2).  8 and 10 stages measured slower at 511^3
     // (0.83 vs 0.79 ms per fine launch): the kernel is not waiting on the TMA depth
     static constexpr int NS = NSX ? NSX : (MODE == 2 ? 7 : 6);
     static constexpr int NT = 32 * 2 * WS_GW;
-    static constexpr int UPL = S_UPL, BPL = S_BPL, EPL = MODE == 2 ? 2 * WS_EPL : 0;
+    static constexpr int UPL = SH ? WS_UPLS : S_UPL, BPL = SH ? WS_BPLS : S_BPL, EPL = MODE == 2 ? 2 * WS_EPL : 0;
+    static constexpr int UW = SH ? WS_UWS : S_UW, BW = SH ? WS_BWS : S_BW;
     static constexpr int SPL = UPL + BPL + EPL;     // one stage: u | b | e(za) | e(za+1)
     static constexpr size_t SMEM = (size_t)NS * SPL + 2 * S_TPL + 8 * NS + 128;
 };
@@ -297,15 +309,16 @@ __device__ __forceinline__ void ws_prolong_plane(double *U, const double *Ea, co
     }
 }
 
-template <int MODE, int NSX = 0>
-__global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __grid_constant__ CUtensorMap tu,
+template <int MODE, int NSX = 0, bool SH = false>
+__global__ void __launch_bounds__(WSCfg<MODE, NSX, SH>::NT, 1) k_smooth2ws(const __grid_constant__ CUtensorMap tu,
                                                                  const __grid_constant__ CUtensorMap tb,
                                                                  const __grid_constant__ CUtensorMap te,
                                                                  double *__restrict__ out, int n, int pitch,
                                                                  long long plane, SCoef c, int zc) {
-    using W = WSCfg<MODE, NSX>;
+    using W = WSCfg<MODE, NSX, SH>;
     constexpr int NS = W::NS, SR = WS_SR;
     constexpr bool ZERO = MODE == 1, PRO = MODE == 2;
+    static_assert(!(SH && PRO), "shifted tiling: MODE 0 / 1 only");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     double *St = reinterpret_cast<double *>(sm);
@@ -322,9 +335,9 @@ __global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __g
         const int p = z0 - 2 + j;
         double *S = stage(j);
         uint64_t *bb = &bar[j % NS];
-        mbar_expect_tx(bb, ((ZERO ? 0 : S_UW * S_UH) + S_BW * S_BH + (PRO ? 2 * WS_EW * WS_EH : 0)) * 8);
-        if (!ZERO) tma_load_3d(S, &tu, x0 - 2, y0 - 2, p, bb);
-        tma_load_3d(S + W::UPL / 8, &tb, x0 - 2, y0 - 1, p - 1, bb);
+        mbar_expect_tx(bb, ((ZERO ? 0 : W::UW * S_UH) + W::BW * S_BH + (PRO ? 2 * WS_EW * WS_EH : 0)) * 8);
+        if (!ZERO) tma_load_3d(S, &tu, x0 - 2, SH ? y0 - 1 : y0 - 2, p, bb);
+        tma_load_3d(S + W::UPL / 8, &tb, SH ? x0 : x0 - 2, SH ? y0 : y0 - 1, p - 1, bb);
         if (PRO) {
             const int za = (p & 1) ? (p - 1) / 2 : p / 2 - 1;   // odd p: (p-1)/2; even p: p/2 - 1 and p/2
             tma_load_3d(S + (W::UPL + W::BPL) / 8, &te, ex0, ey0, za, bb);
@@ -338,6 +351,8 @@ __global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __g
         for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
     }
+    if (SH)            // the t planes' pad ring is the Dirichlet zero read by the boundary outputs
+        for (int q = tid; q < 2 * (S_TPL / 8); q += W::NT) Ts[q] = 0.0;
     __syncthreads();   // (MODE 1 reads no u: the zero-iterate sweep never touches the u stages)
     if (tid == 0)
         for (int j = 0; j < NS && j < nit; ++j) issue(j);
@@ -345,16 +360,22 @@ __global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __g
     const int role = w < WS_GW ? 0 : 1;             // sweep 1 | sweep 2
     const int row0 = SR * (w % WS_GW);
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2, wd = c.wd;
-    const int lx = lane - 1, ly0 = row0 - 1;
+    const int lx = SH ? lane : lane - 1, ly0 = SH ? row0 : row0 - 1;   // region coordinates of the owned points
     const int gx = x0 + lx;
     const bool xin = gx >= 0 && gx < n;
-    const bool xout = lx >= 0 && lx < S_TX && gx < n;
+    // outputs: the region minus its one-point rim, plus the rim points on the domain boundary (SH)
+    const bool xout = SH ? (gx < n && (lane >= 1 || gx == 0) && (lane <= S_TX || gx == n - 1))
+                         : (lx >= 0 && lx < S_TX && gx < n);
+    constexpr int UC0 = SH ? 1 : 0;                 // u box column of the owned point's left neighbour - lane
+    constexpr int BC0 = SH ? 0 : 1;                 // b box column of the owned point - lane
     unsigned inxy = 0u, oks = 0u;
 #pragma unroll
     for (int r = 0; r < SR; ++r) {
         const int ly = ly0 + r, gy = y0 + ly;
         if (xin && gy >= 0 && gy < n) inxy |= 1u << r;
-        if (xout && ly >= 0 && ly < S_TY && gy < n) oks |= 1u << r;
+        const bool yout = SH ? (gy < n && (ly >= 1 || gy == 0) && (ly <= S_TY || gy == n - 1))
+                             : (ly >= 0 && ly < S_TY && gy < n);
+        if (xout && yout) oks |= 1u << r;
     }
     double *optr = out + (long long)(z0 - 4) * plane + (long long)(y0 + ly0) * pitch + gx;
     // rings of one sweep (role 0: u partials; role 1: t partials), indexed by stage mod 3 / mod 2
@@ -384,11 +405,11 @@ __global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __g
                 constexpr int i3 = K % 3, m3 = (K + 2) % 3, mm3 = (K + 1) % 3, i2 = K % 2, m2 = (K + 1) % 2;
                 mbar_wait(&bar[j % NS], (j / NS) & 1);
                 const double *S = stage(j);
-                if (!ZERO) plane_partials<true, SR>(S, S_UW, row0, lane, q[i3], f[i3], e[i2]);
+                if (!ZERO) plane_partials<true, SR>(S, W::UW, row0, lane + UC0, q[i3], f[i3], e[i2]);
                 if (j >= 2) {   // sweep 1 at plane z0 - 3 + j on the 32 x 32 region -> T[j % 2]
                     const int gz = z0 - 3 + j;
                     const unsigned in = ((unsigned)gz < (unsigned)n) ? inxy : 0u;
-                    const double *Bp = S + W::UPL / 8 + row0 * S_BW + lane + 1;
+                    const double *Bp = S + W::UPL / 8 + row0 * W::BW + lane + BC0;
                     double *Tp = Ts + i2 * (S_TPL / 8) + (row0 + 1) * S_TW + lane + 1;
                     double tv[SR];
 #pragma unroll
@@ -397,12 +418,12 @@ __global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __g
                         if (ZERO) {
                             // from the zero iterate: S 0 = +0 whatever the signs of c1, c2, so
                             // u' = 0 + wd (b - S 0) = 0.0 + wd b (the same bits, u never read)
-                            t = 0.0 + wd * Bp[r * S_BW];
+                            t = 0.0 + wd * Bp[r * W::BW];
                         } else {
                             const double faces = f[m3][r] + (q[mm3][r] + q[i3][r]);
                             const double edges = e[m2][r] + (f[mm3][r] + f[i3][r]);
                             const double su = (c0 * q[m3][r] + c1 * faces) + c2 * edges;
-                            t = q[m3][r] + wd * (Bp[r * S_BW] - su);
+                            t = q[m3][r] + wd * (Bp[r * W::BW] - su);
                         }
                         tv[r] = ((in >> r) & 1u) ? t : 0.0;
                     }
@@ -429,14 +450,14 @@ __global__ void __launch_bounds__(WSCfg<MODE, NSX>::NT, 1) k_smooth2ws(const __g
                 plane_partials<true, SR>(Ts + i2 * (S_TPL / 8), S_TW, row0, lane, q[i3], f[i3], e[i2]);
                 if (j2 + 2 < nit) named_bar_arrive(BAR_EMPTY + i2, W::NT);   // T[i2] read (sweep 1 reuses it at j2 + 2)
                 if (j2 >= 4) {   // sweep 2 at plane z0 - 4 + j2 on the 30 x 30 tile, b from stage j2 - 1
-                    const double *Bp = stage(j2 - 1) + W::UPL / 8 + row0 * S_BW + lane + 1;
+                    const double *Bp = stage(j2 - 1) + W::UPL / 8 + row0 * W::BW + lane + BC0;
                     double *op = optr + (long long)j2 * plane;
 #pragma unroll
                     for (int r = 0; r < SR; ++r) {
                         const double faces = f[m3][r] + (q[mm3][r] + q[i3][r]);
                         const double edges = e[m2][r] + (f[mm3][r] + f[i3][r]);
                         const double su = (c0 * q[m3][r] + c1 * faces) + c2 * edges;
-                        const double o = q[m3][r] + wd * (Bp[r * S_BW] - su);
+                        const double o = q[m3][r] + wd * (Bp[r * W::BW] - su);
                         if ((oks >> r) & 1u) *op = o;
                         op += pitch;
                     }
@@ -743,6 +764,8 @@ struct BLArgs {
     int n, pitch;
     long long plane;
     int zc;
+    int sh;                        // shifted tiling (see WSCfg): the region starts at the tile origin, boundary
+                                   // rim points are outputs, ceil((n - 2) / T) tiles per axis
     double *out;                   // RHS: b (pitched); residual: unused
     unsigned long long *slot[BL_MAXNM];   // max |out| per output (RHS: optional, residual: required)
 };
@@ -908,29 +931,37 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
     const int x0 = blockIdx.x * SH::TX, y0 = blockIdx.y * SH::TY;
     const int z0 = blockIdx.z * A.zc, z1 = min(z0 + A.zc, n);
     const int nit = z1 - z0 + 2;              // ingest planes z0-1 .. z1
+    const bool sh = A.sh != 0;
     auto issue = [&](int it) {
         const int s = it % ns, p = z0 - 1 + it;
         mbar_expect_tx(&bar[s], K * SH::FW * SH::FH * 8);
         for (int k = 0; k < K; ++k)
-            tma_load_3d(Fs + ((size_t)s * K + k) * (SH::FPL / 8), &maps.m[k], x0 - 2, y0 - 1, p, &bar[s]);
+            tma_load_3d(Fs + ((size_t)s * K + k) * (SH::FPL / 8), &maps.m[k], sh ? x0 : x0 - 2, sh ? y0 : y0 - 1, p,
+                        &bar[s]);
     };
     if (tid == 0) {
         for (int s = 0; s < ns; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
     }
+    if (sh)   // the pad ring of the (a, c) planes is the zero outside the domain read by the boundary outputs
+        for (int q = tid; q < 4 * NM * (SH::PPL / 8); q += 32 * NWW) Ps[q] = 0.0;
     __syncthreads();
     if (tid == 0)
         for (int it = 0; it < ns && it < nit; ++it) issue(it);
 
-    const int lx = lane - 1, ly0 = RR * w - 1;
+    const int lx = sh ? lane : lane - 1, ly0 = sh ? RR * w : RR * w - 1;
     const int gx = x0 + lx;
-    const bool xin = gx >= 0 && gx < n, xout = lx >= 0 && lx < SH::TX && gx < n;
+    const bool xin = gx >= 0 && gx < n;
+    const bool xout = sh ? (gx < n && (lane >= 1 || gx == 0) && (lane <= SH::TX || gx == n - 1))
+                         : (lx >= 0 && lx < SH::TX && gx < n);
     unsigned inxy = 0u, oks = 0u;
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
         const int ly = ly0 + r, gy = y0 + ly;
         if (xin && gy >= 0 && gy < n) inxy |= 1u << r;
-        if (xout && ly >= 0 && ly < SH::TY && gy < n) oks |= 1u << r;
+        const bool yout = sh ? (gy < n && (ly >= 1 || gy == 0) && (ly <= SH::TY || gy == n - 1))
+                             : (ly >= 0 && ly < SH::TY && gy < n);
+        if (xout && yout) oks |= 1u << r;
     }
     const BLConst c = A.bl;
     double vmax[NM];
@@ -946,7 +977,7 @@ __global__ void __launch_bounds__(32 * NWW, 1) k_bl(const __grid_constant__ BLMa
         mbar_wait(&bar[s], (it / ns) & 1);
         const unsigned in = ((unsigned)p < (unsigned)n) ? inxy : 0u;
         const double *F = Fs + (size_t)s * K * (SH::FPL / 8);
-        const int o0 = (RR * w) * SH::FW + lane + 1;
+        const int o0 = (RR * w) * SH::FW + lane + (sh ? 0 : 1);
         const int po = (RR * w + 1) * SH::PW + lane + 1;
 #pragma unroll
         for (int r = 0; r < RR; ++r) {
@@ -1106,11 +1137,14 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
     const int nit = z1 - z0 + 2;              // ingest planes z0-1 .. z1
     constexpr int PROD0 = 4 * R4_WG;          // first producer warp
     const bool producer = w >= PROD0;
+    const bool sh = A.sh != 0;
+    const int sh1 = sh ? 0 : 1;               // region coordinate -> tile-origin offset
     auto issue = [&](int it) {
         const int s = it % ns, p = z0 - 1 + it;
         mbar_expect_tx(&bar[s], K * SH::FW * SH::FH * 8);
         for (int k = 0; k < K; ++k)
-            tma_load_3d(Fs + ((size_t)s * K + k) * (SH::FPL / 8), &maps.m[k], x0 - 2, y0 - 1, p, &bar[s]);
+            tma_load_3d(Fs + ((size_t)s * K + k) * (SH::FPL / 8), &maps.m[k], sh ? x0 : x0 - 2, sh ? y0 : y0 - 1, p,
+                        &bar[s]);
     };
     const int ptid = tid - 32 * PROD0;        // producer thread index
     if (ptid == 0) {
@@ -1118,6 +1152,8 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
         fence_mbar_init();
         for (int s = 0; s < ns && s < nit; ++s) issue(s);
     }
+    if (sh)   // zero pad ring of the p / z planes (read by the boundary outputs)
+        for (int q = tid; q < 16 * (SH::PPL / 8); q += R4_NT) Ps[q] = 0.0;
     __syncthreads();
     const bool folds = FE == 3 && A.nfold > 0;
     // the two roles run separate loops (so the consumers' rings are not live in the producers' code)
@@ -1134,13 +1170,15 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
             const bool zin = (unsigned)p < (unsigned)n, zout = p >= z0 && p < z1;
             for (int q = ptid; q < RW * SH::RH; q += 32 * R4_PW) {
                 const int col = q & 31, row = q >> 5;        // region column / row
-                const int px = x0 - 1 + col, py = y0 - 1 + row;
+                const int px = x0 - sh1 + col, py = y0 - sh1 + row;
                 double av[NM], cv[NM], fo[NM], wo[NM];
                 // the folds only at the tile's own points (they are stored, not stencilled)
-                const bool fpt = folds && zout && col >= 1 && col - 1 < SH::TX && px < n && row >= 1 &&
-                                 row - 1 < SH::TY && py < n;
+                const bool own = sh ? (px < n && (col >= 1 || px == 0) && (col <= SH::TX || px == n - 1) && py < n &&
+                                       (row >= 1 || py == 0) && (row <= SH::TY || py == n - 1))
+                                    : (col >= 1 && col - 1 < SH::TX && px < n && row >= 1 && row - 1 < SH::TY && py < n);
+                const bool fpt = folds && zout && own;
                 if (zin && (unsigned)px < (unsigned)n && (unsigned)py < (unsigned)n) {
-                    r4_point<FE>(A, F, SH::FPL / 8, row * SH::FW + col + 1, fpt, av, cv, fo, wo);
+                    r4_point<FE>(A, F, SH::FPL / 8, row * SH::FW + col + sh1, fpt, av, cv, fo, wo);
                 } else {
 #pragma unroll
                     for (int k = 0; k < NM; ++k) { av[k] = 0.0; cv[k] = 0.0; }
@@ -1168,13 +1206,16 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
     // consumer role: node kc = w / R4_WG, rows RR*wi .. RR*wi+RR-1 of the region
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R4_CREG) : "memory");
     const int kc = w / R4_WG, wi = w % R4_WG;
-    const int gx = x0 + lane - 1;
-    const bool xout = lane >= 1 && lane - 1 < SH::TX && gx < n;
+    const int gx = x0 + lane - sh1;
+    const bool xout = sh ? (gx < n && (lane >= 1 || gx == 0) && (lane <= SH::TX || gx == n - 1))
+                         : (lane >= 1 && lane - 1 < SH::TX && gx < n);
     unsigned oks = 0u;
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
-        const int ly = RR * wi + r - 1, gy = y0 + ly;
-        if (xout && ly >= 0 && ly < SH::TY && gy < n) oks |= 1u << r;
+        const int ly = RR * wi + r - sh1, gy = y0 + ly;
+        const bool yout = sh ? (gy < n && (ly >= 1 || gy == 0) && (ly <= SH::TY || gy == n - 1))
+                             : (ly >= 0 && ly < SH::TY && gy < n);
+        if (xout && yout) oks |= 1u << r;
     }
     const BLConst c = A.bl;
     double vmax = 0.0;
