@@ -44,7 +44,7 @@ KERNEL_NAMES = {
     (2, "fine_defect_restrict"): "f2d::k_smooth2r: 2 Jacobi sweeps + defect + full weighting (26 B/pt)",
     (2, "fine_prolong_correct"): "f2d::k_smooth2<MODE 2>: bilinear prolongation + correction + 2 Jacobi sweeps (26 B/pt)",
     (2, "fine_smoother"): "f2d::k_smooth2: 2 Jacobi sweeps (24 B/pt)",
-    (3, "fine_smoother"): "f3d::k_smooth2: 2 Jacobi sweeps, z-streaming (24 B/pt)",
+    (3, "fine_smoother"): "f3d::k_smooth2ws: 2 Jacobi sweeps, warp-specialised z-streaming (24 B/pt)",
     (3, "fine_defect_restrict"): "f3d::k_restrict: defect + full weighting (17 B/pt)",
     (3, "fine_prolong_correct"): "f3d::k_prolong: trilinear prolongation + correction (17 B/pt)",
     (3, "residual"): "f3d residual pass (DESIGN.md §6.10)",

@@ -19,7 +19,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # bench.py kernel classes -> kernel-name patterns (the fine level is the launch with the largest grid)
 CLASS_PATTERNS = {
-    "fine_smoother": [r"f3d::k_smooth2<\d+, 0,", r"f3d::k_smooth2ws<0>"],
+    "fine_smoother": [r"f3d::k_smooth2<\d+, 0,", r"f3d::k_smooth2ws<0[,>]"],
     "fine_defect_restrict": [r"f3d::k_restrict", r"f2d::k_smooth2r<0,"],
     "fine_prolong_correct": [r"f3d::k_prolong", r"f2d::k_smooth2<false, 2,", r"f2d::k_smooth2<0, 2,"],
     "residual": [r"k_resid", r"f3d::k_bl<\d+, 1,"],
@@ -94,8 +94,10 @@ def main(path, out, title, workload=None):
         db = json.load(open(tj)) if os.path.exists(tj) else {}
         ent = {}
         for cls, pats in CLASS_PATTERNS.items():
-            # the fine-level launch of a class is its longest one (grid sizes mix tiles and z chunks)
-            cand = [(sum(m.get("gpu__time_duration.sum", 0) for m in ms) / len(ms), name, grid, ms)
+            # the fine-level launch of a class is the (kernel, grid) group with the largest total time
+            # (grid sizes mix tiles and z chunks; a one-off launch such as the first sweep's RHS from
+            # the node fields is not the class's representative)
+            cand = [(sum(m.get("gpu__time_duration.sum", 0) for m in ms), name, grid, ms)
                     for (name, grid, blk), ms in groups.items() if any(re.search(p, name) for p in pats)]
             if not cand:
                 continue
@@ -103,7 +105,7 @@ def main(path, out, title, workload=None):
             rd = sum(m.get("dram__bytes_read.sum", 0) for m in ms) / len(ms)
             wr = sum(m.get("dram__bytes_write.sum", 0) for m in ms) / len(ms)
             ent[cls] = {"kernel": name, "grid": grid, "dram_bytes_per_launch": rd + wr, "dram_read": rd,
-                        "dram_write": wr, "source": f"{os.path.relpath(out, ROOT)} (longest launch of the class = fine level)"}
+                        "dram_write": wr, "source": f"{os.path.relpath(out, ROOT)} (the class's (kernel, grid) group with the largest total time = fine level)"}
         db[workload] = ent
         json.dump(db, open(tj, "w"), indent=1)
         print("traffic ->", tj, list(ent))
