@@ -203,6 +203,27 @@ def test_unweighted_residual_steps_bitwise(gpu, ora, cid, n, mode):
     assert np.array_equal(h.solution(0).cpu().numpy(), u_ref)
 
 
+@pytest.mark.parametrize("n", [63, 127])
+def test_config5_whole_trajectory_bitwise(gpu, ora, n):
+    """All five steps of config 5's trajectory (the one bench.py times) at reduced size, step by
+    step against the oracle: counts, residual bits and the end value of every step.  (At 511^3 the
+    stored oracle results cover steps 1-4, tests/test_gpu_fullsize.py.)"""
+    cfg, u0, G = synth.problem_inputs(5, 0, n)
+    assert cfg.steps == 5
+    h = make(gpu, cfg, G, mode=MODE_ISDC)
+    prob = ora.Problem(cfg, G, mode=MODE_ISDC)
+    h.set_initial(torch.from_numpy(u0).cuda(), 0)
+    u_ref = u0.copy()
+    for s in range(cfg.steps):
+        st = h.step()
+        u_ref, st_ref = ora.step(prob, u_ref, float(s) * cfg.dt)
+        assert st["sweeps"] == st_ref["sweeps"] and st["vcycles"] == st_ref["vcycles"], s
+        assert st["converged"] == st_ref["converged"]
+        assert np.array_equal(st["node_cycles"], st_ref["node_cycles"])
+        assert np.array_equal(st["res_hist"], st_ref["res_hist"]), s
+        assert np.array_equal(h.solution(0).cpu().numpy(), u_ref), s
+
+
 # ------------------------------------------------ alternative execution paths (same bits)
 @pytest.mark.parametrize("env,mode", [({"ISDC_DEVICE_SDC": "0"}, MODE_SDC), ({"ISDC_DEVICE_SDC": "0"}, MODE_ISDC_CAPPED),
                                       ({"ISDC_NO_GRAPHS": "1"}, MODE_ISDC), ({"ISDC_NO_GRAPHS": "1"}, MODE_SDC),
