@@ -100,9 +100,9 @@ def golden_sweeps(cid, seed, mode):
     try:
         with open(name) as f:
             rec = json.load(f)
-        return float(np.mean([s["sweeps"] for s in rec["steps"]]))
+        return float(np.mean([s["sweeps"] for s in rec["steps"]])), len(rec["steps"])
     except Exception:
-        return None
+        return None, 0
 
 
 class ClockSampler:
@@ -226,8 +226,10 @@ def run_reference(a):
     t_start = time.perf_counter()
     mode = synth.MODE_SDC if a.mode == "sdc" else synth.MODE_ISDC
     cfg, u0, G = synth.problem_inputs(a.config, a.seed)
-    kt = golden_sweeps(a.config, a.seed, a.mode)
+    kt, kt_steps = golden_sweeps(a.config, a.seed, a.mode)
     kt_src = "tests/golden (oracle trajectory)"
+    if kt is not None and kt_steps < cfg.steps:
+        kt_src = f"tests/golden (oracle trajectory, steps 1-{kt_steps} of {cfg.steps})"
     if cfg.fixed_sweeps > 0:
         kt, kt_src = float(cfg.fixed_sweeps), "fixed sweeps per step"
     elif kt is None:
