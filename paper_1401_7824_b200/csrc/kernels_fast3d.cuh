@@ -594,12 +594,16 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
         for (int it = 0; it < R_NS && it < nit; ++it) issue(it);
 
     const double c0 = c.c0, c1 = c.c1, c2 = c.c2;
-    // coarse role
-    const bool crole = tid < R_CX * R_CY;
-    const int ci = tid % R_CX, cj = tid / R_CX;
+    // coarse role: 16 x 16 thread grid over the 15 x 15 coarse tile (half-warp = one coarse row).
+    // The defect plane is stored de-interleaved in x -- odd fine columns (the coarse points) at
+    // [0, 16), even ones at [16, 32) -- so a coarse row's centre / left / right loads are unit
+    // stride (2 shared wavefronts per warp load instead of the 4-6 of the stride-2 layout).
+    const int ci = tid & 15, cj = tid >> 4;
+    const bool crole = ci < R_CX && cj < R_CY;
+    const int pcol = (lane & 1) ? (lane >> 1) : 16 + (lane >> 1);   // this lane's column in the d plane
     const int gI = I0 + ci, gJ = J0 + cj;
     const bool cout_ok = crole && gI < nc && gJ < nc;
-    const int dx = 2 * ci + 1, dy = 2 * cj + 1;
+    const int dy = 2 * cj + 1;
     double fdl = 0, edl = 0, dcl = 0, fdm = 0, edm = 0, dcm = 0;   // partials at planes 2K (lower), 2K+1 (mid)
 
     // register rings (plane it at slot it % 3 for q, f and it % 2 for e); the z loop is unrolled by
@@ -622,15 +626,16 @@ __global__ void __launch_bounds__(NT, 1) k_restrict(const __grid_constant__ CUte
                 const double faces = fr[m3][r] + (qr[mm3][r] + qr[i3][r]);
                 const double edges = er[m2][r] + (fr[mm3][r] + fr[i3][r]);
                 const double su = (c0 * qr[m3][r] + c1 * faces) + c2 * edges;
-                D[(R * w + r) * R_DW + lane] = Bp[(R * w + r) * R_BW + lane] - su;
+                D[(R * w + r) * R_DW + pcol] = Bp[(R * w + r) * R_BW + lane] - su;
             }
         }
         __syncthreads();
         if (tid == 0 && it + R_NS < nit) issue(it + R_NS);
         if (dd && crole) {
             const int j = it - 2;    // fine plane 2K0 + j
-            const double *d0 = D + (dy - 1) * R_DW + dx, *d1 = d0 + R_DW, *d2 = d1 + R_DW;
-            const double rd0 = d0[-1] + d0[1], rd1 = d1[-1] + d1[1], rd2 = d2[-1] + d2[1];
+            // fine column dx = 2 ci + 1 sits at ci, its neighbours 2 ci and 2 ci + 2 at 16 + ci, 17 + ci
+            const double *d0 = D + (dy - 1) * R_DW + ci, *d1 = d0 + R_DW, *d2 = d1 + R_DW;
+            const double rd0 = d0[16] + d0[17], rd1 = d1[16] + d1[17], rd2 = d2[16] + d2[17];
             const double fd = rd1 + (d0[0] + d2[0]);
             const double ed = rd0 + rd2;
             const double dc = d1[0];
@@ -1260,7 +1265,7 @@ __global__ void __launch_bounds__(R4_NT, 1) k_resid4(const __grid_constant__ BLM
 // with a 5-plane ring of 36 x 36 boxes at (x0-2, y0-2).  DESIGN.md §6.11.
 // ---------------------------------------------------------------------------------------------
 constexpr int FE_W = RW + 4, FE_H = RH + 4;
-constexpr int FE_NS = 8;   // ring: 5 planes in use + 3 in flight
+constexpr int FE_NS = 8;   // ring: 3 planes in use (arrival .. centre) + 5 in flight
 constexpr int FE_PL = a128(FE_W * FE_H * 8);
 constexpr size_t FE_SMEM = (size_t)FE_NS * FE_PL + 8 * FE_NS + 128;
 
@@ -1288,26 +1293,40 @@ __global__ void __launch_bounds__(NT, 1) k_fe_cd4(const __grid_constant__ CUtens
     if (tid == 0)
         for (int it = 0; it < FE_NS && it < nit; ++it) issue(it);
     const int gx = x0 + lane;
-    for (int it = 0; it < nit; ++it) {
+    // z neighbours from a register ring of the owned points (slot = plane index mod 5; the z loop is
+    // unrolled by 5 so every slot is a compile-time constant): 4 shared loads per thread and plane
+    // instead of 16, and a plane's slot is free two steps after its arrival (not four)
+    double zr[5][R];
+    auto step = [&](auto Kc, int it) {
+        constexpr int K = decltype(Kc)::value;                                  // it % 5
+        constexpr int km2 = (K + 1) % 5, km1 = (K + 2) % 5, kp1 = (K + 4) % 5;   // planes it-4, it-3, it-1
         mbar_wait(&bar[it % FE_NS], (it / FE_NS) & 1);
+        const double *Pn = Us + (it % FE_NS) * (FE_PL / 8);
+#pragma unroll
+        for (int r = 0; r < R; ++r) zr[K][r] = Pn[(R * w + r + 2) * FE_W + lane + 2];
         if (it >= 4) {   // centre plane z = z0-2+it-2
             const int gz = z0 - 4 + it;
-            const double *Pm2 = Us + ((it - 4) % FE_NS) * (FE_PL / 8), *Pm1 = Us + ((it - 3) % FE_NS) * (FE_PL / 8);
-            const double *P0 = Us + ((it - 2) % FE_NS) * (FE_PL / 8), *Pp1 = Us + ((it - 1) % FE_NS) * (FE_PL / 8);
-            const double *Pp2 = Us + (it % FE_NS) * (FE_PL / 8);
+            const double *P0 = Us + ((it - 2) % FE_NS) * (FE_PL / 8);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int ly = R * w + r, gy = y0 + ly;
                 const int o = (ly + 2) * FE_W + lane + 2;
                 const double dx = (8.0 * (P0[o + 1] - P0[o - 1]) - (P0[o + 2] - P0[o - 2])) * kx;
                 const double dy = (8.0 * (P0[o + FE_W] - P0[o - FE_W]) - (P0[o + 2 * FE_W] - P0[o - 2 * FE_W])) * ky;
-                const double dz = (8.0 * (Pp1[o] - Pm1[o]) - (Pp2[o] - Pm2[o])) * kz;
+                const double dz = (8.0 * (zr[kp1][r] - zr[km1][r]) - (zr[K][r] - zr[km2][r])) * kz;
                 if (gx < n && gy < n) Fout[(long long)gz * plane + (long long)gy * pitch + gx] = -((dx + dy) + dz);
             }
         }
         __syncthreads();
-        // the slot of plane it-4 is free now: refill it with plane it+4 (= it-4+FE_NS)
-        if (tid == 0 && it >= 4 && it - 4 + FE_NS < nit) issue(it - 4 + FE_NS);
+        // plane it-2 has been the centre plane (or never is one): refill its slot with plane it-2+FE_NS
+        if (tid == 0 && it >= 2 && it - 2 + FE_NS < nit) issue(it - 2 + FE_NS);
+    };
+    for (int base = 0; base < nit; base += 5) {
+        step(std::integral_constant<int, 0>{}, base);
+        if (base + 1 < nit) step(std::integral_constant<int, 1>{}, base + 1);
+        if (base + 2 < nit) step(std::integral_constant<int, 2>{}, base + 2);
+        if (base + 3 < nit) step(std::integral_constant<int, 3>{}, base + 3);
+        if (base + 4 < nit) step(std::integral_constant<int, 4>{}, base + 4);
     }
 }
 
