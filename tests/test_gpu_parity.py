@@ -207,7 +207,7 @@ def test_unweighted_residual_steps_bitwise(gpu, ora, cid, n, mode):
 def test_config5_whole_trajectory_bitwise(gpu, ora, n):
     """All five steps of config 5's trajectory (the one bench.py times) at reduced size, step by
     step against the oracle: counts, residual bits and the end value of every step.  (At 511^3 the
-    stored oracle results cover steps 1-4, tests/test_gpu_fullsize.py.)"""
+    stored oracle results cover the same five steps, tests/test_gpu_fullsize.py.)"""
     cfg, u0, G = synth.problem_inputs(5, 0, n)
     assert cfg.steps == 5
     h = make(gpu, cfg, G, mode=MODE_ISDC)
