@@ -178,6 +178,7 @@ struct isdc_ctx {
     int rs_chunk_mul = 16;     // its row chunks ~ this x SMs / column tiles (3-stage ring; 5 stages measured no faster)
     bool ws3d = true;          // ISDC_WS3D: warp-specialised 3D smoother on levels n >= ws3d_min
     int ws3d_min = 63;         // ISDC_WS3D_MIN
+    int ws_ns = 8;             // ISDC_WS_NS: TMA stages of the shifted ws smoother with u from memory (6, 8, 10)
     bool shift3d = true;       // ISDC_SHIFT3D: shifted 30-point tiling of the 3D streaming kernels (17 tiles per axis at 511)
     bool fuse3d = false;       // ISDC_FUSE3D: 3D prolongation fused into the post-smoother (needs ws3d;
                                // bitwise equal, measured slower: 1.34 ms vs 0.42 + 0.77 ms at 511^3)
@@ -634,6 +635,8 @@ isdc_status launch_smooth2_3d_ws(isdc_ctx *h, double *out, const double *in, con
     int zc = pick_chunk(h, tx * ty, g.n, 4);
     dim3 grd(tx, ty, (g.n + zc - 1) / zc);
     if (e) kl(h, f3d::k_smooth2ws<2>, grd, f3d::WSCfg<2>::NT, f3d::WSCfg<2>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    else if (sh && in && h->ws_ns == 8) kl(h, f3d::k_smooth2ws<0, 8, true>, grd, f3d::WSCfg<0, 8, true>::NT, f3d::WSCfg<0, 8, true>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
+    else if (sh && in && h->ws_ns == 10) kl(h, f3d::k_smooth2ws<0, 10, true>, grd, f3d::WSCfg<0, 10, true>::NT, f3d::WSCfg<0, 10, true>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     else if (sh && !in) kl(h, f3d::k_smooth2ws<1, 0, true>, grd, f3d::WSCfg<1, 0, true>::NT, f3d::WSCfg<1, 0, true>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     else if (sh) kl(h, f3d::k_smooth2ws<0, 0, true>, grd, f3d::WSCfg<0, 0, true>::NT, f3d::WSCfg<0, 0, true>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
     else if (!in) kl(h, f3d::k_smooth2ws<1>, grd, f3d::WSCfg<1>::NT, f3d::WSCfg<1>::SMEM)(*mu, *mb, *me, out, g.n, g.pitch, g.plane, c, zc);
@@ -2322,6 +2325,7 @@ bool kernel_attrs(isdc_ctx *h) {
     set((const void *)f3d::k_smooth2<4, 0, 8>); set((const void *)f3d::k_smooth2<4, 1, 8>);
     set((const void *)f3d::k_smooth2ws<0>); set((const void *)f3d::k_smooth2ws<1>); set((const void *)f3d::k_smooth2ws<2>);
     set((const void *)f3d::k_smooth2ws<0, 0, true>); set((const void *)f3d::k_smooth2ws<1, 0, true>);
+    set((const void *)f3d::k_smooth2ws<0, 8, true>); set((const void *)f3d::k_smooth2ws<0, 10, true>);
     set((const void *)f3d::k_restrict);
     set((const void *)f3d::k_fe_cd4);
     auto setbl = [&](auto F) {
@@ -2417,6 +2421,7 @@ isdc_status isdc_create(const isdc_problem *prob, void *ws, size_t bytes, void *
     if (const char *w3m = getenv("ISDC_WS3D_MIN")) h->ws3d_min = atoi(w3m);
     if (const char *f3 = getenv("ISDC_FUSE3D")) h->fuse3d = f3[0] != '0';
     if (const char *s3 = getenv("ISDC_SHIFT3D")) h->shift3d = s3[0] != '0';
+    if (const char *s8 = getenv("ISDC_WS_NS")) h->ws_ns = atoi(s8);
     if (const char *s2 = getenv("ISDC_STREAM2D")) h->stream2d = s2[0] != '0';
     if (const char *f2 = getenv("ISDC_FUSE2D")) h->fuse2d = f2[0] != '0';
     if (const char *fo = getenv("ISDC_FOLDS")) h->folds = fo[0] != '0';

@@ -236,7 +236,8 @@ def test_config5_whole_trajectory_bitwise(gpu, ora, n):
                                       ({"ISDC_RESID2D_TMA": "0"}, MODE_ISDC), ({"ISDC_CTAIL": "0"}, MODE_ISDC),
                                       ({"ISDC_CTAIL": "0"}, MODE_SDC), ({"ISDC_CTAIL": "2"}, MODE_ISDC),
                                       ({"ISDC_CTAIL": "2"}, MODE_SDC),
-                                      ({"ISDC_RHS128": "1"}, MODE_ISDC), ({"ISDC_SHIFT3D": "0"}, MODE_ISDC)])
+                                      ({"ISDC_RHS128": "1"}, MODE_ISDC), ({"ISDC_SHIFT3D": "0"}, MODE_ISDC), ({"ISDC_WS_NS": "6"}, MODE_ISDC),
+                                      ({"ISDC_WS_NS": "10"}, MODE_ISDC)])
 def test_execution_paths_bitwise(gpu, ora, monkeypatch, env, mode):
     """Host-side node-solve tests, un-captured sweeps, sweep-by-sweep steps, the generic kernels, the
     fold-free RHS, the unfused tail, the tile-based 2D RHS / residual, the unfused 2D transfers and
