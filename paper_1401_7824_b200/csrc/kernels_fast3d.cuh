@@ -258,8 +258,10 @@ constexpr int WS_UWS = RW + 4, WS_BWS = RW;
 constexpr int WS_UPLS = a128(WS_UWS * S_UH * 8), WS_BPLS = a128(WS_BWS * S_BH * 8);
 template <int MODE, int NSX = 0, bool SH = false>
 struct WSCfg {
-    // TMA stages (3 in use: it - 2 .. it; + 1 in MODE 2).  8 and 10 stages measured slower at 511^3
-    // (0.83 vs 0.79 ms per fine launch): the kernel is not waiting on the TMA depth
+    // TMA stages (3 in use: it - 2 .. it; + 1 in MODE 2).  Default 6; the host picks NSX = 8 for the
+    // shifted tiling with u from memory (one z chunk of 515 planes per tile at 511^3: 0.660 vs 0.694 ms
+    // per fine launch; 10 stages: 0.688).  With the unshifted 18 x 18 x 5-chunk grid 8 and 10 stages
+    // had measured slower (0.83 vs 0.79 ms)
     static constexpr int NS = NSX ? NSX : (MODE == 2 ? 7 : 6);
     static constexpr int NT = 32 * 2 * WS_GW;
     static constexpr int UPL = SH ? WS_UPLS : S_UPL, BPL = SH ? WS_BPLS : S_BPL, EPL = MODE == 2 ? 2 * WS_EPL : 0;
